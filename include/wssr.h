@@ -1,0 +1,183 @@
+/*
+ * wssr.h - C ABI of the B200-native warm-started stochastic-reconfiguration (WSSR) step.
+ *
+ * Drop-in boundary for the reference package `vmcsr` (arXiv 2512.05749).  Every entry point
+ * replaces one reference function; the Python shim in paper_2512_05749_b200/ binds them with
+ * ctypes and keeps the reference's names, argument meaning and exception classes.
+ *
+ *   wssr_assemble_f64    <- vmcsr.estimators.assemble          estimators.py:74-100
+ *                           (+ clip_local_energies              estimators.py:53-71)
+ *   wssr_qr_f64          <- vmcsr.linalg.qr_orthonormalize      linalg.py:29-105
+ *   wssr_ssi_svd_f64     <- vmcsr.svdengine.ssi_svd             svdengine.py:88-158
+ *   wssr_subspace_drift_f64 <- vmcsr.svdengine.subspace_drift   svdengine.py:199-226
+ *   wssr_step_f64        <- vmcsr.optimizers.wssr_step          optimizers.py:292-391
+ *                           (svd_backend="ssi", state.step >= 1)
+ *   wssr_gemm_f64        test/diagnostic export of the DMMA GEMM family (no reference twin)
+ *
+ * All array arguments are DEVICE pointers (CUDA global memory) of IEEE float64, row-major with
+ * an explicit leading dimension.  The per-sample log-derivative matrix is passed sample-major
+ * (N x P row-major, the reference's SampleBatch.theta_logderivs, estimators.py:22); the
+ * reference's parameter-major o_matrix (P x N) is the same memory read column-major, so the
+ * library never makes the transposed/centred copy the reference makes (estimators.py:91,97).
+ *
+ * No C++ exceptions cross this boundary.  Every function returns a WSSR_* status; the message
+ * of the last failure is available from wssr_last_error().  Calls are stream-ordered on the
+ * stream set with wssr_set_stream (default: the legacy default stream) and a context must not
+ * be shared between host threads (reference: single control thread).
+ */
+#ifndef WSSR_H_
+#define WSSR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The shim raises the reference exception class named beside each code. */
+enum {
+  WSSR_OK = 0,
+  WSSR_ERR_VALUE = 1,             /* ValueError (shapes/arguments, svdengine.py:124-125)     */
+  WSSR_ERR_RANK_TOO_LARGE = 2,    /* errors.RankTooLarge   (svdengine.py:116-117)            */
+  WSSR_ERR_DEGENERATE_INPUT = 3,  /* errors.DegenerateInput (svdengine.py:118-119, 149-150)  */
+  WSSR_ERR_ZERO_MATRIX = 4,       /* errors.ZeroMatrix      (linalg.py:53-54, 103-104)       */
+  WSSR_ERR_RANK_COLLAPSE = 5,     /* errors.RankCollapse    (optimizers.py:350-351)          */
+  WSSR_ERR_DEGENERATE_BATCH = 6,  /* errors.DegenerateBatch (estimators.py:61-62, 84-85)     */
+  WSSR_ERR_CUDA = 7,              /* CUDA runtime failure                                     */
+  WSSR_ERR_NCCL = 8,              /* collective failure                                       */
+  WSSR_ERR_UNSUPPORTED = 9        /* configuration not implemented on the device path         */
+};
+
+/* ssi / step flags */
+#define WSSR_FLAG_FINAL_RESIDUAL 0x1 /* also run the look-ahead after the last iteration so   */
+                                     /* SsiReport.subspace_residual is filled (svdengine.py:137) */
+#define WSSR_FLAG_CAREFUL 0x2        /* host-checked QR with the Gram-Schmidt patch path        */
+
+typedef struct wssr_ctx wssr_ctx;
+
+/*
+ * The stacked matrix Ohat of optimizers.py:323, in the sample-major view:
+ *   Ohat^T = [ hist_scale    * hist                       ]   (hist_rank rows)
+ *            [ samples_scale * (samples - 1 * mu^T)       ]   (n_samples rows)
+ * hist = state.obar^T (hist_rank x P), samples = raw log-derivatives (n_samples x P),
+ * mu = column means (P, or NULL for no centring).  samples_fro2 = ||samples_scale*(samples-mu)||_F^2
+ * when known (from wssr_assemble_f64), or < 0 to have the library compute it.
+ * Under row sharding `samples` is this rank's row shard and the history block lives on rank 0.
+ */
+typedef struct wssr_ohat_f64 {
+  int64_t n_params;
+  const double* hist;
+  int64_t hist_rank;
+  int64_t hist_ld;
+  double hist_scale;
+  const double* samples;
+  int64_t n_samples;
+  int64_t samples_ld;
+  const double* mu;
+  double samples_scale;
+  double samples_fro2;
+} wssr_ohat_f64;
+
+/* --- context ------------------------------------------------------------------------------ */
+int wssr_ctx_create(int device, wssr_ctx** out);
+void wssr_ctx_destroy(wssr_ctx* ctx);
+const char* wssr_last_error(const wssr_ctx* ctx);
+int wssr_set_stream(wssr_ctx* ctx, void* cuda_stream);
+int wssr_version(void);
+/* number of kernels this context launched so far (bench.py's gpu_launches) */
+int64_t wssr_kernel_launches(const wssr_ctx* ctx);
+
+/* --- row sharding over NCCL (one process per GPU) ----------------------------------------- */
+/* 128-byte ncclUniqueId produced on rank 0 and broadcast by the caller (torch.distributed). */
+int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]);
+int wssr_nccl_attach(wssr_ctx* ctx, const unsigned char id[128], int rank, int world);
+
+/* --- estimators.assemble (estimators.py:74-100) ------------------------------------------- */
+typedef struct wssr_assemble_out {
+  double* mu;       /* [P]  column means of theta_logderivs (global over ranks)               */
+  double* l_vector; /* [N]  (clip(E) - loss) / sqrt(N_global)                                 */
+  double* gradient; /* [P]  2 * o_matrix @ l_vector                                           */
+  /* host outputs */
+  double loss, raw_loss, e_mean, e_std;
+  double fro2;      /* ||o_matrix||_F^2                                                      */
+  int64_t n_global;
+} wssr_assemble_out;
+int wssr_assemble_f64(wssr_ctx* ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
+                      const double* energies, double clip_n_std, wssr_assemble_out* out);
+
+/* --- linalg.qr_orthonormalize (linalg.py:29-61) ------------------------------------------- */
+int wssr_qr_f64(wssr_ctx* ctx, int64_t rows, int64_t cols, const double* a, int64_t lda,
+                double* q, int64_t ldq, double* r /* cols x cols */, int64_t flags);
+
+/* --- svdengine.ssi_svd (svdengine.py:88-158) ---------------------------------------------- */
+typedef struct wssr_ssi_out {
+  double* u;       /* [P x rank], ld_u: left vectors; first k_pos columns valid              */
+  int64_t ld_u;
+  double* sigma;   /* [rank] sorted singular values (first k_pos valid)                     */
+  double* v;       /* [(hist_rank+n_samples) x rank], ld_v: right vectors as columns, or NULL */
+  int64_t ld_v;
+  /* host outputs */
+  int64_t k_pos;
+  int64_t iterations;
+  double residual; /* NaN when the final look-ahead was skipped (no WSSR_FLAG_FINAL_RESIDUAL) */
+} wssr_ssi_out;
+int wssr_ssi_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, int64_t rank, int64_t max_iters,
+                     const double* u_init, int64_t ld_init, double residual_tol, int64_t flags,
+                     wssr_ssi_out* out);
+
+/* --- svdengine.subspace_drift (svdengine.py:199-226) -------------------------------------- */
+int wssr_subspace_drift_f64(wssr_ctx* ctx, int64_t n_rows, const double* u1, int64_t ld1,
+                            const double* s1, int64_t r1, const double* u2, int64_t ld2,
+                            const double* s2, int64_t r2, double* sigma_drift,
+                            double* projector_drift);
+
+/* --- optimizers.wssr_step (optimizers.py:292-391), warm-started SSI branch ----------------- */
+typedef struct wssr_step_in {
+  const wssr_ohat_f64* ohat; /* hist = state.obar^T, hist_scale = 1 (library applies sqrt(delta));
+                                samples_scale = bundle scale (library applies sqrt(1-delta))  */
+  const double* lbar;        /* [hist_rank] state.lbar                                        */
+  const double* l_vector;    /* [n_samples] bundle.l_vector                                    */
+  const double* gradient;    /* [P] bundle.gradient when it is exactly 2*o_matrix@l_vector
+                                (as produced by wssr_assemble_f64), else NULL -> recomputed   */
+  const double* theta;       /* [P] */
+  double eta;
+  const double* u_init;      /* [P x requested] warm start (optimizers.py:277-289, prepared by
+                                the caller: it owns the host-side PCG64 draws)               */
+  int64_t ld_init;
+  int64_t requested;         /* min(r_max, P, r + N)  (optimizers.py:326)                      */
+  const double* u_prev;      /* state.u_prev [P x r_prev] (drift telemetry)                    */
+  int64_t ld_prev;
+  int64_t r_prev;
+  double delta, sigma_floor, r_reg, eps_grow;
+  int64_t sigma_floor_relative;
+  int64_t r_max;
+  int64_t max_iters;
+  double residual_tol;
+  int64_t flags;
+} wssr_step_in;
+
+typedef struct wssr_step_out {
+  double* theta_next;   /* [P] */
+  double* update;       /* [P] preconditioned direction, or NULL */
+  double* u_next;       /* [P x requested], ld_u: state'.u_prev (first r_eff columns)          */
+  int64_t ld_u;
+  double* obar_next_t;  /* [requested x P], ld_obar: state'.obar^T = (U sigma)^T              */
+  int64_t ld_obar;
+  double* lbar_next;    /* [requested] state'.lbar (first r_eff entries)                     */
+  double* sigma;        /* [requested] sorted singular values                                */
+  /* host outputs */
+  int64_t r_eff, k_pos, iterations, next_r_max, binding;
+  double residual, sigma_drift, projector_drift;
+} wssr_step_out;
+int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
+
+/* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
+int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,
+                  int64_t lda, const double* shift, const double* b, int64_t ldb, double* c,
+                  int64_t ldc, double alpha, int accumulate, int max_splits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WSSR_H_ */

@@ -1,0 +1,194 @@
+"""ctypes binding of the C ABI in include/wssr.h (libwssr.so, built by __graft_entry__.build()).
+
+There is deliberately no fallback: if the shared library is missing or no CUDA device is
+present, every entry point raises.  PyTorch is used only to own device memory and to provide
+the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libwssr.so")
+
+WSSR_OK = 0
+WSSR_FLAG_FINAL_RESIDUAL = 0x1
+WSSR_FLAG_CAREFUL = 0x2
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_dbl = ctypes.c_double
+
+
+class OhatF64(ctypes.Structure):
+    _fields_ = [
+        ("n_params", _i64),
+        ("hist", _vp), ("hist_rank", _i64), ("hist_ld", _i64), ("hist_scale", _dbl),
+        ("samples", _vp), ("n_samples", _i64), ("samples_ld", _i64), ("mu", _vp),
+        ("samples_scale", _dbl), ("samples_fro2", _dbl),
+    ]
+
+
+class AssembleOut(ctypes.Structure):
+    _fields_ = [
+        ("mu", _vp), ("l_vector", _vp), ("gradient", _vp),
+        ("loss", _dbl), ("raw_loss", _dbl), ("e_mean", _dbl), ("e_std", _dbl),
+        ("fro2", _dbl), ("n_global", _i64),
+    ]
+
+
+class SsiOut(ctypes.Structure):
+    _fields_ = [
+        ("u", _vp), ("ld_u", _i64), ("sigma", _vp), ("v", _vp), ("ld_v", _i64),
+        ("k_pos", _i64), ("iterations", _i64), ("residual", _dbl),
+    ]
+
+
+class StepIn(ctypes.Structure):
+    _fields_ = [
+        ("ohat", ctypes.POINTER(OhatF64)),
+        ("lbar", _vp), ("l_vector", _vp), ("gradient", _vp), ("theta", _vp), ("eta", _dbl),
+        ("u_init", _vp), ("ld_init", _i64), ("requested", _i64),
+        ("u_prev", _vp), ("ld_prev", _i64), ("r_prev", _i64),
+        ("delta", _dbl), ("sigma_floor", _dbl), ("r_reg", _dbl), ("eps_grow", _dbl),
+        ("sigma_floor_relative", _i64), ("r_max", _i64), ("max_iters", _i64),
+        ("residual_tol", _dbl), ("flags", _i64),
+    ]
+
+
+class StepOut(ctypes.Structure):
+    _fields_ = [
+        ("theta_next", _vp), ("update", _vp), ("u_next", _vp), ("ld_u", _i64),
+        ("obar_next_t", _vp), ("ld_obar", _i64), ("lbar_next", _vp), ("sigma", _vp),
+        ("r_eff", _i64), ("k_pos", _i64), ("iterations", _i64), ("next_r_max", _i64),
+        ("binding", _i64),
+        ("residual", _dbl), ("sigma_drift", _dbl), ("projector_drift", _dbl),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/wssr.h declares
+SIGNATURES = {
+    "wssr_version": (ctypes.c_int, []),
+    "wssr_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    "wssr_ctx_destroy": (None, [_vp]),
+    "wssr_last_error": (ctypes.c_char_p, [_vp]),
+    "wssr_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "wssr_kernel_launches": (_i64, [_vp]),
+    "wssr_nccl_unique_id": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "wssr_nccl_attach": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+    "wssr_assemble_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _dbl,
+                                         ctypes.POINTER(AssembleOut)]),
+    "wssr_qr_f64": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
+    "wssr_ssi_svd_f64": (ctypes.c_int, [_vp, ctypes.POINTER(OhatF64), _i64, _i64, _vp, _i64,
+                                        _dbl, _i64, ctypes.POINTER(SsiOut)]),
+    "wssr_subspace_drift_f64": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
+                                               _i64, ctypes.POINTER(_dbl),
+                                               ctypes.POINTER(_dbl)]),
+    "wssr_step_f64": (ctypes.c_int, [_vp, ctypes.POINTER(StepIn), ctypes.POINTER(StepOut)]),
+    "wssr_gemm_f64": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _vp,
+                                     _i64, _vp, _i64, _dbl, ctypes.c_int, ctypes.c_int]),
+}
+
+_STATUS = {
+    1: ValueError,
+    2: errors.RankTooLarge,
+    3: errors.DegenerateInput,
+    4: errors.ZeroMatrix,
+    5: errors.RankCollapse,
+    6: errors.DegenerateBatch,
+    7: errors.DeviceError,
+    8: errors.DeviceError,
+    9: errors.Unsupported,
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libwssr.so and declare every prototype.  Raises if it is missing."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(
+                f"libwssr.so not found at {path}; run __graft_entry__.build() first "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+class Context:
+    """One native context per CUDA device (reference: single control thread)."""
+
+    def __init__(self, device: int):
+        lib = load_library()
+        h = _vp()
+        rc = lib.wssr_ctx_create(int(device), ctypes.byref(h))
+        if rc != WSSR_OK:
+            raise errors.DeviceError(f"wssr_ctx_create(device={device}) failed with status {rc}")
+        self.lib = lib
+        self.handle = h
+        self.device = int(device)
+        self.rank = 0
+        self.world = 1
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.lib.wssr_ctx_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def call(self, name, *args):
+        import torch
+
+        lib = self.lib
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        lib.wssr_set_stream(self.handle, _vp(stream))
+        rc = getattr(lib, name)(self.handle, *args)
+        if rc != WSSR_OK:
+            msg = lib.wssr_last_error(self.handle)
+            msg = msg.decode() if msg else ""
+            raise _STATUS.get(rc, errors.DeviceError)(msg or f"{name} failed with status {rc}")
+        return rc
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.wssr_kernel_launches(self.handle))
+
+
+_contexts: dict = {}
+
+
+def context(device=None) -> Context:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise errors.DeviceError("the WSSR drop-in needs a CUDA device (no CPU fallback)")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    ctx = _contexts.get(dev)
+    if ctx is None:
+        ctx = Context(dev)
+        _contexts[dev] = ctx
+    return ctx
+
+
+def ptr(t) -> _vp:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return _vp(0)
+    return _vp(t.data_ptr())

@@ -1,0 +1,985 @@
+// WSSR engine: the reference control flow of assemble / qr_orthonormalize / ssi_svd /
+// subspace_drift / wssr_step, re-expressed as stream-ordered launches of the sm_100a kernels.
+// Every function cites the reference lines it follows.  Host synchronisation happens only where
+// the reference returns a Python scalar that decides control flow (the SSI exit test,
+// svdengine.py:139-141, and the rank cut, optimizers.py:348-355).
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <utility>
+
+#include "engine.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+struct wssr_ctx {
+  wssr::Context c;
+};
+
+namespace wssr {
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define WSSR_CUDA(expr)                                                                      \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw Fail{WSSR_ERR_CUDA, std::string(#expr) + " -> " + cudaGetErrorString(e_)};       \
+  } while (0)
+
+constexpr double kDeficientColumnRel = 1e-12;  // linalg.py:16 DEFICIENT_COLUMN_REL
+constexpr double kZeroMatrixNorm = 1e-300;     // linalg.py:15 ZERO_MATRIX_NORM
+constexpr double kCholPivotRel = 1e-13;        // CholeskyQR2 safety margin (see kernels.cuh)
+constexpr double kDriftZero = 1e-12;           // svdengine.py:222-225
+
+double* Context::splitk_buffer(size_t n) {
+  if (n > splitk_cap) {
+    if (splitk) {
+      cudaStreamSynchronize(stream);
+      cudaFree(splitk);
+      splitk = nullptr;
+    }
+    size_t cap = std::max(n, splitk_cap * 2);
+    if (cudaMalloc(&splitk, cap * sizeof(double)) != cudaSuccess) {
+      splitk = nullptr;
+      splitk_cap = 0;
+      return nullptr;
+    }
+    splitk_cap = cap;
+  }
+  return splitk;
+}
+
+namespace {
+
+// Stream-ordered scratch allocation from the device's default memory pool.
+struct Buf {
+  double* p = nullptr;
+  cudaStream_t st = nullptr;
+  Buf() = default;
+  Buf(size_t n, cudaStream_t s) : st(s) {
+    if (n) WSSR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
+  }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      st = o.st;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  ~Buf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+  operator double*() const { return p; }
+  int64_t* i64() const { return reinterpret_cast<int64_t*>(p); }
+  int* i32() const { return reinterpret_cast<int*>(p); }
+};
+
+inline int blocks_for(int64_t n, int threads, int cap) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+void post_launch(Context& ctx) {
+  ++ctx.kernel_launches;
+  WSSR_CUDA(cudaGetLastError());
+}
+
+void sync(Context& ctx) { WSSR_CUDA(cudaStreamSynchronize(ctx.stream)); }
+
+void d2h(Context& ctx, void* dst, const void* src, size_t bytes) {
+  WSSR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
+}
+
+void allreduce(Context& ctx, double* buf, size_t n) {
+  cudaError_t e = ctx.allreduce(buf, n);
+  if (e != cudaSuccess) throw Fail{WSSR_ERR_NCCL, "allreduce failed"};
+}
+
+// ---- GEMM wrappers ------------------------------------------------------------------------
+// CM: C(MxN) = alpha * sum_k (A[k*lda+m] - shift[m]) B[k*ldb+n]
+void gemm_cm(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+             const double* shift, const double* B, int64_t ldb, double* C, int64_t ldc,
+             double alpha, bool accumulate, int max_splits = 1024) {
+  GemmArgs a{A, lda, B, ldb, shift, C, ldc, M, N, K, 0, alpha, accumulate ? 1 : 0, nullptr};
+  WSSR_CUDA(gemm(ctx, Layout::CM, a, max_splits, ctx.stream));
+}
+// RM: C(MxN) = alpha * sum_k (A[m*lda+k] - shift[k]) B[k*ldb+n]
+void gemm_rm(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+             const double* shift, const double* B, int64_t ldb, double* C, int64_t ldc,
+             double alpha, bool accumulate, int max_splits = 1024) {
+  GemmArgs a{A, lda, B, ldb, shift, C, ldc, M, N, K, 0, alpha, accumulate ? 1 : 0, nullptr};
+  WSSR_CUDA(gemm(ctx, Layout::RM, a, max_splits, ctx.stream));
+}
+
+// Gram G (k x k) = A^T A, A rows x k (lda); allreduced over ranks when rows are sharded.
+void gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* G,
+          bool distributed) {
+  gemm_cm(ctx, k, k, rows, A, lda, nullptr, A, lda, G, k, 1.0, false);
+  if (distributed) allreduce(ctx, G, (size_t)(k * k));
+}
+
+// ---- small helpers -------------------------------------------------------------------------
+void copy2d(Context& ctx, const double* in, int64_t ldi, int64_t rows, int64_t cols, double scale,
+            double* out, int64_t ldo) {
+  if (rows <= 0 || cols <= 0) return;
+  copy2d_kernel<<<blocks_for(rows * cols, 256, 8 * ctx.num_sms), 256, 0, ctx.stream>>>(
+      in, ldi, rows, cols, scale, out, ldo);
+  post_launch(ctx);
+}
+
+// sum of squares of a strided matrix -> device scalar (deterministic)
+void sumsq_matrix(Context& ctx, const double* x, int64_t rows, int64_t cols, int64_t ld,
+                  double* out_dev, double scale = 1.0) {
+  if (rows <= 0 || cols <= 0) {
+    WSSR_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), ctx.stream));
+    return;
+  }
+  const int nblk = std::min<int64_t>(2 * ctx.num_sms, rows);
+  const int64_t rpb = (rows + nblk - 1) / nblk;
+  const int nb = (int)((rows + rpb - 1) / rpb);
+  Buf part(nb, ctx.stream);
+  matrix_sumsq_partials_kernel<<<nb, 256, 0, ctx.stream>>>(x, rows, cols, ld, rpb, part);
+  post_launch(ctx);
+  reduce_final_kernel<<<1, 256, 0, ctx.stream>>>(part, nb, scale, out_dev);
+  post_launch(ctx);
+}
+
+double read_scalar(Context& ctx, const double* dev) {
+  double h = 0.0;
+  d2h(ctx, &h, dev, sizeof(double));
+  sync(ctx);
+  return h;
+}
+
+// ---- k x k Cholesky + inverse ---------------------------------------------------------------
+void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int* status) {
+  const size_t smem = sizeof(double) * ((size_t)k * k + k);
+  const int threads = k <= 32 ? 128 : (k <= 64 ? 256 : 512);
+  if (smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      WSSR_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    chol_inv_smem_kernel<<<1, threads, smem, ctx.stream>>>(G, k, R, Rinv, status, kCholPivotRel);
+    post_launch(ctx);
+  } else {
+    Buf W((size_t)k * k + k, ctx.stream);
+    chol_inv_gmem_kernel<<<1, 1024, 0, ctx.stream>>>(G, k, W, R, Rinv, status, kCholPivotRel);
+    post_launch(ctx);
+  }
+}
+
+// ---- QR: CholeskyQR2 fast path, two-pass Gram-Schmidt with canonical fill as the exact
+// re-statement of linalg.py:64-105 when CholeskyQR2 cannot resolve the block. -------------------
+
+// Fast CholeskyQR2.  Q (rows x k, ldq), R (k x k).  Failure is recorded in status[] (device)
+// and checked by the caller; no host synchronisation.
+void cholqr2(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* Q,
+             int64_t ldq, double* R, int* status, bool distributed) {
+  Buf G((size_t)k * k, ctx.stream), R1((size_t)k * k, ctx.stream), R1i((size_t)k * k, ctx.stream),
+      R2((size_t)k * k, ctx.stream), R2i((size_t)k * k, ctx.stream),
+      T((size_t)rows * k, ctx.stream);
+  gram(ctx, rows, k, A, lda, G, distributed);
+  chol_inv(ctx, G, (int)k, R1, R1i, status);
+  gemm_rm(ctx, rows, k, k, A, lda, nullptr, R1i, k, T, k, 1.0, false);
+  gram(ctx, rows, k, T, k, G, distributed);
+  chol_inv(ctx, G, (int)k, R2, R2i, status);
+  gemm_rm(ctx, rows, k, k, T, k, nullptr, R2i, k, Q, ldq, 1.0, false);
+  triu_mul_kernel<<<blocks_for(k * k, 256, 1 << 20), 256, 0, ctx.stream>>>(R2, R1, (int)k, R);
+  post_launch(ctx);
+}
+
+__global__ void set_entry_kernel(double* p, double v) { *p = v; }
+__global__ void add_col_kernel(double* R, int64_t ldr, int64_t col, const double* c, int64_t n) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) R[i * ldr + col] += c[i];
+}
+
+// linalg.py:64-84 (_gram_schmidt_with_patch) + 87-105 (_canonical_fill), on the device with a
+// host loop over columns.  Single-rank only.
+void cgs2_patch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* Q,
+                int64_t ldq, double* R, double fro) {
+  const double tol = kDeficientColumnRel * fro;
+  WSSR_CUDA(cudaMemsetAsync(R, 0, sizeof(double) * k * k, ctx.stream));
+  Buf coeff(std::max<int64_t>(k, 1), ctx.stream), scal(1, ctx.stream);
+  auto project_out = [&](int64_t j, double* v, int64_t ldv, bool into_r) {
+    // v -= Q[:, :j] (Q[:, :j]^T v), twice
+    for (int pass = 0; pass < 2; ++pass) {
+      if (j == 0) break;
+      gemm_cm(ctx, j, 1, rows, Q, ldq, nullptr, v, ldv, coeff, 1, 1.0, false);
+      if (into_r) {
+        add_col_kernel<<<1, 256, 0, ctx.stream>>>(R, k, j, coeff, j);
+        post_launch(ctx);
+      }
+      gemm_rm(ctx, rows, 1, j, Q, ldq, nullptr, coeff, 1, v, ldv, -1.0, true);
+    }
+  };
+  for (int64_t j = 0; j < k; ++j) {
+    double* qj = Q + j;
+    copy2d(ctx, A + j, lda, rows, 1, 1.0, qj, ldq);
+    project_out(j, qj, ldq, true);
+    sumsq_matrix(ctx, qj, rows, 1, ldq, scal);
+    const double norm = std::sqrt(read_scalar(ctx, scal));
+    if (norm > tol) {
+      copy2d(ctx, qj, ldq, rows, 1, 1.0 / norm, qj, ldq);
+      set_entry_kernel<<<1, 1, 0, ctx.stream>>>(R + j * k + j, norm);
+      post_launch(ctx);
+      continue;
+    }
+    // canonical fill: first e_i whose projected remainder has norm > 0.5, else the best one
+    int64_t best = -1;
+    double best_norm = -1.0;
+    bool done = false;
+    for (int64_t i = 0; i < rows && !done; ++i) {
+      WSSR_CUDA(cudaMemset2DAsync(qj, sizeof(double) * ldq, 0, sizeof(double), rows, ctx.stream));
+      set_entry_kernel<<<1, 1, 0, ctx.stream>>>(qj + i * ldq, 1.0);
+      post_launch(ctx);
+      project_out(j, qj, ldq, false);
+      sumsq_matrix(ctx, qj, rows, 1, ldq, scal);
+      const double nw = std::sqrt(read_scalar(ctx, scal));
+      if (nw > 0.5) {
+        copy2d(ctx, qj, ldq, rows, 1, 1.0 / nw, qj, ldq);
+        done = true;
+      } else if (nw > best_norm) {
+        best_norm = nw;
+        best = i;
+      }
+    }
+    if (!done) {
+      if (best < 0 || best_norm <= 0.0)
+        throw Fail{WSSR_ERR_ZERO_MATRIX, "no canonical direction available for deficiency patch"};
+      WSSR_CUDA(cudaMemset2DAsync(qj, sizeof(double) * ldq, 0, sizeof(double), rows, ctx.stream));
+      set_entry_kernel<<<1, 1, 0, ctx.stream>>>(qj + best * ldq, 1.0);
+      post_launch(ctx);
+      project_out(j, qj, ldq, false);
+      copy2d(ctx, qj, ldq, rows, 1, 1.0 / best_norm, qj, ldq);
+    }
+    // R[j][j] stays 0 (linalg.py:193)
+  }
+}
+
+// qr_orthonormalize (linalg.py:29-61).  careful=false: CholeskyQR2 only, failures flagged in
+// status (device) for the caller's end-of-step check.  careful=true: host-checked; falls back
+// to the Gram-Schmidt patch path exactly where the reference leaves its LAPACK fast path.
+void qr(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* Q,
+        int64_t ldq, double* R, int* status, bool careful, bool distributed) {
+  if (!careful) {
+    cholqr2(ctx, rows, k, A, lda, Q, ldq, R, status, distributed);
+    return;
+  }
+  Buf s(1, ctx.stream);
+  sumsq_matrix(ctx, A, rows, k, lda, s);
+  if (distributed) allreduce(ctx, s, 1);
+  const double fro = std::sqrt(read_scalar(ctx, s));
+  if (fro < kZeroMatrixNorm) {
+    char msg[128];
+    std::snprintf(msg, sizeof msg, "cannot orthonormalize a numerically zero matrix (norm %.3e)",
+                  fro);
+    throw Fail{WSSR_ERR_ZERO_MATRIX, msg};
+  }
+  Buf st(1, ctx.stream);
+  WSSR_CUDA(cudaMemsetAsync(st, 0, sizeof(double), ctx.stream));
+  cholqr2(ctx, rows, k, A, lda, Q, ldq, R, st.i32(), distributed);
+  int hst[2] = {0, 0};
+  d2h(ctx, hst, st, sizeof(hst));
+  sync(ctx);
+  if (hst[0] == 0) return;
+  if (distributed)
+    throw Fail{WSSR_ERR_UNSUPPORTED, "rank-deficient block under row sharding"};
+  cgs2_patch(ctx, rows, k, A, lda, Q, ldq, R, fro);
+}
+
+// ---- the stacked matrix Ohat (optimizers.py:321-324) as a virtual two-block operator ----------
+struct Ohat {
+  int64_t P = 0;
+  const double* hist = nullptr;
+  int64_t r = 0, ldh = 0;
+  double sh = 0.0;
+  const double* samp = nullptr;
+  int64_t n = 0, lds = 0;
+  const double* mu = nullptr;
+  double ss = 1.0;
+  int64_t cols() const { return r + n; }
+};
+
+// v (cols x k, ldv) = Ohat^T q   (svdengine.py:133)
+void apply_OT(Context& ctx, const Ohat& o, const double* q, int64_t ldq, int64_t k, double* v,
+              int64_t ldv) {
+  if (o.r > 0) {
+    if (o.sh == 0.0) {
+      WSSR_CUDA(cudaMemset2DAsync(v, sizeof(double) * ldv, 0, sizeof(double) * k, o.r,
+                                  ctx.stream));
+    } else {
+      gemm_rm(ctx, o.r, k, o.P, o.hist, o.ldh, nullptr, q, ldq, v, ldv, o.sh, false);
+    }
+  }
+  if (o.n > 0)
+    gemm_rm(ctx, o.n, k, o.P, o.samp, o.lds, o.mu, q, ldq, v + o.r * ldv, ldv, o.ss, false);
+}
+
+// u (P x k, ldu) = Ohat v   (svdengine.py:134), summed over ranks
+void apply_O(Context& ctx, const Ohat& o, const double* v, int64_t ldv, int64_t k, double* u,
+             int64_t ldu) {
+  if (o.n > 0) {
+    gemm_cm(ctx, o.P, k, o.n, o.samp, o.lds, o.mu, v + o.r * ldv, ldv, u, ldu, o.ss, false);
+  } else {
+    WSSR_CUDA(cudaMemset2DAsync(u, sizeof(double) * ldu, 0, sizeof(double) * k, o.P, ctx.stream));
+  }
+  if (o.r > 0 && o.sh != 0.0)
+    gemm_cm(ctx, o.P, k, o.r, o.hist, o.ldh, nullptr, v, ldv, u, ldu, o.sh, true);
+  if (ctx.world() > 1) {
+    if (ldu != k) throw Fail{WSSR_ERR_VALUE, "sharded apply_O needs a dense output"};
+    allreduce(ctx, u, (size_t)(o.P * k));
+  }
+}
+
+// ||Ohat||_F^2 (svdengine.py:118,129): history block plus the sample block (known from
+// assemble, or computed).  Returns the host value (global over ranks).
+double ohat_fro2(Context& ctx, const Ohat& o, double samples_fro2, bool hist_owned) {
+  double total = 0.0;
+  Buf s(1, ctx.stream);
+  if (o.r > 0 && o.sh != 0.0 && hist_owned) {
+    sumsq_matrix(ctx, o.hist, o.r, o.P, o.ldh, s, o.sh * o.sh);
+    total += read_scalar(ctx, s);
+  }
+  if (o.n > 0 || ctx.world() > 1) {
+    if (samples_fro2 >= 0.0) {
+      total += samples_fro2;
+    } else {
+      if (o.mu) throw Fail{WSSR_ERR_VALUE, "samples_fro2 required for a centred block"};
+      sumsq_matrix(ctx, o.samp, o.n, o.P, o.lds, s, o.ss * o.ss);
+      allreduce(ctx, s, 1);
+      total += read_scalar(ctx, s);
+    }
+  }
+  return total;
+}
+
+// ---- ssi_svd (svdengine.py:88-158) ------------------------------------------------------------
+struct SsiResult {
+  int64_t k_pos = 0, r_eff = 0, iterations = 0;
+  double residual = std::numeric_limits<double>::quiet_NaN();
+  double sigma0 = 0.0;
+  Buf qv;          // (cols x k) right vectors, columns already in sorted order
+  Buf order;       // int64 [k]
+};
+
+// U_out (P x k, ldU) gets the re-orthonormalised left vectors (first k_pos columns), sigma_out
+// the sorted values.  fro2 is the global ||Ohat||_F^2.
+SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
+                   const double* u_init, int64_t ld_init, double tol, double fro2, bool final_res,
+                   bool careful, double* U_out, int64_t ldU, double* sigma_out, double r_reg,
+                   int* status) {
+  const int64_t P = o.P, cols = o.cols();
+  const bool dist = ctx.world() > 1;
+  cudaStream_t st = ctx.stream;
+  Buf q((size_t)P * k, st), ua((size_t)P * k, st), ub((size_t)P * k, st);
+  Buf va((size_t)std::max<int64_t>(cols, 1) * k, st), vb((size_t)std::max<int64_t>(cols, 1) * k, st);
+  Buf Rk((size_t)k * k, st), quot((size_t)k * k, st), scal(4, st);
+  double* u = ua;
+  double* w = ub;
+  double* v = va;
+  double* v2 = vb;
+
+  qr(ctx, P, k, u_init, ld_init, q, k, Rk, status, careful, false);  // svdengine.py:130
+  apply_OT(ctx, o, q, k, k, v, k);
+  apply_O(ctx, o, v, k, k, u, k);
+  SsiResult res;
+  int64_t it = 0;
+  Buf tmp((size_t)P * k, st);
+  while (true) {  // svdengine.py:132-142
+    qr(ctx, P, k, u, k, q, k, Rk, status, careful, false);
+    ++it;
+    if (it >= max_iters && !final_res) {
+      res.residual = std::numeric_limits<double>::quiet_NaN();  // look-ahead skipped
+      break;
+    }
+    // look-ahead pass: w = Ohat Ohat^T q is also the next iteration's u (svdengine.py:137)
+    apply_OT(ctx, o, q, k, k, v2, k);
+    apply_O(ctx, o, v2, k, k, w, k);
+    gemm_cm(ctx, k, k, P, q, k, nullptr, w, k, quot, k, 1.0, false);  // quotient = q^T w
+    copy2d(ctx, w, k, P, k, 1.0, tmp, k);
+    gemm_rm(ctx, P, k, k, q, k, nullptr, quot, k, tmp, k, -1.0, true);  // w - q quotient
+    sumsq_matrix(ctx, tmp, P, k, k, scal);
+    small_norms_kernel<<<1, 256, 0, st>>>(nullptr, nullptr, 0, quot, (int)k, scal + 1);
+    post_launch(ctx);
+    double h[3];
+    d2h(ctx, h, scal, 3 * sizeof(double));
+    sync(ctx);
+    const double residual = std::sqrt(h[0]) / fro2;
+    const double mixing = h[2] / fro2;
+    res.residual = residual;
+    if (std::max(residual, mixing) < tol || it >= max_iters) break;
+    std::swap(v, v2);
+    std::swap(u, w);
+  }
+  res.iterations = it;
+
+  // sigma from the QR of the final v block, sorted (svdengine.py:144-150)
+  Buf qv_raw((size_t)std::max<int64_t>(cols, 1) * k, st), Rv((size_t)k * k, st);
+  qr(ctx, cols, k, v, k, qv_raw, k, Rv, status, careful, dist);
+  res.order = Buf(k, st);
+  Buf ints(1, st);
+  sort_sigma_kernel<<<1, 256, sizeof(double) * k, st>>>(Rv, (int)k, r_reg, res.order.i64(),
+                                                       sigma_out, ints.i32());
+  post_launch(ctx);
+  int hi[2];
+  d2h(ctx, hi, ints, sizeof(hi));
+  d2h(ctx, &res.sigma0, sigma_out, sizeof(double));
+  sync(ctx);
+  res.k_pos = hi[0];
+  res.r_eff = hi[1];
+  if (res.k_pos == 0)
+    throw Fail{WSSR_ERR_DEGENERATE_INPUT, "iteration produced no positive singular values"};
+  const int64_t kp = res.k_pos;
+  // U = QR(u[:, order[:k]]) and V = q_v[:, order] (svdengine.py:151-152)
+  Buf uperm((size_t)P * kp, st);
+  gather_cols_kernel<<<blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
+      u, k, P, res.order.i64(), (int)kp, uperm, kp);
+  post_launch(ctx);
+  Buf Rf((size_t)kp * kp, st);
+  qr(ctx, P, kp, uperm, kp, U_out, ldU, Rf, status, careful, false);
+  res.qv = Buf((size_t)std::max<int64_t>(cols, 1) * k, st);
+  if (cols > 0) {
+    gather_cols_kernel<<<blocks_for(cols * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
+        qv_raw, k, cols, res.order.i64(), (int)kp, res.qv, k);
+    post_launch(ctx);
+  }
+  return res;
+}
+
+// Runs the SSI optimistically (no per-QR host checks); if any CholeskyQR2 flagged a block it
+// could not resolve, re-runs in careful mode, which reproduces the reference's QR branches.
+template <class F>
+auto with_fallback(Context& ctx, int64_t flags, F&& body) -> decltype(body(false, (int*)nullptr)) {
+  if (!(flags & WSSR_FLAG_CAREFUL)) {
+    Buf status(1, ctx.stream);
+    WSSR_CUDA(cudaMemsetAsync(status, 0, sizeof(double), ctx.stream));
+    auto r = body(false, status.i32());
+    int hs[2];
+    d2h(ctx, hs, status, sizeof(hs));
+    sync(ctx);
+    if (hs[0] == 0) return r;
+  }
+  Buf status(1, ctx.stream);
+  WSSR_CUDA(cudaMemsetAsync(status, 0, sizeof(double), ctx.stream));
+  return body(true, status.i32());
+}
+
+// ---- subspace_drift (svdengine.py:199-226) ----------------------------------------------------
+std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, int64_t ld1,
+                                const double* s1, int64_t r1, const double* u2, int64_t ld2,
+                                const double* s2, int64_t r2) {
+  const int64_t r = std::min(r1, r2);
+  if (r == 0) return {0.0, 0.0};
+  cudaStream_t st = ctx.stream;
+  Buf C((size_t)r * r, st), X((size_t)rows * r, st), GX((size_t)r * r, st), out(3, st);
+  small_norms_kernel<<<1, 256, 0, st>>>(s1, s2, (int)r, nullptr, 0, out);
+  post_launch(ctx);
+  gemm_cm(ctx, r, r, rows, u1, ld1, nullptr, u2, ld2, C, r, 1.0, false);  // u1^T u2
+  copy2d(ctx, u2, ld2, rows, r, 1.0, X, r);
+  gemm_rm(ctx, rows, r, r, u1, ld1, nullptr, C, r, X, r, -1.0, true);  // u2 - u1 (u1^T u2)
+  gemm_cm(ctx, r, r, rows, X, r, nullptr, X, r, GX, r, 1.0, false);
+  const int kk = (int)(r + (r & 1));
+  const size_t smem = sizeof(double) * kk * kk + sizeof(int) * kk;
+  if (smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      WSSR_CUDA(cudaFuncSetAttribute(jacobi_maxeig_smem_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    jacobi_maxeig_smem_kernel<<<1, 512, smem, st>>>(GX, (int)r, out + 2);
+  } else {
+    Buf W((size_t)kk * kk, st);
+    jacobi_maxeig_gmem_kernel<<<1, 1024, sizeof(int) * kk, st>>>(GX, (int)r, W, out + 2);
+  }
+  post_launch(ctx);
+  double h[3];
+  d2h(ctx, h, out, sizeof(h));
+  sync(ctx);
+  double sd = h[0];
+  double pd = std::sqrt(std::max(h[2], 0.0));
+  if (sd < kDriftZero) sd = 0.0;
+  if (pd < kDriftZero) pd = 0.0;
+  return {sd, pd};
+}
+
+// ---- estimators.assemble (estimators.py:74-100) --------------------------------------------
+__global__ void merge_rank_stats_kernel(int64_t p, double n_local, double n_global,
+                                        const double* mu_loc, const double* m2_loc,
+                                        const double* g_loc, double lsum_loc, const double* mu,
+                                        double* m2_out, double* g_out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = mu_loc[i] - mu[i];
+    m2_out[i] = n_local > 0 ? m2_loc[i] + n_local * d * d : 0.0;
+    g_out[i] = n_local > 0 ? g_loc[i] + d * lsum_loc : 0.0;
+  }
+}
+__global__ void scale_kernel(int64_t n, double a, const double* x, double* y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a * x[i];
+}
+
+void assemble(Context& ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
+              const double* energies, double n_std, wssr_assemble_out* out) {
+  cudaStream_t st = ctx.stream;
+  const bool dist = ctx.world() > 1;
+  int64_t n_global = n;
+  int64_t offset = 0;
+  if (dist) {
+    // global sample count and this rank's offset (exact in doubles for n < 2^53)
+    Buf cnt(ctx.world(), st);
+    WSSR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(double) * ctx.world(), st));
+    const double nd = (double)n;
+    WSSR_CUDA(cudaMemcpyAsync(cnt + ctx.comm->rank, &nd, sizeof(double), cudaMemcpyHostToDevice, st));
+    allreduce(ctx, cnt, ctx.world());
+    std::vector<double> h(ctx.world());
+    d2h(ctx, h.data(), cnt, sizeof(double) * h.size());
+    sync(ctx);
+    n_global = 0;
+    for (int r = 0; r < ctx.world(); ++r) {
+      if (r < ctx.comm->rank) offset += (int64_t)h[r];
+      n_global += (int64_t)h[r];
+    }
+  }
+  out->n_global = n_global;
+  if (n_global < 2) throw Fail{WSSR_ERR_DEGENERATE_BATCH, "need at least two samples to center the batch"};
+  if (std::isfinite(n_std) && n_std < 0.0)
+    throw Fail{WSSR_ERR_VALUE, "clipping width must be nonnegative"};
+  const double scale = 1.0 / std::sqrt((double)n_global);
+  const int clip = std::isfinite(n_std) ? 1 : 0;
+
+  // energy statistics on the full (gathered) energy vector; each rank keeps its slice of L
+  Buf e_all, l_all((size_t)n_global, st), lraw_all((size_t)n_global, st), scal(4, st);
+  const double* E = energies;
+  if (dist) {
+    e_all = Buf((size_t)n_global, st);
+    WSSR_CUDA(cudaMemsetAsync(e_all, 0, sizeof(double) * n_global, st));
+    WSSR_CUDA(cudaMemcpyAsync(e_all + offset, energies, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    allreduce(ctx, e_all, (size_t)n_global);
+    E = e_all;
+  }
+  energy_stats_kernel<<<1, 1024, 0, st>>>(E, n_global, n_std, clip, scale, l_all, lraw_all, scal);
+  post_launch(ctx);
+  WSSR_CUDA(cudaMemcpyAsync(out->l_vector, l_all + offset, sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, st));
+  const double* lraw = lraw_all + offset;
+
+  // one pass over O: column means, centred second moments, centred gradient sums
+  Buf m2(p, st), gsum(p, st);
+  if (n > 0) {
+    colstats_kernel<<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
+        derivs, n, p, ld, lraw, out->mu, m2, gsum);
+    post_launch(ctx);
+  } else {
+    WSSR_CUDA(cudaMemsetAsync(out->mu, 0, sizeof(double) * p, st));
+    WSSR_CUDA(cudaMemsetAsync(m2, 0, sizeof(double) * p, st));
+    WSSR_CUDA(cudaMemsetAsync(gsum, 0, sizeof(double) * p, st));
+  }
+  if (dist) {
+    // mu = sum_r n_r mu_r / N ; M2 = sum_r [M2_r + n_r (mu_r - mu)^2] ; G likewise
+    Buf mu_loc(p, st), mu(p, st), lsum(1, st);
+    WSSR_CUDA(cudaMemcpyAsync(mu_loc, out->mu, sizeof(double) * p, cudaMemcpyDeviceToDevice, st));
+    scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, (double)n, mu_loc, mu);
+    post_launch(ctx);
+    allreduce(ctx, mu, p);
+    scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, 1.0 / n_global, mu, mu);
+    post_launch(ctx);
+    Buf parts(1, st);
+    reduce_final_kernel<<<1, 256, 0, st>>>(lraw, (int)n, 1.0, lsum);
+    post_launch(ctx);
+    const double lsum_h = read_scalar(ctx, lsum);
+    merge_rank_stats_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(
+        p, (double)n, (double)n_global, mu_loc, m2, gsum, lsum_h, mu, m2, gsum);
+    post_launch(ctx);
+    allreduce(ctx, m2, p);
+    allreduce(ctx, gsum, p);
+    WSSR_CUDA(cudaMemcpyAsync(out->mu, mu, sizeof(double) * p, cudaMemcpyDeviceToDevice, st));
+  }
+  // gradient = 2 * o_matrix @ l_vector = 2 * gsum / N   (estimators.py:93)
+  scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, 2.0 / n_global, gsum,
+                                                                     out->gradient);
+  post_launch(ctx);
+  Buf fro(1, st);
+  {
+    const int nb = (int)std::min<int64_t>(2 * ctx.num_sms, (p + 255) / 256);
+    const int64_t chunk = (p + nb - 1) / nb;
+    const int nbb = (int)((p + chunk - 1) / chunk);
+    Buf part(nbb, st);
+    reduce_partials_kernel<<<nbb, 256, 0, st>>>(m2, p, chunk, 0, part);
+    post_launch(ctx);
+    reduce_final_kernel<<<1, 256, 0, st>>>(part, nbb, 1.0 / n_global, fro);
+    post_launch(ctx);
+  }
+  double hs[4];
+  d2h(ctx, hs, scal, sizeof(hs));
+  d2h(ctx, &out->fro2, fro, sizeof(double));
+  sync(ctx);
+  out->loss = hs[0];
+  out->raw_loss = hs[1];
+  out->e_mean = hs[2];
+  out->e_std = hs[3];
+}
+
+// ---- wssr_step (optimizers.py:292-391), ssi branch -------------------------------------------
+void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
+  const wssr_ohat_f64& oh = *in->ohat;
+  cudaStream_t st = ctx.stream;
+  const int64_t P = oh.n_params, k = in->requested;
+  const bool dist = ctx.world() > 1;
+  const bool owner = !dist || ctx.comm->rank == 0;  // history block lives on rank 0
+  const double sq_old = std::sqrt(in->delta), sq_new = std::sqrt(1.0 - in->delta);
+  Ohat o;
+  o.P = P;
+  o.hist = oh.hist;
+  o.r = owner ? oh.hist_rank : 0;
+  o.ldh = oh.hist_ld;
+  o.sh = sq_old * oh.hist_scale;
+  o.samp = oh.samples;
+  o.n = oh.n_samples;
+  o.lds = oh.samples_ld;
+  o.mu = oh.mu;
+  o.ss = sq_new * oh.samples_scale;
+  const int64_t cols = o.cols();
+  if (k < 1) throw Fail{WSSR_ERR_RANK_TOO_LARGE, "rank must be at least 1"};
+
+  double samples_fro2 = oh.samples_fro2 >= 0.0 ? oh.samples_fro2 * (sq_new * sq_new) : -1.0;
+  const double fro2 = ohat_fro2(ctx, o, samples_fro2, owner);
+  if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+
+  // lhat = [sqrt(delta) lbar, sqrt(1-delta) L]  (optimizers.py:324)
+  Buf lhat((size_t)std::max<int64_t>(cols, 1), st);
+  if (o.r > 0) copy2d(ctx, in->lbar, 1, o.r, 1, sq_old, lhat, 1);
+  if (o.n > 0) copy2d(ctx, in->l_vector, 1, o.n, 1, sq_new, lhat + o.r, 1);
+
+  SsiResult sr = with_fallback(ctx, in->flags, [&](bool careful, int* status) {
+    return ssi_core(ctx, o, k, in->max_iters, in->u_init, in->ld_init, in->residual_tol, fro2,
+                    (in->flags & WSSR_FLAG_FINAL_RESIDUAL) != 0, careful, out->u_next, out->ld_u,
+                    out->sigma, in->r_reg, status);
+  });
+  const int64_t r_eff = sr.r_eff;
+  if (r_eff < 1) throw Fail{WSSR_ERR_RANK_COLLAPSE, "no singular value passed the relative cutoff"};
+  const bool binding = sr.k_pos == k && k == in->r_max && r_eff == in->r_max;
+  int64_t next_r_max = in->r_max;
+  if (binding) {
+    next_r_max = (int64_t)std::ceil((1.0 + in->eps_grow) * (double)in->r_max);
+    next_r_max = std::min(next_r_max, P);
+  }
+  const double top_sq = sr.sigma0 * sr.sigma0;
+
+  // gbar = Ohat lhat  (optimizers.py:359)
+  Buf gbar(P, st);
+  if (in->gradient) {
+    // bundle.gradient = 2 o_matrix l_vector, exact for bundles assembled by this library
+    scale_kernel<<<blocks_for(P, 256, 8 * ctx.num_sms), 256, 0, st>>>(
+        P, 0.5 * sq_new * sq_new, in->gradient, gbar);
+    post_launch(ctx);
+  } else {
+    if (o.n > 0) {
+      gemm_cm(ctx, P, 1, o.n, o.samp, o.lds, o.mu, in->l_vector, 1, gbar, 1, o.ss * sq_new, false);
+    } else {
+      WSSR_CUDA(cudaMemsetAsync(gbar, 0, sizeof(double) * P, st));
+    }
+    if (dist) allreduce(ctx, gbar, P);
+  }
+  if (oh.hist_rank > 0 && o.sh != 0.0)
+    gemm_cm(ctx, P, 1, oh.hist_rank, oh.hist, oh.hist_ld, nullptr, in->lbar, 1, gbar, 1,
+            o.sh * sq_old, true);
+
+  // preconditioned update (optimizers.py:361-364)
+  Buf c(r_eff, st);
+  gemm_cm(ctx, r_eff, 1, P, out->u_next, out->ld_u, nullptr, gbar, 1, c, 1, 1.0, false);
+  const double floor = in->sigma_floor * (in->sigma_floor_relative ? top_sq : 1.0);
+  {
+    const int threads = 256;
+    const int blocks = blocks_for(P * 32, threads, 16 * ctx.num_sms);
+    precond_update_kernel<<<blocks, threads, sizeof(double) * 2 * r_eff, st>>>(
+        out->u_next, out->ld_u, P, (int)r_eff, c, out->sigma, gbar, 1.0 / floor, in->theta,
+        in->eta, out->theta_next, out->update);
+    post_launch(ctx);
+  }
+
+  // drift telemetry against the previous factors (optimizers.py:366-374)
+  double sd = 0.0, pd = 0.0;
+  if (in->r_prev > 0) {
+    const int64_t r_hist = oh.hist_rank;
+    Buf sprev(std::max<int64_t>(r_hist, 1), st);
+    if (r_hist > 0) {
+      row_norms_kernel<<<(unsigned)r_hist, 256, 0, st>>>(oh.hist, P, oh.hist_ld, sprev, 1);
+      post_launch(ctx);
+    }
+    const int64_t r1 = std::min(r_hist, in->r_prev);
+    auto d = drift(ctx, P, in->u_prev, in->ld_prev, sprev, r1, out->u_next, out->ld_u, out->sigma,
+                   r_eff);
+    sd = d.first;
+    pd = d.second;
+  }
+
+  // state refresh (optimizers.py:376-383): obar = U sigma, lbar = V[:r] lhat
+  {
+    dim3 grid((unsigned)((P + 31) / 32), (unsigned)((r_eff + 31) / 32));
+    transpose_scale_kernel<<<grid, dim3(32, 8), 0, st>>>(out->u_next, out->ld_u, P, (int)r_eff,
+                                                         out->sigma, out->obar_next_t,
+                                                         out->ld_obar);
+    post_launch(ctx);
+  }
+  if (cols > 0) {
+    gemm_cm(ctx, r_eff, 1, cols, sr.qv, k, nullptr, lhat, 1, out->lbar_next, 1, 1.0, false);
+  } else {
+    WSSR_CUDA(cudaMemsetAsync(out->lbar_next, 0, sizeof(double) * r_eff, st));
+  }
+  if (dist) allreduce(ctx, out->lbar_next, r_eff);
+  sync(ctx);
+
+  out->r_eff = r_eff;
+  out->k_pos = sr.k_pos;
+  out->iterations = sr.iterations;
+  out->next_r_max = next_r_max;
+  out->binding = binding ? 1 : 0;
+  out->residual = sr.residual;
+  out->sigma_drift = sd;
+  out->projector_drift = pd;
+}
+
+// ---- NCCL (dlopen'd so the library has no link-time NCCL dependency) ------------------------
+typedef int (*nccl_get_id_fn)(void*);
+typedef int (*nccl_init_rank_fn)(void**, int, const void*, int);
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_destroy_fn)(void*);
+
+struct NcclLib {
+  void* h = nullptr;
+  nccl_get_id_fn get_id = nullptr;
+  nccl_init_rank_fn init_rank = nullptr;
+  nccl_allreduce_fn allreduce = nullptr;
+  nccl_destroy_fn destroy = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    get_id = (nccl_get_id_fn)dlsym(h, "ncclGetUniqueId");
+    init_rank = (nccl_init_rank_fn)dlsym(h, "ncclCommInitRank");
+    allreduce = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+    destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
+    return get_id && init_rank && allreduce && destroy;
+  }
+};
+NcclLib g_nccl;
+
+struct NcclComm : Comm {
+  void* comm = nullptr;
+  cudaError_t allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
+    // ncclFloat64 = 8, ncclSum = 0
+    int r = g_nccl.allreduce(buf, buf, n, 8, 0, comm, st);
+    return r == 0 ? cudaSuccess : cudaErrorUnknown;
+  }
+  ~NcclComm() override {
+    if (comm) g_nccl.destroy(comm);
+  }
+};
+
+}  // namespace
+}  // namespace wssr
+
+// ================================ C ABI =====================================================
+using namespace wssr;
+
+namespace {
+int fail(wssr_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->c.last_error = msg;
+  return code;
+}
+template <class F>
+int guarded(wssr_ctx* ctx, F&& f) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  try {
+    WSSR_CUDA(cudaSetDevice(ctx->c.device));
+    f();
+    return WSSR_OK;
+  } catch (const Fail& e) {
+    return fail(ctx, e.code, e.msg);
+  } catch (const std::exception& e) {
+    return fail(ctx, WSSR_ERR_VALUE, e.what());
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int wssr_version(void) { return 1; }
+
+int wssr_ctx_create(int device, wssr_ctx** out) {
+  if (!out) return WSSR_ERR_VALUE;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return WSSR_ERR_CUDA;
+  if (device < 0 || device >= n) return WSSR_ERR_VALUE;
+  if (cudaSetDevice(device) != cudaSuccess) return WSSR_ERR_CUDA;
+  auto* c = new wssr_ctx();
+  c->c.device = device;
+  cudaDeviceGetAttribute(&c->c.num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return WSSR_OK;
+}
+
+void wssr_ctx_destroy(wssr_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.splitk) {
+    cudaDeviceSynchronize();
+    cudaFree(ctx->c.splitk);
+  }
+  delete ctx->c.comm;
+  delete ctx;
+}
+
+const char* wssr_last_error(const wssr_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : ""; }
+
+int wssr_set_stream(wssr_ctx* ctx, void* stream) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  ctx->c.stream = reinterpret_cast<cudaStream_t>(stream);
+  return WSSR_OK;
+}
+
+int64_t wssr_kernel_launches(const wssr_ctx* ctx) { return ctx ? ctx->c.kernel_launches : 0; }
+
+int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]) {
+  return guarded(ctx, [&] {
+    if (!g_nccl.load()) throw Fail{WSSR_ERR_NCCL, "libnccl.so.2 not loadable"};
+    if (g_nccl.get_id(out_id) != 0) throw Fail{WSSR_ERR_NCCL, "ncclGetUniqueId failed"};
+  });
+}
+
+int wssr_nccl_attach(wssr_ctx* ctx, const unsigned char id[128], int rank, int world) {
+  return guarded(ctx, [&] {
+    if (world < 1 || rank < 0 || rank >= world) throw Fail{WSSR_ERR_VALUE, "bad rank/world"};
+    delete ctx->c.comm;
+    ctx->c.comm = nullptr;
+    if (world == 1) return;
+    if (!g_nccl.load()) throw Fail{WSSR_ERR_NCCL, "libnccl.so.2 not loadable"};
+    auto* cm = new NcclComm();
+    cm->rank = rank;
+    cm->world = world;
+    if (g_nccl.init_rank(&cm->comm, world, id, rank) != 0) {
+      delete cm;
+      throw Fail{WSSR_ERR_NCCL, "ncclCommInitRank failed"};
+    }
+    ctx->c.comm = cm;
+  });
+}
+
+int wssr_assemble_f64(wssr_ctx* ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
+                      const double* energies, double clip_n_std, wssr_assemble_out* out) {
+  return guarded(ctx, [&] {
+    if (!out || p < 1 || n < 0 || ld < p) throw Fail{WSSR_ERR_VALUE, "bad assemble arguments"};
+    assemble(ctx->c, derivs, n, p, ld, energies, clip_n_std, out);
+  });
+}
+
+int wssr_qr_f64(wssr_ctx* ctx, int64_t rows, int64_t cols, const double* a, int64_t lda,
+                double* q, int64_t ldq, double* r, int64_t flags) {
+  return guarded(ctx, [&] {
+    if (rows < cols) throw Fail{WSSR_ERR_VALUE, "need at least as many rows as columns"};
+    if (cols < 1 || lda < cols || ldq < cols) throw Fail{WSSR_ERR_VALUE, "bad qr arguments"};
+    Context& c = ctx->c;
+    with_fallback(c, flags | WSSR_FLAG_CAREFUL, [&](bool careful, int* status) {
+      qr(c, rows, cols, a, lda, q, ldq, r, status, careful, false);
+      return 0;
+    });
+    sync(c);
+  });
+}
+
+int wssr_ssi_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, int64_t rank, int64_t max_iters,
+                     const double* u_init, int64_t ld_init, double residual_tol, int64_t flags,
+                     wssr_ssi_out* out) {
+  return guarded(ctx, [&] {
+    Context& c = ctx->c;
+    if (!ohat || !out || !u_init) throw Fail{WSSR_ERR_VALUE, "null argument"};
+    Ohat o;
+    o.P = ohat->n_params;
+    o.hist = ohat->hist;
+    o.r = (c.world() > 1 && c.comm->rank != 0) ? 0 : ohat->hist_rank;
+    o.ldh = ohat->hist_ld;
+    o.sh = ohat->hist_scale;
+    o.samp = ohat->samples;
+    o.n = ohat->n_samples;
+    o.lds = ohat->samples_ld;
+    o.mu = ohat->mu;
+    o.ss = ohat->samples_scale;
+    if (max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
+    const double fro2 = ohat_fro2(c, o, ohat->samples_fro2, true);
+    if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+    SsiResult sr = with_fallback(c, flags, [&](bool careful, int* status) {
+      return ssi_core(c, o, rank, max_iters, u_init, ld_init, residual_tol, fro2,
+                      (flags & WSSR_FLAG_FINAL_RESIDUAL) != 0, careful, out->u, out->ld_u,
+                      out->sigma, 0.5, status);
+    });
+    if (out->v && o.cols() > 0) copy2d(c, sr.qv, rank, o.cols(), sr.k_pos, 1.0, out->v, out->ld_v);
+    sync(c);
+    out->k_pos = sr.k_pos;
+    out->iterations = sr.iterations;
+    out->residual = sr.residual;
+  });
+}
+
+int wssr_subspace_drift_f64(wssr_ctx* ctx, int64_t n_rows, const double* u1, int64_t ld1,
+                            const double* s1, int64_t r1, const double* u2, int64_t ld2,
+                            const double* s2, int64_t r2, double* sigma_drift,
+                            double* projector_drift) {
+  return guarded(ctx, [&] {
+    auto d = drift(ctx->c, n_rows, u1, ld1, s1, r1, u2, ld2, s2, r2);
+    *sigma_drift = d.first;
+    *projector_drift = d.second;
+  });
+}
+
+int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out) {
+  return guarded(ctx, [&] {
+    if (!in || !out || !in->ohat) throw Fail{WSSR_ERR_VALUE, "null argument"};
+    if (in->max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
+    step(ctx->c, in, out);
+  });
+}
+
+int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,
+                  int64_t lda, const double* shift, const double* b, int64_t ldb, double* c,
+                  int64_t ldc, double alpha, int accumulate, int max_splits) {
+  return guarded(ctx, [&] {
+    if (layout == 0)
+      gemm_cm(ctx->c, m, n, k, a, lda, shift, b, ldb, c, ldc, alpha, accumulate != 0, max_splits);
+    else
+      gemm_rm(ctx->c, m, n, k, a, lda, shift, b, ldb, c, ldc, alpha, accumulate != 0, max_splits);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// Native WSSR engine: owns the device workspace, launches the sm_100a kernels in stream order
+// and implements the reference's control flow (assemble, ssi_svd, wssr_step) in C++.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/wssr.h"
+
+namespace wssr {
+
+enum class Layout : int;
+struct GemmArgs;
+
+// Collective interface for row (sample) sharding.  world == 1 -> no-op.
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() = default;
+  virtual cudaError_t allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
+};
+
+struct Context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  double* splitk = nullptr;
+  size_t splitk_cap = 0;  // doubles
+  int* flags = nullptr;   // device status words (see engine.cu)
+  Comm* comm = nullptr;
+  int64_t gemm_launches = 0;  // statistics for bench.py
+  int64_t kernel_launches = 0;
+
+  double* splitk_buffer(size_t n);
+  int world() const { return comm ? comm->world : 1; }
+  cudaError_t allreduce(double* buf, size_t n) {
+    if (!comm || comm->world == 1 || n == 0) return cudaSuccess;
+    return comm->allreduce_sum(buf, n, stream);
+  }
+};
+
+cudaError_t gemm(Context& ctx, Layout layout, const GemmArgs& args, int max_splits,
+                 cudaStream_t st);
+
+// Status codes mirror include/wssr.h.
+struct Error {
+  int code;
+  std::string msg;
+};
+
+}  // namespace wssr

@@ -1,0 +1,171 @@
+"""Batch estimators on the device: drop-in for vmcsr.estimators (estimators.py:1-110).
+
+``assemble`` runs two kernels - a one-CTA energy-statistics/clipping kernel and ONE pass over
+the raw log-derivative matrix that yields the column means, the centred second moments
+(||o_matrix||_F^2) and the gradient - instead of the reference's centre/scale/transpose copies
+(estimators.py:90-97).  The returned bundle keeps the raw sample-major matrix plus its column
+means and scale; ``o_matrix`` is materialised only if a caller asks for it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _arrays, _lib
+from .errors import DegenerateBatch
+
+
+@dataclass(frozen=True)
+class SampleBatch:
+    """Decorrelated draws with their local energies and log-derivatives (estimators.py:16-31)."""
+
+    configs: tuple
+    local_energies: object   # (batch,)
+    theta_logderivs: object  # (batch, n_params), sample-major
+
+    def __post_init__(self):
+        n = len(self.configs)
+        e_shape = tuple(self.local_energies.shape)
+        d_shape = tuple(self.theta_logderivs.shape)
+        if e_shape != (n,) or d_shape[0] != n:
+            raise ValueError("batch fields disagree on the sample count")
+
+    @property
+    def size(self):
+        return len(self.configs)
+
+
+class EstimatorBundle:
+    """Everything one optimizer step consumes (estimators.py:34-50).
+
+    Constructed either by ``assemble`` (then it holds the raw sample-major derivative block,
+    its column means ``mu`` and ``scale`` = 1/sqrt(N), and ``o_matrix`` is the lazy view
+    ((derivs - mu) * scale).T) or directly with an explicit (n_params, batch) ``o_matrix`` as in
+    the reference's test helpers (test_optimizers.py:27-34).
+    """
+
+    __slots__ = ("loss", "raw_loss", "l_vector", "gradient", "_samples", "_mu", "_scale",
+                 "_fro2", "_gradient_exact", "_o_cache", "_n_global")
+
+    def __init__(self, loss, raw_loss, o_matrix, l_vector, gradient):
+        o = _arrays.to_tensor(o_matrix)
+        if o.dim() == 1:
+            o = o[:, None]
+        samples = o.t()
+        if not (samples.stride(1) == 1 and samples.stride(0) >= samples.shape[1]):
+            samples = samples.contiguous()
+        self._init(float(loss), float(raw_loss), samples, None, 1.0, -1.0,
+                   _arrays.to_tensor(l_vector), _arrays.to_tensor(gradient), False,
+                   samples.shape[0])
+
+    @classmethod
+    def _assembled(cls, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, n_global):
+        self = cls.__new__(cls)
+        self._init(loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, True, n_global)
+        return self
+
+    def _init(self, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, exact,
+              n_global):
+        set_ = object.__setattr__
+        set_(self, "loss", loss)
+        set_(self, "raw_loss", raw_loss)
+        set_(self, "l_vector", l_vector)
+        set_(self, "gradient", gradient)
+        set_(self, "_samples", samples)
+        set_(self, "_mu", mu)
+        set_(self, "_scale", scale)
+        set_(self, "_fro2", fro2)
+        set_(self, "_gradient_exact", exact)
+        set_(self, "_o_cache", None)
+        set_(self, "_n_global", n_global)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("EstimatorBundle is immutable")
+
+    @property
+    def o_matrix(self) -> torch.Tensor:
+        """(n_params, batch) centred and scaled matrix (materialised on first access)."""
+        if self._o_cache is None:
+            if self._mu is None and self._scale == 1.0:
+                o = self._samples.t()
+            else:
+                o = ((self._samples - self._mu[None, :]) * self._scale).t()
+            object.__setattr__(self, "_o_cache", o)
+        return self._o_cache
+
+    @property
+    def n_params(self):
+        return int(self._samples.shape[1])
+
+    @property
+    def batch_size(self):
+        return int(self._samples.shape[0])
+
+
+def clip_local_energies(energies, n_std=5.0):
+    """Clamp outliers to mean +- n_std * population std (estimators.py:53-71), on the device."""
+    e = _arrays.to_tensor(energies).reshape(-1).contiguous()
+    if e.numel() < 2:
+        raise DegenerateBatch("clipping window needs at least two samples")
+    if not math.isfinite(n_std):
+        return e.clone()
+    if n_std < 0:
+        raise ValueError("clipping width must be nonnegative")
+    n = e.numel()
+    bundle = assemble(_Batch(e, torch.zeros(n, 1, dtype=torch.float64, device=e.device)),
+                      clip_n_std=n_std)
+    # l_raw = clip(E) - loss ;  clip(E) = l_vector * sqrt(N) + loss
+    return bundle.l_vector * math.sqrt(n) + bundle.loss
+
+
+class _Batch:
+    """Minimal batch duck type used internally."""
+
+    def __init__(self, energies, derivs):
+        self.local_energies = energies
+        self.theta_logderivs = derivs
+
+    @property
+    def size(self):
+        return int(self.local_energies.shape[0])
+
+
+def assemble(batch, clip_n_std=5.0):
+    """Build the centred estimator bundle from one sample batch (estimators.py:74-100).
+
+    Raises:
+      DegenerateBatch: fewer than two samples (nothing to center).
+    """
+    if batch.size < 2:
+        raise DegenerateBatch("need at least two samples to center the batch")
+    ctx = _lib.context()
+    derivs = _arrays.rows_view(_arrays.to_tensor(batch.theta_logderivs))
+    energies = _arrays.to_tensor(batch.local_energies).reshape(-1).contiguous()
+    n, p = derivs.shape
+    dev = derivs.device
+    mu = torch.empty(p, dtype=torch.float64, device=dev)
+    lvec = torch.empty(n, dtype=torch.float64, device=dev)
+    grad = torch.empty(p, dtype=torch.float64, device=dev)
+    out = _lib.AssembleOut(mu=mu.data_ptr(), l_vector=lvec.data_ptr(), gradient=grad.data_ptr())
+    ctx.call("wssr_assemble_f64", _lib.ptr(derivs), n, p, _arrays.ld(derivs),
+             _lib.ptr(energies), float(clip_n_std), ctypes.byref(out))
+    scale = 1.0 / np.sqrt(out.n_global)
+    return EstimatorBundle._assembled(out.loss, out.raw_loss, derivs, mu, scale, out.fro2, lvec,
+                                      grad, int(out.n_global))
+
+
+def s_matrix(bundle):
+    """Parameter-space covariance O @ O^T (estimators.py:103-105); small-P diagnostics only."""
+    o = bundle.o_matrix
+    return o @ o.t()
+
+
+def t_matrix(bundle):
+    """Sample-space companion O^T @ O (estimators.py:108-110); small-N diagnostics only."""
+    o = bundle.o_matrix
+    return o.t() @ o

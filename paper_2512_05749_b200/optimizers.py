@@ -1,0 +1,221 @@
+"""Warm-started low-rank preconditioned update on the device: drop-in for the WSSR part of
+vmcsr.optimizers (optimizers.py:188-401).
+
+``wssr_step`` keeps the reference signature and returns (theta', state', WssrDiagnostics); the
+whole step after the host-side warm-start preparation is ONE call into libwssr
+(wssr_step_f64): SSI factorisation, rank cut/growth, gbar, the fused preconditioner apply,
+drift telemetry and the state refresh.  State arrays are float64 CUDA tensors; ``obar`` is kept
+parameter-contiguous (a (P, r) view of an (r, P) buffer) because the next step streams it as
+the history block of Ohat.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _arrays, _lib
+from .errors import Unsupported
+from .linalg import qr_orthonormalize
+from .svdengine import SsiReport
+
+DEFAULT_LEARNING_RATE = 0.015      # optimizers.py:28
+DEFAULT_RATE_DECAY = 1000.0
+DEFAULT_TIKHONOV_EPS = 1e-3
+DEFAULT_MOMENTUM = 0.99
+DEFAULT_AVERAGING_WEIGHT = 0.95    # optimizers.py:32
+DEFAULT_SIGMA_FLOOR = 1e-3
+DEFAULT_RANK_CUTOFF = 1e-6
+DEFAULT_RANK_GROWTH = 0.1
+DEFAULT_RANK_INIT = 400
+DEFAULT_SSI_MAX_ITERS = 3          # optimizers.py:37
+SVD_BACKENDS = ("ssi", "randomized", "exact")
+
+
+def _shape(x):
+    return tuple(x.shape)
+
+
+@dataclass(frozen=True)
+class WssrState:
+    """Carry-over for the warm-started low-rank scheme (optimizers.py:188-247)."""
+
+    obar: object
+    lbar: object
+    u_prev: object
+    r_max: int
+    delta: float = DEFAULT_AVERAGING_WEIGHT
+    sigma_floor: float = DEFAULT_SIGMA_FLOOR
+    sigma_floor_relative: bool = False
+    r_reg: float = DEFAULT_RANK_CUTOFF
+    eps_grow: float = DEFAULT_RANK_GROWTH
+    step: int = 0
+
+    def __post_init__(self):
+        if len(_shape(self.obar)) != 2 or len(_shape(self.u_prev)) != 2 or len(_shape(self.lbar)) != 1:
+            raise ValueError("malformed history shapes")
+        if _shape(self.obar)[1] != _shape(self.lbar)[0]:
+            raise ValueError("history rank mismatch between obar and lbar")
+        if self.r_max < 1:
+            raise ValueError("r_max must be at least 1")
+        if not 0.0 <= self.delta < 1.0:
+            raise ValueError("averaging weight must lie in [0, 1)")
+        if self.sigma_floor <= 0.0:
+            raise ValueError("sigma_floor must be positive")
+        if not 0.0 < self.r_reg < 1.0:
+            raise ValueError("rank cutoff must lie in (0, 1)")
+        if self.eps_grow < 0.0:
+            raise ValueError("rank growth factor must be nonnegative")
+
+    @property
+    def history_rank(self):
+        return _shape(self.obar)[1]
+
+    @classmethod
+    def initial(cls, n_params, rank_init=DEFAULT_RANK_INIT, delta=DEFAULT_AVERAGING_WEIGHT,
+                sigma_floor=DEFAULT_SIGMA_FLOOR, sigma_floor_relative=False,
+                r_reg=DEFAULT_RANK_CUTOFF, eps_grow=DEFAULT_RANK_GROWTH):
+        dev = _arrays.default_device()
+        z = torch.zeros(0, n_params, dtype=torch.float64, device=dev)
+        return cls(obar=z.t(), lbar=torch.zeros(0, dtype=torch.float64, device=dev),
+                   u_prev=torch.zeros(n_params, 0, dtype=torch.float64, device=dev),
+                   r_max=int(rank_init), delta=delta, sigma_floor=sigma_floor,
+                   sigma_floor_relative=sigma_floor_relative, r_reg=r_reg, eps_grow=eps_grow)
+
+
+@dataclass(frozen=True)
+class WssrDiagnostics:
+    """Per-step telemetry mirrored into the trace file (optimizers.py:250-258)."""
+
+    ssi: SsiReport
+    effective_rank: int
+    r_max: int
+    sigma_drift: float
+    projector_drift: float
+
+
+def _per_step_seed(rng_seed, step):
+    """optimizers.py:273-274."""
+    return int(np.random.SeedSequence((int(rng_seed), int(step))).generate_state(1)[0])
+
+
+def _prepare_warm_start(u_prev, requested, n_rows, seed):
+    """Previous left vectors widened (or cut) to the requested block size (optimizers.py:277-289).
+
+    The widening draws its Gaussian columns on the host with the reference's PCG64 stream so the
+    warm start is bit-identical; the QR runs on the device.
+    """
+    u_prev = _arrays.to_tensor(u_prev)
+    if u_prev.shape[1] >= requested:
+        return u_prev[:, :requested]
+    extra = np.random.default_rng(seed).standard_normal((n_rows, requested - u_prev.shape[1]))
+    block = torch.cat([u_prev, _arrays.to_tensor(extra)], dim=1)
+    q, _ = qr_orthonormalize(block)
+    return q
+
+
+def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
+              ssi_max_iters=DEFAULT_SSI_MAX_ITERS, ssi_residual_tol=1e-10, rng_seed=0,
+              *, report_final_residual=True, return_update=False):
+    """One step of the warm-started low-rank preconditioned descent (optimizers.py:292-391).
+
+        theta' = theta - eta * (U sigma^-2 U^T + floor^-1 (I - U U^T)) gbar
+
+    Returns:
+      (theta', state', WssrDiagnostics)  [+ the update vector when return_update=True]
+    """
+    if svd_backend not in SVD_BACKENDS:
+        raise ValueError(f"svd_backend must be one of {SVD_BACKENDS}, got {svd_backend!r}")
+    if state.step == 0 or svd_backend == "exact":
+        raise Unsupported("the dense first-step / 'exact' factorisation (optimizers.py:327-330) "
+                          "is not on the device path yet; start from step >= 1 with u_prev")
+    if svd_backend == "randomized":
+        raise Unsupported("svd_backend='randomized' (rssr_step) is not on the device path yet")
+    ctx = _lib.context()
+    theta = _arrays.to_tensor(theta).reshape(-1).contiguous()
+    samples = bundle._samples
+    m = bundle.n_params
+    n = bundle.batch_size
+    obar = _arrays.to_tensor(state.obar)
+    r = obar.shape[1]
+    hist = obar.t()
+    if r > 0 and not (hist.stride(1) == 1 and hist.stride(0) >= m):
+        hist = hist.contiguous()
+    lbar = _arrays.to_tensor(state.lbar).contiguous()
+    requested = min(state.r_max, m, r + n)
+    u_init = _prepare_warm_start(state.u_prev, requested, m,
+                                 _per_step_seed(rng_seed, state.step))
+    u_init = _arrays.rows_view(u_init)
+    u_prev = _arrays.to_tensor(state.u_prev)
+    if u_prev.shape[1] > 0:
+        u_prev = _arrays.rows_view(u_prev)
+    dev = theta.device
+    k = requested
+    theta_next = torch.empty(m, dtype=torch.float64, device=dev)
+    update = torch.empty(m, dtype=torch.float64, device=dev) if return_update else None
+    u_next = torch.empty(m, k, dtype=torch.float64, device=dev)
+    obar_t = torch.empty(k, m, dtype=torch.float64, device=dev)
+    lbar_next = torch.empty(k, dtype=torch.float64, device=dev)
+    sigma = torch.empty(k, dtype=torch.float64, device=dev)
+
+    from .svdengine import _ohat_struct
+    o = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2, hist, 1.0)
+    lvec = bundle.l_vector.contiguous()
+    grad = bundle.gradient if bundle._gradient_exact else None
+    sin = _lib.StepIn(
+        ohat=ctypes.pointer(o), lbar=lbar.data_ptr() if r > 0 else None,
+        l_vector=lvec.data_ptr(), gradient=grad.data_ptr() if grad is not None else None,
+        theta=theta.data_ptr(), eta=float(eta),
+        u_init=u_init.data_ptr(), ld_init=_arrays.ld(u_init), requested=k,
+        u_prev=u_prev.data_ptr() if u_prev.shape[1] > 0 else None,
+        ld_prev=_arrays.ld(u_prev) if u_prev.shape[1] > 0 else 1, r_prev=int(u_prev.shape[1]),
+        delta=float(state.delta), sigma_floor=float(state.sigma_floor), r_reg=float(state.r_reg),
+        eps_grow=float(state.eps_grow), sigma_floor_relative=int(bool(state.sigma_floor_relative)),
+        r_max=int(state.r_max), max_iters=int(ssi_max_iters),
+        residual_tol=float(ssi_residual_tol),
+        flags=_lib.WSSR_FLAG_FINAL_RESIDUAL if report_final_residual else 0,
+    )
+    sout = _lib.StepOut(
+        theta_next=theta_next.data_ptr(), update=update.data_ptr() if update is not None else None,
+        u_next=u_next.data_ptr(), ld_u=k, obar_next_t=obar_t.data_ptr(), ld_obar=m,
+        lbar_next=lbar_next.data_ptr(), sigma=sigma.data_ptr(),
+    )
+    ctx.call("wssr_step_f64", ctypes.byref(sin), ctypes.byref(sout))
+    r_eff = int(sout.r_eff)
+    state_next = replace(
+        state,
+        obar=obar_t[:r_eff].t(),
+        lbar=lbar_next[:r_eff],
+        u_prev=u_next[:, :r_eff],
+        r_max=int(sout.next_r_max),
+        step=state.step + 1,
+    )
+    report = SsiReport(iterations_used=int(sout.iterations),
+                       subspace_residual=float(sout.residual), warm_started=True)
+    diag = WssrDiagnostics(ssi=report, effective_rank=r_eff, r_max=int(state.r_max),
+                           sigma_drift=float(sout.sigma_drift),
+                           projector_drift=float(sout.projector_drift))
+    if return_update:
+        return theta_next, state_next, diag, update
+    return theta_next, state_next, diag
+
+
+def rssr_step(theta, bundle, eta, state, ssi_max_iters=DEFAULT_SSI_MAX_ITERS, rng_seed=0):
+    """optimizers.py:394-401: randomized-sketch variant (SURVEY 8(f) 'next')."""
+    return wssr_step(theta, bundle, eta, state, svd_backend="randomized",
+                     ssi_max_iters=ssi_max_iters, rng_seed=rng_seed)
+
+
+def sigma_of(state) -> torch.Tensor:
+    """Singular values carried by a state: column norms of obar (optimizers.py:370)."""
+    return torch.linalg.vector_norm(_arrays.to_tensor(state.obar), dim=0)
+
+
+__all__ = [
+    "WssrState", "WssrDiagnostics", "wssr_step", "rssr_step", "_prepare_warm_start",
+    "_per_step_seed", "SVD_BACKENDS", "sigma_of", "math",
+]

@@ -1,0 +1,189 @@
+"""Truncated-SVD engine on the device: drop-in for vmcsr.svdengine (svdengine.py:1-226).
+
+``ssi_svd`` is the warm-startable block subspace iteration of svdengine.py:88-158 with every
+O-pass on FP64 tensor cores and every QR by CholeskyQR2; sigma is |diag R| of the QR of the
+final v block, sorted with a stable argsort, exactly as the reference defines it
+(svdengine.py:144-152).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _arrays, _lib
+from .errors import DegenerateInput, RankTooLarge, Unsupported
+
+DEFAULT_RESIDUAL_EXIT = 1e-10   # svdengine.py:16
+_COLD_START_SEED = 0x5EED       # svdengine.py:17
+
+
+@dataclass(frozen=True)
+class TruncatedSvd:
+    """Rank-r factors: a ~= u @ diag(sigma) @ v (svdengine.py:20-44)."""
+
+    u: object      # (m, r)
+    sigma: object  # (r,)
+    v: object      # (r, n)
+
+    def __post_init__(self):
+        r = self.sigma.shape[0]
+        if self.u.dim() != 2 if isinstance(self.u, torch.Tensor) else np.ndim(self.u) != 2:
+            raise ValueError("malformed factor shapes")
+        if tuple(self.u.shape)[1] != r or tuple(self.v.shape)[0] != r or len(self.sigma.shape) != 1:
+            raise ValueError(
+                f"inconsistent ranks: u {tuple(self.u.shape)}, sigma {r}, v {tuple(self.v.shape)}"
+            )
+        if r:
+            s = _arrays.host(self.sigma)
+            if np.any(s <= 0.0) or np.any(np.diff(s) > 0.0):
+                raise ValueError("sigma must be strictly positive and nonincreasing")
+
+    @property
+    def rank(self):
+        return self.sigma.shape[0]
+
+    def reconstruct(self):
+        return (self.u * self.sigma) @ self.v
+
+
+@dataclass(frozen=True)
+class SsiReport:
+    """Telemetry from one factorization call (svdengine.py:47-53)."""
+
+    iterations_used: int
+    subspace_residual: float
+    warm_started: bool
+
+
+def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0.0):
+    """wssr_ohat_f64 for Ohat^T = [hist_scale*hist ; scale*(samples - mu)] (sample-major)."""
+    p = int(samples.shape[1])
+    o = _lib.OhatF64()
+    o.n_params = p
+    if hist is not None and hist.shape[0] > 0:
+        o.hist = hist.data_ptr()
+        o.hist_rank = int(hist.shape[0])
+        o.hist_ld = _arrays.ld(hist)
+        o.hist_scale = float(hist_scale)
+    else:
+        o.hist, o.hist_rank, o.hist_ld, o.hist_scale = None, 0, p, 0.0
+    o.samples = samples.data_ptr() if samples.shape[0] > 0 else None
+    o.n_samples = int(samples.shape[0])
+    o.samples_ld = _arrays.ld(samples) if samples.shape[0] > 0 else p
+    o.mu = mu.data_ptr() if mu is not None else None
+    o.samples_scale = float(scale)
+    o.samples_fro2 = float(fro2)
+    return o
+
+
+def _sample_major(ohat):
+    """(m, n) parameter-major matrix -> its (n, m) sample-major row view (no copy if possible)."""
+    t = _arrays.to_tensor(ohat)
+    if t.dim() != 2:
+        raise ValueError("ohat must be a matrix")
+    return _arrays.rows_view(t.t())
+
+
+def subspace_residual(ohat, u_orthonormal):
+    """||G U - U (U^T G U)||_F / ||ohat||_F^2 with G = ohat ohat^T (svdengine.py:56-67)."""
+    ctx = _lib.context()
+    s = _sample_major(ohat)                       # n x m
+    u = _arrays.rows_view(_arrays.to_tensor(u_orthonormal))
+    m, k = u.shape
+    n = s.shape[0]
+    fro2 = float(torch.linalg.vector_norm(s)) ** 2 if s.numel() else 0.0
+    if fro2 == 0.0:
+        raise DegenerateInput("residual undefined for a zero matrix")
+    dev = u.device
+    y = torch.empty(n, k, dtype=torch.float64, device=dev)
+    w = torch.empty(m, k, dtype=torch.float64, device=dev)
+    quo = torch.empty(k, k, dtype=torch.float64, device=dev)
+    # y = ohat^T u (RM), w = ohat y (CM), quo = u^T w (CM), w -= u quo (RM)
+    ctx.call("wssr_gemm_f64", 1, n, k, m, _lib.ptr(s), _arrays.ld(s), None, _lib.ptr(u),
+             _arrays.ld(u), _lib.ptr(y), k, 1.0, 0, 1024)
+    ctx.call("wssr_gemm_f64", 0, m, k, n, _lib.ptr(s), _arrays.ld(s), None, _lib.ptr(y), k,
+             _lib.ptr(w), k, 1.0, 0, 1024)
+    ctx.call("wssr_gemm_f64", 0, k, k, m, _lib.ptr(u), _arrays.ld(u), None, _lib.ptr(w), k,
+             _lib.ptr(quo), k, 1.0, 0, 1024)
+    ctx.call("wssr_gemm_f64", 1, m, k, k, _lib.ptr(u), _arrays.ld(u), None, _lib.ptr(quo), k,
+             _lib.ptr(w), k, -1.0, 1, 1024)
+    return float(torch.linalg.vector_norm(w)) / fro2
+
+
+def exact_truncated_svd(ohat, rank):
+    """Dense truncated SVD (svdengine.py:75-85): SURVEY 8(f) 'next' row, not on the device yet."""
+    raise Unsupported("exact_truncated_svd (step 0 / svd_backend='exact') is not implemented on "
+                      "the device path yet; seed the state with u_prev and step >= 1")
+
+
+def randomized_svd(ohat, rank, oversample=10, rng_seed=0):
+    """Gaussian range sketch (svdengine.py:161-196): SURVEY 8(f) 'next' row."""
+    raise Unsupported("randomized_svd is not implemented on the device path yet")
+
+
+def ssi_svd(ohat, rank, max_iters=3, u_init=None, residual_tol=DEFAULT_RESIDUAL_EXIT,
+            *, report_final_residual=True):
+    """Dominant singular triplets by warm-startable block subspace iteration
+    (svdengine.py:88-158).
+
+    ``ohat`` is the (m, n) parameter-major matrix of the reference.  Passing the transpose view of
+    a sample-major (n, m) tensor avoids any copy.  ``report_final_residual=False`` skips the
+    look-ahead after the last iteration, whose only output is SsiReport.subspace_residual
+    (returned as NaN then).
+    """
+    s = _sample_major(ohat)
+    n, m = s.shape
+    if rank < 1 or rank > min(m, n):
+        raise RankTooLarge(f"rank {rank} outside [1, {min(m, n)}] for shape {(m, n)}")
+    warm = u_init is not None
+    if warm:
+        block = _arrays.to_tensor(u_init)
+        if tuple(block.shape) != (m, rank):
+            raise ValueError(f"u_init must have shape {(m, rank)}, got {tuple(block.shape)}")
+    else:
+        block = _arrays.to_tensor(
+            np.random.default_rng(_COLD_START_SEED).standard_normal((m, rank)))
+    block = _arrays.rows_view(block)
+    dev = block.device
+    u = torch.empty(m, rank, dtype=torch.float64, device=dev)
+    sig = torch.empty(rank, dtype=torch.float64, device=dev)
+    v = torch.empty(n, rank, dtype=torch.float64, device=dev)
+    o = _ohat_struct(s)
+    out = _lib.SsiOut(u=u.data_ptr(), ld_u=rank, sigma=sig.data_ptr(), v=v.data_ptr(), ld_v=rank)
+    flags = _lib.WSSR_FLAG_FINAL_RESIDUAL if report_final_residual else 0
+    _lib.context().call("wssr_ssi_svd_f64", ctypes.byref(o), int(rank), int(max_iters),
+                        _lib.ptr(block), _arrays.ld(block), float(residual_tol), flags,
+                        ctypes.byref(out))
+    k = int(out.k_pos)
+    factors = TruncatedSvd(u=u[:, :k], sigma=sig[:k], v=v[:, :k].t())
+    report = SsiReport(iterations_used=int(out.iterations),
+                       subspace_residual=float(out.residual), warm_started=warm)
+    return factors, report
+
+
+def subspace_drift(prev, curr):
+    """Change in singular values and in the left-subspace projector (svdengine.py:199-226)."""
+    r = min(prev.rank, curr.rank)
+    if tuple(prev.u.shape)[0] != tuple(curr.u.shape)[0]:
+        raise ValueError("factor sets live in different row spaces")
+    if r == 0:
+        return 0.0, 0.0
+    u1 = _arrays.rows_view(_arrays.to_tensor(prev.u))
+    u2 = _arrays.rows_view(_arrays.to_tensor(curr.u))
+    s1 = _arrays.to_tensor(prev.sigma).contiguous()
+    s2 = _arrays.to_tensor(curr.sigma).contiguous()
+    sd, pd = ctypes.c_double(), ctypes.c_double()
+    _lib.context().call("wssr_subspace_drift_f64", int(u1.shape[0]), _lib.ptr(u1),
+                        _arrays.ld(u1), _lib.ptr(s1), int(prev.rank), _lib.ptr(u2),
+                        _arrays.ld(u2), _lib.ptr(s2), int(curr.rank), ctypes.byref(sd),
+                        ctypes.byref(pd))
+    return float(sd.value), float(pd.value)
+
+
+def _is_nan(x):
+    return isinstance(x, float) and math.isnan(x)

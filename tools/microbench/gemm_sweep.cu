@@ -1,0 +1,77 @@
+// Tile-config sweep for the DMMA GEMM family on the WSSR phase shapes (dev tool).
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+#include <algorithm>
+#include "../../paper_2512_05749_b200/csrc/gemm.cuh"
+
+using namespace wssr;
+
+static double* dalloc(size_t n) { double* p; cudaMalloc(&p, n * 8); return p; }
+__global__ void fill(double* p, size_t n, double s) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = sin(s * (double)(i % 1000003) + 0.1);
+}
+
+template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST>
+void run(const char* tag, int64_t M, int64_t N, int64_t K, double* A, double* B, double* sh, double* C, double* part) {
+  using Cfg = GemmCfg<L, BM, BN, BK, WMW, WNW, ST>;
+  auto kern = gemm_dmma_kernel<L, BM, BN, BK, WMW, WNW, ST, 2, 2>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes) != cudaSuccess) {
+    printf("%s: smem too large\n", tag); cudaGetLastError(); return;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes);
+  int cap = 148 * std::max(occ, 1);
+  int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  double best_ms = 1e30; int best_s = 1;
+  std::vector<int> cands;
+  for (int s = 1; s <= 64; ++s) {
+    double w = (double)(tiles * s) / cap; double eff = w / std::ceil(w);
+    if (eff > 0.9 || s == 1) cands.push_back(s);
+    if (cands.size() > 6) break;
+  }
+  for (int s : cands) {
+    int64_t kc = (K + s - 1) / s; kc = (kc + BK - 1) / BK * BK; int ss = (int)((K + kc - 1) / kc);
+    GemmArgs a{A, L == Layout::CM ? M : K, B, N, sh, C, N, M, N, K, kc, 1.0, 0, ss > 1 ? part : nullptr};
+    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)ss);
+    for (int w = 0; w < 2; ++w) kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(a);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(a);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+    if (cudaGetLastError() != cudaSuccess) { printf("%s: launch error\n", tag); return; }
+    if (ms < best_ms) { best_ms = ms; best_s = ss; }
+  }
+  printf("%-34s M=%-7lld N=%-4lld K=%-7lld occ=%d smem=%6zu  best_s=%-3d %.3f ms  %.2f TF/s\n", tag,
+         (long long)M, (long long)N, (long long)K, occ, Cfg::kSmemBytes, best_s, best_ms,
+         2.0 * M * N * K / best_ms / 1e9);
+}
+
+#define RUNRM(BM, BN, BK, WM, WN, ST) run<Layout::RM, BM, BN, BK, WM, WN, ST>("RM<" #BM "," #BN "," #BK "," #WM "x" #WN ",s" #ST ">", M, N, K, A, B, sh, C, part)
+#define RUNCM(BM, BN, BK, WM, WN, ST) run<Layout::CM, BM, BN, BK, WM, WN, ST>("CM<" #BM "," #BN "," #BK "," #WM "x" #WN ",s" #ST ">", M, N, K, A, B, sh, C, part)
+
+int main() {
+  const size_t big = (size_t)16384 * 65536;
+  double* A = dalloc(big); double* B = dalloc(1 << 24); double* sh0 = dalloc(1 << 22); double* C = dalloc(1 << 24);
+  double* part = dalloc((size_t)1 << 27);
+  fill<<<1024, 256>>>(A, big, 1.1); fill<<<1024, 256>>>(B, 1 << 24, 0.7); fill<<<1024, 256>>>(sh0, 1 << 22, 0.3);
+  cudaDeviceSynchronize();
+  for (int ns = 0; ns < 2; ++ns) {
+    double* shp = ns ? nullptr : sh0;
+    printf("shift=%s\n", ns ? "none" : "mu");
+    { int64_t M = 4096, N = 64, K = 131072; double* sh = shp;
+      RUNRM(128, 64, 8, 4, 2, 4); RUNRM(128, 64, 16, 2, 2, 3); RUNRM(128, 64, 16, 4, 2, 2); }
+    { int64_t M = 131072, N = 64, K = 4096; double* sh = shp;
+      RUNCM(128, 64, 16, 4, 2, 4); RUNCM(64, 64, 16, 2, 2, 4); }
+    { int64_t M = 65536, N = 128, K = 16384; double* sh = shp;
+      RUNCM(64, 128, 16, 2, 4, 4); }
+    { int64_t M = 16384, N = 128, K = 65536; double* sh = shp;
+      RUNRM(128, 128, 16, 4, 4, 3); RUNRM(128, 128, 8, 4, 4, 4); RUNRM(64, 128, 8, 2, 4, 4);}
+  }
+  printf("done %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
