@@ -1,0 +1,386 @@
+"""WSSR-step benchmark (BASELINE.json metric: WSSR steps/sec at N x P x k, FP64, and % of the
+FP64-tensor / HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl reference]
+
+One JSON line on rank 0.  Workload at N=1: BASELINE configs[1] ("c1": N=4096 samples,
+P=131072 params, k=64, float64, lambda=1e-4, seeded synthetic data of SURVEY.md 8(d), generated
+on the device).  A "step" is estimators.assemble + optimizers.wssr_step (svd_backend="ssi",
+ssi_max_iters=3, ssi_residual_tol=1e-10) on one drifted batch; the drift O_t = O_{t-1} +
+1e-3 G_t is applied between steps outside the timed intervals.  Inputs (4.3 GB)
+are larger than L2 (126 MB), so no L2 flush is needed.  Multi-GPU: rows of O are sharded over
+ranks (torchrun, NCCL); the total work is fixed ("strong" scaling) and the time is the max over
+ranks.
+
+--impl reference times the reference algorithm's CPU implementation (the numpy/LAPACK port in
+oracle/, the reference package itself does not travel to the GPU box) on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+METRIC = "WSSR steps/sec at NxPxk (FP64)"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fast-report", action="store_true",
+                    help="skip the telemetry-only final look-ahead (SsiReport.subspace_residual)")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, f[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline_run(cfg, index, steps, budget_s=None):
+    """The reference algorithm on the host (oracle port, numpy/LAPACK on all host cores)."""
+    import numpy as np
+
+    from oracle import wssr_oracle as orc
+    from paper_2512_05749_b200 import synthetic
+
+    # LAPACK/BLAS initialisation outside the timed region (first call costs ~1 s)
+    small = synthetic.HostWorkload.from_config(synthetic.config("c0", N=64, P=256, k=8, L=8), 0)
+    o, e = small.next()
+    b = orc.assemble(o, e)
+    st = orc.baseline_state(256, 8, small.v0_raw(), 0.0, 1e-3)
+    orc.wssr_step(np.zeros(256), b["o_matrix"], b["l_vector"], 1.0, st)
+
+    wl = synthetic.HostWorkload.from_config(cfg, index)
+    st = orc.baseline_state(cfg["P"], cfg["k"], wl.v0_raw(), cfg["delta"], cfg["lam"])
+    times = []
+    for t in range(steps):
+        o, e = wl.next()
+        t0 = time.perf_counter()
+        b = orc.assemble(o, e)
+        _, st, info = orc.wssr_step(np.zeros(cfg["P"]), b["o_matrix"], b["l_vector"], 1.0, st)
+        times.append(time.perf_counter() - t0)
+        if budget_s is not None and sum(times) + times[-1] > budget_s:
+            break
+    return times
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from paper_2512_05749_b200 import synthetic
+
+    cfg = synthetic.config(args.config)
+    idx = int(args.config[1:]) if args.config[1:].isdigit() else 1
+    times = cpu_baseline_run(cfg, idx, max(1, args.steps), budget_s=150.0)
+    total = sum(times)
+    value = len(times) / total
+    cores = host_cores()
+    sample = (f"{len(times)} full {args.config} step(s) (N={cfg['N']}, P={cfg['P']}, k={cfg['k']}), "
+              f"host numpy/OpenBLAS, first steps of the seeded synthetic workload; timed steps "
+              f"capped by a 150 s budget")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
+        "n_gpus": args.gpus, "steps": len(times), "requested_steps": args.steps,
+        "warmup": 1, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generator, SURVEY.md 8(d))",
+        "config": workload_config(cfg, args),
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args):
+    return {
+        "workload": f"{cfg['name']}: BASELINE configs[{cfg['name'][1:]}] N={cfg['N']} samples, "
+                    f"P={cfg['P']} params, k={cfg['k']}, {cfg['dtype']}",
+        "N": cfg["N"], "P": cfg["P"], "k": cfg["k"], "lambda": cfg["lam"],
+        "delta": cfg["delta"], "latent_rank": cfg["L"], "alpha": cfg["alpha"],
+        "drift": cfg["drift"], "ssi_max_iters": 3, "ssi_residual_tol": 1e-10,
+        "report_final_residual": not args.fast_report,
+        "parallelism": f"rows x{args.gpus}",
+        "l2": "inputs larger than L2 (O = %.2f GB vs 126 MB); no flush" % (
+            cfg["N"] * cfg["P"] * 8 / 1e9),
+    }
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_05749_b200 import _lib, distributed, estimators, linalg, optimizers, synthetic
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synthetic.config(args.config)
+    N, P, k = cfg["N"], cfg["P"], cfg["k"]
+    row0, rows = distributed.row_shard(N, rank, world)
+    ctx = _lib.context(local_rank)
+    if world > 1:
+        distributed.attach_nccl(ctx)
+    wl = synthetic.DeviceWorkload(N, P, k, cfg["L"], cfg["alpha"], cfg["drift"], seed=101,
+                                  row0=row0, rows=rows, device=dev)
+    v0 = linalg.qr_orthonormalize(wl.v0_raw())[0]
+    state = optimizers.WssrState(obar=torch.zeros(0, P, dtype=torch.float64, device=dev).t(),
+                                 lbar=torch.zeros(0, dtype=torch.float64, device=dev),
+                                 u_prev=v0, r_max=k, delta=cfg["delta"], sigma_floor=cfg["lam"],
+                                 eps_grow=0.0, step=1)
+    theta = torch.zeros(P, dtype=torch.float64, device=dev)
+    final_res = not args.fast_report
+    configs_tuple = (None,) * rows
+
+    def step(O, E, st, th):
+        bundle = estimators.assemble(estimators.SampleBatch(configs_tuple, E, O))
+        return optimizers.wssr_step(th, bundle, 1.0, st, report_final_residual=final_res)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        O, E = wl.next()
+        theta, state, diag = step(O, E, state, theta)
+    torch.cuda.synchronize()
+    peak = ctx.dmma_peak_tflops()
+
+    stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local_rank)
+    ctx.set_timing(True)
+    launches0 = ctx.kernel_launches()
+    iters = []
+    intervals = []
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        O, E = wl.next()                       # drift: excluded from the timed intervals
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        theta, state, diag = step(O, E, state, theta)
+        b.record(stream)
+        intervals.append((a, b))
+        iters.append(diag.ssi.iterations_used)
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    launches = ctx.kernel_launches() - launches0
+    phases = [ctx.phase_stats(i) for i in range(3)]
+    ctx.set_timing(False)
+    step_ms = sum(x.elapsed_time(y) for x, y in intervals)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
+    ms_per_step = step_ms / args.steps
+    value = args.steps / (step_ms / 1e3)
+
+    # ---- roofline (dominant kernels: the two O-pass DMMA GEMMs) ---------------------------
+    g_ms = phases[0]["ms"] + phases[1]["ms"]
+    g_fl = phases[0]["flops"] + phases[1]["flops"]
+    g_n = phases[0]["launches"] + phases[1]["launches"]
+    achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    m_avg = sum(iters) / len(iters)
+    flops_alg = 2 * m_avg * 2.0 * N * P * k
+    bytes_alg = (1 + 2 * m_avg) * N * P * 8.0
+    traffic = None
+    if os.path.exists(NCU_SUMMARY):
+        try:
+            with open(NCU_SUMMARY) as f:
+                traffic = json.load(f).get("gemm_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    hbm_peak = None
+    try:
+        with open(PEAKS_FILE) as f:
+            hbm_peak = json.load(f).get("hbm_gbs")
+    except Exception:
+        hbm_peak = 6449.4
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak if peak else None, "traffic": traffic,
+        "kernel": "gemm_dmma_kernel (O-passes v=Ohat^T q and u=Ohat v)",
+        "launches": g_n, "avg_launch_ms": g_ms / g_n if g_n else None,
+        "flops_per_launch": g_fl / g_n if g_n else None,
+        "peak_source": "measured live: DMMA.8x8x4 probe (wssr_dmma_peak_probe); "
+                       "MEASURED_PEAKS.json has no FP64 figure (datasheet ~37-40 TF/s)",
+        "per_phase": {
+            name: {"ms_avg": ph["ms"] / ph["launches"] if ph["launches"] else None,
+                   "tflops": ph["flops"] / (ph["ms"] * 1e-3) / 1e12 if ph["ms"] else None,
+                   "gbs": ph["bytes"] / (ph["ms"] * 1e-3) / 1e9 if ph["ms"] else None,
+                   "launches": ph["launches"]}
+            for name, ph in zip(["v=OhatT_q", "u=Ohat_v", "assemble_colstats"], phases)},
+        "step": {
+            "flops_alg": flops_alg, "bytes_alg": bytes_alg, "ssi_iterations": m_avg,
+            "t_roof_ms": max(flops_alg / (peak * 1e12 * world), bytes_alg / (hbm_peak * 1e9 * world)) * 1e3,
+            "frac": max(flops_alg / (peak * 1e12 * world), bytes_alg / (hbm_peak * 1e9 * world))
+            / (ms_per_step * 1e-3),
+            "hbm_peak_gbs": hbm_peak,
+        },
+    }
+
+    # ---- end to end through the public API with host buffers ------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, 5))
+        O_h = torch.empty(rows, P, dtype=torch.float64, pin_memory=True)
+        E_h = torch.empty(rows, dtype=torch.float64, pin_memory=True)
+        theta_h = torch.zeros(P, dtype=torch.float64, pin_memory=True)
+        out_h = torch.empty(P, dtype=torch.float64, pin_memory=True)
+        e2e_ms = 0.0
+        for _ in range(e2e_steps):
+            O, E = wl.next()
+            O_h.copy_(O)
+            E_h.copy_(E)
+            torch.cuda.synchronize()
+            barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            O_d = O_h.to(dev, non_blocking=True)
+            E_d = E_h.to(dev, non_blocking=True)
+            th_d = theta_h.to(dev, non_blocking=True)
+            th_next, state, diag = step(O_d, E_d, state, th_d)
+            out_h.copy_(th_next, non_blocking=False)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms += a.elapsed_time(b)
+            del O_d
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": e2e_steps / (float(t.item()) / 1e3), "unit": "steps/s",
+               "h2d_bytes_per_step": rows * P * 8 + rows * 8 + P * 8,
+               "d2h_bytes_per_step": P * 8, "steps": e2e_steps,
+               "path": "estimators.assemble + optimizers.wssr_step on tensors copied from pinned "
+                       "host memory each step; theta' read back to the host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        idx = int(args.config[1:]) if args.config[1:].isdigit() else 1
+        times = cpu_baseline_run(cfg, idx, 1)
+        cpu = {"value": 1.0 / times[0], "unit": "steps/s", "cores": host_cores(), "kind": "port",
+               "sample": f"1 full {args.config} step (assemble + wssr_step) of the seeded host "
+                         f"workload, oracle/wssr_oracle.py on numpy/OpenBLAS"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded device generator, SURVEY.md 8(d) shapes/distributions)",
+            "config": workload_config(cfg, args),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+            "wall_s_timed_region": wall,
+            "ssi_iterations": iters,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

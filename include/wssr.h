@@ -87,6 +87,15 @@ int wssr_version(void);
 /* number of kernels this context launched so far (bench.py's gpu_launches) */
 int64_t wssr_kernel_launches(const wssr_ctx* ctx);
 
+/* bench instrumentation: per-phase CUDA-event timing of the O-passes.
+ * phase 0 = v = Ohat^T q (svdengine.py:133), 1 = u = Ohat v (svdengine.py:134),
+ * 2 = assemble's column-statistics pass (estimators.py:91,93).  Enabling resets the totals. */
+int wssr_set_timing(wssr_ctx* ctx, int enabled);
+int wssr_phase_stats(wssr_ctx* ctx, int phase, double* ms, int64_t* launches, double* flops,
+                     double* bytes);
+/* measured FP64 tensor-core (DMMA) peak of this device, TFLOP/s (roofline denominator) */
+int wssr_dmma_peak_probe(wssr_ctx* ctx, double* tflops);
+
 /* --- row sharding over NCCL (one process per GPU) ----------------------------------------- */
 /* 128-byte ncclUniqueId produced on rank 0 and broadcast by the caller (torch.distributed). */
 int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]);

@@ -80,6 +80,11 @@ SIGNATURES = {
     "wssr_last_error": (ctypes.c_char_p, [_vp]),
     "wssr_set_stream": (ctypes.c_int, [_vp, _vp]),
     "wssr_kernel_launches": (_i64, [_vp]),
+    "wssr_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_phase_stats": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_dbl),
+                                        ctypes.POINTER(_i64), ctypes.POINTER(_dbl),
+                                        ctypes.POINTER(_dbl)]),
+    "wssr_dmma_peak_probe": (ctypes.c_int, [_vp, ctypes.POINTER(_dbl)]),
     "wssr_nccl_unique_id": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "wssr_nccl_attach": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
     "wssr_assemble_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _dbl,
@@ -169,6 +174,20 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(self.lib.wssr_kernel_launches(self.handle))
+
+    def set_timing(self, enabled: bool) -> None:
+        self.lib.wssr_set_timing(self.handle, int(bool(enabled)))
+
+    def phase_stats(self, phase: int) -> dict:
+        ms, n, fl, by = _dbl(), _i64(), _dbl(), _dbl()
+        self.lib.wssr_phase_stats(self.handle, int(phase), ctypes.byref(ms), ctypes.byref(n),
+                                  ctypes.byref(fl), ctypes.byref(by))
+        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def dmma_peak_tflops(self) -> float:
+        out = _dbl()
+        self.call("wssr_dmma_peak_probe", ctypes.byref(out))
+        return float(out.value)
 
 
 _contexts: dict = {}

@@ -100,7 +100,11 @@ void post_launch(Context& ctx) {
   WSSR_CUDA(cudaGetLastError());
 }
 
-void sync(Context& ctx) { WSSR_CUDA(cudaStreamSynchronize(ctx.stream)); }
+void collect_timing(Context& ctx);
+void sync(Context& ctx) {
+  WSSR_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (!ctx.pending.empty()) collect_timing(ctx);
+}
 
 void d2h(Context& ctx, void* dst, const void* src, size_t bytes) {
   WSSR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
@@ -109,6 +113,51 @@ void d2h(Context& ctx, void* dst, const void* src, size_t bytes) {
 void allreduce(Context& ctx, double* buf, size_t n) {
   cudaError_t e = ctx.allreduce(buf, n);
   if (e != cudaSuccess) throw Fail{WSSR_ERR_NCCL, "allreduce failed"};
+}
+
+// ---- phase timing (bench.py roofline) ------------------------------------------------------
+cudaEvent_t take_event(Context& ctx) {
+  if (!ctx.event_pool.empty()) {
+    cudaEvent_t e = ctx.event_pool.back();
+    ctx.event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  WSSR_CUDA(cudaEventCreate(&e));
+  return e;
+}
+struct PhaseTimer {
+  Context& ctx;
+  int phase;
+  double flops, bytes;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(Context& c, int ph, double f, double b) : ctx(c), phase(ph), flops(f), bytes(b) {
+    if (ctx.timing) {
+      a = take_event(ctx);
+      WSSR_CUDA(cudaEventRecord(a, ctx.stream));
+    }
+  }
+  ~PhaseTimer() {
+    if (!a) return;
+    cudaEvent_t b = take_event(ctx);
+    cudaEventRecord(b, ctx.stream);
+    ctx.pending.push_back({phase, a, b, flops, bytes});
+  }
+};
+// fold finished event pairs into the per-phase totals (call after a stream sync)
+void collect_timing(Context& ctx) {
+  for (auto& pe : ctx.pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pe.a, pe.b) == cudaSuccess) {
+      ctx.phase_ms[pe.phase] += ms;
+      ctx.phase_flops[pe.phase] += pe.flops;
+      ctx.phase_bytes[pe.phase] += pe.bytes;
+      ctx.phase_count[pe.phase] += 1;
+    }
+    ctx.event_pool.push_back(pe.a);
+    ctx.event_pool.push_back(pe.b);
+  }
+  ctx.pending.clear();
 }
 
 // ---- GEMM wrappers ------------------------------------------------------------------------
@@ -330,14 +379,17 @@ void apply_OT(Context& ctx, const Ohat& o, const double* q, int64_t ldq, int64_t
       gemm_rm(ctx, o.r, k, o.P, o.hist, o.ldh, nullptr, q, ldq, v, ldv, o.sh, false);
     }
   }
-  if (o.n > 0)
+  if (o.n > 0) {
+    PhaseTimer tm(ctx, 0, 2.0 * o.n * o.P * k, 8.0 * o.n * o.P);
     gemm_rm(ctx, o.n, k, o.P, o.samp, o.lds, o.mu, q, ldq, v + o.r * ldv, ldv, o.ss, false);
+  }
 }
 
 // u (P x k, ldu) = Ohat v   (svdengine.py:134), summed over ranks
 void apply_O(Context& ctx, const Ohat& o, const double* v, int64_t ldv, int64_t k, double* u,
              int64_t ldu) {
   if (o.n > 0) {
+    PhaseTimer tm(ctx, 1, 2.0 * o.n * o.P * k, 8.0 * o.n * o.P);
     gemm_cm(ctx, o.P, k, o.n, o.samp, o.lds, o.mu, v + o.r * ldv, ldv, u, ldu, o.ss, false);
   } else {
     WSSR_CUDA(cudaMemset2DAsync(u, sizeof(double) * ldu, 0, sizeof(double) * k, o.P, ctx.stream));
@@ -588,6 +640,7 @@ void assemble(Context& ctx, const double* derivs, int64_t n, int64_t p, int64_t 
   // one pass over O: column means, centred second moments, centred gradient sums
   Buf m2(p, st), gsum(p, st);
   if (n > 0) {
+    PhaseTimer tm(ctx, 2, 4.0 * n * p, 8.0 * n * p);
     colstats_kernel<<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
         derivs, n, p, ld, lraw, out->mu, m2, gsum);
     post_launch(ctx);
@@ -805,6 +858,23 @@ struct NcclComm : Comm {
 }  // namespace
 }  // namespace wssr
 
+namespace wssr {
+__global__ void dmma_peak_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma884(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+}  // namespace wssr
+
 // ================================ C ABI =====================================================
 using namespace wssr;
 
@@ -871,6 +941,49 @@ int wssr_set_stream(wssr_ctx* ctx, void* stream) {
 }
 
 int64_t wssr_kernel_launches(const wssr_ctx* ctx) { return ctx ? ctx->c.kernel_launches : 0; }
+
+int wssr_set_timing(wssr_ctx* ctx, int enabled) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  ctx->c.timing = enabled != 0;
+  for (int i = 0; i < Context::kPhases; ++i) {
+    ctx->c.phase_ms[i] = ctx->c.phase_flops[i] = ctx->c.phase_bytes[i] = 0.0;
+    ctx->c.phase_count[i] = 0;
+  }
+  return WSSR_OK;
+}
+
+int wssr_phase_stats(wssr_ctx* ctx, int phase, double* ms, int64_t* launches, double* flops,
+                     double* bytes) {
+  if (!ctx || phase < 0 || phase >= Context::kPhases) return WSSR_ERR_VALUE;
+  *ms = ctx->c.phase_ms[phase];
+  *launches = ctx->c.phase_count[phase];
+  *flops = ctx->c.phase_flops[phase];
+  *bytes = ctx->c.phase_bytes[phase];
+  return WSSR_OK;
+}
+
+// FP64 tensor-core peak probe: DMMA.8x8x4 with independent accumulators, 4 CTAs of 8 warps per
+// SM, timed with CUDA events.  Gives the measured roofline denominator (TFLOP/s).
+int wssr_dmma_peak_probe(wssr_ctx* ctx, double* tflops) {
+  return guarded(ctx, [&] {
+    const int iters = 4096;
+    const int blocks = ctx->c.num_sms * 4, threads = 256;
+    Buf sink(threads, ctx->c.stream);
+    cudaEvent_t a, b;
+    WSSR_CUDA(cudaEventCreate(&a));
+    WSSR_CUDA(cudaEventCreate(&b));
+    dmma_peak_kernel<<<blocks, threads, 0, ctx->c.stream>>>(sink, iters);
+    WSSR_CUDA(cudaEventRecord(a, ctx->c.stream));
+    dmma_peak_kernel<<<blocks, threads, 0, ctx->c.stream>>>(sink, iters);
+    WSSR_CUDA(cudaEventRecord(b, ctx->c.stream));
+    WSSR_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *tflops = 2.0 * 8 * 256 * (double)iters * blocks * (threads / 32) / (ms * 1e-3) / 1e12;
+  });
+}
 
 int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]) {
   return guarded(ctx, [&] {

@@ -35,6 +35,21 @@ struct Context {
   int64_t gemm_launches = 0;  // statistics for bench.py
   int64_t kernel_launches = 0;
 
+  // optional per-phase timing of the O-passes (CUDA events on the launching stream)
+  static constexpr int kPhases = 3;  // 0: v = Ohat^T q, 1: u = Ohat v, 2: assemble column pass
+  bool timing = false;
+  struct PendingEvent {
+    int phase;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<PendingEvent> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double phase_ms[kPhases] = {0, 0, 0};
+  double phase_flops[kPhases] = {0, 0, 0};
+  double phase_bytes[kPhases] = {0, 0, 0};
+  int64_t phase_count[kPhases] = {0, 0, 0};
+
   double* splitk_buffer(size_t n);
   int world() const { return comm ? comm->world : 1; }
   cudaError_t allreduce(double* buf, size_t n) {

@@ -208,18 +208,24 @@ __global__ void matrix_sumsq_partials_kernel(const double* __restrict__ x, int64
 __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, double* dX,
                               double* __restrict__ R, double* __restrict__ Rinv,
                               int* __restrict__ status, double pivot_rel) {
-  __shared__ double s_gmax;
+  __shared__ double s_gmax, s_trace;
   __shared__ int s_fail;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < k * k; e += nt) W[e] = G[e];
+  for (int j = tid; j < k; j += nt) dX[j] = G[j * k + j];  // original diagonal
   if (tid == 0) {
-    double gm = 0.0;
-    for (int j = 0; j < k; ++j) gm = fmax(gm, G[j * k + j]);
+    double gm = 0.0, tr = 0.0;
+    for (int j = 0; j < k; ++j) {
+      gm = fmax(gm, G[j * k + j]);
+      tr += G[j * k + j];
+    }
     s_gmax = gm;
+    s_trace = tr;
     s_fail = 0;
   }
   __syncthreads();
-  const double floor_abs = pivot_rel * s_gmax;
+  // |R_jj| <= 1e-12 ||A||_F is the reference's switch to the patch path (linalg.py:58-61)
+  const double deficient_sq = 1.0000001e-24 * s_trace;
   if (s_gmax == 0.0 || !(s_gmax < 1.0 / 0.0)) {
     if (tid == 0) {
       if (s_gmax == 0.0) atomicExch(status + 1, 1);
@@ -231,7 +237,9 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
   for (int j = 0; j < k; ++j) {
     if (tid == 0) {
       const double d = W[j * k + j];
-      if (!(d > floor_abs)) {
+      // scale-invariant pivot test (Schur complement vs the column's own norm) + the
+      // reference's deficiency rule; either sends the block to the careful path
+      if (!(d > pivot_rel * dX[j]) || !(d > deficient_sq)) {
         s_fail = j + 1;
       } else {
         W[j * k + j] = sqrt(d);
