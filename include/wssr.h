@@ -87,6 +87,10 @@ int wssr_version(void);
 /* number of kernels this context launched so far (bench.py's gpu_launches) */
 int64_t wssr_kernel_launches(const wssr_ctx* ctx);
 
+/* GEMM main loop: 0 = auto (TMA + mbarrier warp-specialised pipeline when operands allow it),
+ * 1 = force the cp.async pipeline (A/B comparisons and tests). */
+int wssr_set_gemm_path(wssr_ctx* ctx, int path);
+
 /* bench instrumentation: per-phase CUDA-event timing of the O-passes.
  * phase 0 = v = Ohat^T q (svdengine.py:133), 1 = u = Ohat v (svdengine.py:134),
  * 2 = assemble's column-statistics pass (estimators.py:91,93).  Enabling resets the totals. */
@@ -179,6 +183,12 @@ typedef struct wssr_step_out {
   double residual, sigma_drift, projector_drift;
 } wssr_step_out;
 int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
+
+/* --- diagnostics: small k x k device routines (tests).  op 0: CholeskyQR core, in = G (k x k),
+ * out1 = R, out2 = R^-1, status[2] = {failed pivot (1-based) or 0, zero-matrix flag};
+ * op 1: largest eigenvalue of symmetric `in`, out1[0] = lambda_max. */
+int wssr_debug_small_f64(wssr_ctx* ctx, int op, int k, const double* in, double* out1,
+                         double* out2, int* status);
 
 /* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
 int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,

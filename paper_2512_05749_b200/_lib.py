@@ -80,6 +80,7 @@ SIGNATURES = {
     "wssr_last_error": (ctypes.c_char_p, [_vp]),
     "wssr_set_stream": (ctypes.c_int, [_vp, _vp]),
     "wssr_kernel_launches": (_i64, [_vp]),
+    "wssr_set_gemm_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_phase_stats": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_dbl),
                                         ctypes.POINTER(_i64), ctypes.POINTER(_dbl),
@@ -96,6 +97,8 @@ SIGNATURES = {
                                                _i64, ctypes.POINTER(_dbl),
                                                ctypes.POINTER(_dbl)]),
     "wssr_step_f64": (ctypes.c_int, [_vp, ctypes.POINTER(StepIn), ctypes.POINTER(StepOut)]),
+    "wssr_debug_small_f64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp,
+                                            ctypes.POINTER(ctypes.c_int)]),
     "wssr_gemm_f64": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _vp,
                                      _i64, _vp, _i64, _dbl, ctypes.c_int, ctypes.c_int]),
 }

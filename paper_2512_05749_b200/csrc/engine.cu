@@ -165,15 +165,24 @@ void collect_timing(Context& ctx) {
 void gemm_cm(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
              const double* shift, const double* B, int64_t ldb, double* C, int64_t ldc,
              double alpha, bool accumulate, int max_splits = 1024) {
-  GemmArgs a{A, lda, B, ldb, shift, C, ldc, M, N, K, 0, alpha, accumulate ? 1 : 0, nullptr};
+  GemmArgs a{A, lda, B, ldb, shift, C, ldc, M, N, K, 0, alpha, accumulate ? 1 : 0, nullptr,
+             nullptr, 0};
   WSSR_CUDA(gemm(ctx, Layout::CM, a, max_splits, ctx.stream));
 }
 // RM: C(MxN) = alpha * sum_k (A[m*lda+k] - shift[k]) B[k*ldb+n]
 void gemm_rm(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
              const double* shift, const double* B, int64_t ldb, double* C, int64_t ldc,
              double alpha, bool accumulate, int max_splits = 1024) {
-  GemmArgs a{A, lda, B, ldb, shift, C, ldc, M, N, K, 0, alpha, accumulate ? 1 : 0, nullptr};
+  GemmArgs a{A, lda, B, ldb, shift, C, ldc, M, N, K, 0, alpha, accumulate ? 1 : 0, nullptr,
+             nullptr, 0};
   WSSR_CUDA(gemm(ctx, Layout::RM, a, max_splits, ctx.stream));
+}
+// C = Cin + alpha * A(MxK, row-major) B   (the "w - q * quotient" / "u2 - u1 C" shape)
+void gemm_rm_add(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, const double* Cin, int64_t ldcin, double* C,
+                 int64_t ldc, double alpha) {
+  GemmArgs a{A, lda, B, ldb, nullptr, C, ldc, M, N, K, 0, alpha, 0, nullptr, Cin, ldcin};
+  WSSR_CUDA(gemm(ctx, Layout::RM, a, 1024, ctx.stream));
 }
 
 // Gram G (k x k) = A^T A, A rows x k (lda); allreduced over ranks when rows are sharded.
@@ -209,6 +218,20 @@ void sumsq_matrix(Context& ctx, const double* x, int64_t rows, int64_t cols, int
   post_launch(ctx);
 }
 
+// out[r] = ||x[r, :]|| for an (rows x cols, ld) matrix
+void row_norms(Context& ctx, const double* x, int64_t rows, int64_t cols, int64_t ld,
+               double* out) {
+  const int64_t chunk = 8192;
+  const int nb = (int)std::max<int64_t>(1, (cols + chunk - 1) / chunk);
+  Buf part((size_t)rows * nb, ctx.stream);
+  row_sumsq_partials_kernel<<<dim3(nb, (unsigned)rows), 256, 0, ctx.stream>>>(x, cols, ld, chunk,
+                                                                               part);
+  post_launch(ctx);
+  row_norms_final_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, ctx.stream>>>(part, nb,
+                                                                                (int)rows, out, 1);
+  post_launch(ctx);
+}
+
 double read_scalar(Context& ctx, const double* dev) {
   double h = 0.0;
   d2h(ctx, &h, dev, sizeof(double));
@@ -218,8 +241,7 @@ double read_scalar(Context& ctx, const double* dev) {
 
 // ---- k x k Cholesky + inverse ---------------------------------------------------------------
 void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int* status) {
-  const size_t smem = sizeof(double) * ((size_t)k * k + k);
-  const int threads = k <= 32 ? 128 : (k <= 64 ? 256 : 512);
+  const size_t smem = sizeof(double) * chol_scratch_doubles(k);
   if (smem <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {
@@ -227,13 +249,12 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    chol_inv_smem_kernel<<<1, threads, smem, ctx.stream>>>(G, k, R, Rinv, status, kCholPivotRel);
-    post_launch(ctx);
+    chol_inv_smem_kernel<<<1, 256, smem, ctx.stream>>>(G, k, R, Rinv, status, kCholPivotRel);
   } else {
-    Buf W((size_t)k * k + k, ctx.stream);
-    chol_inv_gmem_kernel<<<1, 1024, 0, ctx.stream>>>(G, k, W, R, Rinv, status, kCholPivotRel);
-    post_launch(ctx);
+    Buf W(chol_scratch_doubles(k), ctx.stream);
+    chol_inv_gmem_kernel<<<1, 256, 0, ctx.stream>>>(G, k, W, R, Rinv, status, kCholPivotRel);
   }
+  post_launch(ctx);
 }
 
 // ---- QR: CholeskyQR2 fast path, two-pass Gram-Schmidt with canonical fill as the exact
@@ -467,8 +488,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
     apply_OT(ctx, o, q, k, k, v2, k);
     apply_O(ctx, o, v2, k, k, w, k);
     gemm_cm(ctx, k, k, P, q, k, nullptr, w, k, quot, k, 1.0, false);  // quotient = q^T w
-    copy2d(ctx, w, k, P, k, 1.0, tmp, k);
-    gemm_rm(ctx, P, k, k, q, k, nullptr, quot, k, tmp, k, -1.0, true);  // w - q quotient
+    gemm_rm_add(ctx, P, k, k, q, k, quot, k, w, k, tmp, k, -1.0);  // w - q quotient
     sumsq_matrix(ctx, tmp, P, k, k, scal);
     small_norms_kernel<<<1, 256, 0, st>>>(nullptr, nullptr, 0, quot, (int)k, scal + 1);
     post_launch(ctx);
@@ -501,13 +521,24 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   if (res.k_pos == 0)
     throw Fail{WSSR_ERR_DEGENERATE_INPUT, "iteration produced no positive singular values"};
   const int64_t kp = res.k_pos;
-  // U = QR(u[:, order[:k]]) and V = q_v[:, order] (svdengine.py:151-152)
-  Buf uperm((size_t)P * kp, st);
-  gather_cols_kernel<<<blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
-      u, k, P, res.order.i64(), (int)kp, uperm, kp);
-  post_launch(ctx);
-  Buf Rf((size_t)kp * kp, st);
-  qr(ctx, P, kp, uperm, kp, U_out, ldU, Rf, status, careful, false);
+  // U = QR(u[:, order[:k]]) and V = q_v[:, order] (svdengine.py:151-152).  When the order is
+  // the identity the QR is exactly the one already computed at the top of the last iteration
+  // (q = QR(u), same inputs, same deterministic kernels), so it is reused.
+  std::vector<int64_t> hord(k);
+  d2h(ctx, hord.data(), res.order, sizeof(int64_t) * k);
+  sync(ctx);
+  bool identity = kp == k;
+  for (int64_t j = 0; j < kp && identity; ++j) identity = hord[j] == j;
+  if (identity) {
+    copy2d(ctx, q, k, P, k, 1.0, U_out, ldU);
+  } else {
+    Buf uperm((size_t)P * kp, st);
+    gather_cols_kernel<<<blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
+        u, k, P, res.order.i64(), (int)kp, uperm, kp);
+    post_launch(ctx);
+    Buf Rf((size_t)kp * kp, st);
+    qr(ctx, P, kp, uperm, kp, U_out, ldU, Rf, status, careful, false);
+  }
   res.qv = Buf((size_t)std::max<int64_t>(cols, 1) * k, st);
   if (cols > 0) {
     gather_cols_kernel<<<blocks_for(cols * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
@@ -535,6 +566,23 @@ auto with_fallback(Context& ctx, int64_t flags, F&& body) -> decltype(body(false
   return body(true, status.i32());
 }
 
+// ---- largest eigenvalue of a small symmetric matrix ---------------------------------------
+void maxeig(Context& ctx, const double* A, int k, double* out_dev) {
+  const size_t smem = sizeof(double) * ((size_t)k * (k + 1) + 4 * (size_t)k);
+  if (smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      WSSR_CUDA(cudaFuncSetAttribute(maxeig_smem_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    maxeig_smem_kernel<<<1, 256, smem, ctx.stream>>>(A, k, out_dev);
+  } else {
+    Buf W((size_t)k * (k + 1) + 4 * (size_t)k, ctx.stream);
+    maxeig_gmem_kernel<<<1, 256, 0, ctx.stream>>>(A, k, W, out_dev);
+  }
+}
+
 // ---- subspace_drift (svdengine.py:199-226) ----------------------------------------------------
 std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, int64_t ld1,
                                 const double* s1, int64_t r1, const double* u2, int64_t ld2,
@@ -546,23 +594,9 @@ std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, in
   small_norms_kernel<<<1, 256, 0, st>>>(s1, s2, (int)r, nullptr, 0, out);
   post_launch(ctx);
   gemm_cm(ctx, r, r, rows, u1, ld1, nullptr, u2, ld2, C, r, 1.0, false);  // u1^T u2
-  copy2d(ctx, u2, ld2, rows, r, 1.0, X, r);
-  gemm_rm(ctx, rows, r, r, u1, ld1, nullptr, C, r, X, r, -1.0, true);  // u2 - u1 (u1^T u2)
+  gemm_rm_add(ctx, rows, r, r, u1, ld1, C, r, u2, ld2, X, r, -1.0);  // u2 - u1 (u1^T u2)
   gemm_cm(ctx, r, r, rows, X, r, nullptr, X, r, GX, r, 1.0, false);
-  const int kk = (int)(r + (r & 1));
-  const size_t smem = sizeof(double) * kk * kk + sizeof(int) * kk;
-  if (smem <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      WSSR_CUDA(cudaFuncSetAttribute(jacobi_maxeig_smem_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
-    jacobi_maxeig_smem_kernel<<<1, 512, smem, st>>>(GX, (int)r, out + 2);
-  } else {
-    Buf W((size_t)kk * kk, st);
-    jacobi_maxeig_gmem_kernel<<<1, 1024, sizeof(int) * kk, st>>>(GX, (int)r, W, out + 2);
-  }
+  maxeig(ctx, GX, (int)r, out + 2);
   post_launch(ctx);
   double h[3];
   d2h(ctx, h, out, sizeof(h));
@@ -777,10 +811,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   if (in->r_prev > 0) {
     const int64_t r_hist = oh.hist_rank;
     Buf sprev(std::max<int64_t>(r_hist, 1), st);
-    if (r_hist > 0) {
-      row_norms_kernel<<<(unsigned)r_hist, 256, 0, st>>>(oh.hist, P, oh.hist_ld, sprev, 1);
-      post_launch(ctx);
-    }
+    if (r_hist > 0) row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
     const int64_t r1 = std::min(r_hist, in->r_prev);
     auto d = drift(ctx, P, in->u_prev, in->ld_prev, sprev, r1, out->u_next, out->ld_u, out->sigma,
                    r_eff);
@@ -942,6 +973,12 @@ int wssr_set_stream(wssr_ctx* ctx, void* stream) {
 
 int64_t wssr_kernel_launches(const wssr_ctx* ctx) { return ctx ? ctx->c.kernel_launches : 0; }
 
+int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
+  if (!ctx || path < 0 || path > 1) return WSSR_ERR_VALUE;
+  ctx->c.disable_tma = path == 1;
+  return WSSR_OK;
+}
+
 int wssr_set_timing(wssr_ctx* ctx, int enabled) {
   if (!ctx) return WSSR_ERR_VALUE;
   ctx->c.timing = enabled != 0;
@@ -1081,6 +1118,24 @@ int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out) {
     if (!in || !out || !in->ohat) throw Fail{WSSR_ERR_VALUE, "null argument"};
     if (in->max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
     step(ctx->c, in, out);
+  });
+}
+
+int wssr_debug_small_f64(wssr_ctx* ctx, int op, int k, const double* in, double* out1,
+                         double* out2, int* status) {
+  return guarded(ctx, [&] {
+    Context& c = ctx->c;
+    if (op == 0) {
+      Buf st(1, c.stream);
+      WSSR_CUDA(cudaMemsetAsync(st, 0, sizeof(double), c.stream));
+      chol_inv(c, in, k, out1, out2, st.i32());
+      WSSR_CUDA(cudaMemcpyAsync(status, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    } else if (op == 1) {
+      maxeig(c, in, k, out1);
+    } else {
+      throw Fail{WSSR_ERR_VALUE, "unknown op"};
+    }
+    sync(c);
   });
 }
 

@@ -34,6 +34,7 @@ struct Context {
   Comm* comm = nullptr;
   int64_t gemm_launches = 0;  // statistics for bench.py
   int64_t kernel_launches = 0;
+  bool disable_tma = false;  // force the cp.async GEMM path (tests / A-B comparisons)
 
   // optional per-phase timing of the O-passes (CUDA events on the launching stream)
   static constexpr int kPhases = 3;  // 0: v = Ohat^T q, 1: u = Ohat v, 2: assemble column pass

@@ -45,6 +45,8 @@ struct GemmArgs {
   double alpha;
   int accumulate;
   double* partial;
+  const double* Cin;  // optional: result = Cin + alpha*acc (ld = ldcin); used when !partial
+  int64_t ldcin;
 };
 
 __host__ __device__ constexpr int pad_doubles(int base, int mod_bytes, int target_bytes) {
@@ -260,26 +262,73 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
           args.partial[((int64_t)blockIdx.z * M + m) * N + n] = val;
         } else {
           double* dst = args.C + m * args.ldc + n;
-          *dst = args.accumulate ? *dst + val : val;
+          if (args.Cin)
+            *dst = args.Cin[m * args.ldcin + n] + val;
+          else
+            *dst = args.accumulate ? *dst + val : val;
         }
       }
     }
   }
 }
 
-// C(m,n) = alpha * sum_{z<S} partial[z][m][n]  (+ C if accumulate), summed in z order.
-static __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int S, int64_t M,
-                                     int64_t N, double* __restrict__ C, int64_t ldc, double alpha,
-                                     int accumulate) {
+// Few slabs (S <= 8): one thread per output, slabs summed in order; bandwidth-bound.
+static __global__ void __launch_bounds__(256)
+    splitk_reduce_few_kernel(const double* __restrict__ partial, int S, int64_t M, int64_t N,
+                             double* __restrict__ C, int64_t ldc, double alpha, int accumulate,
+                             const double* __restrict__ Cin, int64_t ldcin) {
   const int64_t total = M * N;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int z = 0; z < S; ++z) s += partial[(int64_t)z * total + idx];
+    double s = partial[idx];
+    for (int z = 1; z < S; ++z) s += partial[(int64_t)z * total + idx];
     const int64_t m = idx / N, n = idx % N;
     double* dst = C + m * ldc + n;
     const double val = alpha * s;
-    *dst = accumulate ? *dst + val : val;
+    *dst = Cin ? Cin[m * ldcin + n] + val : (accumulate ? *dst + val : val);
+  }
+}
+
+// C(m,n) = alpha * sum_{z<S} partial[z][m][n]  (+ C if accumulate).
+// Block = 8 warps x 32 lanes: lane <-> 32 consecutive outputs (coalesced), warp w sums the slabs
+// z = w, w+8, ... in order, then warp partials are added in warp order - a fixed order, so the
+// result is bitwise reproducible while S up to a few hundred slabs stays latency-cheap.
+static __global__ void __launch_bounds__(256)
+    splitk_reduce_kernel(const double* __restrict__ partial, int S, int64_t M, int64_t N,
+                         double* __restrict__ C, int64_t ldc, double alpha, int accumulate,
+                         const double* __restrict__ Cin, int64_t ldcin) {
+  __shared__ double red[8][33];
+  const int64_t total = M * N;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    const int64_t idx = base + lane;
+    double s = 0.0;
+    if (idx < total) {
+      int z = w;
+      for (; z + 24 < S; z += 32) {
+        const double a0 = partial[(int64_t)z * total + idx];
+        const double a1 = partial[(int64_t)(z + 8) * total + idx];
+        const double a2 = partial[(int64_t)(z + 16) * total + idx];
+        const double a3 = partial[(int64_t)(z + 24) * total + idx];
+        s += a0;
+        s += a1;
+        s += a2;
+        s += a3;
+      }
+      for (; z < S; z += 8) s += partial[(int64_t)z * total + idx];
+    }
+    red[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && idx < total) {
+      double t = red[0][lane];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) t += red[q][lane];
+      const int64_t m = idx / N, n = idx % N;
+      double* dst = C + m * ldc + n;
+      const double val = alpha * t;
+      *dst = Cin ? Cin[m * ldcin + n] + val : (accumulate ? *dst + val : val);
+    }
+    __syncthreads();
   }
 }
 

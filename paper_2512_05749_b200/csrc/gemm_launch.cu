@@ -1,7 +1,12 @@
 // Host-side dispatch for the DMMA GEMM family: tile-config choice by output width, operand
 // vector width (16-byte cp.async when rows are 16-byte aligned) and split-K sizing.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "engine.h"
 #include "gemm.cuh"
+#include "gemm_tma.cuh"
 
 namespace wssr {
 
@@ -52,6 +57,103 @@ struct Tile {
   }
 };
 
+// ---- TMA + mbarrier warp-specialised tiles (gemm_tma.cuh) ----------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a row-major (outer x inner) FP64 array with row pitch `pitch` elements;
+// box = 16 doubles (128 B, SWIZZLE_128B) x box_outer rows.
+bool make_map_2d(CUtensorMap* map, const double* ptr, int64_t inner, int64_t outer, int64_t pitch,
+                 int box_outer) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(pitch * 8, 16)};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool make_map_1d(CUtensorMap* map, const double* ptr, int64_t n, int box) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t bx[1] = {(cuuint32_t)box};
+  cuuint32_t es[1] = {1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double*>(ptr), dims, strides, bx,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST>
+struct TmaTile {
+  static constexpr int kBM = BM, kBN = BN, kBK = BK;
+  using Cfg = TmaCfg<L, BM, BN, BK, WMW, WNW, ST>;
+  static cudaError_t launch(const GemmArgs& a, int splits, bool, bool, cudaStream_t st) {
+    auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)Cfg::kSmemBytes);
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    CUtensorMap tA, tB, tS;
+    std::memset(&tS, 0, sizeof(tS));
+    bool ok;
+    if (L == Layout::CM)
+      ok = make_map_2d(&tA, a.A, a.M, a.K, a.lda, BK);
+    else
+      ok = make_map_2d(&tA, a.A, a.K, a.M, a.lda, BM);
+    ok = ok && make_map_2d(&tB, a.B, a.N, a.K, a.ldb, BK);
+    if (L == Layout::RM && a.shift) ok = ok && make_map_1d(&tS, a.shift, a.K, BK);
+    if (!ok) return cudaErrorInvalidValue;
+    dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((a.N + BN - 1) / BN), (unsigned)splits);
+    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tS, a);
+    ++g_launches;
+    return cudaGetLastError();
+  }
+  static int ctas_per_sm() {
+    static int occ = -1;
+    if (occ < 0) {
+      auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)Cfg::kSmemBytes);
+      int o = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads,
+                                                        Cfg::kSmemBytes) != cudaSuccess)
+        o = 1;
+      occ = o < 1 ? 1 : o;
+    }
+    return occ;
+  }
+};
+
+using TCM32 = TmaTile<Layout::CM, 256, 32, 16, 8, 1, 3>;
+using TCM64 = TmaTile<Layout::CM, 128, 64, 16, 4, 2, 4>;
+using TCM128 = TmaTile<Layout::CM, 64, 128, 16, 2, 4, 4>;
+using TCM256 = TmaTile<Layout::CM, 32, 256, 16, 1, 8, 3>;
+using TCMsq32 = TmaTile<Layout::CM, 32, 32, 16, 1, 1, 4>;
+using TCMsq64 = TmaTile<Layout::CM, 64, 64, 16, 2, 2, 4>;
+using TRM32 = TmaTile<Layout::RM, 256, 32, 16, 8, 1, 3>;
+using TRM64 = TmaTile<Layout::RM, 128, 64, 16, 4, 2, 4>;
+using TRM128 = TmaTile<Layout::RM, 64, 128, 16, 2, 4, 4>;
+using TRM256 = TmaTile<Layout::RM, 32, 256, 16, 1, 8, 3>;
+
 // Config table.
 using CM32 = Tile<Layout::CM, 256, 32, 16, 8, 1, 4>;
 using CM64 = Tile<Layout::CM, 128, 64, 16, 4, 2, 4>;
@@ -66,14 +168,21 @@ using RM256 = Tile<Layout::RM, 32, 256, 16, 1, 8, 3>;
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int choose_splits(int64_t tiles, int64_t K, int BK, int capacity, int max_splits) {
+// Split-K only pays when the contraction is long and there are too few output tiles to fill
+// the machine: every split adds an M x N slab of partial traffic plus a reduction.
+int choose_splits(int64_t tiles, int64_t M, int64_t N, int64_t K, int BK, int capacity,
+                  int max_splits) {
   if (max_splits <= 1) return 1;
-  int64_t kmax = (K + 4 * BK - 1) / (4 * BK);  // keep >= 4 k-tiles per split
+  constexpr int64_t kMinChunk = 512;  // minimum K per split
+  int64_t kmax = K / kMinChunk;
   int smax = (int)std::min<int64_t>(max_splits, std::max<int64_t>(1, kmax));
-  if (tiles >= 6LL * capacity) return 1;
+  if (smax <= 1 || tiles >= 8LL * capacity) return 1;
+  // partial slabs must stay small next to the streamed operand
+  const double slab = (double)M * N, stream = (double)M * K + (double)K * N;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= smax; ++s) {
+    if (s > 1 && s * slab > 0.25 * stream) break;
     double waves = (double)(tiles * s) / capacity;
     double eff = waves / std::ceil(waves);
     if (eff >= 0.94) return s;
@@ -90,7 +199,7 @@ cudaError_t run_tile(Context& ctx, GemmArgs a, bool va2, bool vb2, int max_split
                      cudaStream_t st) {
   const int64_t tiles = ((a.M + T::kBM - 1) / T::kBM) * ((a.N + T::kBN - 1) / T::kBN);
   const int cap = ctx.num_sms * T::ctas_per_sm();
-  int s = choose_splits(tiles, a.K, T::kBK, cap, max_splits);
+  int s = choose_splits(tiles, a.M, a.N, a.K, T::kBK, cap, max_splits);
   int64_t kc = (a.K + s - 1) / s;
   kc = ((kc + T::kBK - 1) / T::kBK) * T::kBK;
   if (kc <= 0) kc = T::kBK;
@@ -112,9 +221,15 @@ cudaError_t run_tile(Context& ctx, GemmArgs a, bool va2, bool vb2, int max_split
   cudaError_t e = T::launch(a, s, va2, vb2, st);
   if (e != cudaSuccess) return e;
   const int64_t total = a.M * a.N;
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, 4LL * ctx.num_sms);
-  if (blocks < 1) blocks = 1;
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(part, s, a.M, a.N, C, ldc, alpha, acc);
+  if (s <= 8) {
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 16LL * ctx.num_sms);
+    splitk_reduce_few_kernel<<<std::max(blocks, 1), 256, 0, st>>>(part, s, a.M, a.N, C, ldc, alpha,
+                                                                  acc, a.Cin, a.ldcin);
+  } else {
+    int blocks = (int)std::min<int64_t>((total + 31) / 32, 8LL * ctx.num_sms);
+    splitk_reduce_kernel<<<std::max(blocks, 1), 256, 0, st>>>(part, s, a.M, a.N, C, ldc, alpha,
+                                                              acc, a.Cin, a.ldcin);
+  }
   ++g_launches;
   return cudaGetLastError();
 }
@@ -139,12 +254,33 @@ cudaError_t gemm_dispatch(Context& ctx, Layout layout, const GemmArgs& args, int
   GemmArgs a = args;
   if (a.K <= 0) {
     // empty contraction: C = 0 (or unchanged when accumulating)
+    if (a.Cin)
+      return cudaMemcpy2DAsync(a.C, sizeof(double) * a.ldc, a.Cin, sizeof(double) * a.ldcin,
+                               sizeof(double) * a.N, a.M, cudaMemcpyDeviceToDevice, st);
     if (!a.accumulate)
       return cudaMemset2DAsync(a.C, sizeof(double) * a.ldc, 0, sizeof(double) * a.N, a.M, st);
     return cudaSuccess;
   }
   const bool va2 = (a.lda % 2 == 0) && aligned16(a.A);
   const bool vb2 = (a.ldb % 2 == 0) && aligned16(a.B);
+  const bool small = a.M * a.N * a.K < (int64_t)1 << 22;  // tiny problems: plain cp.async path
+  const bool tma = va2 && vb2 && !small && !ctx.disable_tma && tma_encode_fn() != nullptr &&
+                   (layout == Layout::CM || !a.shift || aligned16(a.shift)) &&
+                   a.M < (1LL << 31) && a.N < (1LL << 31) && a.K < (1LL << 31);
+  if (tma) {
+    if (layout == Layout::CM) {
+      if (a.M <= 32 && a.N <= 32) return run_tile<TCMsq32>(ctx, a, va2, vb2, max_splits, st);
+      if (a.M <= 64 && a.N <= 64) return run_tile<TCMsq64>(ctx, a, va2, vb2, max_splits, st);
+      if (a.N <= 32) return run_tile<TCM32>(ctx, a, va2, vb2, max_splits, st);
+      if (a.N <= 64) return run_tile<TCM64>(ctx, a, va2, vb2, max_splits, st);
+      if (a.N <= 128) return run_tile<TCM128>(ctx, a, va2, vb2, max_splits, st);
+      return run_tile<TCM256>(ctx, a, va2, vb2, max_splits, st);
+    }
+    if (a.N <= 32) return run_tile<TRM32>(ctx, a, va2, vb2, max_splits, st);
+    if (a.N <= 64) return run_tile<TRM64>(ctx, a, va2, vb2, max_splits, st);
+    if (a.N <= 128) return run_tile<TRM128>(ctx, a, va2, vb2, max_splits, st);
+    return run_tile<TRM256>(ctx, a, va2, vb2, max_splits, st);
+  }
   if (layout == Layout::CM) {
     if (a.M <= 32 && a.N <= 32) return run_tile<CMsq32>(ctx, a, va2, vb2, max_splits, st);
     if (a.M <= 64 && a.N <= 64) return run_tile<CMsq64>(ctx, a, va2, vb2, max_splits, st);

@@ -1,0 +1,283 @@
+// Warp-specialised TMA + mbarrier pipeline for the FP64 DMMA tall-skinny GEMMs (same contract as
+// gemm_dmma_kernel in gemm.cuh: Layout::CM / Layout::RM, centring shift, alpha, split-K slabs).
+//
+//   warp W (the last one)  : producer - one elected lane issues cp.async.bulk.tensor (TMA) loads of
+//                            the A/B tiles (and the shift slice) into a STAGES-deep ring, arming the
+//                            stage's "full" mbarrier with the transaction byte count;
+//   warps 0..W-1           : consumers - wait on "full", run mma.sync.m8n8k4.f64 (DMMA.8x8x4) from
+//                            swizzled shared memory, then arrive on the stage's "empty" mbarrier.
+// No CTA-wide barrier sits in the k-loop, so DMMA issue never waits for the slowest warp.
+//
+// Tiles land in shared memory through 2-D tensor maps with 16-double (128 B) inner boxes and
+// SWIZZLE_128B: inside every 1 KB atom the 16-byte unit index is XORed with the line index mod 8.
+// Each lane fetches pairs of doubles with LDS.128; which pair a lane owns is permuted
+// (f(g) = (g>>1) | ((g&1)<<2) on the swizzled axes) so that every quarter-warp touches 8 distinct
+// 16-byte bank groups - conflict-free - and the permutation is undone in the epilogue.
+#pragma once
+#include <cuda.h>
+
+#include "gemm.cuh"
+
+namespace wssr {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, int c0,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2}], [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__host__ __device__ constexpr int fperm(int g) { return (g >> 1) | ((g & 1) << 2); }
+
+template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+struct TmaCfg {
+  static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
+  static constexpr int kThreads = 32 * (kConsumerWarps + 1);
+  static constexpr int WM = BM / WARPS_M;
+  static constexpr int WN = BN / WARPS_N;
+  static constexpr int MS = WM / 8;
+  static constexpr int NS = WN / 8;
+  static constexpr bool kCM = (L == Layout::CM);
+  static constexpr int A_BYTES = BM * BK * 8;
+  static constexpr int B_BYTES = BK * BN * 8;
+  static constexpr int S_BYTES = kCM ? 0 : 1024;  // shift slice (BK doubles), padded
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + S_BYTES;
+  static constexpr size_t kSmemBytes = (size_t)STAGE_BYTES * STAGES + 1024 /*align*/ + 256;
+  static_assert(BK % 16 == 0 && BM % 16 == 0 && BN % 16 == 0, "16-double boxes");
+  static_assert(WM % 16 == 0 || (!kCM && WM % 8 == 0), "warp M tile");
+  static_assert(WN % 16 == 0, "warp N tile");
+  static_assert(STAGE_BYTES % 1024 == 0, "swizzle atoms");
+};
+
+template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+__global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmS, const GemmArgs args) {
+  using Cfg = TmaCfg<L, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+  constexpr bool CM = Cfg::kCM;
+  constexpr int MS = Cfg::MS, NS = Cfg::NS;
+  constexpr int NCW = Cfg::kConsumerWarps;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)Cfg::STAGE_BYTES * STAGES);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool has_shift = args.shift != nullptr;
+  const int64_t M = args.M, N = args.N;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * args.k_chunk;
+  const int64_t kend = min(args.K, kbeg + args.k_chunk);
+  const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      if (!CM && has_shift) prefetch_tmap(&tmS);
+      const uint32_t bytes = Cfg::A_BYTES + Cfg::B_BYTES + ((!CM && has_shift) ? BK * 8 : 0);
+      for (int it = 0; it < ntiles; ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(empty + s, ((it / STAGES) - 1) & 1);
+        unsigned char* st = smem + (size_t)s * Cfg::STAGE_BYTES;
+        const int k0 = (int)(kbeg + (int64_t)it * BK);
+        mbar_arrive_expect_tx(full + s, bytes);
+        if (CM) {
+#pragma unroll
+          for (int c = 0; c < BM / 16; ++c)
+            tma_load_2d(st + c * (BK * 128), &tmA, (int)m0 + 16 * c, k0, full + s);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BK / 16; ++c)
+            tma_load_2d(st + c * (BM * 128), &tmA, k0 + 16 * c, (int)m0, full + s);
+          if (has_shift) tma_load_1d(st + Cfg::A_BYTES + Cfg::B_BYTES, &tmS, k0, full + s);
+        }
+#pragma unroll
+        for (int c = 0; c < BN / 16; ++c)
+          tma_load_2d(st + Cfg::A_BYTES + c * (BK * 128), &tmB, (int)n0 + 16 * c, k0, full + s);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ consumers ------------------------------
+  const int g = lane >> 2, t = lane & 3;
+  const int fg = fperm(g);
+  const int wm0 = (warp % WARPS_M) * Cfg::WM;
+  const int wn0 = (warp / WARPS_M) * Cfg::WN;
+
+  double acc[MS][NS][2];
+#pragma unroll
+  for (int i = 0; i < MS; ++i)
+#pragma unroll
+    for (int j = 0; j < NS; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double mu[MS];
+#pragma unroll
+  for (int i = 0; i < MS; ++i) {
+    mu[i] = 0.0;
+    if (CM && has_shift) {
+      const int64_t m = m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1);
+      if (m < M) mu[i] = args.shift[m];
+    }
+  }
+
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % STAGES;
+    mbar_wait(full + s, (it / STAGES) & 1);
+    const unsigned char* sA = smem + (size_t)s * Cfg::STAGE_BYTES;
+    const unsigned char* sB = sA + Cfg::A_BYTES;
+    if (CM) {
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        const int k = kk + t;  // row inside the box (BK rows of 128 B)
+        const int sw = k & 7;
+        double a[MS], b[NS];
+#pragma unroll
+        for (int i = 0; i < MS / 2; ++i) {
+          const int c = (wm0 >> 4) + i;
+          const double2 x = *reinterpret_cast<const double2*>(
+              sA + c * (BK * 128) + k * 128 + ((fg ^ sw) << 4));
+          a[2 * i] = x.x - mu[2 * i];
+          a[2 * i + 1] = x.y - mu[2 * i + 1];
+        }
+#pragma unroll
+        for (int j = 0; j < NS / 2; ++j) {
+          const int c = (wn0 >> 4) + j;
+          const double2 y = *reinterpret_cast<const double2*>(
+              sB + c * (BK * 128) + k * 128 + ((fg ^ sw) << 4));
+          b[2 * j] = y.x;
+          b[2 * j + 1] = y.y;
+        }
+#pragma unroll
+        for (int i = 0; i < MS; ++i)
+#pragma unroll
+          for (int j = 0; j < NS; ++j) dmma884(acc[i][j], a[i], b[j]);
+      }
+    } else {
+      const double* sS = reinterpret_cast<const double*>(sB + Cfg::B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 8) {
+        double2 sh = make_double2(0.0, 0.0);
+        if (has_shift) sh = *reinterpret_cast<const double2*>(sS + kk + 2 * t);
+        const int ca = kk >> 4;
+        const int unit = 4 * ((kk >> 3) & 1) + t;
+        double a0[MS], a1[MS], b0[NS], b1[NS];
+#pragma unroll
+        for (int i = 0; i < MS; ++i) {
+          const int m = wm0 + 8 * i + fg;  // m & 7 == fg
+          const double2 x = *reinterpret_cast<const double2*>(
+              sA + ca * (BM * 128) + m * 128 + ((unit ^ fg) << 4));
+          a0[i] = x.x - sh.x;
+          a1[i] = x.y - sh.y;
+        }
+        const int k0r = kk + 2 * t, k1r = k0r + 1;
+#pragma unroll
+        for (int j = 0; j < NS / 2; ++j) {
+          const int c = (wn0 >> 4) + j;
+          const double2 y0 = *reinterpret_cast<const double2*>(
+              sB + c * (BK * 128) + k0r * 128 + ((g ^ (k0r & 7)) << 4));
+          const double2 y1 = *reinterpret_cast<const double2*>(
+              sB + c * (BK * 128) + k1r * 128 + ((g ^ (k1r & 7)) << 4));
+          b0[2 * j] = y0.x;
+          b0[2 * j + 1] = y0.y;
+          b1[2 * j] = y1.x;
+          b1[2 * j + 1] = y1.y;
+        }
+#pragma unroll
+        for (int i = 0; i < MS; ++i)
+#pragma unroll
+          for (int j = 0; j < NS; ++j) dmma884(acc[i][j], a0[i], b0[j]);
+#pragma unroll
+        for (int i = 0; i < MS; ++i)
+#pragma unroll
+          for (int j = 0; j < NS; ++j) dmma884(acc[i][j], a1[i], b1[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+  }
+
+  // epilogue: undo the lane permutations and store
+  const double alpha = args.alpha;
+#pragma unroll
+  for (int i = 0; i < MS; ++i) {
+    const int64_t m = CM ? m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1) : m0 + wm0 + 8 * i + fg;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        // fragment column c = 2t+e of sub-tile j
+        const int64_t n = CM ? n0 + wn0 + 16 * (j >> 1) + 2 * fperm(2 * t + e) + (j & 1)
+                             : n0 + wn0 + 16 * (j >> 1) + 2 * (2 * t + e) + (j & 1);
+        if (n >= N) continue;
+        const double val = alpha * acc[i][j][e];
+        if (args.partial) {
+          args.partial[((int64_t)blockIdx.z * M + m) * N + n] = val;
+        } else {
+          double* dst = args.C + m * args.ldc + n;
+          if (args.Cin)
+            *dst = args.Cin[m * args.ldcin + n] + val;
+          else
+            *dst = args.accumulate ? *dst + val : val;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace wssr

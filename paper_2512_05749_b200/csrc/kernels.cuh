@@ -168,32 +168,61 @@ __global__ void reduce_final_kernel(const double* __restrict__ partials, int npa
   if (threadIdx.x == 0) *out = s * scale;
 }
 
-// Row sums of squares of an (rows x cols, ld) matrix: out[r] = sqrt(sum_c x[r,c]^2) if sqrt_out.
-// One block per row, fixed order.  Used for ||obar[:, j]|| (optimizers.py:370).
-__global__ void row_norms_kernel(const double* __restrict__ x, int64_t cols, int64_t ld,
-                                 double* __restrict__ out, int sqrt_out) {
+// Row norms of an (rows x cols, ld) matrix, two levels: block (r, b) sums the b-th chunk of row r
+// into partial[r * nb + b]; row_norms_final sums the nb chunks in order.  Used for ||obar[:, j]||
+// (optimizers.py:370), where rows are P = 10^5..10^6 long.
+__global__ void row_sumsq_partials_kernel(const double* __restrict__ x, int64_t cols, int64_t ld,
+                                          int64_t chunk, double* __restrict__ partial) {
   __shared__ double scratch[32];
-  const double* row = x + (int64_t)blockIdx.x * ld;
+  const int64_t r = blockIdx.y, b = blockIdx.x;
+  const double* row = x + r * ld;
+  const int64_t c0 = b * chunk, c1 = min(cols, c0 + chunk);
+  double s0 = 0.0, s1 = 0.0;
+  int64_t c = c0 + threadIdx.x;
+  for (; c + blockDim.x < c1; c += 2 * blockDim.x) {
+    const double a0 = row[c], a1 = row[c + blockDim.x];
+    s0 = fma(a0, a0, s0);
+    s1 = fma(a1, a1, s1);
+  }
+  if (c < c1) s0 = fma(row[c], row[c], s0);
+  const double s = block_sum(s0 + s1, scratch);
+  if (threadIdx.x == 0) partial[r * gridDim.x + b] = s;
+}
+__global__ void row_norms_final_kernel(const double* __restrict__ partial, int nb, int rows,
+                                       double* __restrict__ out, int sqrt_out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
   double s = 0.0;
-  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) s = fma(row[c], row[c], s);
-  s = block_sum(s, scratch);
-  if (threadIdx.x == 0) out[blockIdx.x] = sqrt_out ? sqrt(s) : s;
+  for (int b = 0; b < nb; ++b) s += partial[(int64_t)r * nb + b];
+  out[r] = sqrt_out ? sqrt(s) : s;
 }
 
 // Sum of squares of a strided (rows x cols, ld) matrix into per-block partials (row chunks).
+// Dense rows (ld == cols) are streamed as one flat vector.
 __global__ void matrix_sumsq_partials_kernel(const double* __restrict__ x, int64_t rows,
                                              int64_t cols, int64_t ld, int64_t rows_per_block,
                                              double* __restrict__ partials) {
   __shared__ double scratch[32];
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-  double s = 0.0;
-  const int64_t total = (r1 - r0) * cols;
-  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-    const int64_t r = r0 + e / cols, c = e % cols;
-    const double v = x[r * ld + c];
-    s = fma(v, v, s);
+  double s0 = 0.0, s1 = 0.0;
+  if (ld == cols) {
+    const double* base = x + r0 * cols;
+    const int64_t n = (r1 - r0) * cols;
+    int64_t e = threadIdx.x;
+    for (; e + blockDim.x < n; e += 2 * blockDim.x) {
+      const double a0 = base[e], a1 = base[e + blockDim.x];
+      s0 = fma(a0, a0, s0);
+      s1 = fma(a1, a1, s1);
+    }
+    if (e < n) s0 = fma(base[e], base[e], s0);
+  } else {
+    for (int64_t r = r0; r < r1; ++r)
+      for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+        const double v = x[r * ld + c];
+        s0 = fma(v, v, s0);
+      }
   }
-  s = block_sum(s, scratch);
+  const double s = block_sum(s0 + s1, scratch);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
@@ -205,14 +234,28 @@ __global__ void matrix_sumsq_partials_kernel(const double* __restrict__ x, int64
 // orthogonality there) - the host then takes the two-pass Gram-Schmidt path of
 // linalg.py:64-105.  A zero matrix (trace 0) sets status[1] (ZeroMatrix, linalg.py:53-54).
 // ---------------------------------------------------------------------------------------------
-__device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, double* dX,
-                              double* __restrict__ R, double* __restrict__ Rinv,
+// k x k Cholesky + triangular inverse for CholeskyQR2 (replaces LAPACK dgeqrf/dorgqr behind
+// linalg.py:56).  One CTA of 256 threads laid out as a 16 x 16 grid; right-looking sweeps with two
+// block barriers per column and no integer division in the inner loops (the k^3 work is spread
+// over the grid, the k-long dependency chain costs ~2k cheap barriers).
+//   G = L L^T  ->  R = L^T, Rinv = L^-T (upper, zero below the diagonal).
+// W is k x (k+1) scratch (odd stride).  status[0] = 1-based index of the first pivot that is not
+// safely positive (CholeskyQR2 would lose orthogonality there: the host re-runs the block on the
+// Gram-Schmidt path of linalg.py:64-105); status[1] = zero matrix (linalg.py:53-54).
+__device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, double* X,
+                              double* dorig, double* __restrict__ R, double* __restrict__ Rinv,
                               int* __restrict__ status, double pivot_rel) {
   __shared__ double s_gmax, s_trace;
   __shared__ int s_fail;
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < k * k; e += nt) W[e] = G[e];
-  for (int j = tid; j < k; j += nt) dX[j] = G[j * k + j];  // original diagonal
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 grid (blockDim.x == 256)
+  const int ld = k + 1;
+  for (int r = ty; r < k; r += 16)
+    for (int c = tx; c < k; c += 16) {
+      W[r * ld + c] = G[r * k + c];
+      X[r * ld + c] = (r == c) ? 1.0 : 0.0;
+    }
+  for (int j = tid; j < k; j += nt) dorig[j] = G[j * k + j];
   if (tid == 0) {
     double gm = 0.0, tr = 0.0;
     for (int j = 0; j < k; ++j) {
@@ -233,27 +276,22 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     }
     return;
   }
-  // right-looking Cholesky, lower triangle in place
   for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
-      const double d = W[j * k + j];
-      // scale-invariant pivot test (Schur complement vs the column's own norm) + the
-      // reference's deficiency rule; either sends the block to the careful path
-      if (!(d > pivot_rel * dX[j]) || !(d > deficient_sq)) {
-        s_fail = j + 1;
-      } else {
-        W[j * k + j] = sqrt(d);
-      }
+    const double piv = W[j * ld + j];
+    // scale-invariant pivot test (Schur complement vs the column's own norm) + the reference's
+    // deficiency rule; every thread evaluates it on the same value, so the branch is uniform
+    if (!(piv > pivot_rel * dorig[j]) || !(piv > deficient_sq)) {
+      if (tid == 0) s_fail = j + 1;
+      break;
     }
+    const double sq = sqrt(piv), invs = 1.0 / sq;
+    for (int i = j + 1 + tid; i < k; i += nt) W[i * ld + j] *= invs;
     __syncthreads();
-    if (s_fail) break;
-    const double piv = W[j * k + j];
-    for (int i = j + 1 + tid; i < k; i += nt) W[i * k + j] /= piv;
-    __syncthreads();
-    const int m = k - j - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int i = j + 1 + e / m, l = j + 1 + e % m;
-      if (l <= i) W[i * k + l] -= W[i * k + j] * W[l * k + j];
+    if (tid == 0) W[j * ld + j] = sq;
+    // trailing update of the lower triangle: W[i][c] -= L[i][j] L[c][j], j < c <= i
+    for (int i = j + 1 + ty; i < k; i += 16) {
+      const double lij = W[i * ld + j];
+      for (int c = j + 1 + tx; c <= i; c += 16) W[i * ld + c] = fma(-lij, W[c * ld + j], W[i * ld + c]);
     }
     __syncthreads();
   }
@@ -261,45 +299,48 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     if (tid == 0) atomicCAS(status, 0, s_fail);
     return;
   }
-  // X = L^-1 (lower): row i of X from rows < i.  X[i][j] (i>j) is stored at W[j][i].
-  for (int i = 0; i < k; ++i) {
-    const double lii = W[i * k + i];
-    for (int j = tid; j <= i; j += nt) {
-      if (j == i) {
-        dX[i] = 1.0 / lii;
-      } else {
-        double s = 0.0;
-        // sum_{l=j}^{i-1} L[i][l] * X[l][j]
-        s = fma(W[i * k + j], dX[j], s);
-        for (int l = j + 1; l < i; ++l) s = fma(W[i * k + l], W[j * k + l], s);
-        W[j * k + i] = -s / lii;
-      }
+  // X = L^-1 by column sweeps: row l of X is final after scaling, then eliminated from rows below
+  for (int l = 0; l < k; ++l) {
+    const double dl = 1.0 / W[l * ld + l];
+    for (int c = tid; c <= l; c += nt) X[l * ld + c] *= dl;
+    __syncthreads();
+    for (int i = l + 1 + ty; i < k; i += 16) {
+      const double lil = W[i * ld + l];
+      for (int c = tx; c <= l; c += 16) X[i * ld + c] = fma(-lil, X[l * ld + c], X[i * ld + c]);
     }
     __syncthreads();
   }
-  for (int e = tid; e < k * k; e += nt) {
-    const int r = e / k, c = e % k;
-    if (c < r) {
-      R[e] = 0.0;
-      Rinv[e] = 0.0;
-    } else if (c == r) {
-      R[e] = W[r * k + r];
-      Rinv[e] = dX[r];
-    } else {
-      R[e] = W[c * k + r];   // L[c][r]
-      Rinv[e] = W[r * k + c];  // X[c][r]
+  for (int r = ty; r < k; r += 16)
+    for (int c = tx; c < k; c += 16) {
+      const int e = r * k + c;
+      if (c < r) {
+        R[e] = 0.0;
+        Rinv[e] = 0.0;
+      } else {
+        R[e] = W[c * ld + r];     // L[c][r]
+        Rinv[e] = X[c * ld + r];  // X[c][r]
+      }
     }
-  }
 }
 
-__global__ void chol_inv_smem_kernel(const double* G, int k, double* R, double* Rinv, int* status,
-                                     double pivot_rel) {
-  extern __shared__ __align__(16) double smem[];
-  chol_inv_body(G, k, smem, smem + k * k, R, Rinv, status, pivot_rel);
+__host__ __device__ inline size_t chol_scratch_doubles(int k) {
+  return 2 * (size_t)k * (k + 1) + (size_t)k;
 }
-__global__ void chol_inv_gmem_kernel(const double* G, int k, double* W, double* R, double* Rinv,
-                                     int* status, double pivot_rel) {
-  chol_inv_body(G, k, W, W + (size_t)k * k, R, Rinv, status, pivot_rel);
+
+__global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int k, double* R,
+                                                            double* Rinv, int* status,
+                                                            double pivot_rel) {
+  extern __shared__ __align__(16) double smem[];
+  double* W = smem;
+  double* X = W + (size_t)k * (k + 1);
+  chol_inv_body(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
+}
+__global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int k, double* ws,
+                                                            double* R, double* Rinv, int* status,
+                                                            double pivot_rel) {
+  double* W = ws;
+  double* X = W + (size_t)k * (k + 1);
+  chol_inv_body(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
 }
 
 // C = A * B for k x k upper-triangular A, B (row-major, ld k).
@@ -453,98 +494,123 @@ __global__ void precond_update_kernel(const double* __restrict__ U, int64_t ldu,
 // pairing so k/2 rotations run concurrently).  Gives ||U2 - U1 (U1^T U2)||_2^2 for the projector
 // drift (svdengine.py:217-221) from the k x k Gram of the out-of-span block.
 // ---------------------------------------------------------------------------------------------
-__device__ void jacobi_maxeig_body(const double* __restrict__ Ain, int k, double* A, int* perm,
-                                   double* out) {
-  __shared__ double s_off, s_tot;
+// Largest eigenvalue of a symmetric k x k matrix (one CTA): Householder reduction to
+// tridiagonal form, then Sturm-count multisection on the tridiagonal (every thread evaluates the
+// inertia at its own shift, 256-way per round).  Gives ||U2 - U1 (U1^T U2)||_2^2 for the
+// projector drift (svdengine.py:217-221) from the k x k Gram of the out-of-span block.
+__device__ void maxeig_body(const double* __restrict__ Ain, int k, double* A, double* vbuf,
+                            double* out) {
   __shared__ double scratch[32];
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int kk = k + (k & 1);  // pad to even with a dummy index
-  for (int e = tid; e < kk * kk; e += nt) {
-    const int r = e / kk, c = e % kk;
-    A[e] = (r < k && c < k) ? 0.5 * (Ain[r * k + c] + Ain[c * k + r]) : 0.0;
-  }
-  for (int i = tid; i < kk; i += nt) perm[i] = i;
+  const int ld = k + 1;      // odd stride: conflict-free row-parallel matvec
+  double* v = vbuf;          // [k] Householder vector
+  double* p = vbuf + k;      // [k]
+  double* dg = vbuf + 2 * k; // [k] diagonal
+  double* od = vbuf + 3 * k; // [k] off-diagonal (od[j] couples j and j+1)
+  for (int r = tid >> 4; r < k; r += 16)
+    for (int c = tid & 15; c < k; c += 16) A[r * ld + c] = 0.5 * (Ain[r * k + c] + Ain[c * k + r]);
   __syncthreads();
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int e = tid; e < kk * kk; e += nt) {
-      const int r = e / kk, c = e % kk;
-      const double v = A[e] * A[e];
-      tot += v;
-      if (r != c) off += v;
+  for (int j = 0; j + 2 < k; ++j) {
+    const int n = k - j - 1;  // length of x = A[j+1:, j]
+    double s = 0.0;
+    for (int i = tid; i < n; i += nt) {
+      const double x = A[(j + 1 + i) * ld + j];
+      s = fma(x, x, s);
     }
-    off = block_sum(off, scratch);
-    tot = block_sum(tot, scratch);
+    const double xnorm2 = block_sum(s, scratch);
+    const double x0 = A[(j + 1) * ld + j];
+    const double xn = sqrt(xnorm2);
+    const double alpha = x0 >= 0.0 ? -xn : xn;
+    // v = x - alpha e1, beta = 2 / v^T v  (v^T v = 2 xn (xn + |x0|))
+    const double vtv = 2.0 * xn * (xn + fabs(x0));
+    for (int i = tid; i < n; i += nt) v[i] = A[(j + 1 + i) * ld + j] - (i == 0 ? alpha : 0.0);
     if (tid == 0) {
-      s_off = off;
-      s_tot = tot;
+      dg[j] = A[j * ld + j];
+      od[j] = (vtv > 0.0) ? alpha : x0;
     }
     __syncthreads();
-    if (!(s_off > 1e-30 * s_tot) || s_tot == 0.0) break;
-    for (int round = 0; round < kk - 1; ++round) {
-      // pairs (perm[i], perm[kk-1-i]) for i < kk/2: compute rotation per pair then apply to rows
-      // and columns in two phases.
-      __shared__ double cs[2 * 256 + 2];
-      for (int i = tid; i < kk / 2; i += nt) {
-        int p = perm[i], q = perm[kk - 1 - i];
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        const double apq = A[p * kk + q];
-        double c = 1.0, s = 0.0;
-        if (apq != 0.0) {
-          const double app = A[p * kk + p], aqq = A[q * kk + q];
-          const double tau = (aqq - app) / (2.0 * apq);
-          const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + tt * tt);
-          s = tt * c;
-        }
-        cs[2 * i] = c;
-        cs[2 * i + 1] = s;
-      }
-      __syncthreads();
-      // rows: for each pair, rotate rows p,q across all columns
-      for (int e = tid; e < (kk / 2) * kk; e += nt) {
-        const int i = e / kk, col = e % kk;
-        int p = perm[i], q = perm[kk - 1 - i];
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        const double c = cs[2 * i], s = cs[2 * i + 1];
-        const double ap = A[p * kk + col], aq = A[q * kk + col];
-        A[p * kk + col] = c * ap - s * aq;
-        A[q * kk + col] = s * ap + c * aq;
-      }
-      __syncthreads();
-      for (int e = tid; e < (kk / 2) * kk; e += nt) {
-        const int i = e / kk, row = e % kk;
-        int p = perm[i], q = perm[kk - 1 - i];
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        const double c = cs[2 * i], s = cs[2 * i + 1];
-        const double ap = A[row * kk + p], aq = A[row * kk + q];
-        A[row * kk + p] = c * ap - s * aq;
-        A[row * kk + q] = s * ap + c * aq;
-      }
-      __syncthreads();
-      // round-robin: keep perm[0], rotate the rest
-      if (tid == 0) {
-        const int last = perm[kk - 1];
-        for (int i = kk - 1; i > 1; --i) perm[i] = perm[i - 1];
-        perm[1] = last;
-      }
-      __syncthreads();
+    if (!(vtv > 0.0)) continue;  // column already reduced
+    const double beta = 2.0 / vtv;
+    // p = beta * A' v  (A' = trailing n x n block)
+    for (int i = tid; i < n; i += nt) {
+      const double* row = A + (j + 1 + i) * ld + (j + 1);
+      double q = 0.0;
+      for (int l = 0; l < n; ++l) q = fma(row[l], v[l], q);
+      p[i] = beta * q;
     }
+    __syncthreads();
+    double t = 0.0;
+    for (int i = tid; i < n; i += nt) t = fma(v[i], p[i], t);
+    const double Kc = 0.5 * beta * block_sum(t, scratch);
+    // A' -= v w^T + w v^T,  w = p - K v   (16 x 16 thread grid, no integer division)
+    {
+      const int tx = tid & 15, ty = tid >> 4;
+      for (int r = ty; r < n; r += 16) {
+        const double vr = v[r], wr = p[r] - Kc * v[r];
+        double* Arow = A + (j + 1 + r) * ld + (j + 1);
+        for (int c = tx; c < n; c += 16) Arow[c] -= vr * (p[c] - Kc * v[c]) + wr * v[c];
+      }
+    }
+    __syncthreads();
   }
-  double mx = -1.0 / 0.0;
-  for (int i = tid; i < k; i += nt) mx = fmax(mx, A[i * kk + i]);
-  mx = block_max(mx, scratch);
-  if (tid == 0) *out = mx;
+  if (tid == 0) {
+    if (k >= 2) {
+      dg[k - 2] = A[(k - 2) * ld + (k - 2)];
+      od[k - 2] = A[(k - 1) * ld + (k - 2)];
+    }
+    dg[k - 1] = A[(k - 1) * ld + (k - 1)];
+  }
+  __syncthreads();
+  // Gershgorin bracket, then multisection on the largest eigenvalue:
+  // count(x) = #eigenvalues < x from the signs of the LDL^T pivots of T - x I.
+  __shared__ double s_lo, s_hi;
+  __shared__ int s_best;
+  if (tid == 0) {
+    double lo = 1.0 / 0.0, hi = -1.0 / 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double r = (i > 0 ? fabs(od[i - 1]) : 0.0) + (i + 1 < k ? fabs(od[i]) : 0.0);
+      lo = fmin(lo, dg[i] - r);
+      hi = fmax(hi, dg[i] + r);
+    }
+    s_lo = lo;
+    s_hi = hi;
+  }
+  __syncthreads();
+  for (int round = 0; round < 12; ++round) {
+    const double lo = s_lo, hi = s_hi;
+    if (!(hi - lo > 2e-16 * fmax(fabs(hi), fabs(lo)))) break;
+    // thread t tests x_t = lo + (t+1) (hi-lo)/(nt+1): all k eigenvalues < x_t  <=>  x_t > lambda_max
+    const double x = lo + (hi - lo) * (double)(tid + 1) / (double)(nt + 1);
+    int cnt = 0;
+    double d = 1.0;
+    for (int i = 0; i < k; ++i) {
+      const double e2 = i > 0 ? od[i - 1] * od[i - 1] : 0.0;
+      d = (dg[i] - x) - (i > 0 ? e2 / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      cnt += d < 0.0;
+    }
+    const int above = cnt == k;  // x > lambda_max
+    if (tid == 0) s_best = nt;
+    __syncthreads();
+    if (above) atomicMin(&s_best, tid);
+    __syncthreads();
+    if (tid == 0) {
+      const int b = s_best;  // first shift above lambda_max
+      const double step = (hi - lo) / (double)(nt + 1);
+      s_lo = lo + step * (double)b;
+      s_hi = (b < nt) ? lo + step * (double)(b + 1) : hi;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *out = 0.5 * (s_lo + s_hi);
 }
 
-__global__ void jacobi_maxeig_smem_kernel(const double* Ain, int k, double* out) {
+__global__ void maxeig_smem_kernel(const double* Ain, int k, double* out) {
   extern __shared__ __align__(16) double smem[];
-  const int kk = k + (k & 1);
-  jacobi_maxeig_body(Ain, k, smem, reinterpret_cast<int*>(smem + kk * kk), out);
+  maxeig_body(Ain, k, smem, smem + (size_t)k * (k + 1), out);
 }
-__global__ void jacobi_maxeig_gmem_kernel(const double* Ain, int k, double* W, double* out) {
-  extern __shared__ int perm_sm[];
-  jacobi_maxeig_body(Ain, k, W, perm_sm, out);
+__global__ void maxeig_gmem_kernel(const double* Ain, int k, double* W, double* out) {
+  maxeig_body(Ain, k, W, W + (size_t)k * (k + 1), out);
 }
 
 // ||a[:r] - b[:r]||_2 and the off-diagonal Frobenius norm of a k x k matrix (svdengine.py:216,

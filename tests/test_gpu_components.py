@@ -22,12 +22,16 @@ def H(x):
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("M,N,K", [(5, 3, 7), (37, 5, 129), (300, 64, 1000), (64, 64, 50000),
                                    (1000, 33, 77), (257, 128, 999), (96, 200, 333),
-                                   (4096, 1, 2000), (3, 3, 100000), (2000, 128, 5000)])
-@pytest.mark.parametrize("pad,acc", [(0, False), (1, True)])
-def test_gemm_matches_torch(layout, M, N, K, pad, acc):
+                                   (4096, 1, 2000), (3, 3, 100000), (2000, 128, 5000),
+                                   (20000, 64, 64), (4096, 64, 8192), (777, 256, 3000),
+                                   (3000, 32, 5000)])
+@pytest.mark.parametrize("pad,acc", [(0, False), (1, True), (2, False)])
+@pytest.mark.parametrize("path", [0, 1])
+def test_gemm_matches_torch(layout, M, N, K, pad, acc, path):
     from paper_2512_05749_b200 import _lib
 
     ctx = _lib.context()
+    ctx.lib.wssr_set_gemm_path(ctx.handle, path)
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
     opt = dict(dtype=torch.float64, device="cuda", generator=g)
     if layout == 0:
@@ -48,6 +52,7 @@ def test_gemm_matches_torch(layout, M, N, K, pad, acc):
              ldb, _lib.ptr(C), N + pad, 0.7, int(acc), 1024)
     ref = 0.7 * (X @ B[:, :N]) + (C0[:, :N] if acc else 0.0)
     err = (C[:, :N] - ref).abs().max().item() / ref.abs().max().item()
+    ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
     assert err < 1e-13
     if pad:
         assert torch.equal(C[:, N:], C0[:, N:])  # leading-dimension padding untouched

@@ -1,0 +1,63 @@
+"""k x k device routines (CholeskyQR core, largest-eigenvalue solver) against numpy."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _small(op, a):
+    from paper_2512_05749_b200 import _lib
+
+    k = a.shape[0]
+    A = torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+    o1 = torch.zeros(k, k, dtype=torch.float64, device="cuda")
+    o2 = torch.zeros(k, k, dtype=torch.float64, device="cuda")
+    st = (ctypes.c_int * 2)()
+    _lib.context().call("wssr_debug_small_f64", op, k, _lib.ptr(A), _lib.ptr(o1), _lib.ptr(o2), st)
+    return o1.cpu().numpy(), o2.cpu().numpy(), (st[0], st[1])
+
+
+@pytest.mark.parametrize("k", [1, 2, 7, 32, 64, 100, 128, 200])
+def test_cholesky_inverse(k):
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((3 * k + 5, k)) * np.exp(rng.uniform(-3, 3, k))
+    g = x.T @ x
+    r, rinv, st = _small(0, g)
+    assert st == (0, 0)
+    ref = np.linalg.cholesky(g).T
+    np.testing.assert_allclose(r, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+    np.testing.assert_allclose(rinv @ r, np.eye(k), atol=1e-10)
+    assert np.all(np.tril(rinv, -1) == 0.0) and np.all(np.tril(r, -1) == 0.0)
+
+
+def test_cholesky_flags_deficient_and_zero():
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((20, 4))
+    x[:, 2] = x[:, 0]
+    _, _, st = _small(0, x.T @ x)
+    assert st[0] == 3
+    _, _, st = _small(0, np.zeros((3, 3)))
+    assert st == (1, 1)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 17, 64, 128, 255])
+def test_maxeig(k):
+    rng = np.random.default_rng(100 + k)
+    x = rng.standard_normal((k + 3, k)) * 1e-3
+    a = x.T @ x
+    lam, _, _ = _small(1, a)
+    ref = np.linalg.eigvalsh(a)[-1]
+    assert abs(lam[0, 0] - ref) <= 1e-12 * abs(ref)
+
+
+def test_maxeig_clustered_top():
+    rng = np.random.default_rng(7)
+    q = np.linalg.qr(rng.standard_normal((64, 64)))[0]
+    ev = np.concatenate([[1.0, 1.0 - 1e-12, 1.0 - 2e-12], np.linspace(0.5, 1e-8, 61)])
+    a = (q * ev) @ q.T
+    lam, _, _ = _small(1, a)
+    assert abs(lam[0, 0] - 1.0) < 1e-13

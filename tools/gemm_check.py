@@ -90,10 +90,14 @@ def main():
         return
     worst = {}
     cases = []
+    path = int(sys.argv[sys.argv.index("--path") + 1]) if "--path" in sys.argv else 0
+    ctx.lib.wssr_set_gemm_path(ctx.handle, path)
     for layout in (0, 1):
         for (M, N, K) in [(5, 3, 7), (37, 5, 129), (128, 64, 4096), (300, 64, 1000), (64, 64, 50000),
                           (1000, 33, 77), (257, 128, 999), (96, 200, 333), (31, 256, 2048),
-                          (4096, 1, 2000), (3, 3, 100000), (2000, 128, 5000)]:
+                          (4096, 1, 2000), (3, 3, 100000), (2000, 128, 5000),
+                          (131072, 64, 64), (64, 64, 131072), (4096, 64, 8192), (8192, 64, 4096),
+                          (1000, 256, 3000), (3000, 32, 5000)]:
             for pad in (0, 1):
                 for acc in (False, True):
                     e = check(ctx, layout, M, N, K, pad=pad, acc=acc, seed=M + N + K)
