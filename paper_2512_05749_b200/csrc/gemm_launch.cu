@@ -143,16 +143,17 @@ struct TmaTile {
   }
 };
 
-using TCM32 = TmaTile<Layout::CM, 256, 32, 16, 8, 1, 3>;
-using TCM64 = TmaTile<Layout::CM, 128, 64, 16, 4, 2, 4>;
-using TCM128 = TmaTile<Layout::CM, 64, 128, 16, 2, 4, 4>;
-using TCM256 = TmaTile<Layout::CM, 32, 256, 16, 1, 8, 3>;
-using TCMsq32 = TmaTile<Layout::CM, 32, 32, 16, 1, 1, 4>;
-using TCMsq64 = TmaTile<Layout::CM, 64, 64, 16, 2, 2, 4>;
-using TRM32 = TmaTile<Layout::RM, 256, 32, 16, 8, 1, 3>;
-using TRM64 = TmaTile<Layout::RM, 128, 64, 16, 4, 2, 4>;
-using TRM128 = TmaTile<Layout::RM, 64, 128, 16, 2, 4, 4>;
-using TRM256 = TmaTile<Layout::RM, 32, 256, 16, 1, 8, 3>;
+// (BM, BN, BK, warps M x N, stages) from tools/microbench/gemm_sweep on B200
+using TCM32 = TmaTile<Layout::CM, 256, 32, 32, 8, 1, 2>;
+using TCM64 = TmaTile<Layout::CM, 128, 64, 64, 4, 2, 2>;
+using TCM128 = TmaTile<Layout::CM, 64, 128, 32, 2, 4, 3>;
+using TCM256 = TmaTile<Layout::CM, 32, 256, 32, 1, 8, 2>;
+using TCMsq32 = TmaTile<Layout::CM, 32, 32, 32, 1, 1, 4>;
+using TCMsq64 = TmaTile<Layout::CM, 64, 64, 32, 2, 2, 4>;
+using TRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2>;
+using TRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2>;
+using TRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3>;
+using TRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2>;
 
 // Config table.
 using CM32 = Tile<Layout::CM, 256, 32, 16, 8, 1, 4>;
