@@ -675,8 +675,13 @@ void assemble(Context& ctx, const double* derivs, int64_t n, int64_t p, int64_t 
   Buf m2(p, st), gsum(p, st);
   if (n > 0) {
     PhaseTimer tm(ctx, 2, 4.0 * n * p, 8.0 * n * p);
-    colstats_kernel<<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
-        derivs, n, p, ld, lraw, out->mu, m2, gsum);
+    if (ld % 2 == 0 && (reinterpret_cast<uintptr_t>(derivs) & 15) == 0) {
+      colstats_kernel<2, 8><<<(unsigned)((p + 63) / 64), 32 * kColStatsWarps, 0, st>>>(
+          derivs, n, p, ld, lraw, out->mu, m2, gsum);
+    } else {
+      colstats_kernel<1, 8><<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
+          derivs, n, p, ld, lraw, out->mu, m2, gsum);
+    }
     post_launch(ctx);
   } else {
     WSSR_CUDA(cudaMemsetAsync(out->mu, 0, sizeof(double) * p, st));

@@ -154,6 +154,9 @@ using TRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2>;
 using TRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2>;
 using TRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3>;
 using TRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2>;
+// short contractions (K <= 256: X * R^-1, X * C, w - q * quotient): small CTAs, 3-4 resident
+using TRMs64 = TmaTile<Layout::RM, 64, 64, 16, 2, 2, 4>;
+using TRMs128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 2>;
 
 // Config table.
 using CM32 = Tile<Layout::CM, 256, 32, 16, 8, 1, 4>;
@@ -277,6 +280,8 @@ cudaError_t gemm_dispatch(Context& ctx, Layout layout, const GemmArgs& args, int
       if (a.N <= 128) return run_tile<TCM128>(ctx, a, va2, vb2, max_splits, st);
       return run_tile<TCM256>(ctx, a, va2, vb2, max_splits, st);
     }
+    if (a.K <= 256 && a.N <= 64) return run_tile<TRMs64>(ctx, a, va2, vb2, max_splits, st);
+    if (a.K <= 256 && a.N <= 128) return run_tile<TRMs128>(ctx, a, va2, vb2, max_splits, st);
     if (a.N <= 32) return run_tile<TRM32>(ctx, a, va2, vb2, max_splits, st);
     if (a.N <= 64) return run_tile<TRM64>(ctx, a, va2, vb2, max_splits, st);
     if (a.N <= 128) return run_tile<TRM128>(ctx, a, va2, vb2, max_splits, st);

@@ -252,32 +252,11 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
   }
 
   // epilogue: undo the lane permutations into a shared-memory C tile (the operand ring is idle -
-  // every TMA write has been consumed), then write rows out coalesced.
+  // every TMA write has been consumed), then write rows out coalesced.  Tiles whose C block does
+  // not fit the ring store straight from registers.
   constexpr int SC = BN + 1;  // odd stride
-  static_assert((size_t)BM * SC * 8 <= (size_t)Cfg::STAGE_BYTES * STAGES, "C tile fits the ring");
-  double* sC = reinterpret_cast<double*>(smem);
-  asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");  // all consumers left the ring
   const double alpha = args.alpha;
-#pragma unroll
-  for (int i = 0; i < MS; ++i) {
-    const int ml = CM ? wm0 + 16 * (i >> 1) + 2 * fg + (i & 1) : wm0 + 8 * i + fg;
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int nl = CM ? wn0 + 16 * (j >> 1) + 2 * fperm(2 * t + e) + (j & 1)
-                          : wn0 + 16 * (j >> 1) + 2 * (2 * t + e) + (j & 1);
-        sC[ml * SC + nl] = alpha * acc[i][j][e];
-      }
-    }
-  }
-  asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");
-  const int rows = (int)min((int64_t)BM, M - m0), cols = (int)min((int64_t)BN, N - n0);
-  for (int e = tid; e < BM * BN; e += NCW * 32) {
-    const int ml = e / BN, nl = e % BN;  // BN is a power of two
-    if (ml >= rows || nl >= cols) continue;
-    const int64_t m = m0 + ml, n = n0 + nl;
-    const double val = sC[ml * SC + nl];
+  auto store = [&](int64_t m, int64_t n, double val) {
     if (args.partial) {
       args.partial[((int64_t)blockIdx.z * M + m) * N + n] = val;
     } else {
@@ -286,6 +265,45 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
         *dst = args.Cin[m * args.ldcin + n] + val;
       else
         *dst = args.accumulate ? *dst + val : val;
+    }
+  };
+  if constexpr ((size_t)BM * SC * 8 <= (size_t)Cfg::STAGE_BYTES * STAGES) {
+    double* sC = reinterpret_cast<double*>(smem);
+    asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");  // all consumers left the ring
+#pragma unroll
+    for (int i = 0; i < MS; ++i) {
+      const int ml = CM ? wm0 + 16 * (i >> 1) + 2 * fg + (i & 1) : wm0 + 8 * i + fg;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int nl = CM ? wn0 + 16 * (j >> 1) + 2 * fperm(2 * t + e) + (j & 1)
+                            : wn0 + 16 * (j >> 1) + 2 * (2 * t + e) + (j & 1);
+          sC[ml * SC + nl] = alpha * acc[i][j][e];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");
+    const int rows = (int)min((int64_t)BM, M - m0), cols = (int)min((int64_t)BN, N - n0);
+    for (int e = tid; e < BM * BN; e += NCW * 32) {
+      const int ml = e / BN, nl = e % BN;  // BN is a power of two
+      if (ml >= rows || nl >= cols) continue;
+      store(m0 + ml, n0 + nl, sC[ml * SC + nl]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < MS; ++i) {
+      const int64_t m = CM ? m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1) : m0 + wm0 + 8 * i + fg;
+      if (m >= M) continue;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t n = CM ? n0 + wn0 + 16 * (j >> 1) + 2 * fperm(2 * t + e) + (j & 1)
+                               : n0 + wn0 + 16 * (j >> 1) + 2 * (2 * t + e) + (j & 1);
+          if (n < N) store(m, n, alpha * acc[i][j][e]);
+        }
+      }
     }
   }
 }

@@ -59,69 +59,102 @@ __global__ void energy_stats_kernel(const double* __restrict__ E, int64_t n, dou
 // ---------------------------------------------------------------------------------------------
 constexpr int kColStatsWarps = 8;
 
-__global__ void __launch_bounds__(32 * kColStatsWarps)
+// VEC columns per lane (VEC = 2: 16-byte loads, a warp streams 512 contiguous bytes per row);
+// UNROLL rows in flight per lane so each SM keeps >= 64 KB of loads outstanding.
+template <int VEC, int UNROLL>
+__global__ void __launch_bounds__(32 * kColStatsWarps, 3)
     colstats_kernel(const double* __restrict__ O, int64_t n, int64_t p, int64_t ld,
                     const double* __restrict__ lraw, double* __restrict__ mu,
                     double* __restrict__ m2, double* __restrict__ gsum) {
-  __shared__ double sh[kColStatsWarps][5][32];
+  __shared__ double sh[kColStatsWarps][5][32 * VEC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t col = (int64_t)blockIdx.x * 32 + lane;
-  const bool active = col < p;
+  const int64_t col0 = (int64_t)blockIdx.x * (32 * VEC) + (int64_t)lane * VEC;
+  bool act[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) act[v] = col0 + v < p;
   const int64_t rows_per = (n + kColStatsWarps - 1) / kColStatsWarps;
   const int64_t r0 = min(n, (int64_t)w * rows_per), r1 = min(n, r0 + rows_per);
-  double K = 0.0, s1 = 0.0, s2 = 0.0, sl = 0.0, lsum = 0.0;
-  if (r1 > r0) {
-    if (active) K = O[r0 * ld + col];
-    const double* src = O + col;
-    int64_t r = r0;
-    for (; r + 4 <= r1; r += 4) {
-      double x[4], l[4];
+  double K[VEC], s1[VEC], s2[VEC], sl[VEC];
+  double lsum = 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        x[u] = active ? __ldg(src + (r + u) * ld) : 0.0;
+  for (int v = 0; v < VEC; ++v) K[v] = s1[v] = s2[v] = sl[v] = 0.0;
+  auto load = [&](int64_t r, double (&x)[VEC]) {
+    if (VEC == 2 && act[1]) {
+      const double2 y = __ldg(reinterpret_cast<const double2*>(O + r * ld + col0));
+      x[0] = y.x;
+      x[VEC - 1] = y.y;
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) x[v] = act[v] ? __ldg(O + r * ld + col0 + v) : 0.0;
+    }
+  };
+  if (r1 > r0) {
+    double x0[VEC];
+    load(r0, x0);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) K[v] = act[v] ? x0[v] : 0.0;
+    int64_t r = r0;
+    for (; r + UNROLL <= r1; r += UNROLL) {
+      double x[UNROLL][VEC], l[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        load(r + u, x[u]);
         l[u] = __ldg(lraw + r + u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double d = active ? x[u] - K : 0.0;
-        s1 += d;
-        s2 = fma(d, d, s2);
-        sl = fma(d, l[u], sl);
+      for (int u = 0; u < UNROLL; ++u) {
         lsum += l[u];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const double d = act[v] ? x[u][v] - K[v] : 0.0;
+          s1[v] += d;
+          s2[v] = fma(d, d, s2[v]);
+          sl[v] = fma(d, l[u], sl[v]);
+        }
       }
     }
     for (; r < r1; ++r) {
-      const double x = active ? __ldg(src + r * ld) : 0.0;
+      double x[VEC];
+      load(r, x);
       const double l = __ldg(lraw + r);
-      const double d = active ? x - K : 0.0;
-      s1 += d;
-      s2 = fma(d, d, s2);
-      sl = fma(d, l, sl);
       lsum += l;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const double d = act[v] ? x[v] - K[v] : 0.0;
+        s1[v] += d;
+        s2[v] = fma(d, d, s2[v]);
+        sl[v] = fma(d, l, sl[v]);
+      }
     }
   }
   const double cnt = (double)(r1 - r0);
-  double mean = 0.0, M2 = 0.0, G = 0.0;
-  if (cnt > 0) {
-    const double dm = s1 / cnt;
-    mean = K + dm;
-    M2 = fmax(s2 - s1 * dm, 0.0);
-    G = sl - dm * lsum;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    double mean = 0.0, M2 = 0.0, G = 0.0;
+    if (cnt > 0) {
+      const double dm = s1[v] / cnt;
+      mean = K[v] + dm;
+      M2 = fmax(s2[v] - s1[v] * dm, 0.0);
+      G = sl[v] - dm * lsum;
+    }
+    const int c = lane * VEC + v;
+    sh[w][0][c] = cnt;
+    sh[w][1][c] = mean;
+    sh[w][2][c] = M2;
+    sh[w][3][c] = G;
+    sh[w][4][c] = lsum;
   }
-  sh[w][0][lane] = cnt;
-  sh[w][1][lane] = mean;
-  sh[w][2][lane] = M2;
-  sh[w][3][lane] = G;
-  sh[w][4][lane] = lsum;
   __syncthreads();
-  if (w == 0) {
-    double na = sh[0][0][lane], ma = sh[0][1][lane], Ma = sh[0][2][lane], Ga = sh[0][3][lane],
-           La = sh[0][4][lane];
-    for (int c = 1; c < kColStatsWarps; ++c) {
-      const double nb = sh[c][0][lane];
+  // Chan merge of the row chunks, fixed order, one thread per column
+  for (int c = threadIdx.x; c < 32 * VEC; c += blockDim.x) {
+    const int64_t col = (int64_t)blockIdx.x * (32 * VEC) + c;
+    if (col >= p) continue;
+    double na = sh[0][0][c], ma = sh[0][1][c], Ma = sh[0][2][c], Ga = sh[0][3][c],
+           La = sh[0][4][c];
+    for (int q = 1; q < kColStatsWarps; ++q) {
+      const double nb = sh[q][0][c];
       if (nb == 0) continue;
-      const double mb = sh[c][1][lane], Mb = sh[c][2][lane], Gb = sh[c][3][lane],
-                   Lb = sh[c][4][lane];
+      const double mb = sh[q][1][c], Mb = sh[q][2][c], Gb = sh[q][3][c], Lb = sh[q][4][c];
       if (na == 0) {
         na = nb; ma = mb; Ma = Mb; Ga = Gb; La = Lb;
         continue;
@@ -135,11 +168,9 @@ __global__ void __launch_bounds__(32 * kColStatsWarps)
       ma = mnew;
       na = nn;
     }
-    if (active) {
-      mu[col] = ma;
-      m2[col] = Ma;
-      gsum[col] = Ga;
-    }
+    mu[col] = ma;
+    m2[col] = Ma;
+    gsum[col] = Ga;
   }
 }
 
@@ -256,11 +287,12 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
       X[r * ld + c] = (r == c) ? 1.0 : 0.0;
     }
   for (int j = tid; j < k; j += nt) dorig[j] = G[j * k + j];
-  if (tid == 0) {
+  __syncthreads();
+  if (tid == 0) {  // from shared memory: a serial loop over global loads would cost ~k x 600 cycles
     double gm = 0.0, tr = 0.0;
     for (int j = 0; j < k; ++j) {
-      gm = fmax(gm, G[j * k + j]);
-      tr += G[j * k + j];
+      gm = fmax(gm, dorig[j]);
+      tr += dorig[j];
     }
     s_gmax = gm;
     s_trace = tr;
@@ -276,39 +308,50 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     }
     return;
   }
-  for (int j = 0; j < k; ++j) {
-    const double piv = W[j * ld + j];
-    // scale-invariant pivot test (Schur complement vs the column's own norm) + the reference's
-    // deficiency rule; every thread evaluates it on the same value, so the branch is uniform
-    if (!(piv > pivot_rel * dorig[j]) || !(piv > deficient_sq)) {
-      if (tid == 0) s_fail = j + 1;
-      break;
+  // Fused sweep, two barriers per column j:
+  //   A: scale column j of L by 1/sqrt(pivot) and row j of X = L^-1 by the same factor;
+  //   B: rank-1 trailing update of W (columns j < c <= i) and elimination of X (columns c <= j).
+  // The thread that produces W[j+1][j+1] in phase B checks the next pivot and precomputes its
+  // square root and inverse, so no thread waits on sqrt/div at the top of a step.
+  __shared__ double s_sq, s_inv;
+  auto pivot = [&](int j, double d) {
+    if (!(d > pivot_rel * dorig[j]) || !(d > deficient_sq)) {
+      s_fail = j + 1;
+    } else {
+      const double sq = sqrt(d);
+      s_sq = sq;
+      s_inv = 1.0 / sq;
     }
-    const double sq = sqrt(piv), invs = 1.0 / sq;
-    for (int i = j + 1 + tid; i < k; i += nt) W[i * ld + j] *= invs;
+  };
+  if (tid == 0) pivot(0, W[0]);
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (s_fail) break;
+    const double inv = s_inv;
+    for (int i = j + 1 + tid; i < k; i += nt) W[i * ld + j] *= inv;
+    for (int c = tid; c <= j; c += nt) X[j * ld + c] *= inv;
+    if (tid == 0) W[j * ld + j] = s_sq;
     __syncthreads();
-    if (tid == 0) W[j * ld + j] = sq;
-    // trailing update of the lower triangle: W[i][c] -= L[i][j] L[c][j], j < c <= i
     for (int i = j + 1 + ty; i < k; i += 16) {
       const double lij = W[i * ld + j];
-      for (int c = j + 1 + tx; c <= i; c += 16) W[i * ld + c] = fma(-lij, W[c * ld + j], W[i * ld + c]);
+      double* wi = W + i * ld;
+      double* xi = X + i * ld;
+      const double* xj = X + j * ld;
+      for (int c = tx; c <= i; c += 16) {
+        if (c <= j) {
+          xi[c] = fma(-lij, xj[c], xi[c]);
+        } else {
+          const double nv = fma(-lij, W[c * ld + j], wi[c]);
+          wi[c] = nv;
+          if (c == j + 1 && i == j + 1) pivot(j + 1, nv);
+        }
+      }
     }
     __syncthreads();
   }
   if (s_fail) {
     if (tid == 0) atomicCAS(status, 0, s_fail);
     return;
-  }
-  // X = L^-1 by column sweeps: row l of X is final after scaling, then eliminated from rows below
-  for (int l = 0; l < k; ++l) {
-    const double dl = 1.0 / W[l * ld + l];
-    for (int c = tid; c <= l; c += nt) X[l * ld + c] *= dl;
-    __syncthreads();
-    for (int i = l + 1 + ty; i < k; i += 16) {
-      const double lil = W[i * ld + l];
-      for (int c = tx; c <= l; c += 16) X[i * ld + c] = fma(-lil, X[l * ld + c], X[i * ld + c]);
-    }
-    __syncthreads();
   }
   for (int r = ty; r < k; r += 16)
     for (int c = tx; c < k; c += 16) {

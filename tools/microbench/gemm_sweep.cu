@@ -121,35 +121,23 @@ int main() {
   fill<<<1024, 256>>>(A, big, 1.1); fill<<<1024, 256>>>(B, 1 << 24, 0.7); fill<<<1024, 256>>>(sh0, 1 << 22, 0.3);
   cudaDeviceSynchronize();
   {
-    int64_t M = 4096, N = 64, K = 131072; double* sh = sh0;
-    RUNTRM(128, 64, 16, 4, 2, 4); RUNTRM(128, 64, 16, 4, 2, 6); RUNTRM(128, 64, 32, 4, 2, 3);
-    RUNTRM(128, 64, 32, 4, 2, 4); RUNTRM(256, 64, 16, 8, 2, 3); RUNTRM(256, 64, 16, 4, 2, 4);
-    RUNTRM(128, 64, 16, 2, 2, 6); RUNTRM(64, 64, 32, 2, 2, 4); RUNTRM(128, 64, 64, 4, 2, 2);
+    int64_t M = 131072, N = 64, K = 64; double* sh = nullptr;  // TRMM
+    RUNTRM(128, 64, 64, 4, 2, 1); RUNTRM(64, 64, 64, 2, 2, 1); RUNTRM(64, 64, 32, 2, 2, 2);
+    RUNTRM(32, 64, 64, 1, 2, 1); RUNTRM(64, 64, 16, 2, 2, 4); RUNTRM(128, 64, 32, 4, 2, 2);
   }
   {
-    int64_t M = 131072, N = 64, K = 4096; double* sh = sh0;
-    RUNTCM(128, 64, 16, 4, 2, 4); RUNTCM(128, 64, 16, 4, 2, 6); RUNTCM(128, 64, 32, 4, 2, 3);
-    RUNTCM(128, 64, 32, 4, 2, 4); RUNTCM(256, 64, 16, 8, 2, 3); RUNTCM(256, 64, 16, 4, 2, 4);
-    RUNTCM(128, 64, 16, 2, 2, 6); RUNTCM(64, 64, 32, 2, 2, 4); RUNTCM(128, 64, 64, 4, 2, 2);
-  }
-  {
-    int64_t M = 16384, N = 128, K = 65536; double* sh = sh0;
-    RUNTRM(64, 128, 16, 2, 4, 4); RUNTRM(128, 128, 16, 4, 4, 3); RUNTRM(128, 128, 16, 2, 4, 4);
-    RUNTRM(64, 128, 32, 2, 4, 3); RUNTRM(128, 128, 32, 4, 4, 2);
-  }
-  {
-    int64_t M = 65536, N = 128, K = 16384; double* sh = sh0;
-    RUNTCM(64, 128, 16, 2, 4, 4); RUNTCM(128, 128, 16, 4, 4, 3); RUNTCM(128, 128, 16, 2, 4, 4);
-    RUNTCM(64, 128, 32, 2, 4, 3); RUNTCM(128, 128, 32, 4, 4, 2);
+    int64_t M = 1048576, N = 128, K = 128; double* sh = nullptr;  // TRMM c2
+    RUNTRM(64, 128, 32, 2, 4, 2); RUNTRM(64, 128, 64, 2, 4, 2); RUNTRM(32, 128, 64, 1, 4, 2);
+    RUNTRM(64, 128, 128, 2, 4, 1);
   }
   {
     int64_t M = 64, N = 64, K = 131072; double* sh = nullptr;  // Gram
-    RUNTCM(64, 64, 16, 2, 2, 4); RUNTCM(64, 64, 32, 2, 2, 4); RUNTCM(64, 64, 64, 2, 2, 3);
+    RUNTCM(64, 64, 32, 2, 2, 4); RUNTCM(64, 64, 64, 2, 2, 2); RUNTCM(64, 64, 32, 2, 2, 2);
+    RUNTCM(64, 64, 64, 2, 2, 3); RUNTCM(64, 64, 16, 2, 2, 6);
   }
   {
-    int64_t M = 131072, N = 64, K = 64; double* sh = nullptr;  // TRMM
-    RUNTRM(128, 64, 16, 4, 2, 4); RUNTRM(128, 64, 32, 4, 2, 2); RUNTRM(64, 64, 32, 2, 2, 2);
-    RUNTRM(128, 64, 64, 4, 2, 1); RUNTRM(64, 64, 64, 2, 2, 1);
+    int64_t M = 128, N = 128, K = 1048576; double* sh = nullptr;  // Gram c2
+    RUNTCM(64, 128, 32, 2, 4, 3); RUNTCM(128, 128, 32, 4, 4, 2); RUNTCM(64, 128, 64, 2, 4, 2);
   }
   printf("done %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
