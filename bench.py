@@ -179,7 +179,7 @@ def workload_config(cfg, args):
         "report_final_residual": not args.fast_report,
         "parallelism": f"rows x{args.gpus}",
         "l2": "inputs larger than L2 (O = %.2f GB vs 126 MB); no flush" % (
-            cfg["N"] * cfg["P"] * 8 / 1e9),
+            cfg["N"] * cfg["P"] * (4 if cfg["dtype"] == "f32" else 8) / 1e9),
     }
 
 
@@ -199,8 +199,11 @@ def run_ours(args, rank, world, local_rank):
     ctx = _lib.context(local_rank)
     if world > 1:
         distributed.attach_nccl(ctx)
+    f32 = cfg["dtype"] == "f32"
+    esize = 4 if f32 else 8
     wl = synthetic.DeviceWorkload(N, P, k, cfg["L"], cfg["alpha"], cfg["drift"], seed=101,
-                                  row0=row0, rows=rows, device=dev)
+                                  row0=row0, rows=rows, device=dev,
+                                  dtype=torch.float32 if f32 else torch.float64)
     v0 = linalg.qr_orthonormalize(wl.v0_raw())[0]
     state = optimizers.WssrState(obar=torch.zeros(0, P, dtype=torch.float64, device=dev).t(),
                                  lbar=torch.zeros(0, dtype=torch.float64, device=dev),
@@ -265,7 +268,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     m_avg = sum(iters) / len(iters)
     flops_alg = 2 * m_avg * 2.0 * N * P * k
-    bytes_alg = (1 + 2 * m_avg) * N * P * 8.0
+    bytes_alg = (1 + 2 * m_avg) * N * P * float(esize)
     traffic = None
     if os.path.exists(NCU_SUMMARY):
         try:
@@ -306,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         e2e_steps = max(1, min(args.steps, 5))
-        O_h = torch.empty(rows, P, dtype=torch.float64, pin_memory=True)
+        O_h = torch.empty(rows, P, dtype=wl.O.dtype, pin_memory=True)
         E_h = torch.empty(rows, dtype=torch.float64, pin_memory=True)
         theta_h = torch.zeros(P, dtype=torch.float64, pin_memory=True)
         out_h = torch.empty(P, dtype=torch.float64, pin_memory=True)
@@ -333,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": e2e_steps / (float(t.item()) / 1e3), "unit": "steps/s",
-               "h2d_bytes_per_step": rows * P * 8 + rows * 8 + P * 8,
+               "h2d_bytes_per_step": rows * P * esize + rows * 8 + P * 8,
                "d2h_bytes_per_step": P * 8, "steps": e2e_steps,
                "path": "estimators.assemble + optimizers.wssr_step on tensors copied from pinned "
                        "host memory each step; theta' read back to the host"}
@@ -350,7 +353,8 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 storage, f64 arithmetic" if f32 else "f64",
             "data": "synthetic (seeded device generator, SURVEY.md 8(d) shapes/distributions)",
             "config": workload_config(cfg, args),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

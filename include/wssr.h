@@ -76,6 +76,9 @@ typedef struct wssr_ohat_f64 {
   const double* mu;
   double samples_scale;
   double samples_fro2;
+  int64_t samples_f32; /* 1: `samples` points to float32 data (FP32 variant, BASELINE configs[3]);
+                          the library widens it to FP64 in registers. Requires ld % 4 == 0,
+                          16-byte alignment, mu and samples_fro2 (i.e. an assembled bundle). */
 } wssr_ohat_f64;
 
 /* --- context ------------------------------------------------------------------------------ */
@@ -116,6 +119,10 @@ typedef struct wssr_assemble_out {
   int64_t n_global;
 } wssr_assemble_out;
 int wssr_assemble_f64(wssr_ctx* ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
+                      const double* energies, double clip_n_std, wssr_assemble_out* out);
+
+/* FP32 variant of wssr_assemble_f64: float32 derivs, FP64 statistics and outputs */
+int wssr_assemble_f32(wssr_ctx* ctx, const float* derivs, int64_t n, int64_t p, int64_t ld,
                       const double* energies, double clip_n_std, wssr_assemble_out* out);
 
 /* --- linalg.qr_orthonormalize (linalg.py:29-61) ------------------------------------------- */
@@ -189,6 +196,11 @@ int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
  * op 1: largest eigenvalue of symmetric `in`, out1[0] = lambda_max. */
 int wssr_debug_small_f64(wssr_ctx* ctx, int op, int k, const double* in, double* out1,
                          double* out2, int* status);
+
+/* diagnostics: the FP32-operand GEMM (A float32, widened to FP64; layouts as wssr_gemm_f64) */
+int wssr_debug_gemm_f32a(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k,
+                         const float* a, int64_t lda, const double* shift, const double* b,
+                         int64_t ldb, double* c, int64_t ldc, double alpha);
 
 /* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
 int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,

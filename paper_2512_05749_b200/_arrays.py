@@ -29,6 +29,13 @@ def to_tensor(x, dtype=torch.float64, dev=None) -> torch.Tensor:
     return torch.as_tensor(np.asarray(x, dtype=np.float64), dtype=dtype).to(dev)
 
 
+def to_tensor_f64_or_f32(x, dev=None) -> torch.Tensor:
+    """Like to_tensor, but float32 data stays float32 (the FP32 variant streams O as float32)."""
+    is_f32 = (isinstance(x, torch.Tensor) and x.dtype == torch.float32) or \
+        (isinstance(x, np.ndarray) and x.dtype == np.float32)
+    return to_tensor(x, dtype=torch.float32 if is_f32 else torch.float64, dev=dev)
+
+
 def rows_view(x: torch.Tensor) -> torch.Tensor:
     """2-D tensor with unit column stride (row-major with a leading dimension)."""
     if x.dim() != 2:

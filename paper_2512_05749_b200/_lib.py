@@ -31,7 +31,7 @@ class OhatF64(ctypes.Structure):
         ("n_params", _i64),
         ("hist", _vp), ("hist_rank", _i64), ("hist_ld", _i64), ("hist_scale", _dbl),
         ("samples", _vp), ("n_samples", _i64), ("samples_ld", _i64), ("mu", _vp),
-        ("samples_scale", _dbl), ("samples_fro2", _dbl),
+        ("samples_scale", _dbl), ("samples_fro2", _dbl), ("samples_f32", _i64),
     ]
 
 
@@ -90,6 +90,8 @@ SIGNATURES = {
     "wssr_nccl_attach": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
     "wssr_assemble_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _dbl,
                                          ctypes.POINTER(AssembleOut)]),
+    "wssr_assemble_f32": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _dbl,
+                                         ctypes.POINTER(AssembleOut)]),
     "wssr_qr_f64": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     "wssr_ssi_svd_f64": (ctypes.c_int, [_vp, ctypes.POINTER(OhatF64), _i64, _i64, _vp, _i64,
                                         _dbl, _i64, ctypes.POINTER(SsiOut)]),
@@ -99,6 +101,8 @@ SIGNATURES = {
     "wssr_step_f64": (ctypes.c_int, [_vp, ctypes.POINTER(StepIn), ctypes.POINTER(StepOut)]),
     "wssr_debug_small_f64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp,
                                             ctypes.POINTER(ctypes.c_int)]),
+    "wssr_debug_gemm_f32a": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp,
+                                            _vp, _i64, _vp, _i64, _dbl]),
     "wssr_gemm_f64": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _vp,
                                      _i64, _vp, _i64, _dbl, ctypes.c_int, ctypes.c_int]),
 }

@@ -386,8 +386,22 @@ struct Ohat {
   int64_t n = 0, lds = 0;
   const double* mu = nullptr;
   double ss = 1.0;
+  bool f32 = false;  // samples stored as float32 (BASELINE configs[3])
   int64_t cols() const { return r + n; }
 };
+
+// O-pass GEMMs over the sample block in its storage type
+void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t N, int64_t K,
+                  const double* B, int64_t ldb, double* C, int64_t ldc, double alpha) {
+  GemmArgs a{o.samp, o.lds, B, ldb, o.mu, C, ldc, M, N, K, 0, alpha, 0, nullptr, nullptr, 0};
+  if (o.f32) {
+    if (!gemm_f32_supported(layout, a))
+      throw Fail{WSSR_ERR_UNSUPPORTED, "fp32 samples need 16-byte aligned rows (ld % 4 == 0)"};
+    WSSR_CUDA(gemm_f32a(ctx, layout, a, 1024, ctx.stream));
+  } else {
+    WSSR_CUDA(gemm(ctx, layout, a, 1024, ctx.stream));
+  }
+}
 
 // v (cols x k, ldv) = Ohat^T q   (svdengine.py:133)
 void apply_OT(Context& ctx, const Ohat& o, const double* q, int64_t ldq, int64_t k, double* v,
@@ -401,8 +415,8 @@ void apply_OT(Context& ctx, const Ohat& o, const double* q, int64_t ldq, int64_t
     }
   }
   if (o.n > 0) {
-    PhaseTimer tm(ctx, 0, 2.0 * o.n * o.P * k, 8.0 * o.n * o.P);
-    gemm_rm(ctx, o.n, k, o.P, o.samp, o.lds, o.mu, q, ldq, v + o.r * ldv, ldv, o.ss, false);
+    PhaseTimer tm(ctx, 0, 2.0 * o.n * o.P * k, (o.f32 ? 4.0 : 8.0) * o.n * o.P);
+    gemm_samples(ctx, Layout::RM, o, o.n, k, o.P, q, ldq, v + o.r * ldv, ldv, o.ss);
   }
 }
 
@@ -410,8 +424,8 @@ void apply_OT(Context& ctx, const Ohat& o, const double* q, int64_t ldq, int64_t
 void apply_O(Context& ctx, const Ohat& o, const double* v, int64_t ldv, int64_t k, double* u,
              int64_t ldu) {
   if (o.n > 0) {
-    PhaseTimer tm(ctx, 1, 2.0 * o.n * o.P * k, 8.0 * o.n * o.P);
-    gemm_cm(ctx, o.P, k, o.n, o.samp, o.lds, o.mu, v + o.r * ldv, ldv, u, ldu, o.ss, false);
+    PhaseTimer tm(ctx, 1, 2.0 * o.n * o.P * k, (o.f32 ? 4.0 : 8.0) * o.n * o.P);
+    gemm_samples(ctx, Layout::CM, o, o.P, k, o.n, v + o.r * ldv, ldv, u, ldu, o.ss);
   } else {
     WSSR_CUDA(cudaMemset2DAsync(u, sizeof(double) * ldu, 0, sizeof(double) * k, o.P, ctx.stream));
   }
@@ -436,7 +450,8 @@ double ohat_fro2(Context& ctx, const Ohat& o, double samples_fro2, bool hist_own
     if (samples_fro2 >= 0.0) {
       total += samples_fro2;
     } else {
-      if (o.mu) throw Fail{WSSR_ERR_VALUE, "samples_fro2 required for a centred block"};
+      if (o.mu || o.f32)
+        throw Fail{WSSR_ERR_VALUE, "samples_fro2 required for a centred or fp32 block"};
       sumsq_matrix(ctx, o.samp, o.n, o.P, o.lds, s, o.ss * o.ss);
       allreduce(ctx, s, 1);
       total += read_scalar(ctx, s);
@@ -626,7 +641,8 @@ __global__ void scale_kernel(int64_t n, double a, const double* x, double* y) {
     y[i] = a * x[i];
 }
 
-void assemble(Context& ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
+template <typename T>
+void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
               const double* energies, double n_std, wssr_assemble_out* out) {
   cudaStream_t st = ctx.stream;
   const bool dist = ctx.world() > 1;
@@ -674,12 +690,16 @@ void assemble(Context& ctx, const double* derivs, int64_t n, int64_t p, int64_t 
   // one pass over O: column means, centred second moments, centred gradient sums
   Buf m2(p, st), gsum(p, st);
   if (n > 0) {
-    PhaseTimer tm(ctx, 2, 4.0 * n * p, 8.0 * n * p);
-    if (ld % 2 == 0 && (reinterpret_cast<uintptr_t>(derivs) & 15) == 0) {
-      colstats_kernel<2, 8><<<(unsigned)((p + 63) / 64), 32 * kColStatsWarps, 0, st>>>(
+    PhaseTimer tm(ctx, 2, 4.0 * n * p, (double)sizeof(T) * n * p);
+    const bool al16 = (reinterpret_cast<uintptr_t>(derivs) & 15) == 0;
+    if (sizeof(T) == 8 && ld % 2 == 0 && al16) {
+      colstats_kernel<T, 2, 8><<<(unsigned)((p + 63) / 64), 32 * kColStatsWarps, 0, st>>>(
+          derivs, n, p, ld, lraw, out->mu, m2, gsum);
+    } else if (sizeof(T) == 4 && ld % 4 == 0 && al16) {
+      colstats_kernel<T, 4, 8><<<(unsigned)((p + 127) / 128), 32 * kColStatsWarps, 0, st>>>(
           derivs, n, p, ld, lraw, out->mu, m2, gsum);
     } else {
-      colstats_kernel<1, 8><<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
+      colstats_kernel<T, 1, 8><<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
           derivs, n, p, ld, lraw, out->mu, m2, gsum);
     }
     post_launch(ctx);
@@ -752,6 +772,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   o.lds = oh.samples_ld;
   o.mu = oh.mu;
   o.ss = sq_new * oh.samples_scale;
+  o.f32 = oh.samples_f32 != 0;
   const int64_t cols = o.cols();
   if (k < 1) throw Fail{WSSR_ERR_RANK_TOO_LARGE, "rank must be at least 1"};
 
@@ -787,6 +808,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
         P, 0.5 * sq_new * sq_new, in->gradient, gbar);
     post_launch(ctx);
   } else {
+    if (o.f32) throw Fail{WSSR_ERR_UNSUPPORTED, "fp32 samples need the assembled gradient"};
     if (o.n > 0) {
       gemm_cm(ctx, P, 1, o.n, o.samp, o.lds, o.mu, in->l_vector, 1, gbar, 1, o.ss * sq_new, false);
     } else {
@@ -1060,6 +1082,14 @@ int wssr_assemble_f64(wssr_ctx* ctx, const double* derivs, int64_t n, int64_t p,
   });
 }
 
+int wssr_assemble_f32(wssr_ctx* ctx, const float* derivs, int64_t n, int64_t p, int64_t ld,
+                      const double* energies, double clip_n_std, wssr_assemble_out* out) {
+  return guarded(ctx, [&] {
+    if (!out || p < 1 || n < 0 || ld < p) throw Fail{WSSR_ERR_VALUE, "bad assemble arguments"};
+    assemble(ctx->c, derivs, n, p, ld, energies, clip_n_std, out);
+  });
+}
+
 int wssr_qr_f64(wssr_ctx* ctx, int64_t rows, int64_t cols, const double* a, int64_t lda,
                 double* q, int64_t ldq, double* r, int64_t flags) {
   return guarded(ctx, [&] {
@@ -1091,6 +1121,7 @@ int wssr_ssi_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, int64_t rank, int
     o.lds = ohat->samples_ld;
     o.mu = ohat->mu;
     o.ss = ohat->samples_scale;
+    o.f32 = ohat->samples_f32 != 0;
     if (max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
     const double fro2 = ohat_fro2(c, o, ohat->samples_fro2, true);
     if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
@@ -1141,6 +1172,18 @@ int wssr_debug_small_f64(wssr_ctx* ctx, int op, int k, const double* in, double*
       throw Fail{WSSR_ERR_VALUE, "unknown op"};
     }
     sync(c);
+  });
+}
+
+int wssr_debug_gemm_f32a(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k,
+                         const float* a, int64_t lda, const double* shift, const double* b,
+                         int64_t ldb, double* c, int64_t ldc, double alpha) {
+  return guarded(ctx, [&] {
+    GemmArgs g{reinterpret_cast<const double*>(a), lda, b, ldb, shift, c, ldc, m, n, k, 0, alpha,
+               0, nullptr, nullptr, 0};
+    const Layout L = layout == 0 ? Layout::CM : Layout::RM;
+    if (!gemm_f32_supported(L, g)) throw Fail{WSSR_ERR_UNSUPPORTED, "operands not TMA-aligned"};
+    WSSR_CUDA(gemm_f32a(ctx->c, L, g, 1024, ctx->c.stream));
   });
 }
 

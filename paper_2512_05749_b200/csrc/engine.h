@@ -61,6 +61,10 @@ struct Context {
 
 cudaError_t gemm(Context& ctx, Layout layout, const GemmArgs& args, int max_splits,
                  cudaStream_t st);
+// A operand stored as float32 (O of the FP32 variant)
+bool gemm_f32_supported(Layout layout, const GemmArgs& args);
+cudaError_t gemm_f32a(Context& ctx, Layout layout, const GemmArgs& args, int max_splits,
+                      cudaStream_t st);
 
 // Status codes mirror include/wssr.h.
 struct Error {

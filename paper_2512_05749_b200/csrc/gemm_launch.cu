@@ -75,15 +75,16 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
 
 // 2-D map over a row-major (outer x inner) FP64 array with row pitch `pitch` elements;
 // box = 16 doubles (128 B, SWIZZLE_128B) x box_outer rows.
-bool make_map_2d(CUtensorMap* map, const double* ptr, int64_t inner, int64_t outer, int64_t pitch,
-                 int box_outer) {
+bool make_map_2d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch,
+                 int box_outer, int esize = 8) {
   auto fn = tma_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(pitch * 8, 16)};
-  cuuint32_t box[2] = {16u, (cuuint32_t)box_outer};
+  cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(pitch * esize, 16)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esize), (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1u, 1u};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+  return fn(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+            const_cast<void*>(ptr), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -99,12 +100,12 @@ bool make_map_1d(CUtensorMap* map, const double* ptr, int64_t n, int box) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST>
+template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST, typename TA = double>
 struct TmaTile {
   static constexpr int kBM = BM, kBN = BN, kBK = BK;
-  using Cfg = TmaCfg<L, BM, BN, BK, WMW, WNW, ST>;
+  using Cfg = TmaCfg<L, BM, BN, BK, WMW, WNW, ST, TA>;
   static cudaError_t launch(const GemmArgs& a, int splits, bool, bool, cudaStream_t st) {
-    auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST>;
+    auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA>;
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -116,9 +117,9 @@ struct TmaTile {
     std::memset(&tS, 0, sizeof(tS));
     bool ok;
     if (L == Layout::CM)
-      ok = make_map_2d(&tA, a.A, a.M, a.K, a.lda, BK);
+      ok = make_map_2d(&tA, a.A, a.M, a.K, a.lda, BK, (int)sizeof(TA));
     else
-      ok = make_map_2d(&tA, a.A, a.K, a.M, a.lda, BM);
+      ok = make_map_2d(&tA, a.A, a.K, a.M, a.lda, BM, (int)sizeof(TA));
     ok = ok && make_map_2d(&tB, a.B, a.N, a.K, a.ldb, BK);
     if (L == Layout::RM && a.shift) ok = ok && make_map_1d(&tS, a.shift, a.K, BK);
     if (!ok) return cudaErrorInvalidValue;
@@ -130,7 +131,7 @@ struct TmaTile {
   static int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-      auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST>;
+      auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)Cfg::kSmemBytes);
       int o = 0;
@@ -154,6 +155,16 @@ using TRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2>;
 using TRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2>;
 using TRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3>;
 using TRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2>;
+// FP32 A operand (O stored as float32, BASELINE configs[3]); widened to FP64 in registers
+using FCM32 = TmaTile<Layout::CM, 256, 32, 32, 8, 1, 2, float>;
+using FCM64 = TmaTile<Layout::CM, 128, 64, 64, 4, 2, 2, float>;
+using FCM128 = TmaTile<Layout::CM, 64, 128, 32, 2, 4, 3, float>;
+using FCM256 = TmaTile<Layout::CM, 32, 256, 32, 1, 8, 2, float>;
+using FRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2, float>;
+using FRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2, float>;
+using FRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3, float>;
+using FRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2, float>;
+
 // short contractions (K <= 256: X * R^-1, X * C, w - q * quotient): small CTAs, 3-4 resident
 using TRMs64 = TmaTile<Layout::RM, 64, 64, 16, 2, 2, 4>;
 using TRMs128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 2>;
@@ -242,6 +253,38 @@ cudaError_t run_tile(Context& ctx, GemmArgs a, bool va2, bool vb2, int max_split
 
 cudaError_t gemm_dispatch(Context& ctx, Layout layout, const GemmArgs& args, int max_splits,
                           cudaStream_t st);
+
+bool gemm_f32_supported(Layout layout, const GemmArgs& a) {
+  (void)layout;
+  return tma_encode_fn() != nullptr && (a.lda % 4 == 0) && aligned16(a.A) && (a.ldb % 2 == 0) &&
+         aligned16(a.B) && (!a.shift || aligned16(a.shift)) && a.M < (1LL << 31) &&
+         a.N < (1LL << 31) && a.K < (1LL << 31);
+}
+
+// A operand stored as float32 (args.A reinterpreted); TMA path only - callers check
+// gemm_f32_supported() and otherwise widen the operand to FP64 first.
+cudaError_t gemm_f32a(Context& ctx, Layout layout, const GemmArgs& args, int max_splits,
+                      cudaStream_t st) {
+  g_launches = 0;
+  cudaError_t e = cudaSuccess;
+  GemmArgs a = args;
+  if (a.M > 0 && a.N > 0 && a.K > 0) {
+    if (layout == Layout::CM) {
+      if (a.N <= 32) e = run_tile<FCM32>(ctx, a, true, true, max_splits, st);
+      else if (a.N <= 64) e = run_tile<FCM64>(ctx, a, true, true, max_splits, st);
+      else if (a.N <= 128) e = run_tile<FCM128>(ctx, a, true, true, max_splits, st);
+      else e = run_tile<FCM256>(ctx, a, true, true, max_splits, st);
+    } else {
+      if (a.N <= 32) e = run_tile<FRM32>(ctx, a, true, true, max_splits, st);
+      else if (a.N <= 64) e = run_tile<FRM64>(ctx, a, true, true, max_splits, st);
+      else if (a.N <= 128) e = run_tile<FRM128>(ctx, a, true, true, max_splits, st);
+      else e = run_tile<FRM256>(ctx, a, true, true, max_splits, st);
+    }
+  }
+  ctx.kernel_launches += g_launches;
+  ctx.gemm_launches += g_launches;
+  return e;
+}
 
 cudaError_t gemm(Context& ctx, Layout layout, const GemmArgs& args, int max_splits,
                  cudaStream_t st) {

@@ -69,8 +69,14 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 }
 __host__ __device__ constexpr int fperm(int g) { return (g >> 1) | ((g & 1) << 2); }
 
-template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+// TA = element type of the streamed A operand (O): double, or float for the FP32 variant
+// (BASELINE configs[3]).  FP32 tiles are widened to FP64 in registers, so products and sums are
+// exact FP64 arithmetic on the FP32 inputs.
+template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES,
+          typename TA = double>
 struct TmaCfg {
+  static constexpr bool kF32 = sizeof(TA) == 4;
+  static constexpr int EA = 128 / (int)sizeof(TA);  // A elements per 128-byte box line
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
   static constexpr int kThreads = 32 * (kConsumerWarps + 1);
   static constexpr int WM = BM / WARPS_M;
@@ -78,7 +84,7 @@ struct TmaCfg {
   static constexpr int MS = WM / 8;
   static constexpr int NS = WN / 8;
   static constexpr bool kCM = (L == Layout::CM);
-  static constexpr int A_BYTES = BM * BK * 8;
+  static constexpr int A_BYTES = BM * BK * (int)sizeof(TA);
   static constexpr int B_BYTES = BK * BN * 8;
   static constexpr int S_BYTES = kCM ? 0 : 1024;  // shift slice (BK doubles), padded
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + S_BYTES;
@@ -87,14 +93,18 @@ struct TmaCfg {
   static_assert(WM % 16 == 0 || (!kCM && WM % 8 == 0), "warp M tile");
   static_assert(WN % 16 == 0, "warp N tile");
   static_assert(STAGE_BYTES % 1024 == 0, "swizzle atoms");
+  static_assert(!kF32 || (kCM ? (WM % 32 == 0 && BM % 32 == 0) : BK % 32 == 0), "fp32 tiling");
 };
 
-template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES,
+          typename TA = double>
 __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmS, const GemmArgs args) {
-  using Cfg = TmaCfg<L, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+  using Cfg = TmaCfg<L, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TA>;
   constexpr bool CM = Cfg::kCM;
+  constexpr bool F32 = Cfg::kF32;
+  constexpr int EA = Cfg::EA;
   constexpr int MS = Cfg::MS, NS = Cfg::NS;
   constexpr int NCW = Cfg::kConsumerWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -137,12 +147,12 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
         mbar_arrive_expect_tx(full + s, bytes);
         if (CM) {
 #pragma unroll
-          for (int c = 0; c < BM / 16; ++c)
-            tma_load_2d(st + c * (BK * 128), &tmA, (int)m0 + 16 * c, k0, full + s);
+          for (int c = 0; c < BM / EA; ++c)
+            tma_load_2d(st + c * (BK * 128), &tmA, (int)m0 + EA * c, k0, full + s);
         } else {
 #pragma unroll
-          for (int c = 0; c < BK / 16; ++c)
-            tma_load_2d(st + c * (BM * 128), &tmA, k0 + 16 * c, (int)m0, full + s);
+          for (int c = 0; c < BK / EA; ++c)
+            tma_load_2d(st + c * (BM * 128), &tmA, k0 + EA * c, (int)m0, full + s);
           if (has_shift) tma_load_1d(st + Cfg::A_BYTES + Cfg::B_BYTES, &tmS, k0, full + s);
         }
 #pragma unroll
@@ -170,7 +180,8 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
   for (int i = 0; i < MS; ++i) {
     mu[i] = 0.0;
     if (CM && has_shift) {
-      const int64_t m = m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1);
+      const int64_t m = F32 ? m0 + wm0 + 32 * (i >> 2) + 4 * fg + (i & 3)
+                            : m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1);
       if (m < M) mu[i] = args.shift[m];
     }
   }
@@ -186,13 +197,27 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
         const int k = kk + t;  // row inside the box (BK rows of 128 B)
         const int sw = k & 7;
         double a[MS], b[NS];
+        if constexpr (F32) {
+          // one LDS.128 = 4 consecutive m of one 8-row sub-tile quartet
 #pragma unroll
-        for (int i = 0; i < MS / 2; ++i) {
-          const int c = (wm0 >> 4) + i;
-          const double2 x = *reinterpret_cast<const double2*>(
-              sA + c * (BK * 128) + k * 128 + ((fg ^ sw) << 4));
-          a[2 * i] = x.x - mu[2 * i];
-          a[2 * i + 1] = x.y - mu[2 * i + 1];
+          for (int i = 0; i < MS / 4; ++i) {
+            const int c = (wm0 >> 5) + i;
+            const float4 x = *reinterpret_cast<const float4*>(
+                sA + c * (BK * 128) + k * 128 + ((fg ^ sw) << 4));
+            a[4 * i] = (double)x.x - mu[4 * i];
+            a[4 * i + 1] = (double)x.y - mu[4 * i + 1];
+            a[4 * i + 2] = (double)x.z - mu[4 * i + 2];
+            a[4 * i + 3] = (double)x.w - mu[4 * i + 3];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < MS / 2; ++i) {
+            const int c = (wm0 >> 4) + i;
+            const double2 x = *reinterpret_cast<const double2*>(
+                sA + c * (BK * 128) + k * 128 + ((fg ^ sw) << 4));
+            a[2 * i] = x.x - mu[2 * i];
+            a[2 * i + 1] = x.y - mu[2 * i + 1];
+          }
         }
 #pragma unroll
         for (int j = 0; j < NS / 2; ++j) {
@@ -206,6 +231,51 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
         for (int i = 0; i < MS; ++i)
 #pragma unroll
           for (int j = 0; j < NS; ++j) dmma884(acc[i][j], a[i], b[j]);
+      }
+    } else if constexpr (F32) {
+      // K-quads: lane t holds k = kk + 4t + s for MMA step s (same permutation on A and B)
+      const double* sS = reinterpret_cast<const double*>(sB + Cfg::B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 16) {
+        double sh[4] = {0.0, 0.0, 0.0, 0.0};
+        if (has_shift) {
+          const double2 s0 = *reinterpret_cast<const double2*>(sS + kk + 4 * t);
+          const double2 s1 = *reinterpret_cast<const double2*>(sS + kk + 4 * t + 2);
+          sh[0] = s0.x;
+          sh[1] = s0.y;
+          sh[2] = s1.x;
+          sh[3] = s1.y;
+        }
+        const int ca = kk >> 5;
+        const int unit = 4 * ((kk >> 4) & 1) + t;
+        double aq[4][MS];
+#pragma unroll
+        for (int i = 0; i < MS; ++i) {
+          const int m = wm0 + 8 * i + fg;
+          const float4 x = *reinterpret_cast<const float4*>(
+              sA + ca * (BM * 128) + m * 128 + ((unit ^ fg) << 4));
+          aq[0][i] = (double)x.x - sh[0];
+          aq[1][i] = (double)x.y - sh[1];
+          aq[2][i] = (double)x.z - sh[2];
+          aq[3][i] = (double)x.w - sh[3];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int kr = kk + 4 * t + q;
+          double bq[NS];
+#pragma unroll
+          for (int j = 0; j < NS / 2; ++j) {
+            const int c = (wn0 >> 4) + j;
+            const double2 y = *reinterpret_cast<const double2*>(
+                sB + c * (BK * 128) + kr * 128 + ((g ^ (kr & 7)) << 4));
+            bq[2 * j] = y.x;
+            bq[2 * j + 1] = y.y;
+          }
+#pragma unroll
+          for (int i = 0; i < MS; ++i)
+#pragma unroll
+            for (int j = 0; j < NS; ++j) dmma884(acc[i][j], aq[q][i], bq[j]);
+        }
       }
     } else {
       const double* sS = reinterpret_cast<const double*>(sB + Cfg::B_BYTES);
@@ -272,7 +342,9 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
     asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32) : "memory");  // all consumers left the ring
 #pragma unroll
     for (int i = 0; i < MS; ++i) {
-      const int ml = CM ? wm0 + 16 * (i >> 1) + 2 * fg + (i & 1) : wm0 + 8 * i + fg;
+      const int ml = CM ? (F32 ? wm0 + 32 * (i >> 2) + 4 * fg + (i & 3)
+                               : wm0 + 16 * (i >> 1) + 2 * fg + (i & 1))
+                        : wm0 + 8 * i + fg;
 #pragma unroll
       for (int j = 0; j < NS; ++j) {
 #pragma unroll
@@ -293,7 +365,9 @@ __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
   } else {
 #pragma unroll
     for (int i = 0; i < MS; ++i) {
-      const int64_t m = CM ? m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1) : m0 + wm0 + 8 * i + fg;
+      const int64_t m = CM ? (F32 ? m0 + wm0 + 32 * (i >> 2) + 4 * fg + (i & 3)
+                                  : m0 + wm0 + 16 * (i >> 1) + 2 * fg + (i & 1))
+                           : m0 + wm0 + 8 * i + fg;
       if (m >= M) continue;
 #pragma unroll
       for (int j = 0; j < NS; ++j) {

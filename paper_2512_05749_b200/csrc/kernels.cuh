@@ -61,9 +61,9 @@ constexpr int kColStatsWarps = 8;
 
 // VEC columns per lane (VEC = 2: 16-byte loads, a warp streams 512 contiguous bytes per row);
 // UNROLL rows in flight per lane so each SM keeps >= 64 KB of loads outstanding.
-template <int VEC, int UNROLL>
+template <typename T, int VEC, int UNROLL>
 __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
-    colstats_kernel(const double* __restrict__ O, int64_t n, int64_t p, int64_t ld,
+    colstats_kernel(const T* __restrict__ O, int64_t n, int64_t p, int64_t ld,
                     const double* __restrict__ lraw, double* __restrict__ mu,
                     double* __restrict__ m2, double* __restrict__ gsum) {
   __shared__ double sh[kColStatsWarps][5][32 * VEC];
@@ -79,14 +79,25 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
 #pragma unroll
   for (int v = 0; v < VEC; ++v) K[v] = s1[v] = s2[v] = sl[v] = 0.0;
   auto load = [&](int64_t r, double (&x)[VEC]) {
-    if (VEC == 2 && act[1]) {
-      const double2 y = __ldg(reinterpret_cast<const double2*>(O + r * ld + col0));
-      x[0] = y.x;
-      x[VEC - 1] = y.y;
-    } else {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) x[v] = act[v] ? __ldg(O + r * ld + col0 + v) : 0.0;
+    if constexpr (sizeof(T) == 8 && VEC == 2) {
+      if (act[VEC - 1]) {
+        const double2 y = __ldg(reinterpret_cast<const double2*>(O + r * ld + col0));
+        x[0] = y.x;
+        x[VEC - 1] = y.y;
+        return;
+      }
+    } else if constexpr (sizeof(T) == 4 && VEC == 4) {
+      if (act[VEC - 1]) {
+        const float4 y = __ldg(reinterpret_cast<const float4*>(O + r * ld + col0));
+        x[0] = y.x;
+        x[1 % VEC] = y.y;
+        x[2 % VEC] = y.z;
+        x[3 % VEC] = y.w;
+        return;
+      }
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) x[v] = act[v] ? (double)__ldg(O + r * ld + col0 + v) : 0.0;
   };
   if (r1 > r0) {
     double x0[VEC];

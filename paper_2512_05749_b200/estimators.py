@@ -91,10 +91,11 @@ class EstimatorBundle:
     def o_matrix(self) -> torch.Tensor:
         """(n_params, batch) centred and scaled matrix (materialised on first access)."""
         if self._o_cache is None:
+            x = self._samples.to(torch.float64)
             if self._mu is None and self._scale == 1.0:
-                o = self._samples.t()
+                o = x.t()
             else:
-                o = ((self._samples - self._mu[None, :]) * self._scale).t()
+                o = ((x - self._mu[None, :]) * self._scale).t()
             object.__setattr__(self, "_o_cache", o)
         return self._o_cache
 
@@ -144,7 +145,7 @@ def assemble(batch, clip_n_std=5.0):
     if batch.size < 2:
         raise DegenerateBatch("need at least two samples to center the batch")
     ctx = _lib.context()
-    derivs = _arrays.rows_view(_arrays.to_tensor(batch.theta_logderivs))
+    derivs = _arrays.rows_view(_arrays.to_tensor_f64_or_f32(batch.theta_logderivs))
     energies = _arrays.to_tensor(batch.local_energies).reshape(-1).contiguous()
     n, p = derivs.shape
     dev = derivs.device
@@ -152,11 +153,23 @@ def assemble(batch, clip_n_std=5.0):
     lvec = torch.empty(n, dtype=torch.float64, device=dev)
     grad = torch.empty(p, dtype=torch.float64, device=dev)
     out = _lib.AssembleOut(mu=mu.data_ptr(), l_vector=lvec.data_ptr(), gradient=grad.data_ptr())
-    ctx.call("wssr_assemble_f64", _lib.ptr(derivs), n, p, _arrays.ld(derivs),
+    entry = "wssr_assemble_f32" if derivs.dtype == torch.float32 else "wssr_assemble_f64"
+    if derivs.dtype == torch.float32 and (derivs.stride(0) % 4 or derivs.data_ptr() % 16):
+        derivs = _pad_rows_f32(derivs)
+    ctx.call(entry, _lib.ptr(derivs), n, p, _arrays.ld(derivs),
              _lib.ptr(energies), float(clip_n_std), ctypes.byref(out))
     scale = 1.0 / np.sqrt(out.n_global)
     return EstimatorBundle._assembled(out.loss, out.raw_loss, derivs, mu, scale, out.fro2, lvec,
                                       grad, int(out.n_global))
+
+
+def _pad_rows_f32(x):
+    """float32 rows padded to a multiple of 4 elements (16-byte TMA pitch)."""
+    n, p = x.shape
+    ldp = (p + 3) // 4 * 4
+    buf = torch.zeros(n, ldp, dtype=torch.float32, device=x.device)
+    buf[:, :p] = x
+    return buf[:, :p]
 
 
 def s_matrix(bundle):

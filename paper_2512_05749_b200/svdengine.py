@@ -78,6 +78,7 @@ def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0
     o.mu = mu.data_ptr() if mu is not None else None
     o.samples_scale = float(scale)
     o.samples_fro2 = float(fro2)
+    o.samples_f32 = int(samples.dtype == torch.float32)
     return o
 
 
