@@ -100,12 +100,23 @@ bool make_map_1d(CUtensorMap* map, const double* ptr, int64_t n, int box) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST, typename TA = double>
+template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST, typename TA = double,
+          bool PERSIST = false>
 struct TmaTile {
   static constexpr int kBM = BM, kBN = BN, kBK = BK;
   using Cfg = TmaCfg<L, BM, BN, BK, WMW, WNW, ST, TA>;
+  static int num_sms() {
+    static int n = 0;
+    if (!n) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      if (n < 1) n = 148;
+    }
+    return n;
+  }
   static cudaError_t launch(const GemmArgs& a, int splits, bool, bool, cudaStream_t st) {
-    auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA>;
+    auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA, PERSIST>;
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -123,15 +134,22 @@ struct TmaTile {
     ok = ok && make_map_2d(&tB, a.B, a.N, a.K, a.ldb, BK);
     if (L == Layout::RM && a.shift) ok = ok && make_map_1d(&tS, a.shift, a.K, BK);
     if (!ok) return cudaErrorInvalidValue;
-    dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((a.N + BN - 1) / BN), (unsigned)splits);
-    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tS, a);
+    if (PERSIST) {
+      const int64_t units = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * splits;
+      const int64_t cap = (int64_t)num_sms() * ctas_per_sm();
+      kern<<<(unsigned)std::min(units, cap), Cfg::kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tS, a);
+    } else {
+      dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((a.N + BN - 1) / BN),
+                (unsigned)splits);
+      kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tS, a);
+    }
     ++g_launches;
     return cudaGetLastError();
   }
   static int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-      auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA>;
+      auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA, PERSIST>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)Cfg::kSmemBytes);
       int o = 0;
@@ -145,25 +163,25 @@ struct TmaTile {
 };
 
 // (BM, BN, BK, warps M x N, stages) from tools/microbench/gemm_sweep on B200
-using TCM32 = TmaTile<Layout::CM, 256, 32, 32, 8, 1, 2>;
-using TCM64 = TmaTile<Layout::CM, 128, 64, 64, 4, 2, 2>;
-using TCM128 = TmaTile<Layout::CM, 64, 128, 32, 2, 4, 3>;
-using TCM256 = TmaTile<Layout::CM, 32, 256, 32, 1, 8, 2>;
+using TCM32 = TmaTile<Layout::CM, 256, 32, 32, 8, 1, 2, double, true>;
+using TCM64 = TmaTile<Layout::CM, 128, 64, 64, 4, 2, 2, double, true>;
+using TCM128 = TmaTile<Layout::CM, 64, 128, 32, 2, 4, 3, double, true>;
+using TCM256 = TmaTile<Layout::CM, 32, 256, 32, 1, 8, 2, double, true>;
 using TCMsq32 = TmaTile<Layout::CM, 32, 32, 32, 1, 1, 4>;
 using TCMsq64 = TmaTile<Layout::CM, 64, 64, 32, 2, 2, 4>;
-using TRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2>;
-using TRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2>;
-using TRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3>;
-using TRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2>;
+using TRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2, double, true>;
+using TRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2, double, true>;
+using TRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3, double, true>;
+using TRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2, double, true>;
 // FP32 A operand (O stored as float32, BASELINE configs[3]); widened to FP64 in registers
-using FCM32 = TmaTile<Layout::CM, 256, 32, 32, 8, 1, 2, float>;
-using FCM64 = TmaTile<Layout::CM, 128, 64, 64, 4, 2, 2, float>;
-using FCM128 = TmaTile<Layout::CM, 64, 128, 32, 2, 4, 3, float>;
-using FCM256 = TmaTile<Layout::CM, 32, 256, 32, 1, 8, 2, float>;
-using FRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2, float>;
-using FRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2, float>;
-using FRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3, float>;
-using FRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2, float>;
+using FCM32 = TmaTile<Layout::CM, 256, 32, 32, 8, 1, 2, float, true>;
+using FCM64 = TmaTile<Layout::CM, 128, 64, 64, 4, 2, 2, float, true>;
+using FCM128 = TmaTile<Layout::CM, 64, 128, 32, 2, 4, 3, float, true>;
+using FCM256 = TmaTile<Layout::CM, 32, 256, 32, 1, 8, 2, float, true>;
+using FRM32 = TmaTile<Layout::RM, 256, 32, 32, 8, 1, 2, float, true>;
+using FRM64 = TmaTile<Layout::RM, 128, 64, 64, 4, 2, 2, float, true>;
+using FRM128 = TmaTile<Layout::RM, 64, 128, 32, 2, 4, 3, float, true>;
+using FRM256 = TmaTile<Layout::RM, 32, 256, 32, 1, 8, 2, float, true>;
 
 // short contractions (K <= 256: X * R^-1, X * C, w - q * quotient): small CTAs, 3-4 resident
 using TRMs64 = TmaTile<Layout::RM, 64, 64, 16, 2, 2, 4>;
