@@ -174,6 +174,16 @@ typedef struct wssr_step_in {
   int64_t max_iters;
   double residual_tol;
   int64_t flags;
+  /* optional externally computed factors (dense 'exact' / 'randomized' backends and the first
+     step, optimizers.py:327-338): when ext_u != NULL the SSI is skipped and the rank cut, gbar,
+     preconditioner, drift and state refresh run on U [P x ext_k_pos], sigma (sorted, positive)
+     and V [(hist_rank+n_samples) x ext_k_pos] (right vectors as columns). */
+  const double* ext_u;
+  int64_t ext_ld_u;
+  const double* ext_sigma;
+  const double* ext_v;
+  int64_t ext_ld_v;
+  int64_t ext_k_pos;
 } wssr_step_in;
 
 typedef struct wssr_step_out {
@@ -190,6 +200,14 @@ typedef struct wssr_step_out {
   double residual, sigma_drift, projector_drift;
 } wssr_step_out;
 int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
+
+/* --- linalg.exact_svd (linalg.py:108-121) for min(m, n) <= 512: u [m x q], sigma [q] sorted
+ * descending, vt [q x n], q = min(m, n).  Larger problems return WSSR_ERR_UNSUPPORTED. */
+int wssr_exact_svd_f64(wssr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                       double* u, int64_t ldu, double* sigma, double* vt, int64_t ldvt);
+/* Ohat of optimizers.py:323 written out parameter-major: out [P x (hist_rank + n_samples)]. */
+int wssr_materialize_ohat_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, double delta, double* out,
+                              int64_t ldo);
 
 /* --- diagnostics: small k x k device routines (tests).  op 0: CholeskyQR core, in = G (k x k),
  * out1 = R, out2 = R^-1, status[2] = {failed pivot (1-based) or 0, zero-matrix flag};

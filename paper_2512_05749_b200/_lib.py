@@ -59,6 +59,8 @@ class StepIn(ctypes.Structure):
         ("delta", _dbl), ("sigma_floor", _dbl), ("r_reg", _dbl), ("eps_grow", _dbl),
         ("sigma_floor_relative", _i64), ("r_max", _i64), ("max_iters", _i64),
         ("residual_tol", _dbl), ("flags", _i64),
+        ("ext_u", _vp), ("ext_ld_u", _i64), ("ext_sigma", _vp), ("ext_v", _vp),
+        ("ext_ld_v", _i64), ("ext_k_pos", _i64),
     ]
 
 
@@ -99,6 +101,8 @@ SIGNATURES = {
                                                _i64, ctypes.POINTER(_dbl),
                                                ctypes.POINTER(_dbl)]),
     "wssr_step_f64": (ctypes.c_int, [_vp, ctypes.POINTER(StepIn), ctypes.POINTER(StepOut)]),
+    "wssr_exact_svd_f64": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64]),
+    "wssr_materialize_ohat_f64": (ctypes.c_int, [_vp, ctypes.POINTER(OhatF64), _dbl, _vp, _i64]),
     "wssr_debug_small_f64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp,
                                             ctypes.POINTER(ctypes.c_int)]),
     "wssr_debug_gemm_f32a": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp,

@@ -753,6 +753,70 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
   out->e_std = hs[3];
 }
 
+// ---- dense SVD (linalg.py:108-121) for min(m, n) <= 512 ---------------------------------------
+// QR pre-reduction of the tall orientation (the reference's QR with its deficiency patch), then
+// one-sided Jacobi on the small square R.  Singular vectors carry an arbitrary joint sign, like
+// LAPACK's; everything the WSSR step derives from them (update, obar obar^T, obar lbar) is
+// sign-invariant.
+constexpr int64_t kDenseSvdMax = 512;
+
+void transpose(Context& ctx, const double* in, int64_t ldi, int64_t rows, int64_t cols,
+               const double* shift, double scale, double* out, int64_t ldo) {
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
+  transpose_shift_kernel<<<grid, dim3(32, 8), 0, ctx.stream>>>(in, ldi, rows, cols, shift, scale,
+                                                               out, ldo);
+  post_launch(ctx);
+}
+
+void dense_svd(Context& ctx, int64_t m, int64_t n, const double* A, int64_t lda, double* U,
+               int64_t ldu, double* S, double* VT, int64_t ldvt) {
+  cudaStream_t st = ctx.stream;
+  const int64_t q = std::min(m, n), rows = std::max(m, n);
+  if (q > kDenseSvdMax)
+    throw Fail{WSSR_ERR_UNSUPPORTED, "dense SVD on the device is limited to min(m, n) <= 512"};
+  Buf T;
+  const double* Tp = A;
+  int64_t ldt = lda;
+  if (m < n) {
+    T = Buf((size_t)n * m, st);
+    transpose(ctx, A, lda, m, n, nullptr, 1.0, T, m);
+    Tp = T;
+    ldt = m;
+  }
+  Buf Q((size_t)rows * q, st), R((size_t)q * q, st);
+  qr(ctx, rows, q, Tp, ldt, Q, q, R, nullptr, true, false);
+  Buf W((size_t)q * q, st), V((size_t)q * q, st), Us((size_t)q * q, st), Vs((size_t)q * q, st),
+      sw(1, st);
+  copy2d(ctx, R, q, q, q, 1.0, W, q);
+  jacobi_svd_kernel<<<1, 1024, 0, st>>>(W, V, (int)q, (int)q, 60, sw.i32());
+  post_launch(ctx);
+  svd_finalize_kernel<<<1, 1024, 2 * sizeof(double) * q, st>>>(W, V, (int)q, (int)q, S, Us, Vs,
+                                                              (int)q);
+  post_launch(ctx);
+  if (m >= n) {
+    gemm_rm(ctx, m, q, q, Q, q, nullptr, Us, q, U, ldu, 1.0, false);  // u = Q U_R
+    transpose(ctx, Vs, q, q, q, nullptr, 1.0, VT, ldvt);              // vt = V_R^T
+  } else {
+    copy2d(ctx, Vs, q, q, q, 1.0, U, ldu);                            // u = V_R
+    Buf QU((size_t)n * q, st);
+    gemm_rm(ctx, n, q, q, Q, q, nullptr, Us, q, QU, q, 1.0, false);
+    transpose(ctx, QU, q, n, q, nullptr, 1.0, VT, ldvt);             // vt = (Q U_R)^T
+  }
+}
+
+// Ohat (P x cols, parameter-major like optimizers.py:323) written out explicitly - only the
+// dense backends need it.
+void materialize_ohat(Context& ctx, const wssr_ohat_f64& oh, double delta, double* out,
+                      int64_t ldo) {
+  if (oh.samples_f32)
+    throw Fail{WSSR_ERR_UNSUPPORTED, "dense backends need float64 samples"};
+  const double sh = std::sqrt(delta) * oh.hist_scale, ss = std::sqrt(1.0 - delta) * oh.samples_scale;
+  const int64_t P = oh.n_params, r = oh.hist_rank;
+  if (r > 0) transpose(ctx, oh.hist, oh.hist_ld, r, P, nullptr, sh, out, ldo);
+  if (oh.n_samples > 0)
+    transpose(ctx, oh.samples, oh.samples_ld, oh.n_samples, P, oh.mu, ss, out + r, ldo);
+}
+
 // ---- wssr_step (optimizers.py:292-391), ssi branch -------------------------------------------
 void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   const wssr_ohat_f64& oh = *in->ohat;
@@ -785,11 +849,32 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   if (o.r > 0) copy2d(ctx, in->lbar, 1, o.r, 1, sq_old, lhat, 1);
   if (o.n > 0) copy2d(ctx, in->l_vector, 1, o.n, 1, sq_new, lhat + o.r, 1);
 
-  SsiResult sr = with_fallback(ctx, in->flags, [&](bool careful, int* status) {
-    return ssi_core(ctx, o, k, in->max_iters, in->u_init, in->ld_init, in->residual_tol, fro2,
-                    (in->flags & WSSR_FLAG_FINAL_RESIDUAL) != 0, careful, out->u_next, out->ld_u,
-                    out->sigma, in->r_reg, status);
-  });
+  SsiResult sr;
+  if (in->ext_u) {
+    // factors from a dense backend (optimizers.py:327-338): U (P x k_pos), sigma, V as columns
+    const int64_t kp = in->ext_k_pos;
+    if (kp < 1 || kp > k) throw Fail{WSSR_ERR_VALUE, "bad external factor rank"};
+    copy2d(ctx, in->ext_u, in->ext_ld_u, P, kp, 1.0, out->u_next, out->ld_u);
+    copy2d(ctx, in->ext_sigma, 1, kp, 1, 1.0, out->sigma, 1);
+    sr.qv = Buf((size_t)std::max<int64_t>(cols, 1) * k, st);
+    if (cols > 0) copy2d(ctx, in->ext_v, in->ext_ld_v, cols, kp, 1.0, sr.qv, k);
+    std::vector<double> hs(kp);
+    d2h(ctx, hs.data(), in->ext_sigma, sizeof(double) * kp);
+    sync(ctx);
+    sr.k_pos = kp;
+    sr.sigma0 = hs[0];
+    const double top = hs[0] * hs[0];
+    sr.r_eff = 0;
+    for (int64_t j = 0; j < kp; ++j) sr.r_eff += (hs[j] * hs[j] >= in->r_reg * top) ? 1 : 0;
+    sr.iterations = 0;
+    sr.residual = 0.0;
+  } else {
+    sr = with_fallback(ctx, in->flags, [&](bool careful, int* status) {
+      return ssi_core(ctx, o, k, in->max_iters, in->u_init, in->ld_init, in->residual_tol, fro2,
+                      (in->flags & WSSR_FLAG_FINAL_RESIDUAL) != 0, careful, out->u_next,
+                      out->ld_u, out->sigma, in->r_reg, status);
+    });
+  }
   const int64_t r_eff = sr.r_eff;
   if (r_eff < 1) throw Fail{WSSR_ERR_RANK_COLLAPSE, "no singular value passed the relative cutoff"};
   const bool binding = sr.k_pos == k && k == in->r_max && r_eff == in->r_max;
@@ -1154,6 +1239,23 @@ int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out) {
     if (!in || !out || !in->ohat) throw Fail{WSSR_ERR_VALUE, "null argument"};
     if (in->max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
     step(ctx->c, in, out);
+  });
+}
+
+int wssr_exact_svd_f64(wssr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                       double* u, int64_t ldu, double* sigma, double* vt, int64_t ldvt) {
+  return guarded(ctx, [&] {
+    if (m < 1 || n < 1) throw Fail{WSSR_ERR_VALUE, "empty matrix"};
+    dense_svd(ctx->c, m, n, a, lda, u, ldu, sigma, vt, ldvt);
+    sync(ctx->c);
+  });
+}
+
+int wssr_materialize_ohat_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, double delta, double* out,
+                              int64_t ldo) {
+  return guarded(ctx, [&] {
+    if (!ohat || !out) throw Fail{WSSR_ERR_VALUE, "null argument"};
+    materialize_ohat(ctx->c, *ohat, delta, out, ldo);
   });
 }
 

@@ -667,6 +667,119 @@ __global__ void maxeig_gmem_kernel(const double* Ain, int k, double* W, double* 
   maxeig_body(Ain, k, W, W + (size_t)k * (k + 1), out);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Dense SVD core for the step-0 / 'exact' / 'randomized' backends (svdengine.py:75-85, 161-196;
+// linalg.py:108-121): one-sided (Hestenes) Jacobi on a small square factor W (n x n, n <= 512,
+// the R of a QR pre-reduction).  Columns of W are orthogonalised by plane rotations that are
+// accumulated into V; round-robin pairing lets every warp rotate a disjoint pair concurrently.
+// One CTA; W and V live in global memory (L2-resident at these sizes).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ int rr_index(int pos, int round, int kk) {
+  // circle-method round-robin: position 0 fixed, the others rotate by one each round
+  return pos == 0 ? 0 : 1 + (pos - 1 + round) % (kk - 1);
+}
+
+__global__ void jacobi_svd_kernel(double* __restrict__ W, double* __restrict__ V, int n, int ld,
+                                  int max_sweeps, int* __restrict__ sweeps_out) {
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int nn = n + (n & 1);
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int r = e / n, c = e % n;
+    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < nn - 1; ++round) {
+      for (int i = warp; i < nn / 2; i += nw) {
+        int p = rr_index(i, round, nn), q = rr_index(nn - 1 - i, round, nn);
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        if (q >= n) continue;  // dummy partner for odd n
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int r = lane; r < n; r += 32) {
+          const double wp = W[r * ld + p], wq = W[r * ld + q];
+          a = fma(wp, wp, a);
+          b = fma(wq, wq, b);
+          c = fma(wp, wq, c);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        c = warp_sum(c);
+        if (c == 0.0 || !(fabs(c) > 1e-15 * sqrt(a * b))) continue;
+        const double zeta = (b - a) / (2.0 * c);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int r = lane; r < n; r += 32) {
+          const double wp = W[r * ld + p], wq = W[r * ld + q];
+          W[r * ld + p] = cs * wp - sn * wq;
+          W[r * ld + q] = sn * wp + cs * wq;
+          const double vp = V[r * ld + p], vq = V[r * ld + q];
+          V[r * ld + p] = cs * vp - sn * vq;
+          V[r * ld + q] = sn * vp + cs * vq;
+        }
+        if (lane == 0) atomicAdd(&s_rot, 1);
+      }
+      __syncthreads();
+    }
+    if (s_rot == 0) break;
+    __syncthreads();
+  }
+  if (tid == 0) *sweeps_out = sweep;
+}
+
+// sigma_j = ||W[:, j]||, sorted descending (stable); Us[:, j] = W[:, order_j] / sigma_j (0 when
+// sigma_j = 0), Vs[:, j] = V[:, order_j].  One CTA.
+__global__ void svd_finalize_kernel(const double* __restrict__ W, const double* __restrict__ V,
+                                    int n, int ld, double* __restrict__ sigma,
+                                    double* __restrict__ Us, double* __restrict__ Vs, int lds) {
+  extern __shared__ double sn[];  // [n] norms, then [n] order (as double)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nw) {
+    double a = 0.0;
+    for (int r = lane; r < n; r += 32) a = fma(W[r * ld + j], W[r * ld + j], a);
+    a = warp_sum(a);
+    if (lane == 0) sn[j] = sqrt(a);
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double si = sn[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += (sn[j] > si) || (sn[j] == si && j < i);
+    sn[n + rank] = (double)i;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int r = e / n, j = e % n;
+    const int src = (int)sn[n + j];
+    const double sg = sn[src];
+    Us[r * lds + j] = sg > 0.0 ? W[r * ld + src] / sg : 0.0;
+    Vs[r * lds + j] = V[r * ld + src];
+  }
+  for (int j = tid; j < n; j += blockDim.x) sigma[j] = sn[(int)sn[n + j]];
+}
+
+// out (cols x rows) = scale * (in (rows x cols, ldi) - shift[col])^T, shift optional
+__global__ void transpose_shift_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows,
+                                       int64_t cols, const double* __restrict__ shift,
+                                       double scale, double* __restrict__ out, int64_t ldo) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + tx;
+    tile[i][tx] = (r < rows && c < cols) ? scale * (in[r * ldi + c] - (shift ? shift[c] : 0.0))
+                                         : 0.0;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t c = c0 + i, r = r0 + tx;
+    if (c < cols && r < rows) out[c * ldo + r] = tile[tx][i];
+  }
+}
+
 // ||a[:r] - b[:r]||_2 and the off-diagonal Frobenius norm of a k x k matrix (svdengine.py:216,
 // svdengine.py:140).  One CTA.
 __global__ void small_norms_kernel(const double* __restrict__ a, const double* __restrict__ b,

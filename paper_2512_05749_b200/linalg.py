@@ -26,6 +26,31 @@ def _as_matrix(a):
     return t
 
 
+def exact_svd(a):
+    """Economy SVD a = u @ diag(sigma) @ vt with sigma nonincreasing (linalg.py:108-121).
+
+    On the device for min(m, n) <= 512 (QR pre-reduction + one-sided Jacobi); singular vectors
+    carry an arbitrary joint sign, as LAPACK's do.
+    """
+    a = _as_matrix(a)
+    if not bool(torch.isfinite(a).all()):
+        raise ValueError("matrix has non-finite entries")
+    m, n = a.shape
+    q = min(m, n)
+    dev = a.device
+    u = torch.zeros(m, q, dtype=torch.float64, device=dev)
+    sig = torch.zeros(q, dtype=torch.float64, device=dev)
+    vt = torch.zeros(q, n, dtype=torch.float64, device=dev)
+    if not bool((a != 0).any()):
+        u[:q, :q] = torch.eye(q, dtype=torch.float64, device=dev)
+        vt[:q, :q] = torch.eye(q, dtype=torch.float64, device=dev)
+        return u, sig, vt
+    a = _arrays.rows_view(a)
+    _lib.context().call("wssr_exact_svd_f64", m, n, _lib.ptr(a), _arrays.ld(a), _lib.ptr(u), q,
+                        _lib.ptr(sig), _lib.ptr(vt), n)
+    return u, sig, vt
+
+
 def qr_orthonormalize(a):
     """Thin QR with orthonormal Q and a nonnegative diagonal of R (linalg.py:29-61).
 

@@ -19,7 +19,6 @@ import numpy as np
 import torch
 
 from . import _arrays, _lib
-from .errors import Unsupported
 from .linalg import qr_orthonormalize
 from .svdengine import SsiReport
 
@@ -130,11 +129,7 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     """
     if svd_backend not in SVD_BACKENDS:
         raise ValueError(f"svd_backend must be one of {SVD_BACKENDS}, got {svd_backend!r}")
-    if state.step == 0 or svd_backend == "exact":
-        raise Unsupported("the dense first-step / 'exact' factorisation (optimizers.py:327-330) "
-                          "is not on the device path yet; start from step >= 1 with u_prev")
-    if svd_backend == "randomized":
-        raise Unsupported("svd_backend='randomized' (rssr_step) is not on the device path yet")
+    dense = state.step == 0 or svd_backend in ("exact", "randomized")
     ctx = _lib.context()
     theta = _arrays.to_tensor(theta).reshape(-1).contiguous()
     samples = bundle._samples
@@ -147,9 +142,12 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         hist = hist.contiguous()
     lbar = _arrays.to_tensor(state.lbar).contiguous()
     requested = min(state.r_max, m, r + n)
-    u_init = _prepare_warm_start(state.u_prev, requested, m,
-                                 _per_step_seed(rng_seed, state.step))
-    u_init = _arrays.rows_view(u_init)
+    if dense:
+        u_init = None
+    else:
+        u_init = _prepare_warm_start(state.u_prev, requested, m,
+                                     _per_step_seed(rng_seed, state.step))
+        u_init = _arrays.rows_view(u_init)
     u_prev = _arrays.to_tensor(state.u_prev)
     if u_prev.shape[1] > 0:
         u_prev = _arrays.rows_view(u_prev)
@@ -166,11 +164,30 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     o = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2, hist, 1.0)
     lvec = bundle.l_vector.contiguous()
     grad = bundle.gradient if bundle._gradient_exact else None
+    ext = None
+    if dense:
+        # optimizers.py:327-338: dense first step / 'exact' backend, or the randomized sketch
+        from .svdengine import exact_truncated_svd, randomized_svd
+        ohat = torch.empty(m, r + n, dtype=torch.float64, device=dev)
+        ctx.call("wssr_materialize_ohat_f64", ctypes.byref(o), float(state.delta),
+                 _lib.ptr(ohat), r + n)
+        if state.step == 0 or svd_backend == "exact":
+            factors = exact_truncated_svd(ohat, requested)
+        else:
+            room = min(ohat.shape) - requested
+            factors = randomized_svd(ohat, requested, oversample=min(10, max(0, room)),
+                                     rng_seed=_per_step_seed(rng_seed, state.step))
+        del ohat
+        fu = _arrays.rows_view(factors.u)
+        fs = factors.sigma.contiguous()
+        fv = factors.v.t().contiguous()
+        ext = (fu, fs, fv, int(factors.rank))
     sin = _lib.StepIn(
         ohat=ctypes.pointer(o), lbar=lbar.data_ptr() if r > 0 else None,
         l_vector=lvec.data_ptr(), gradient=grad.data_ptr() if grad is not None else None,
         theta=theta.data_ptr(), eta=float(eta),
-        u_init=u_init.data_ptr(), ld_init=_arrays.ld(u_init), requested=k,
+        u_init=u_init.data_ptr() if u_init is not None else None,
+        ld_init=_arrays.ld(u_init) if u_init is not None else 1, requested=k,
         u_prev=u_prev.data_ptr() if u_prev.shape[1] > 0 else None,
         ld_prev=_arrays.ld(u_prev) if u_prev.shape[1] > 0 else 1, r_prev=int(u_prev.shape[1]),
         delta=float(state.delta), sigma_floor=float(state.sigma_floor), r_reg=float(state.r_reg),
@@ -179,6 +196,10 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         residual_tol=float(ssi_residual_tol),
         flags=_lib.WSSR_FLAG_FINAL_RESIDUAL if report_final_residual else 0,
     )
+    if ext is not None:
+        sin.ext_u, sin.ext_ld_u = ext[0].data_ptr(), _arrays.ld(ext[0])
+        sin.ext_sigma, sin.ext_v = ext[1].data_ptr(), ext[2].data_ptr()
+        sin.ext_ld_v, sin.ext_k_pos = _arrays.ld(ext[2]) if ext[2].shape[0] > 1 else ext[3], ext[3]
     sout = _lib.StepOut(
         theta_next=theta_next.data_ptr(), update=update.data_ptr() if update is not None else None,
         u_next=u_next.data_ptr(), ld_u=k, obar_next_t=obar_t.data_ptr(), ld_obar=m,
@@ -195,7 +216,7 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         step=state.step + 1,
     )
     report = SsiReport(iterations_used=int(sout.iterations),
-                       subspace_residual=float(sout.residual), warm_started=True)
+                       subspace_residual=float(sout.residual), warm_started=not dense)
     diag = WssrDiagnostics(ssi=report, effective_rank=r_eff, r_max=int(state.r_max),
                            sigma_drift=float(sout.sigma_drift),
                            projector_drift=float(sout.projector_drift))
@@ -205,7 +226,7 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
 
 
 def rssr_step(theta, bundle, eta, state, ssi_max_iters=DEFAULT_SSI_MAX_ITERS, rng_seed=0):
-    """optimizers.py:394-401: randomized-sketch variant (SURVEY 8(f) 'next')."""
+    """Low-rank step with a fresh random sketch each step (optimizers.py:394-401)."""
     return wssr_step(theta, bundle, eta, state, svd_backend="randomized",
                      ssi_max_iters=ssi_max_iters, rng_seed=rng_seed)
 

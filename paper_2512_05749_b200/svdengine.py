@@ -116,15 +116,69 @@ def subspace_residual(ohat, u_orthonormal):
     return float(torch.linalg.vector_norm(w)) / fro2
 
 
+def _positive_prefix(sigma, limit):
+    """svdengine.py:70-72."""
+    return int((sigma[:limit] > 0.0).sum().item())
+
+
 def exact_truncated_svd(ohat, rank):
-    """Dense truncated SVD (svdengine.py:75-85): SURVEY 8(f) 'next' row, not on the device yet."""
-    raise Unsupported("exact_truncated_svd (step 0 / svd_backend='exact') is not implemented on "
-                      "the device path yet; seed the state with u_prev and step >= 1")
+    """Dense SVD truncated to the leading triplets, exact zeros dropped (svdengine.py:75-85).
+
+    Device path for min(m, n) <= 512 (linalg.exact_svd); larger problems raise Unsupported.
+    """
+    from .linalg import exact_svd
+
+    a = _arrays.to_tensor(ohat)
+    m, n = a.shape
+    if rank < 1 or rank > min(m, n):
+        raise RankTooLarge(f"rank {rank} outside [1, {min(m, n)}] for shape {(m, n)}")
+    if not bool((a != 0).any()):
+        raise DegenerateInput("cannot factorize an all-zero matrix")
+    u, sigma, vt = exact_svd(a)
+    k = _positive_prefix(sigma, rank)
+    return TruncatedSvd(u=u[:, :k], sigma=sigma[:k], v=vt[:k, :])
 
 
 def randomized_svd(ohat, rank, oversample=10, rng_seed=0):
-    """Gaussian range sketch (svdengine.py:161-196): SURVEY 8(f) 'next' row."""
-    raise Unsupported("randomized_svd is not implemented on the device path yet")
+    """Rank-r factors from a Gaussian range sketch (svdengine.py:161-196).
+
+    The sketch omega is drawn on the host with the reference's PCG64 stream (bit-identical),
+    y = ohat (ohat^T omega) and b = q^T ohat run as DMMA GEMMs, q by the device QR, and the small
+    b is factorised by the device dense SVD.
+    """
+    from .linalg import exact_svd, qr_orthonormalize
+
+    s = _sample_major(ohat)  # n x m (= ohat^T, row-major)
+    n, m = s.shape
+    width = rank + oversample
+    if rank < 1 or oversample < 0 or width > min(m, n):
+        raise RankTooLarge(
+            f"rank+oversample {width} outside [1, {min(m, n)}] for shape {(m, n)}")
+    if not bool((s != 0).any()):
+        raise DegenerateInput("cannot factorize an all-zero matrix")
+    ctx = _lib.context()
+    dev = s.device
+    omega = _arrays.rows_view(_arrays.to_tensor(
+        np.random.default_rng(rng_seed).standard_normal((m, width))))
+    t = torch.empty(n, width, dtype=torch.float64, device=dev)
+    y = torch.empty(m, width, dtype=torch.float64, device=dev)
+    ctx.call("wssr_gemm_f64", 1, n, width, m, _lib.ptr(s), _arrays.ld(s), None, _lib.ptr(omega),
+             width, _lib.ptr(t), width, 1.0, 0, 1024)                       # ohat^T omega
+    ctx.call("wssr_gemm_f64", 0, m, width, n, _lib.ptr(s), _arrays.ld(s), None, _lib.ptr(t),
+             width, _lib.ptr(y), width, 1.0, 0, 1024)                       # ohat (ohat^T omega)
+    q, _ = qr_orthonormalize(y)
+    bt = torch.empty(n, width, dtype=torch.float64, device=dev)
+    ctx.call("wssr_gemm_f64", 1, n, width, m, _lib.ptr(s), _arrays.ld(s), None, _lib.ptr(q),
+             width, _lib.ptr(bt), width, 1.0, 0, 1024)                      # b^T = ohat^T q
+    ub_t, sigma, vt_t = exact_svd(bt)                                      # b = vt_t^T S ub_t^T
+    k = _positive_prefix(sigma, rank)
+    if k == 0:
+        raise DegenerateInput("sketch captured no positive singular values")
+    u_b = vt_t.t()[:, :k].contiguous()
+    uu = torch.empty(m, k, dtype=torch.float64, device=dev)
+    ctx.call("wssr_gemm_f64", 1, m, k, width, _lib.ptr(q), width, None, _lib.ptr(u_b), k,
+             _lib.ptr(uu), k, 1.0, 0, 1024)                                 # q @ u_b
+    return TruncatedSvd(u=uu, sigma=sigma[:k], v=ub_t[:, :k].t())
 
 
 def ssi_svd(ohat, rank, max_iters=3, u_init=None, residual_tol=DEFAULT_RESIDUAL_EXIT,
