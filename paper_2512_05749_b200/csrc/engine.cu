@@ -242,7 +242,9 @@ double read_scalar(Context& ctx, const double* dev) {
 // ---- k x k Cholesky + inverse ---------------------------------------------------------------
 void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int* status) {
   const size_t smem = sizeof(double) * chol_scratch_doubles(k);
-  if (smem <= 200 * 1024) {
+  if (k <= 64) {
+    chol_inv_reg64_kernel<<<1, 256, 0, ctx.stream>>>(G, k, R, Rinv, status, kCholPivotRel);
+  } else if (smem <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {
       WSSR_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel,

@@ -329,9 +329,9 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     if (!(d > pivot_rel * dorig[j]) || !(d > deficient_sq)) {
       s_fail = j + 1;
     } else {
-      const double sq = sqrt(d);
-      s_sq = sq;
-      s_inv = 1.0 / sq;
+      const double y = fast_rsqrt(d);
+      s_sq = d * y;
+      s_inv = y;
     }
   };
   if (tid == 0) pivot(0, W[0]);
@@ -373,6 +373,153 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
       } else {
         R[e] = W[c * ld + r];     // L[c][r]
         Rinv[e] = X[c * ld + r];  // X[c][r]
+      }
+    }
+}
+
+// k <= 64: register-resident variant.  The matrix is padded to 64 x 64 with an identity tail;
+// thread (ty, tx) of the 16 x 16 grid owns rows {ty + 16 a} x columns {tx + 16 b}, a, b < 4, of
+// both L (lower part of W) and X = L^-1, in registers.  Per column j: the owners of column j of L
+// and of row j of X publish them (scaled) through shared memory, one barrier, every thread
+// applies its 16 + 16 rank-1 updates, the owner of the next pivot precomputes sqrt and 1/sqrt,
+// one barrier.  ~60 instructions per thread per column instead of strided shared-memory loops.
+__global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __restrict__ G, int k,
+                                                             double* __restrict__ R,
+                                                             double* __restrict__ Rinv,
+                                                             int* __restrict__ status,
+                                                             double pivot_rel) {
+  __shared__ double colL[64], rowX[64], dg[64];
+  __shared__ double s_sq, s_inv, s_tr, s_gmax;
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double w[4][4], x[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      w[a][b] = (i < k && c < k) ? G[i * k + c] : (i == c ? 1.0 : 0.0);
+      x[a][b] = (i == c) ? 1.0 : 0.0;
+    }
+  if (tid < 64) dg[tid] = tid < k ? G[tid * k + tid] : 1.0;
+  __syncthreads();
+  if (tid == 0) {
+    double gm = 0.0, tr = 0.0;
+    for (int j = 0; j < k; ++j) {
+      gm = fmax(gm, dg[j]);
+      tr += dg[j];
+    }
+    s_gmax = gm;
+    s_tr = tr;
+    s_fail = 0;
+    const double d = dg[0];
+    const double defic = 1.0000001e-24 * tr;
+    if (!(gm > 0.0) || !(gm < 1.0 / 0.0)) {
+      s_fail = -1;
+    } else if (!(d > pivot_rel * dg[0]) || !(d > defic)) {
+      s_fail = 1;
+    } else {
+      const double y = fast_rsqrt(d);
+      s_inv = y;
+      s_sq = d * y;
+    }
+  }
+  __syncthreads();
+  if (s_fail < 0) {
+    if (tid == 0) {
+      if (s_gmax == 0.0) atomicExch(status + 1, 1);
+      atomicCAS(status, 0, 1);
+    }
+    return;
+  }
+  const double deficient_sq = 1.0000001e-24 * s_tr;
+  // Published vectors carry exact zeros where an update must not land, so the rank-1 updates
+  // below are branch-free: colL[i] = L[i][j] for i > j (0 for i <= j, the diagonal stays in its
+  // owner's register), rowX[c] = X[j][c] for c <= j (0 above).
+  for (int j = 0; j < 64; ++j) {
+    if (s_fail) break;
+    const double inv = s_inv, sq = s_sq;
+    const int jt = j & 15, ja = j >> 4;
+    if (tx == jt) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = ty + 16 * a;
+        double v = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b == ja) {
+            const double sc = w[a][b] * inv;
+            v = (i > j) ? sc : 0.0;
+            w[a][b] = (i > j) ? sc : ((i == j) ? sq : w[a][b]);
+          }
+        }
+        colL[i] = v;
+      }
+    }
+    if (ty == jt) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int c = tx + 16 * b;
+        double v = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          if (a == ja) {
+            const double sc = x[a][b] * inv;
+            x[a][b] = sc;
+            v = (c <= j) ? sc : 0.0;
+          }
+        }
+        rowX[c] = v;
+      }
+    }
+    __syncthreads();
+    double li[4], lc[4], xr[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) li[a] = colL[ty + 16 * a];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      lc[b] = colL[tx + 16 * b];
+      xr[b] = rowX[tx + 16 * b];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        w[a][b] = fma(-li[a], lc[b], w[a][b]);  // only j < c, i touched (else a factor is 0)
+        x[a][b] = fma(-li[a], xr[b], x[a][b]);  // only i > j, c <= j touched
+      }
+    // next pivot W[j+1][j+1] lives with thread (ty, tx) = ((j+1) & 15, (j+1) & 15)
+    const int jn = j + 1;
+    if (jn < 64 && ty == (jn & 15) && tx == (jn & 15)) {
+      const int an = jn >> 4;
+      double d = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (a == an) d = w[a][a];
+      if (!(d > pivot_rel * dg[jn]) || !(d > deficient_sq)) {
+        if (jn < k) s_fail = jn + 1;
+        else { s_sq = 1.0; s_inv = 1.0; }  // padded identity tail
+      } else {
+        const double y = fast_rsqrt(d);
+        s_inv = y;
+        s_sq = d * y;
+      }
+    }
+    __syncthreads();
+  }
+  if (s_fail) {
+    if (tid == 0) atomicCAS(status, 0, s_fail);
+    return;
+  }
+  // R = L^T, Rinv = X^T
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      if (i < k && c < k) {
+        R[c * k + i] = (c <= i) ? w[a][b] : 0.0;
+        Rinv[c * k + i] = (c <= i) ? x[a][b] : 0.0;
       }
     }
 }
@@ -584,7 +731,7 @@ __device__ void maxeig_body(const double* __restrict__ Ain, int k, double* A, do
     }
     __syncthreads();
     if (!(vtv > 0.0)) continue;  // column already reduced
-    const double beta = 2.0 / vtv;
+    const double beta = 2.0 * fast_rcp(vtv);
     // p = beta * A' v  (A' = trailing n x n block)
     for (int i = tid; i < n; i += nt) {
       const double* row = A + (j + 1 + i) * ld + (j + 1);
@@ -639,7 +786,7 @@ __device__ void maxeig_body(const double* __restrict__ Ain, int k, double* A, do
     double d = 1.0;
     for (int i = 0; i < k; ++i) {
       const double e2 = i > 0 ? od[i - 1] * od[i - 1] : 0.0;
-      d = (dg[i] - x) - (i > 0 ? e2 / d : 0.0);
+      d = (dg[i] - x) - (i > 0 ? e2 * fast_rcp(d) : 0.0);
       if (d == 0.0) d = -1e-300;
       cnt += d < 0.0;
     }
