@@ -108,6 +108,19 @@ int wssr_dmma_peak_probe(wssr_ctx* ctx, double* tflops);
 int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]);
 int wssr_nccl_attach(wssr_ctx* ctx, const unsigned char id[128], int rank, int world);
 
+/* Thread-emulated communicator for testing the sharded engine on one GPU: `world` host threads,
+ * each with its own context and stream, attach to one group; collectives synchronise on the host
+ * and sum in rank order.  Not for production use (no GPU-side waits, no overlap). */
+int wssr_emu_group_create(int world, void** group);
+void wssr_emu_group_abort(void* group); /* a failed rank releases its waiting peers */
+void wssr_emu_group_destroy(void* group);
+int wssr_emu_attach(wssr_ctx* ctx, void* group, int rank);
+
+/* In-place sum over the attached communicator's ranks (no-op when none is attached).  Used by
+ * the host mirror to gather the dense first-step matrix of a row-sharded run
+ * (optimizers.py:327-331 factorises the whole Ohat). */
+int wssr_allreduce_f64(wssr_ctx* ctx, double* buf, int64_t n);
+
 /* --- estimators.assemble (estimators.py:74-100) ------------------------------------------- */
 typedef struct wssr_assemble_out {
   double* mu;       /* [P]  column means of theta_logderivs (global over ranks)               */

@@ -90,6 +90,11 @@ SIGNATURES = {
     "wssr_dmma_peak_probe": (ctypes.c_int, [_vp, ctypes.POINTER(_dbl)]),
     "wssr_nccl_unique_id": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "wssr_nccl_attach": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int]),
+    "wssr_allreduce_f64": (ctypes.c_int, [_vp, _vp, ctypes.c_int64]),
+    "wssr_emu_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    "wssr_emu_group_abort": (None, [_vp]),
+    "wssr_emu_group_destroy": (None, [_vp]),
+    "wssr_emu_attach": (ctypes.c_int, [_vp, _vp, ctypes.c_int]),
     "wssr_assemble_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _dbl,
                                          ctypes.POINTER(AssembleOut)]),
     "wssr_assemble_f32": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _dbl,
@@ -202,11 +207,20 @@ class Context:
 
 
 _contexts: dict = {}
+_thread_ctx = threading.local()
+
+
+def set_thread_context(ctx) -> None:
+    """Route this host thread's drop-in calls to `ctx` (None: the per-device default)."""
+    _thread_ctx.ctx = ctx
 
 
 def context(device=None) -> Context:
     import torch
 
+    override = getattr(_thread_ctx, "ctx", None)
+    if override is not None:
+        return override
     if not torch.cuda.is_available():
         raise errors.DeviceError("the WSSR drop-in needs a CUDA device (no CPU fallback)")
     dev = torch.cuda.current_device() if device is None else int(device)

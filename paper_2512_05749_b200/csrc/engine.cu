@@ -5,6 +5,9 @@
 // svdengine.py:139-141, and the rank cut, optimizers.py:348-355).
 #include <dlfcn.h>
 
+#include <condition_variable>
+#include <mutex>
+
 #include <cstdio>
 #include <cstring>
 #include <limits>
@@ -843,7 +846,9 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   if (k < 1) throw Fail{WSSR_ERR_RANK_TOO_LARGE, "rank must be at least 1"};
 
   double samples_fro2 = oh.samples_fro2 >= 0.0 ? oh.samples_fro2 * (sq_new * sq_new) : -1.0;
-  const double fro2 = ohat_fro2(ctx, o, samples_fro2, owner);
+  Ohat ofull = o;  // the history block is replicated: every rank adds its norm
+  ofull.r = oh.hist_rank;
+  const double fro2 = ohat_fro2(ctx, ofull, samples_fro2, true);
   if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
 
   // lhat = [sqrt(delta) lbar, sqrt(1-delta) L]  (optimizers.py:324)
@@ -997,6 +1002,89 @@ struct NcclComm : Comm {
   }
   ~NcclComm() override {
     if (comm) g_nccl.destroy(comm);
+  }
+};
+
+// ---- thread-emulated communicator (tests the sharded engine on ONE GPU) ------------------------
+// Each emulated rank is a host thread with its own context and stream.  allreduce: every rank
+// publishes its buffer after a stream sync, rank 0 sums the buffers in rank order into a scratch
+// buffer, everyone copies it back.  All waiting happens on the host; no kernel waits on another.
+struct EmuSumArgs {
+  const double* src[8];
+};
+__global__ void emu_sum_kernel(EmuSumArgs a, int world, size_t n, double* out) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double s = a.src[0][i];
+    for (int r = 1; r < world; ++r) s += a.src[r][i];
+    out[i] = s;
+  }
+}
+
+struct EmuGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  bool aborted = false;
+  std::vector<double*> bufs;
+  double* scratch = nullptr;
+  size_t cap = 0;
+  // false when a rank aborted the group (its peers then fail instead of waiting forever)
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
+    const int64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen || aborted; });
+    }
+    return !aborted;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+struct EmuComm : Comm {
+  EmuGroup* g = nullptr;
+  cudaError_t allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      g->abort();
+      return e;
+    }
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->bufs[rank] = buf;
+    }
+    if (!g->barrier()) return cudaErrorUnknown;
+    if (rank == 0) {
+      if (n > g->cap) {
+        if (g->scratch) cudaFree(g->scratch);
+        if ((e = cudaMalloc(&g->scratch, n * sizeof(double))) != cudaSuccess) {
+          g->abort();
+          return e;
+        }
+        g->cap = n;
+      }
+      EmuSumArgs a{};
+      for (int r = 0; r < world; ++r) a.src[r] = g->bufs[r];
+      emu_sum_kernel<<<256, 256, 0, st>>>(a, world, n, g->scratch);
+      e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) g->abort();
+    }
+    if (!g->barrier()) return cudaErrorUnknown;
+    e = cudaMemcpyAsync(buf, g->scratch, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (!g->barrier()) return cudaErrorUnknown;
+    return e;
   }
 };
 
@@ -1158,6 +1246,48 @@ int wssr_nccl_attach(wssr_ctx* ctx, const unsigned char id[128], int rank, int w
       throw Fail{WSSR_ERR_NCCL, "ncclCommInitRank failed"};
     }
     ctx->c.comm = cm;
+  });
+}
+
+int wssr_emu_group_create(int world, void** group) {
+  if (!group || world < 1 || world > 8) return WSSR_ERR_VALUE;
+  auto* g = new EmuGroup();
+  g->world = world;
+  g->bufs.assign(world, nullptr);
+  *group = g;
+  return WSSR_OK;
+}
+
+void wssr_emu_group_abort(void* group) {
+  if (group) static_cast<EmuGroup*>(group)->abort();
+}
+
+void wssr_emu_group_destroy(void* group) {
+  auto* g = static_cast<EmuGroup*>(group);
+  if (!g) return;
+  if (g->scratch) cudaFree(g->scratch);
+  delete g;
+}
+
+int wssr_emu_attach(wssr_ctx* ctx, void* group, int rank) {
+  return guarded(ctx, [&] {
+    auto* g = static_cast<EmuGroup*>(group);
+    if (!g || rank < 0 || rank >= g->world) throw Fail{WSSR_ERR_VALUE, "bad emulated rank"};
+    delete ctx->c.comm;
+    ctx->c.comm = nullptr;
+    if (g->world == 1) return;
+    auto* cm = new EmuComm();
+    cm->g = g;
+    cm->rank = rank;
+    cm->world = g->world;
+    ctx->c.comm = cm;
+  });
+}
+
+int wssr_allreduce_f64(wssr_ctx* ctx, double* buf, int64_t n) {
+  return guarded(ctx, [&] {
+    if (n < 0 || (n > 0 && !buf)) throw Fail{WSSR_ERR_VALUE, "bad buffer"};
+    if (ctx->c.world() > 1 && n > 0) allreduce(ctx->c, buf, (size_t)n);
   });
 }
 

@@ -42,3 +42,72 @@ def attach_nccl(ctx, group=None):
     ident = ctypes.create_string_buffer(obj[0], 128)
     ctx.call("wssr_nccl_attach", ident, rank, world)
     ctx.rank, ctx.world = rank, world
+
+
+class EmulatedGroup:
+    """`world` ranks on ONE GPU, one host thread each, joined by libwssr's thread-emulated
+    communicator (wssr_emu_*): exercises every sharded code path of the engine (row-split
+    assemble, per-pass allreduces, history ownership, sharded dense first step) where only one
+    GPU is available.  Collectives synchronise on the host, so no kernel ever waits on another.
+    Test infrastructure, not a production transport.
+    """
+
+    def __init__(self, world: int, device: int = 0):
+        lib = _lib.load_library()
+        h = _lib._vp()
+        if lib.wssr_emu_group_create(int(world), ctypes.byref(h)) != _lib.WSSR_OK:
+            raise ValueError(f"bad emulated world size {world}")
+        self._lib, self._group, self.world = lib, h, int(world)
+        self.contexts = []
+        for r in range(self.world):
+            c = _lib.Context(device)
+            c.call("wssr_emu_attach", h, r)
+            c.rank, c.world = r, self.world
+            self.contexts.append(c)
+
+    def run(self, fn, timeout: float = 300.0):
+        """fn(rank, world) on every rank concurrently, each on its own CUDA stream; returns the
+        per-rank results (re-raises the first rank failure)."""
+        import threading
+
+        import torch
+
+        results, failures = [None] * self.world, []
+
+        def body(r):
+            ctx = self.contexts[r]
+            _lib.set_thread_context(ctx)
+            try:
+                with torch.cuda.device(ctx.device), torch.cuda.stream(torch.cuda.Stream(ctx.device)):
+                    results[r] = fn(r, self.world)
+                    torch.cuda.current_stream().synchronize()
+            except BaseException as e:  # noqa: BLE001 - surfaced below
+                failures.append((r, e))
+                self._lib.wssr_emu_group_abort(self._group)
+            finally:
+                _lib.set_thread_context(None)
+
+        threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout)
+        if any(t.is_alive() for t in threads):
+            raise TimeoutError("an emulated rank did not finish (collective mismatch?)")
+        if failures:
+            raise failures[0][1]
+        return results
+
+    def close(self):
+        for c in self.contexts:
+            c.__del__()
+        self.contexts = []
+        if self._group:
+            self._lib.wssr_emu_group_destroy(self._group)
+            self._group = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -141,7 +141,8 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     if r > 0 and not (hist.stride(1) == 1 and hist.stride(0) >= m):
         hist = hist.contiguous()
     lbar = _arrays.to_tensor(state.lbar).contiguous()
-    requested = min(state.r_max, m, r + n)
+    n_global = int(getattr(bundle, "_n_global", n))
+    requested = min(state.r_max, m, r + n_global)
     if dense:
         u_init = None
     else:
@@ -168,9 +169,28 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     if dense:
         # optimizers.py:327-338: dense first step / 'exact' backend, or the randomized sketch
         from .svdengine import exact_truncated_svd, randomized_svd
-        ohat = torch.empty(m, r + n, dtype=torch.float64, device=dev)
-        ctx.call("wssr_materialize_ohat_f64", ctypes.byref(o), float(state.delta),
-                 _lib.ptr(ohat), r + n)
+        world = int(getattr(ctx, "world", 1))
+        if world > 1:
+            # row-sharded: every rank writes its own columns of the global Ohat
+            # [hist | samples of rank 0 | rank 1 | ...] and one sum gathers them (disjoint, so
+            # the sum is exact); every rank then factorises the same matrix.
+            counts = torch.zeros(world, dtype=torch.float64, device=dev)
+            counts[ctx.rank] = n
+            ctx.call("wssr_allreduce_f64", _lib.ptr(counts), world)
+            counts = [int(c) for c in counts.tolist()]
+            c0 = 0 if ctx.rank == 0 else r + sum(counts[:ctx.rank])
+            n_local = (r if ctx.rank == 0 else 0) + n
+            ohat = torch.zeros(m, r + sum(counts), dtype=torch.float64, device=dev)
+            o_local = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2,
+                                   hist if ctx.rank == 0 else hist[:0], 1.0)
+            ctx.call("wssr_materialize_ohat_f64", ctypes.byref(o_local), float(state.delta),
+                     _lib._vp(ohat.data_ptr() + 8 * c0), ohat.shape[1])
+            ctx.call("wssr_allreduce_f64", _lib.ptr(ohat), ohat.numel())
+        else:
+            c0, n_local = 0, r + n
+            ohat = torch.empty(m, r + n, dtype=torch.float64, device=dev)
+            ctx.call("wssr_materialize_ohat_f64", ctypes.byref(o), float(state.delta),
+                     _lib.ptr(ohat), r + n)
         if state.step == 0 or svd_backend == "exact":
             factors = exact_truncated_svd(ohat, requested)
         else:
@@ -180,7 +200,7 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         del ohat
         fu = _arrays.rows_view(factors.u)
         fs = factors.sigma.contiguous()
-        fv = factors.v.t().contiguous()
+        fv = factors.v[:, c0:c0 + n_local].t().contiguous()
         ext = (fu, fs, fv, int(factors.rank))
     sin = _lib.StepIn(
         ohat=ctypes.pointer(o), lbar=lbar.data_ptr() if r > 0 else None,

@@ -38,8 +38,11 @@ def oracle_run(name, g):
     return out
 
 
-def device_run(name, g, report_final_residual=True):
-    """Closed-loop replay through the drop-in API on the GPU."""
+def device_run(name, g, report_final_residual=True, rows=None, dtype=None):
+    """Closed-loop replay through the drop-in API on the GPU.
+
+    rows=(row0, n): this rank's shard of the samples (row-sharded runs); dtype: cast O to it.
+    """
     import torch
 
     from paper_2512_05749_b200 import estimators, optimizers, linalg
@@ -56,6 +59,10 @@ def device_run(name, g, report_final_residual=True):
     out = []
     for t in range(T):
         o, e = wl.next()
+        if rows is not None:
+            o, e = o[rows[0]:rows[0] + rows[1]], e[rows[0]:rows[0] + rows[1]]
+        if dtype is not None:
+            o = o.astype(dtype)
         batch = estimators.SampleBatch((None,) * o.shape[0], e, o)
         b = estimators.assemble(batch)
         th, st, diag, upd = optimizers.wssr_step(torch.zeros(P, dtype=torch.float64, device=dev), b,

@@ -1,0 +1,141 @@
+"""Row-sharded engine on one GPU: 2-3 ranks as host threads joined by libwssr's
+thread-emulated communicator (distributed.EmulatedGroup) run the SAME sharded code paths as the
+NCCL build -- row-split assemble with merged column statistics, per-pass allreduces of u, the
+k x k Grams of QR(v), gbar and lbar, history owned by rank 0, the gathered dense first step --
+and must reproduce the reference fixtures and the single-rank device results.
+
+Tolerances are the parity suite's (test_gpu_parity.py): the sharded sums differ from the
+unsharded ones only in summation order.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel, subspace_sine
+from _runs import FIXTURES, device_run
+from test_gpu_parity import _check_run
+
+pytestmark = pytest.mark.gpu
+
+
+def _sharded(name, g, world, **kw):
+    from paper_2512_05749_b200.distributed import EmulatedGroup, row_shard
+    from _runs import fixture_config
+
+    n = fixture_config(name, g)[0]["N"]
+    with EmulatedGroup(world) as grp:
+        return grp.run(lambda r, w: device_run(name, g, rows=row_shard(n, r, w), **kw))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_sharded_closed_loop_matches_reference_fixture(golden, name, world):
+    g = golden(name)
+    per_rank = _sharded(name, g, world)
+    for t in range(len(per_rank[0])):
+        lv = np.concatenate([pr[t]["l_vector"] for pr in per_rank])
+        for pr in per_rank:
+            pr[t]["l_vector"] = lv
+    for r, runs in enumerate(per_rank):
+        _check_run(runs, g, f"{name}@rank{r}/{world}")
+    # replicated outputs agree across ranks
+    for t in range(len(per_rank[0])):
+        for pr in per_rank[1:]:
+            assert rel(pr[t]["update"], per_rank[0][t]["update"]) < 1e-14
+            assert subspace_sine(pr[t]["V"], per_rank[0][t]["V"]) < 1e-12
+
+
+def test_sharded_matches_single_rank(golden):
+    g = golden("hist_T4.npz")
+    single = device_run("hist_T4.npz", g)
+    sharded = _sharded("hist_T4.npz", g, 2)[1]
+    for a, b in zip(single, sharded):
+        assert a["r_eff"] == b["r_eff"] and a["iterations"] == b["iterations"]
+        assert rel(b["update"], a["update"]) < 1e-11
+        assert rel(b["sigma"], a["sigma"]) < 1e-11
+        assert subspace_sine(b["V"], a["V"]) < 1e-9
+
+
+def test_sharded_fp32_samples(golden):
+    g = golden("c0_T5.npz")
+    single = device_run("c0_T5.npz", g, dtype=np.float32)
+    sharded = _sharded("c0_T5.npz", g, 2, dtype=np.float32)
+    for a, b in zip(single, sharded[0]):
+        assert a["r_eff"] == b["r_eff"] and a["iterations"] == b["iterations"]
+        assert rel(b["update"], a["update"]) < 1e-10
+        assert rel(b["sigma"], a["sigma"]) < 1e-10
+
+
+def _first_steps(rows, world_rank, T=3):
+    """Closed loop from WssrState.initial (dense first step, then SSI) on c0-sized data."""
+    import torch
+
+    from paper_2512_05749_b200 import estimators, optimizers, synthetic
+
+    cfg = synthetic.config("c0", N=120, P=384, k=10, L=16, delta=0.8, lam=1e-3)
+    wl = synthetic.HostWorkload.from_config(cfg, 11)
+    st = optimizers.WssrState.initial(cfg["P"], rank_init=cfg["k"], delta=cfg["delta"],
+                                      sigma_floor=cfg["lam"])
+    out = []
+    for _ in range(T):
+        o, e = wl.next()
+        if rows is not None:
+            o, e = o[rows[0]:rows[0] + rows[1]], e[rows[0]:rows[0] + rows[1]]
+        b = estimators.assemble(estimators.SampleBatch((None,) * o.shape[0], e, o))
+        th, st, diag, upd = optimizers.wssr_step(
+            torch.zeros(cfg["P"], dtype=torch.float64, device="cuda"), b, 1.0, st,
+            return_update=True)
+        out.append(dict(update=upd.cpu().numpy(), V=st.u_prev.cpu().numpy(),
+                        sigma=optimizers.sigma_of(st).cpu().numpy(), r_eff=diag.effective_rank,
+                        lbar=st.lbar.cpu().numpy()))
+    return cfg["N"], out
+
+
+def test_sharded_dense_first_step():
+    from paper_2512_05749_b200.distributed import EmulatedGroup, row_shard
+
+    n, single = _first_steps(None, 0)
+    with EmulatedGroup(2) as grp:
+        per_rank = grp.run(lambda r, w: _first_steps(row_shard(n, r, w), r)[1])
+    for runs in per_rank:
+        for a, b in zip(single, runs):
+            assert a["r_eff"] == b["r_eff"]
+            assert rel(b["update"], a["update"]) < 1e-10
+            assert rel(b["sigma"], a["sigma"]) < 1e-10
+            assert rel(b["lbar"], a["lbar"]) < 1e-8
+            assert subspace_sine(b["V"], a["V"]) < 1e-8
+
+
+def test_emulated_group_surfaces_rank_failure():
+    """A rank that raises releases its peers (no hang) and the error reaches the caller."""
+    import torch
+
+    from paper_2512_05749_b200 import _lib
+    from paper_2512_05749_b200.distributed import EmulatedGroup
+
+    def body(r, w):
+        buf = torch.ones(16, dtype=torch.float64, device="cuda")
+        if r == 1:
+            raise RuntimeError("rank 1 failed")
+        _lib.context().call("wssr_allreduce_f64", _lib.ptr(buf), 16)
+        return buf
+
+    with EmulatedGroup(2) as grp:
+        with pytest.raises(RuntimeError, match="rank 1 failed"):
+            grp.run(body, timeout=60)
+
+
+def test_emulated_allreduce_sums_in_rank_order():
+    import torch
+
+    from paper_2512_05749_b200 import _lib
+    from paper_2512_05749_b200.distributed import EmulatedGroup
+
+    def body(r, w):
+        buf = torch.full((1000,), float(r + 1), dtype=torch.float64, device="cuda")
+        _lib.context().call("wssr_allreduce_f64", _lib.ptr(buf), 1000)
+        return buf.cpu().numpy()
+
+    with EmulatedGroup(3) as grp:
+        for out in grp.run(body):
+            np.testing.assert_array_equal(out, 6.0)
