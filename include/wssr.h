@@ -90,8 +90,12 @@ int wssr_version(void);
 /* number of kernels this context launched so far (bench.py's gpu_launches) */
 int64_t wssr_kernel_launches(const wssr_ctx* ctx);
 
-/* GEMM main loop: 0 = auto (TMA + mbarrier warp-specialised pipeline when operands allow it),
- * 1 = force the cp.async pipeline (A/B comparisons and tests). */
+/* GEMM path of the O-passes:
+ *   0 = auto: large sample blocks on the int8 tensor cores (exact digit products, ozaki.cu),
+ *       the rest on FP64 DMMA with the TMA + mbarrier pipeline;
+ *   1 = FP64 DMMA with the cp.async pipeline only;
+ *   2 = FP64 DMMA only (TMA where operands allow it);
+ *   3 = int8 tensor-core path for every sample block it supports (tests). */
 int wssr_set_gemm_path(wssr_ctx* ctx, int path);
 
 /* bench instrumentation: per-phase CUDA-event timing of the O-passes.
@@ -232,6 +236,13 @@ int wssr_debug_small_f64(wssr_ctx* ctx, int op, int k, const double* in, double*
 int wssr_debug_gemm_f32a(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k,
                          const float* a, int64_t lda, const double* shift, const double* b,
                          int64_t ldb, double* c, int64_t ldc, double alpha);
+
+/* test hook: one O-pass GEMM on the int8 tensor-core path (scales computed from `a`).
+ * layout 0: C (m x n) = alpha (A - 1 shift^T)^T B with A stored (k x m) row-major;
+ * layout 1: C (m x n) = alpha (A - 1 shift^T) B with A (m x k) row-major.  a_f32: A is float. */
+int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k,
+                          const void* a, int64_t lda, int a_f32, const double* shift,
+                          const double* b, int64_t ldb, double* c, int64_t ldc, double alpha);
 
 /* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
 int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,

@@ -112,6 +112,10 @@ SIGNATURES = {
                                             ctypes.POINTER(ctypes.c_int)]),
     "wssr_debug_gemm_f32a": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp,
                                             _vp, _i64, _vp, _i64, _dbl]),
+    "wssr_debug_ozaki_gemm": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
+                                              _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                              ctypes.c_double]),
     "wssr_gemm_f64": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _vp,
                                      _i64, _vp, _i64, _dbl, ctypes.c_int, ctypes.c_int]),
 }

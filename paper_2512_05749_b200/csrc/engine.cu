@@ -15,6 +15,7 @@
 #include <utility>
 
 #include "engine.h"
+#include "ozaki.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -392,6 +393,8 @@ struct Ohat {
   const double* mu = nullptr;
   double ss = 1.0;
   bool f32 = false;  // samples stored as float32 (BASELINE configs[3])
+  // per-parameter scale table of the int8 tensor-core path, built on first use (shared by copies)
+  mutable std::shared_ptr<Buf> oz_scale;
   int64_t cols() const { return r + n; }
 };
 
@@ -399,6 +402,15 @@ struct Ohat {
 void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t N, int64_t K,
                   const double* B, int64_t ldb, double* C, int64_t ldc, double alpha) {
   GemmArgs a{o.samp, o.lds, B, ldb, o.mu, C, ldc, M, N, K, 0, alpha, 0, nullptr, nullptr, 0};
+  if (ctx.ozaki && !ctx.disable_tma && (double)M * (double)K >= ctx.oz_min_elems &&
+      ozaki_supported(layout, a, o.f32)) {
+    if (!o.oz_scale) {
+      o.oz_scale = std::make_shared<Buf>(2 * ozaki_scale_len(o.P), ctx.stream);
+      WSSR_CUDA(ozaki_scales(ctx, o.samp, o.f32, o.lds, o.n, o.P, o.mu, *o.oz_scale, ctx.stream));
+    }
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, *o.oz_scale, ctx.stream));
+    return;
+  }
   if (o.f32) {
     if (!gemm_f32_supported(layout, a))
       throw Fail{WSSR_ERR_UNSUPPORTED, "fp32 samples need 16-byte aligned rows (ld % 4 == 0)"};
@@ -1157,10 +1169,9 @@ int wssr_ctx_create(int device, wssr_ctx** out) {
 void wssr_ctx_destroy(wssr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
-  if (ctx->c.splitk) {
-    cudaDeviceSynchronize();
-    cudaFree(ctx->c.splitk);
-  }
+  if (ctx->c.splitk || ctx->c.oz_ws) cudaDeviceSynchronize();
+  if (ctx->c.splitk) cudaFree(ctx->c.splitk);
+  if (ctx->c.oz_ws) cudaFree(ctx->c.oz_ws);
   delete ctx->c.comm;
   delete ctx;
 }
@@ -1176,8 +1187,10 @@ int wssr_set_stream(wssr_ctx* ctx, void* stream) {
 int64_t wssr_kernel_launches(const wssr_ctx* ctx) { return ctx ? ctx->c.kernel_launches : 0; }
 
 int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
-  if (!ctx || path < 0 || path > 1) return WSSR_ERR_VALUE;
+  if (!ctx || path < 0 || path > 3) return WSSR_ERR_VALUE;
   ctx->c.disable_tma = path == 1;
+  ctx->c.ozaki = path == 0 || path == 3;
+  ctx->c.oz_min_elems = path == 3 ? 0.0 : 4194304.0;
   return WSSR_OK;
 }
 
@@ -1418,6 +1431,24 @@ int wssr_debug_gemm_f32a(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_
     const Layout L = layout == 0 ? Layout::CM : Layout::RM;
     if (!gemm_f32_supported(L, g)) throw Fail{WSSR_ERR_UNSUPPORTED, "operands not TMA-aligned"};
     WSSR_CUDA(gemm_f32a(ctx->c, L, g, 1024, ctx->c.stream));
+  });
+}
+
+int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k,
+                          const void* a, int64_t lda, int a_f32, const double* shift,
+                          const double* b, int64_t ldb, double* c, int64_t ldc, double alpha) {
+  return guarded(ctx, [&] {
+    Context& cx = ctx->c;
+    const Layout L = layout == 0 ? Layout::CM : Layout::RM;
+    GemmArgs g{reinterpret_cast<const double*>(a), lda, b, ldb, shift, c, ldc, m, n, k, 0, alpha,
+               0, nullptr, nullptr, 0};
+    if (!ozaki_supported(L, g, a_f32 != 0)) throw Fail{WSSR_ERR_UNSUPPORTED, "operands not TMA-aligned"};
+    // parameters run along K (RM) or M (CM); samples along the other
+    const int64_t params = L == Layout::RM ? k : m, samples = L == Layout::RM ? m : k;
+    Buf scale((size_t)2 * ozaki_scale_len(params), cx.stream);
+    WSSR_CUDA(ozaki_scales(cx, a, a_f32 != 0, lda, samples, params, shift, scale, cx.stream));
+    WSSR_CUDA(ozaki_gemm(cx, L, g, a_f32 != 0, scale, cx.stream));
+    sync(cx);
   });
 }
 

@@ -35,6 +35,10 @@ struct Context {
   int64_t gemm_launches = 0;  // statistics for bench.py
   int64_t kernel_launches = 0;
   bool disable_tma = false;  // force the cp.async GEMM path (tests / A-B comparisons)
+  bool ozaki = true;         // O-passes on the int8 tensor cores (exact digit products)
+  double oz_min_elems = 4194304.0;  // smallest sample block (elements) sent to that path
+  double* oz_ws = nullptr;   // Ozaki thin-operand digits + factors
+  size_t oz_ws_cap = 0;      // doubles
 
   // optional per-phase timing of the O-passes (CUDA events on the launching stream)
   static constexpr int kPhases = 3;  // 0: v = Ohat^T q, 1: u = Ohat v, 2: assemble column pass

@@ -10,6 +10,49 @@
 
 namespace wssr {
 
+// ---- TMA + mbarrier warp-specialised tiles (gemm_tma.cuh) ----------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a row-major (outer x inner) FP64 array with row pitch `pitch` elements;
+// box = 16 doubles (128 B, SWIZZLE_128B) x box_outer rows.
+bool make_map_2d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch,
+                 int box_outer, int esize = 8) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(pitch * esize, 16)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esize), (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1u, 1u};
+  return fn(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+            const_cast<void*>(ptr), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool make_map_1d(CUtensorMap* map, const double* ptr, int64_t n, int box) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t bx[1] = {(cuuint32_t)box};
+  cuuint32_t es[1] = {1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double*>(ptr), dims, strides, bx,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 namespace {
 
 thread_local int64_t g_launches = 0;
@@ -56,49 +99,6 @@ struct Tile {
     return occ;
   }
 };
-
-// ---- TMA + mbarrier warp-specialised tiles (gemm_tma.cuh) ----------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// 2-D map over a row-major (outer x inner) FP64 array with row pitch `pitch` elements;
-// box = 16 doubles (128 B, SWIZZLE_128B) x box_outer rows.
-bool make_map_2d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch,
-                 int box_outer, int esize = 8) {
-  auto fn = tma_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)std::max<int64_t>(pitch * esize, 16)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / esize), (cuuint32_t)box_outer};
-  cuuint32_t es[2] = {1u, 1u};
-  return fn(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-            const_cast<void*>(ptr), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-bool make_map_1d(CUtensorMap* map, const double* ptr, int64_t n, int box) {
-  auto fn = tma_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[1] = {(cuuint64_t)n};
-  cuuint64_t strides[1] = {0};
-  cuuint32_t bx[1] = {(cuuint32_t)box};
-  cuuint32_t es[1] = {1u};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double*>(ptr), dims, strides, bx,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST, typename TA = double,
           bool PERSIST = false>

@@ -1,0 +1,812 @@
+// FP64 O-pass GEMMs as exact integer digit products on the 5th-generation tensor cores.
+//
+// FP64 tensor math on sm_100a is DMMA (mma.sync m8n8k4, ~37 TF/s measured), which puts the two
+// O-passes of every SSI iteration (svdengine.py:133-134) 3x above the HBM time of streaming O.
+// This path computes the same FP64 products exactly in integer arithmetic on tcgen05.mma
+// kind::i8 (the Ozaki splitting):
+//
+//   * every element of the centred sample block  x = O - mu  is scaled by a power of two per
+//     parameter column p (2^(54-e_p), e_p = exponent bound of max_n |O_np - mu_p|) and rounded to
+//     an integer |X| < 2^54, split into 7 signed base-256 digits  X = sum_i d_i 256^i,
+//     d_i in [-128, 127] (bytes of X + 0x0080808080808080, each XOR 0x80);
+//   * the thin operand (q or v, P x k / N x k) is split the same way per output column;
+//   * digit products are exact int8 x int8 -> int32 tensor-core MMAs; the 34 digit pairs (a, b)
+//     with a + b <= 7 (most-significant-first) are kept - the dropped ones sum below 2^-59 of
+//     the product of the column scales - and pairs of equal significance a + b = s share one
+//     int32 TMEM accumulator D_s, 8 x 64 columns = all 512 (no overflow: 7 pairs x 2^14 x
+//     K-chunk <= 16384 < 2^31);
+//   * the epilogue combines sum_s D_s 2^(96 - 8 s) in FP64 and applies the power-of-two scales.
+//
+// Each element is thus represented to 2^-54 of its column's magnitude and every product and sum
+// of digits is exact, so the result is FP64-grade (tests/test_gpu_ozaki.py compares the error
+// with DMMA's against an exact reference).  O is read once per pass in its storage type (FP64
+// or FP32) and digitised in shared memory on the fly: the pass is HBM-bound instead of
+// FP64-tensor-bound.
+//
+// Kernel structure (one CTA per SM, persistent over work units = (row tile, 64-column block,
+// K chunk)):
+//   warp 0      TMA producer of the raw ring: O tile (+ mu/scale slice), 4 stages, freed by the
+//               converters as soon as they have digitised it;
+//   warp 2      TMA producer of the thin-operand digit tiles (4-stage ring);
+//   warp 1      TMEM allocator and the single MMA-issuing thread (tcgen05.mma kind::i8, D in
+//               TMEM, tcgen05.commit frees the digit stage);
+//   warps 4-11  converters: FP64 tile -> 7 int8 digit planes (K-major, 32-byte swizzle) in shared
+//               memory, then the epilogue (tcgen05.ld of the 8 accumulators, FP64 combine, store).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "engine.h"
+#include "gemm.cuh"
+#include "gemm_tma.cuh"
+#include "ozaki.h"
+
+namespace wssr {
+
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn();
+bool make_map_2d(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch,
+                 int box_outer, int esize);
+bool make_map_1d(CUtensorMap* map, const double* ptr, int64_t n, int box);
+
+namespace oz {
+
+constexpr int BM = 128;            // rows of the output tile (TMEM lanes)
+constexpr int BK = 32;             // K per stage (one kind::i8 MMA-K)
+constexpr int ND = 7;              // digits per operand
+constexpr int NL = 8;              // significance levels kept (s = a + b <= 7), one TMEM block each
+constexpr int NB = 64;             // output columns per unit
+constexpr int BROWS = ND * NB;     // thin-operand digit rows per stage (448)
+constexpr int RSTAGES = 3;         // raw tile ring (TMA -> converters)
+constexpr int DSTAGES = 2;         // sample-digit ring (converters -> MMA)
+constexpr int BSTAGES = 4;         // thin-operand digit ring (TMA -> MMA)
+constexpr int KCHUNK = 16384;      // int32 accumulator bound (see header)
+constexpr int kConvWarps = 16;
+constexpr int kThreads = 32 * (4 + kConvWarps);
+constexpr uint64_t kBias = 0x0080808080808080ull;
+
+constexpr int A_RAW = BM * BK * 8;            // 32 KB (FP64 tile; FP32 uses half)
+constexpr int A_DIG = ND * BM * BK;           // 28 KB
+constexpr int B_DIG = BROWS * BK;             // 14 KB
+constexpr int MI_BYTES = 2 * BK * 8;          // mu / scale slice (row-major mode only)
+constexpr int RSTAGE = A_RAW;                 // raw tile, 1 KB aligned
+constexpr int DSTAGE = A_DIG;                 // 28 KB, 1 KB aligned
+constexpr int BSTAGE = B_DIG;                 // 14 KB, 1 KB aligned
+constexpr size_t kSmem = (size_t)RSTAGE * RSTAGES + (size_t)DSTAGE * DSTAGES +
+                         (size_t)BSTAGE * BSTAGES + (size_t)MI_BYTES * RSTAGES + 256 + 1024;
+static_assert(kSmem <= 232448, "shared memory budget");
+
+// ---- tcgen05 / TMEM wrappers ------------------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t addr) {
+  // K-major, SWIZZLE_32B: rows of 32 B, 8-row groups 256 B apart (SBO); LBO unused (1);
+  // version 1 (sm_100); layout type 6.
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | (16ull << 32) | (1ull << 46) |
+         (6ull << 61);
+}
+__device__ __forceinline__ uint32_t idesc_i8(int n) {
+  // D s32 (bits 4-5 = 2), A/B signed 8-bit (bits 7-9, 10-12 = 1), both K-major,
+  // N >> 3 at bits 17-22, M >> 4 at bits 24-28 (M = 128).
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// Biased integers Y = X + kBias -> digit planes: plane a holds byte (6 - a) of every Y (most
+// significant digit first), XOR 0x80 = the signed digit.
+// 8 biased integers -> 7 digit planes x 8 bytes (2 words each)
+__device__ __forceinline__ void pack_digits8(const uint64_t (&y)[8], uint32_t (&w)[ND][2]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t l0 = (uint32_t)y[4 * q], l1 = (uint32_t)y[4 * q + 1];
+    const uint32_t l2 = (uint32_t)y[4 * q + 2], l3 = (uint32_t)y[4 * q + 3];
+    const uint32_t h0 = (uint32_t)(y[4 * q] >> 32), h1 = (uint32_t)(y[4 * q + 1] >> 32);
+    const uint32_t h2 = (uint32_t)(y[4 * q + 2] >> 32), h3 = (uint32_t)(y[4 * q + 3] >> 32);
+    uint32_t u0 = __byte_perm(l0, l1, 0x5140), u1 = __byte_perm(l0, l1, 0x7362);
+    uint32_t v0 = __byte_perm(l2, l3, 0x5140), v1 = __byte_perm(l2, l3, 0x7362);
+    w[6][q] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
+    w[5][q] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
+    w[4][q] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
+    w[3][q] = __byte_perm(u1, v1, 0x7632) ^ 0x80808080u;
+    u0 = __byte_perm(h0, h1, 0x5140);
+    u1 = __byte_perm(h0, h1, 0x7362);
+    v0 = __byte_perm(h2, h3, 0x5140);
+    v1 = __byte_perm(h2, h3, 0x7362);
+    w[2][q] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
+    w[1][q] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
+    w[0][q] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
+  }
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// mbarrier wait that suspends the thread in hardware until the phase flips (single-thread
+// producer / MMA roles: no issue slots burnt spinning)
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t to_biased(double x) {
+  return (uint64_t)__double2ll_rn(x) + kBias;
+}
+
+struct Params {
+  // A: the sample block.  RM: A is (M x K) row-major (rows = samples, K = parameters, the
+  // v = Ohat^T q pass); CM: A is stored (K x M) row-major (K = samples, M = parameters, the
+  // u = Ohat v pass).
+  int64_t M, K, N;
+  int nblk, nch, mtiles;
+  int64_t kblocks;
+  const double* mu_inv;    // [Kpad or M][2] = {mu_p, 2^(54 - e_p)} per parameter column
+  const double* colfac;    // [nblk * 64] thin-operand column factors
+  double alpha;
+  double* C;
+  int64_t ldc;
+  int accumulate;
+  double* slab;            // nch > 1: [nch][M][N] partial results
+  int debug;               // profiling only: 1 = skip digitising, 2 = skip MMAs, 3 = both, 4 = skip the sample-block loads too
+};
+
+template <bool RM, typename TA>
+__global__ void __launch_bounds__(kThreads, 1)
+    ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmS, const Params p) {
+  constexpr bool F32 = sizeof(TA) == 4;
+  constexpr int A_BYTES = BM * BK * (int)sizeof(TA);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1 KB-aligned base, derived from smem_raw without an integer round trip so every access
+  // stays an explicit shared-memory instruction
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* dring = smem + (size_t)RSTAGE * RSTAGES;
+  unsigned char* bring = dring + (size_t)DSTAGE * DSTAGES;
+  unsigned char* miring = bring + (size_t)BSTAGE * BSTAGES;
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(miring + (size_t)MI_BYTES * RSTAGES);
+  uint64_t* rempty = rfull + RSTAGES;
+  uint64_t* bfull = rempty + RSTAGES;
+  uint64_t* bempty = bfull + BSTAGES;
+  uint64_t* conv = bempty + BSTAGES;
+  uint64_t* dempty = conv + DSTAGES;
+  uint64_t* tfull = dempty + DSTAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto a_raw = [&](int s) { return smem + (size_t)s * RSTAGE; };
+  auto s_mi = [&](int s) { return reinterpret_cast<const double*>(miring + (size_t)s * MI_BYTES); };
+  auto a_dig = [&](int d) { return dring + (size_t)d * DSTAGE; };
+  auto b_dig = [&](int b) { return bring + (size_t)b * BSTAGE; };
+
+  if (tid == 0) {
+    for (int s = 0; s < RSTAGES; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], kConvWarps);
+    }
+    for (int d = 0; d < DSTAGES; ++d) {
+      mbar_init(&conv[d], kConvWarps);
+      mbar_init(&dempty[d], 1);
+    }
+    for (int b = 0; b < BSTAGES; ++b) {
+      mbar_init(&bfull[b], 1);
+      mbar_init(&bempty[b], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kConvWarps);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t units = (int64_t)p.mtiles * p.nblk * p.nch;
+  auto decode = [&](int64_t u, int64_t& m0, int& nb, int& kc, int64_t& kb0, int64_t& kb1) {
+    m0 = (u % p.mtiles) * BM;
+    const int64_t rest = u / p.mtiles;
+    nb = (int)(rest % p.nblk);
+    kc = (int)(rest / p.nblk);
+    kb0 = p.kblocks * kc / p.nch;
+    kb1 = p.kblocks * (kc + 1) / p.nch;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer: raw ring =====
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      if (RM) prefetch_tmap(&tmS);
+      uint32_t g = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t m0, kb0, kb1;
+        int nb, kc;
+        decode(u, m0, nb, kc, kb0, kb1);
+        for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % RSTAGES;
+          mbar_sleep_wait(&rempty[s], ((g / RSTAGES) & 1) ^ 1);
+          const int k0 = (int)(kb * BK);
+          if (p.debug == 4) {  // profiling: no sample-block traffic at all
+            mbar_arrive(&rfull[s]);
+            continue;
+          }
+          mbar_arrive_expect_tx(&rfull[s], A_BYTES + (RM ? MI_BYTES : 0));
+          if (RM) {
+            tma_load_2d(a_raw(s), &tmA, k0, (int)m0, &rfull[s]);
+            if (!F32) tma_load_2d(a_raw(s) + 16384, &tmA, k0 + 16, (int)m0, &rfull[s]);
+            tma_load_1d((void*)s_mi(s), &tmS, 2 * k0, &rfull[s]);
+          } else {
+            tma_load_2d(a_raw(s), &tmA, (int)m0, k0, &rfull[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ===== TMA producer: thin-operand digit tiles =====
+    if (lane == 0) {
+      prefetch_tmap(&tmB);
+      uint32_t g = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t m0, kb0, kb1;
+        int nb, kc;
+        decode(u, m0, nb, kc, kb0, kb1);
+        for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+          const int b = g % BSTAGES;
+          mbar_sleep_wait(&bempty[b], ((g / BSTAGES) & 1) ^ 1);
+          const int k0 = (int)(kb * BK);
+          mbar_arrive_expect_tx(&bfull[b], B_DIG);
+          tma_load_2d(b_dig(b), &tmB, k0, nb * BROWS, &bfull[b]);
+          tma_load_2d(b_dig(b) + 224 * BK, &tmB, k0, nb * BROWS + 224, &bfull[b]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: the whole warp walks the schedule (descriptors stay warp-uniform), one
+    // elected lane issues =====
+    uint32_t g = 0, t = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      int64_t m0, kb0, kb1;
+      int nb, kc;
+      decode(u, m0, nb, kc, kb0, kb1);
+      mbar_sleep_wait(tempty, (t & 1) ^ 1);
+      tc_fence_after();
+      for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        const int d = g % DSTAGES, bs = g % BSTAGES;
+        mbar_sleep_wait(&bfull[bs], (g / BSTAGES) & 1);
+        mbar_sleep_wait(&conv[d], (g / DSTAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          if (p.debug != 2 && p.debug != 3) {
+            const uint32_t abase = smem_u32(a_dig(d)), bbase = smem_u32(b_dig(bs));
+            // 11 MMAs: digit a of the sample block against the thin digits b <= min(6, 7 - a),
+            // written to the level blocks D_(a+b) (TMEM columns 64 (a+b) ...).  Digit 1 goes
+            // first and digit 0's range is split at column 64, so on a unit's first K-block
+            // every TMEM column is first written by an MMA with accumulate = 0.
+            const uint32_t first = kb == kb0 ? 0u : 1u;
+            const uint64_t ad1 = smem_desc_sw32(abase + 1 * BM * BK);
+            const uint64_t ad0 = smem_desc_sw32(abase);
+            mma_i8(tmem + 64, ad1, smem_desc_sw32(bbase), idesc_i8(256), first);
+            mma_i8(tmem + 320, ad1, smem_desc_sw32(bbase + 256 * BK), idesc_i8(192), first);
+            mma_i8(tmem + 0, ad0, smem_desc_sw32(bbase), idesc_i8(64), first);
+            mma_i8(tmem + 64, ad0, smem_desc_sw32(bbase + 64 * BK), idesc_i8(256), 1u);
+            mma_i8(tmem + 320, ad0, smem_desc_sw32(bbase + 320 * BK), idesc_i8(128), 1u);
+#pragma unroll
+            for (int a = 2; a < ND; ++a) {
+              const uint64_t adesc = smem_desc_sw32(abase + a * BM * BK);
+              int col = NB * a, brow = 0, left = NB * (NL - a);
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                if (left > 0) {
+                  const int n = left > 256 ? 256 : left;
+                  mma_i8(tmem + col, adesc, smem_desc_sw32(bbase + brow * BK), idesc_i8(n), 1u);
+                  col += n;
+                  brow += n;
+                  left -= n;
+                }
+              }
+            }
+          }
+          mma_commit(&dempty[d]);
+          mma_commit(&bempty[bs]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(tfull);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ===== converters + epilogue =====
+    // converter warp cw owns tile rows 8 (cw % 16) .. +7; lane = r8 + 8 q: row r8, K quarter q
+    // (8 consecutive K values) - quarter-warps read 8 rows of one K range (conflict-free under
+    // the 128-byte swizzle) and a warp's digit stores cover 8 full 32-byte rows.
+    const int cw = warp - 4;
+    const int q = lane >> 3;
+    const int row = 8 * cw + (lane & 7);
+    const int quad = warp & 3;                // TMEM lane quadrant of this warp (epilogue)
+    const int ecol = 16 * (cw >> 2);          // epilogue column group
+    const int erow = quad * 32 + lane;
+    uint32_t g = 0, t = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      int64_t m0, kb0, kb1;
+      int nb, kc;
+      decode(u, m0, nb, kc, kb0, kb1);
+      double mu_r = 0.0, inv_r = 0.0;
+      if (!RM) {
+        const int64_t pm = m0 + row;
+        if (pm < p.M) {
+          mu_r = p.mu_inv[2 * pm];
+          inv_r = p.mu_inv[2 * pm + 1];
+        }
+      }
+      for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        const int s = g % RSTAGES, d = g % DSTAGES;
+        mbar_wait(&rfull[s], (g / RSTAGES) & 1);
+        uint64_t y[8];
+        if (p.debug == 1 || p.debug == 3 || p.debug == 4) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rempty[s]);
+          mbar_wait(&dempty[d], ((g / DSTAGES) & 1) ^ 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[d]);
+          continue;
+        }
+        if (RM) {
+          const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + 8 * q;
+          if (F32) {
+            const unsigned char* base = a_raw(s) + row * 128;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const float4 f = *reinterpret_cast<const float4*>(
+                  base + (((2 * q + c) ^ (row & 7)) << 4));
+              const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const double2 m = mi[4 * c + e];
+                y[4 * c + e] = to_biased(((double)fv[e] - m.x) * m.y);
+              }
+            }
+          } else {
+            const unsigned char* base = a_raw(s) + (q >> 1) * 16384 + row * 128;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double2 v = *reinterpret_cast<const double2*>(
+                  base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
+              const double2 m0v = mi[2 * c], m1v = mi[2 * c + 1];
+              y[2 * c] = to_biased((v.x - m0v.x) * m0v.y);
+              y[2 * c + 1] = to_biased((v.y - m1v.x) * m1v.y);
+            }
+          }
+        } else {
+          const TA* base = reinterpret_cast<const TA*>(a_raw(s)) + (8 * q) * BM + row;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) y[i] = to_biased(((double)base[i * BM] - mu_r) * inv_r);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[s]);  // raw tile consumed (values are in registers)
+        uint32_t w[ND][2];
+        pack_digits8(y, w);
+        mbar_wait(&dempty[d], ((g / DSTAGES) & 1) ^ 1);  // MMA done with this digit slot
+        unsigned char* dst =
+            a_dig(d) + row * BK + ((((q >> 1) ^ ((row >> 2) & 1))) << 4) + ((q & 1) << 3);
+#pragma unroll
+        for (int a = 0; a < ND; ++a)
+          *reinterpret_cast<uint2*>(dst + a * BM * BK) = make_uint2(w[a][0], w[a][1]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[d]);
+      }
+      // ---- epilogue: D_s (s = 0..7) -> FP64 ----
+      mbar_sleep_wait(tfull, t & 1);
+      tc_fence_after();
+      const int64_t gm = m0 + erow;
+      double rowfac = 1.0;
+      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[2 * gm + 1];
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int sd = 0; sd < NL; ++sd) {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + NB * sd + ecol, r);
+        tmem_ld_wait();
+        const double wgt = __longlong_as_double((long long)(1023 + 96 - 8 * sd) << 52);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)r[j], wgt, acc[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);  // TMEM may be overwritten by the next unit
+      if (gm < p.M) {
+        const int64_t gj0 = (int64_t)nb * NB + ecol;
+        const double rf = p.alpha * rowfac;
+        if (p.nch > 1) {
+          double* dst = p.slab + ((int64_t)kc * p.M + gm) * p.N;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (gj0 + j < p.N) dst[gj0 + j] = rf * p.colfac[gj0 + j] * acc[j];
+        } else {
+          double* dst = p.C + gm * p.ldc;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (gj0 + j < p.N) {
+              const double v = rf * p.colfac[gj0 + j] * acc[j];
+              dst[gj0 + j] = p.accumulate ? dst[gj0 + j] + v : v;
+            }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem)
+                 : "memory");
+  }
+}
+
+// ---- column scales of the centred sample block -------------------------------------------------
+// max_n |fl(O_np - mu_p)| per parameter column p, as the bit pattern of a nonnegative double
+// (order-preserving as an unsigned integer, so atomicMax is exact and order-independent).
+template <typename TA, bool RM>
+__global__ void __launch_bounds__(256)
+    colmax_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                  const double* __restrict__ mu, unsigned long long* __restrict__ out) {
+  // element (sample n, parameter p) at A[n * lda + p] in both layouts (row-major sample block)
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= cols) return;
+  const double m = mu ? mu[p] : 0.0;
+  const int64_t r0 = rows * blockIdx.y / gridDim.y, r1 = rows * (blockIdx.y + 1) / gridDim.y;
+  double best = 0.0;
+  int64_t n = r0;
+  for (; n + 4 <= r1; n += 4) {
+    const double a0 = fabs((double)A[n * lda + p] - m);
+    const double a1 = fabs((double)A[(n + 1) * lda + p] - m);
+    const double a2 = fabs((double)A[(n + 2) * lda + p] - m);
+    const double a3 = fabs((double)A[(n + 3) * lda + p] - m);
+    best = fmax(best, fmax(fmax(a0, a1), fmax(a2, a3)));
+  }
+  for (; n < r1; ++n) best = fmax(best, fabs((double)A[n * lda + p] - m));
+  if (best > 0.0) atomicMax(out + p, (unsigned long long)__double_as_longlong(best));
+}
+
+// mu_inv[p] = {mu_p, 2^(54 - e_p)} with max_p < 2^e_p; padding columns {0, 0}.
+__global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
+                              const double* __restrict__ mu, int64_t cols, int64_t cols_pad,
+                              double* __restrict__ mu_inv) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cols_pad;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    double m = 0.0, inv = 0.0;
+    if (p < cols) {
+      m = mu ? mu[p] : 0.0;
+      int e = 0;
+      frexp(__longlong_as_double((long long)cmax[p]), &e);  // max < 2^e (0 -> e = 0)
+      inv = ldexp(1.0, 54 - e);
+    }
+    mu_inv[2 * p] = m;
+    mu_inv[2 * p + 1] = inv;
+  }
+}
+
+// ---- thin operand: column maxima and digits ---------------------------------------------------
+// w_kj = B_kj * rowmul_k (rowmul_k = 2^e_k = 2^54 / inv_k of the K-side parameter column, or 1)
+__device__ __forceinline__ double thin_value(const double* B, int64_t ldb, int64_t k, int64_t j,
+                                             const double* mu_inv) {
+  const double b = B[k * ldb + j];
+  if (!mu_inv) return b;
+  // 2^54 / inv exactly, from the exponent field of the power of two inv (no division)
+  const long long ebits = __double_as_longlong(mu_inv[2 * k + 1]) >> 52;
+  return b * __longlong_as_double((long long)(2046 + 54 - ebits) << 52);
+}
+
+__global__ void __launch_bounds__(256)
+    thin_colmax_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
+                       const double* __restrict__ mu_inv, unsigned long long* __restrict__ out) {
+  // block: 4 k-lanes x 64 columns over 128 rows of K
+  const int j = threadIdx.x & 63, kl = threadIdx.x >> 6;
+  const int64_t jj = (int64_t)blockIdx.y * 64 + j;
+  double best = 0.0;
+  if (jj < N) {
+    const int64_t k1 = min(K, (int64_t)(blockIdx.x + 1) * 128);
+    for (int64_t k = (int64_t)blockIdx.x * 128 + kl; k < k1; k += 4) {
+      if (mu_inv && mu_inv[2 * k + 1] == 0.0) continue;
+      best = fmax(best, fabs(thin_value(B, ldb, k, jj, mu_inv)));
+    }
+  }
+  __shared__ double red[4][64];
+  red[kl][j] = best;
+  __syncthreads();
+  if (kl == 0 && jj < N) {
+    best = fmax(fmax(red[0][j], red[1][j]), fmax(red[2][j], red[3][j]));
+    if (best > 0.0) atomicMax(out + jj, (unsigned long long)__double_as_longlong(best));
+  }
+}
+
+// digits: Bd[(nb*7 + a)*64 + jj][k] (K contiguous, kpad columns), colfac[nb*64 + jj]
+__global__ void __launch_bounds__(256)
+    thin_digits_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
+                       int64_t kpad, const double* __restrict__ mu_inv,
+                       const unsigned long long* __restrict__ cmax, int extra_exp,
+                       int8_t* __restrict__ Bd, double* __restrict__ colfac) {
+  // block tile: 32 k x 64 columns of one 64-column block nb = blockIdx.y
+  __shared__ __align__(16) uint8_t tile[ND][64][32 + 16];
+  const int nb = blockIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  const int j = threadIdx.x & 63, kq = threadIdx.x >> 6;  // 4 k-lanes
+  const int64_t jj = (int64_t)nb * 64 + j;
+  double inv = 0.0;
+  int e = 0;
+  if (jj < N) {
+    frexp(__longlong_as_double((long long)cmax[jj]), &e);
+    inv = ldexp(1.0, 54 - e);
+    if (blockIdx.x == 0 && kq == 0) colfac[jj] = ldexp(1.0, e - 54 - extra_exp);
+  } else if (blockIdx.x == 0 && kq == 0) {
+    colfac[jj] = 0.0;
+  }
+  for (int kk = kq; kk < 32; kk += 4) {
+    const int64_t k = k0 + kk;
+    double x = 0.0;
+    if (jj < N && k < K && !(mu_inv && mu_inv[2 * k + 1] == 0.0))
+      x = thin_value(B, ldb, k, jj, mu_inv) * inv;
+    const uint64_t y = to_biased(x);
+#pragma unroll
+    for (int a = 0; a < ND; ++a) tile[a][j][kk] = (uint8_t)((y >> (8 * (6 - a))) & 0xFF) ^ 0x80;
+  }
+  __syncthreads();
+  // write out: 7 x 64 rows x 32 bytes, 16 bytes per thread-step
+  for (int idx = threadIdx.x; idx < ND * 64 * 2; idx += blockDim.x) {
+    const int half = idx & 1, rr = idx >> 1, a = rr / 64, jr = rr % 64;
+    const int64_t kk0 = k0 + 16 * half;
+    if (kk0 >= kpad) continue;
+    const uint4 v = *reinterpret_cast<const uint4*>(&tile[a][jr][16 * half]);
+    *reinterpret_cast<uint4*>(Bd + ((int64_t)(nb * ND + a) * 64 + jr) * kpad + kk0) = v;
+  }
+}
+
+bool make_map_i8(CUtensorMap* map, const int8_t* ptr, int64_t inner, int64_t outer) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)inner};
+  cuuint32_t box[2] = {(cuuint32_t)BK, 224u};
+  cuuint32_t es[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(ptr), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// (K x M) row-major sample block, box = 128 parameters x 32 samples, no swizzle
+bool make_map_cm(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch,
+                 int esize) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(pitch * esize)};
+  cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)BK};
+  cuuint32_t es[2] = {1u, 1u};
+  return fn(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+            const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool RM, typename TA>
+cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tS,
+                   const Params& p, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<RM, TA>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  ozaki_gemm_kernel<RM, TA><<<grid, kThreads, kSmem, st>>>(tA, tB, tS, p);
+  return cudaGetLastError();
+}
+
+}  // namespace oz
+
+// ---- host side ---------------------------------------------------------------------------------
+int64_t ozaki_scale_len(int64_t cols) { return ((cols + oz::BK - 1) / oz::BK) * oz::BK; }
+
+cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
+                         int64_t cols, const double* mu, double* mu_inv, cudaStream_t st) {
+  const int64_t cpad = ozaki_scale_len(cols);
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ctx.splitk_buffer(cols));
+  if (!cmax) return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(double) * cols, st);
+  if (e != cudaSuccess) return e;
+  const int gx = (int)((cols + 255) / 256);
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(rows / 64, (8 * ctx.num_sms + gx - 1) / gx));
+  if (f32)
+    oz::colmax_kernel<float, true><<<dim3(gx, gy), 256, 0, st>>>(
+        static_cast<const float*>(A), lda, rows, cols, mu, cmax);
+  else
+    oz::colmax_kernel<double, true><<<dim3(gx, gy), 256, 0, st>>>(
+        static_cast<const double*>(A), lda, rows, cols, mu, cmax);
+  oz::mu_inv_kernel<<<(int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0, st>>>(
+      cmax, mu, cols, cpad, mu_inv);
+  ctx.kernel_launches += 2;
+  return cudaGetLastError();
+}
+
+bool ozaki_supported(Layout L, const GemmArgs& a, bool f32) {
+  const size_t es = f32 ? 4 : 8;
+  return tma_encode_fn() != nullptr && (reinterpret_cast<uintptr_t>(a.A) % 16 == 0) &&
+         ((a.lda * es) % 16 == 0) && a.M < (1LL << 31) && a.K < (1LL << 31) &&
+         a.N <= 4096 && !a.partial && !a.Cin && (L == Layout::RM || L == Layout::CM);
+}
+
+cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
+                       cudaStream_t st) {
+  using namespace oz;
+  const bool RMm = L == Layout::RM;
+  const int64_t M = a.M, N = a.N, K = a.K;
+  if (M == 0 || N == 0) return cudaSuccess;
+  const int nblk = (int)((N + NB - 1) / NB);
+  const int64_t kpad = ((K + BK - 1) / BK) * BK;
+  const int64_t kblocks = kpad / BK;
+  const int mtiles = (int)((M + BM - 1) / BM);
+  // thin-operand digits + factors (workspace owned by the context)
+  const size_t dig_bytes = (size_t)nblk * BROWS * kpad;
+  const size_t ws_doubles = (dig_bytes + 7) / 8 + (size_t)nblk * NB + N + 64;
+  if (ctx.oz_ws_cap < ws_doubles) {
+    if (ctx.oz_ws) cudaFreeAsync(ctx.oz_ws, st);
+    ctx.oz_ws = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ctx.oz_ws), ws_doubles * 8, st);
+    if (e != cudaSuccess) return e;
+    ctx.oz_ws_cap = ws_doubles;
+  }
+  int8_t* Bd = reinterpret_cast<int8_t*>(ctx.oz_ws);
+  double* colfac = ctx.oz_ws + (dig_bytes + 7) / 8;
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(colfac + (size_t)nblk * NB);
+  cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(double) * N, st);
+  if (e != cudaSuccess) return e;
+  // RM (v = Ohat^T q): the thin operand's rows are parameters -> carries the column scales
+  const double* bmu = RMm ? mu_inv : nullptr;
+  {
+    thin_colmax_kernel<<<dim3((unsigned)((K + 127) / 128), nblk), 256, 0, st>>>(a.B, a.ldb, K, N,
+                                                                               bmu, cmax);
+    thin_digits_kernel<<<dim3((unsigned)((kpad + 31) / 32), nblk), 256, 0, st>>>(
+        a.B, a.ldb, K, N, kpad, bmu, cmax, RMm ? 54 : 0, Bd, colfac);
+    ctx.kernel_launches += 2;
+  }
+  // K chunks: int32 bound, then enough units to fill the machine evenly
+  int nch = (int)((kpad + KCHUNK - 1) / KCHUNK);
+  {
+    const int64_t base = (int64_t)mtiles * nblk;
+    int best = nch;
+    double best_eff = 0.0;
+    for (int c = nch; c <= std::max(nch, 64); ++c) {
+      if ((int64_t)c > kblocks) break;
+      const int64_t units = base * c;
+      const int64_t waves = (units + ctx.num_sms - 1) / ctx.num_sms;
+      const double eff = (double)units / ((double)waves * ctx.num_sms);
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        best = c;
+      }
+      if (eff >= 0.92 && units >= ctx.num_sms) break;
+    }
+    nch = best;
+  }
+  Params p{};
+  p.M = M;
+  p.K = K;
+  p.N = N;
+  p.nblk = nblk;
+  p.nch = nch;
+  p.mtiles = mtiles;
+  p.kblocks = kblocks;
+  p.mu_inv = mu_inv;
+  p.colfac = colfac;
+  p.alpha = a.alpha;
+  p.C = a.C;
+  p.ldc = a.ldc;
+  p.accumulate = a.accumulate;
+  p.slab = nullptr;
+  {
+    static const int dbg = [] {
+      const char* e = std::getenv("WSSR_OZ_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    p.debug = dbg;
+  }
+  if (nch > 1) {
+    p.slab = ctx.splitk_buffer((size_t)nch * M * N);
+    if (!p.slab) return cudaErrorMemoryAllocation;
+  }
+  CUtensorMap tA, tB, tS;
+  std::memset(&tS, 0, sizeof(tS));
+  const int es = f32 ? 4 : 8;
+  bool ok;
+  if (RMm) {
+    ok = make_map_2d(&tA, a.A, K, M, a.lda, BM, es) &&
+         make_map_1d(&tS, mu_inv, 2 * kpad, 2 * BK);
+  } else {
+    ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
+  }
+  ok = ok && make_map_i8(&tB, Bd, kpad, (int64_t)nblk * BROWS);
+  if (!ok) return cudaErrorInvalidValue;
+  const int64_t units = (int64_t)mtiles * nblk * nch;
+  const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
+  if (RMm)
+    e = f32 ? launch<true, float>(tA, tB, tS, p, grid, st) : launch<true, double>(tA, tB, tS, p, grid, st);
+  else
+    e = f32 ? launch<false, float>(tA, tB, tS, p, grid, st) : launch<false, double>(tA, tB, tS, p, grid, st);
+  ctx.kernel_launches += 1;
+  ctx.gemm_launches += 1;
+  if (e != cudaSuccess || nch == 1) return e;
+  const int64_t total = M * N;
+  const int rb = (int)std::min<int64_t>((total + 255) / 256, 16 * ctx.num_sms);
+  if (nch <= 8)
+    splitk_reduce_few_kernel<<<rb, 256, 0, st>>>(p.slab, nch, M, N, a.C, a.ldc, 1.0, a.accumulate,
+                                                nullptr, 0);
+  else
+    splitk_reduce_kernel<<<(int)std::min<int64_t>((total + 31) / 32, 16 * ctx.num_sms), 256, 0,
+                           st>>>(p.slab, nch, M, N, a.C, a.ldc, 1.0, a.accumulate, nullptr, 0);
+  ctx.kernel_launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace wssr

@@ -1,0 +1,144 @@
+"""The O-pass GEMMs on the int8 tensor cores (csrc/ozaki.cu: exact digit products, the Ozaki
+splitting) against an extended-precision reference, side by side with the FP64 DMMA path.
+
+Both paths start from the same FP64 centred values fl(O - mu); the reference product is then
+taken in 80-bit long double.  The int8 path must be at least as accurate as FP64 DMMA up to a
+small factor, and well inside the parity tolerances (BASELINE.json: update 1e-10 relative).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift=True):
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    g = torch.Generator(device="cuda").manual_seed(seed + 31 * M + 7 * N + K)
+    opt = dict(dtype=torch.float64, device="cuda", generator=g)
+    params = K if layout == 1 else M
+    # rows 16-byte aligned (the TMA requirement; the engine falls back to DMMA otherwise)
+    if layout == 0:
+        lda = (M + 3) // 4 * 4 + pad * 4
+        A = torch.randn(K, lda, **opt)
+    else:
+        lda = (K + 3) // 4 * 4 + pad * 4
+        A = torch.randn(M, lda, **opt)
+    if scale_cols:  # parameter columns spanning ~12 decades, as real log-derivatives can
+        colscale = torch.logspace(-6, 6, params, dtype=torch.float64, device="cuda")
+        if layout == 0:
+            A[:, :M] *= colscale[None, :]
+        else:
+            A[:, :K] *= colscale[None, :]
+    A = A + 3.0  # a mean to centre away
+    if f32:
+        A = A.float()
+    shift = (A[:, :params].double().mean(0)).contiguous() if with_shift else None
+    ldb = N + 2 * pad
+    B = torch.randn(K, ldb, **opt)
+    out = {}
+    Ad = A.double()
+    sh = shift if shift is not None else torch.zeros(params, dtype=torch.float64, device="cuda")
+    X = (Ad[:, :M] - sh[None, :]).t() if layout == 0 else Ad[:, :K] - sh[None, :]
+    for name in ("ozaki", "dmma"):
+        C = torch.full((M, N + pad), 7.0, dtype=torch.float64, device="cuda")
+        if name == "ozaki":
+            ctx.call("wssr_debug_ozaki_gemm", layout, M, N, K, _lib.ptr(A), lda, int(f32),
+                     _lib.ptr(shift), _lib.ptr(B), ldb, _lib.ptr(C), N + pad, 0.5)
+        else:
+            ctx.lib.wssr_set_gemm_path(ctx.handle, 2)
+            try:
+                if f32:
+                    ctx.call("wssr_debug_gemm_f32a", layout, M, N, K, _lib.ptr(A), lda,
+                             _lib.ptr(shift), _lib.ptr(B), ldb, _lib.ptr(C), N + pad, 0.5)
+                else:
+                    ctx.call("wssr_gemm_f64", layout, M, N, K, _lib.ptr(A), lda, _lib.ptr(shift),
+                             _lib.ptr(B), ldb, _lib.ptr(C), N + pad, 0.5, 0, 1024)
+            finally:
+                ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
+        out[name] = C
+    Xl = X.cpu().numpy().astype(np.longdouble)
+    Bl = B[:, :N].cpu().numpy().astype(np.longdouble)
+    ref = 0.5 * (Xl @ Bl)
+    absref = 0.5 * (np.abs(Xl) @ np.abs(Bl))
+    res = {}
+    for name, C in out.items():
+        Cn = C.cpu().numpy()
+        d = Cn[:, :N].astype(np.longdouble) - ref
+        res[name] = (float(np.sqrt((d * d).sum() / (ref * ref).sum())),
+                     float(np.max(np.abs(d) / absref)))
+        if pad:
+            assert np.all(Cn[:, N:] == 7.0), "leading-dimension padding overwritten"
+    return res
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("M,N,K", [(128, 64, 32), (300, 10, 1000), (1000, 64, 777),
+                                   (513, 65, 4097), (200, 130, 20000), (4096, 1, 512),
+                                   (96, 200, 3000)])
+def test_ozaki_accuracy_vs_dmma(layout, M, N, K):
+    r = _run(layout, M, N, K)
+    oz, dm = r["ozaki"], r["dmma"]
+    assert oz[0] < 2e-15, r
+    assert oz[1] < 1e-14, r
+    assert oz[0] <= 4 * dm[0] + 1e-16, r
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_ozaki_fp32_samples(layout):
+    r = _run(layout, 700, 64, 3000, f32=True, pad=1)
+    assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_ozaki_wide_column_scales(layout):
+    """Per-parameter power-of-two scaling keeps columns spanning 12 decades at FP64 accuracy."""
+    r = _run(layout, 600, 64, 2000, scale_cols=True)
+    assert r["ozaki"][0] < 2e-15, r
+    assert r["ozaki"][1] < 1e-13, r
+
+
+def test_ozaki_no_shift_and_padding():
+    r = _run(1, 257, 33, 1500, with_shift=False, pad=1)
+    assert r["ozaki"][0] < 2e-15, r
+
+
+def test_ozaki_k_chunks_beyond_int32_bound():
+    """K > 16384 splits into chunks (int32 accumulator bound) reduced in fixed order."""
+    r = _run(1, 256, 64, 40000)
+    assert r["ozaki"][0] < 2e-15, r
+    r = _run(0, 300, 64, 40000)
+    assert r["ozaki"][0] < 2e-15, r
+
+
+def test_ozaki_rejects_unaligned_rows():
+    from paper_2512_05749_b200 import _lib, errors
+
+    ctx = _lib.context()
+    A = torch.randn(64, 777, dtype=torch.float64, device="cuda")
+    B = torch.randn(777, 8, dtype=torch.float64, device="cuda")
+    C = torch.empty(64, 8, dtype=torch.float64, device="cuda")
+    with pytest.raises(errors.Unsupported):
+        ctx.call("wssr_debug_ozaki_gemm", 1, 64, 8, 777, _lib.ptr(A), 777, 0, None, _lib.ptr(B), 8,
+                 _lib.ptr(C), 8, 1.0)
+
+
+def test_ozaki_is_deterministic():
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(2048, 4096, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(4096, 64, dtype=torch.float64, device="cuda", generator=g)
+    mu = A.mean(0)
+    outs = []
+    for _ in range(2):
+        C = torch.empty(2048, 64, dtype=torch.float64, device="cuda")
+        ctx.call("wssr_debug_ozaki_gemm", 1, 2048, 64, 4096, _lib.ptr(A), 4096, 0, _lib.ptr(mu),
+                 _lib.ptr(B), 64, _lib.ptr(C), 64, 1.0)
+        outs.append(C)
+    assert torch.equal(outs[0], outs[1])
