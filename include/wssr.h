@@ -79,6 +79,10 @@ typedef struct wssr_ohat_f64 {
   int64_t samples_f32; /* 1: `samples` points to float32 data (FP32 variant, BASELINE configs[3]);
                           the library widens it to FP64 in registers. Requires ld % 4 == 0,
                           16-byte alignment, mu and samples_fro2 (i.e. an assembled bundle). */
+  const double* samples_scale_table; /* optional [2 * roundup(n_params, 32)]: the per-parameter
+                          {mu_p, 2^(54 - e_p)} table of the int8 tensor-core O-passes, as written
+                          by assemble (wssr_assemble_out.scale_table); NULL: computed on demand
+                          with one extra read of the sample block. */
 } wssr_ohat_f64;
 
 /* --- context ------------------------------------------------------------------------------ */
@@ -134,6 +138,8 @@ typedef struct wssr_assemble_out {
   double loss, raw_loss, e_mean, e_std;
   double fro2;      /* ||o_matrix||_F^2                                                      */
   int64_t n_global;
+  double* scale_table; /* optional [2 * roundup(P, 32)]: per-parameter scales of the int8
+                          tensor-core O-passes, from the same column pass (this rank's rows) */
 } wssr_assemble_out;
 int wssr_assemble_f64(wssr_ctx* ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
                       const double* energies, double clip_n_std, wssr_assemble_out* out);
@@ -243,6 +249,10 @@ int wssr_debug_gemm_f32a(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_
 int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k,
                           const void* a, int64_t lda, int a_f32, const double* shift,
                           const double* b, int64_t ldb, double* c, int64_t ldc, double alpha);
+
+/* profiling hook: per-K-block timestamps (SM clock) of CTA 0 of the last int8 O-pass launched
+ * with WSSR_OZ_DEBUG=9, 8 rows x 96 K-blocks (producer, MMA issuers, converter group leaders). */
+int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
 
 /* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
 int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,

@@ -32,6 +32,7 @@ class OhatF64(ctypes.Structure):
         ("hist", _vp), ("hist_rank", _i64), ("hist_ld", _i64), ("hist_scale", _dbl),
         ("samples", _vp), ("n_samples", _i64), ("samples_ld", _i64), ("mu", _vp),
         ("samples_scale", _dbl), ("samples_fro2", _dbl), ("samples_f32", _i64),
+        ("samples_scale_table", _vp),
     ]
 
 
@@ -39,7 +40,7 @@ class AssembleOut(ctypes.Structure):
     _fields_ = [
         ("mu", _vp), ("l_vector", _vp), ("gradient", _vp),
         ("loss", _dbl), ("raw_loss", _dbl), ("e_mean", _dbl), ("e_std", _dbl),
-        ("fro2", _dbl), ("n_global", _i64),
+        ("fro2", _dbl), ("n_global", _i64), ("scale_table", _vp),
     ]
 
 
@@ -116,6 +117,7 @@ SIGNATURES = {
                                               ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
                                               _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                                               ctypes.c_double]),
+    "wssr_debug_ozaki_trace": (ctypes.c_int, [_vp, _vp, ctypes.c_int64]),
     "wssr_gemm_f64": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp, _vp,
                                      _i64, _vp, _i64, _dbl, ctypes.c_int, ctypes.c_int]),
 }
@@ -208,6 +210,11 @@ class Context:
         out = _dbl()
         self.call("wssr_dmma_peak_probe", ctypes.byref(out))
         return float(out.value)
+
+
+def scale_table_len(n_params: int) -> int:
+    """Doubles in the per-parameter scale table of the int8 tensor-core O-passes."""
+    return 2 * ((int(n_params) + 31) // 32 * 32)
 
 
 _contexts: dict = {}

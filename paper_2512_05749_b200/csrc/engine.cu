@@ -393,7 +393,9 @@ struct Ohat {
   const double* mu = nullptr;
   double ss = 1.0;
   bool f32 = false;  // samples stored as float32 (BASELINE configs[3])
-  // per-parameter scale table of the int8 tensor-core path, built on first use (shared by copies)
+  // per-parameter scale table of the int8 tensor-core path: from assemble, or built on first use
+  // (shared by copies)
+  const double* scale_tab = nullptr;
   mutable std::shared_ptr<Buf> oz_scale;
   int64_t cols() const { return r + n; }
 };
@@ -404,11 +406,15 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
   GemmArgs a{o.samp, o.lds, B, ldb, o.mu, C, ldc, M, N, K, 0, alpha, 0, nullptr, nullptr, 0};
   if (ctx.ozaki && !ctx.disable_tma && (double)M * (double)K >= ctx.oz_min_elems &&
       ozaki_supported(layout, a, o.f32)) {
-    if (!o.oz_scale) {
-      o.oz_scale = std::make_shared<Buf>(2 * ozaki_scale_len(o.P), ctx.stream);
-      WSSR_CUDA(ozaki_scales(ctx, o.samp, o.f32, o.lds, o.n, o.P, o.mu, *o.oz_scale, ctx.stream));
+    const double* tab = o.scale_tab;
+    if (!tab) {
+      if (!o.oz_scale) {
+        o.oz_scale = std::make_shared<Buf>(2 * ozaki_scale_len(o.P), ctx.stream);
+        WSSR_CUDA(ozaki_scales(ctx, o.samp, o.f32, o.lds, o.n, o.P, o.mu, *o.oz_scale, ctx.stream));
+      }
+      tab = *o.oz_scale;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, *o.oz_scale, ctx.stream));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream));
     return;
   }
   if (o.f32) {
@@ -705,19 +711,26 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
   const double* lraw = lraw_all + offset;
 
   // one pass over O: column means, centred second moments, centred gradient sums
-  Buf m2(p, st), gsum(p, st);
+  Buf m2(p, st), gsum(p, st), cext;
+  double* cmin = nullptr;
+  double* cmax = nullptr;
+  if (out->scale_table && n > 0) {
+    cext = Buf((size_t)2 * p, st);
+    cmin = cext;
+    cmax = cext + p;
+  }
   if (n > 0) {
     PhaseTimer tm(ctx, 2, 4.0 * n * p, (double)sizeof(T) * n * p);
     const bool al16 = (reinterpret_cast<uintptr_t>(derivs) & 15) == 0;
     if (sizeof(T) == 8 && ld % 2 == 0 && al16) {
       colstats_kernel<T, 2, 8><<<(unsigned)((p + 63) / 64), 32 * kColStatsWarps, 0, st>>>(
-          derivs, n, p, ld, lraw, out->mu, m2, gsum);
+          derivs, n, p, ld, lraw, out->mu, m2, gsum, cmin, cmax);
     } else if (sizeof(T) == 4 && ld % 4 == 0 && al16) {
       colstats_kernel<T, 4, 8><<<(unsigned)((p + 127) / 128), 32 * kColStatsWarps, 0, st>>>(
-          derivs, n, p, ld, lraw, out->mu, m2, gsum);
+          derivs, n, p, ld, lraw, out->mu, m2, gsum, cmin, cmax);
     } else {
       colstats_kernel<T, 1, 8><<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
-          derivs, n, p, ld, lraw, out->mu, m2, gsum);
+          derivs, n, p, ld, lraw, out->mu, m2, gsum, cmin, cmax);
     }
     post_launch(ctx);
   } else {
@@ -744,6 +757,13 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     allreduce(ctx, m2, p);
     allreduce(ctx, gsum, p);
     WSSR_CUDA(cudaMemcpyAsync(out->mu, mu, sizeof(double) * p, cudaMemcpyDeviceToDevice, st));
+  }
+  if (out->scale_table) {
+    if (n > 0) {
+      WSSR_CUDA(ozaki_scales_minmax(ctx, cmin, cmax, out->mu, p, out->scale_table, st));
+    } else {
+      WSSR_CUDA(cudaMemsetAsync(out->scale_table, 0, sizeof(double) * 2 * ozaki_scale_len(p), st));
+    }
   }
   // gradient = 2 * o_matrix @ l_vector = 2 * gsum / N   (estimators.py:93)
   scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, 2.0 / n_global, gsum,
@@ -854,6 +874,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   o.mu = oh.mu;
   o.ss = sq_new * oh.samples_scale;
   o.f32 = oh.samples_f32 != 0;
+  o.scale_tab = oh.samples_scale_table;
   const int64_t cols = o.cols();
   if (k < 1) throw Fail{WSSR_ERR_RANK_TOO_LARGE, "rank must be at least 1"};
 
@@ -1352,6 +1373,7 @@ int wssr_ssi_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, int64_t rank, int
     o.mu = ohat->mu;
     o.ss = ohat->samples_scale;
     o.f32 = ohat->samples_f32 != 0;
+    o.scale_tab = ohat->samples_scale_table;
     if (max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
     const double fro2 = ohat_fro2(c, o, ohat->samples_fro2, true);
     if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
@@ -1449,6 +1471,13 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
     WSSR_CUDA(ozaki_scales(cx, a, a_f32 != 0, lda, samples, params, shift, scale, cx.stream));
     WSSR_CUDA(ozaki_gemm(cx, L, g, a_f32 != 0, scale, cx.stream));
     sync(cx);
+  });
+}
+
+int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n) {
+  return guarded(ctx, [&] {
+    sync(ctx->c);
+    WSSR_CUDA(ozaki_trace(out, (size_t)n * sizeof(long long)));
   });
 }
 

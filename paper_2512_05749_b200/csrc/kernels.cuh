@@ -65,7 +65,8 @@ template <typename T, int VEC, int UNROLL>
 __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
     colstats_kernel(const T* __restrict__ O, int64_t n, int64_t p, int64_t ld,
                     const double* __restrict__ lraw, double* __restrict__ mu,
-                    double* __restrict__ m2, double* __restrict__ gsum) {
+                    double* __restrict__ m2, double* __restrict__ gsum,
+                    double* __restrict__ cmin, double* __restrict__ cmax) {
   __shared__ double sh[kColStatsWarps][5][32 * VEC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t col0 = (int64_t)blockIdx.x * (32 * VEC) + (int64_t)lane * VEC;
@@ -74,10 +75,14 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
   for (int v = 0; v < VEC; ++v) act[v] = col0 + v < p;
   const int64_t rows_per = (n + kColStatsWarps - 1) / kColStatsWarps;
   const int64_t r0 = min(n, (int64_t)w * rows_per), r1 = min(n, r0 + rows_per);
-  double K[VEC], s1[VEC], s2[VEC], sl[VEC];
+  double K[VEC], s1[VEC], s2[VEC], sl[VEC], mn[VEC], mx[VEC];
   double lsum = 0.0;
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) K[v] = s1[v] = s2[v] = sl[v] = 0.0;
+  for (int v = 0; v < VEC; ++v) {
+    K[v] = s1[v] = s2[v] = sl[v] = 0.0;
+    mn[v] = 1.0 / 0.0;
+    mx[v] = -1.0 / 0.0;
+  }
   auto load = [&](int64_t r, double (&x)[VEC]) {
     if constexpr (sizeof(T) == 8 && VEC == 2) {
       if (act[VEC - 1]) {
@@ -121,6 +126,8 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
           s1[v] += d;
           s2[v] = fma(d, d, s2[v]);
           sl[v] = fma(d, l[u], sl[v]);
+          mn[v] = x[u][v] < mn[v] ? x[u][v] : mn[v];  // (no NaN propagation: 3 instructions)
+          mx[v] = x[u][v] > mx[v] ? x[u][v] : mx[v];
         }
       }
     }
@@ -135,6 +142,8 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
         s1[v] += d;
         s2[v] = fma(d, d, s2[v]);
         sl[v] = fma(d, l, sl[v]);
+        mn[v] = x[v] < mn[v] ? x[v] : mn[v];
+        mx[v] = x[v] > mx[v] ? x[v] : mx[v];
       }
     }
   }
@@ -182,6 +191,26 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
     mu[col] = ma;
     m2[col] = Ma;
     gsum[col] = Ga;
+  }
+  if (cmin) {  // column extrema (scale table of the int8 tensor-core O-passes), order-free
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      sh[w][0][lane * VEC + v] = mn[v];
+      sh[w][1][lane * VEC + v] = mx[v];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < 32 * VEC; c += blockDim.x) {
+      const int64_t col = (int64_t)blockIdx.x * (32 * VEC) + c;
+      if (col >= p) continue;
+      double a = sh[0][0][c], b = sh[0][1][c];
+      for (int q = 1; q < kColStatsWarps; ++q) {
+        a = fmin(a, sh[q][0][c]);
+        b = fmax(b, sh[q][1][c]);
+      }
+      cmin[col] = a;
+      cmax[col] = b;
+    }
   }
 }
 

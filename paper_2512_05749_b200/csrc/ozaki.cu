@@ -28,10 +28,10 @@
 //   warp 0      TMA producer of the raw ring: O tile (+ mu/scale slice), 4 stages, freed by the
 //               converters as soon as they have digitised it;
 //   warp 2      TMA producer of the thin-operand digit tiles (4-stage ring);
-//   warp 1      TMEM allocator and the single MMA-issuing thread (tcgen05.mma kind::i8, D in
-//               TMEM, tcgen05.commit frees the digit stage);
-//   warps 4-11  converters: FP64 tile -> 7 int8 digit planes (K-major, 32-byte swizzle) in shared
-//               memory, then the epilogue (tcgen05.ld of the 8 accumulators, FP64 combine, store).
+//   warps 1, 3  MMA issuers taking alternate K-blocks (tcgen05.mma kind::i8, D in TMEM,
+//               tcgen05.commit frees the stages); warp 1 also owns the TMEM allocation;
+//   warps 4-19  converters in two groups taking alternate K-blocks: raw tile -> 7 int8 digit
+//               planes (K-major, 32-byte swizzle) in shared memory; then all 16 run the epilogue (tcgen05.ld of the 8 accumulators, FP64 combine, store).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -183,9 +183,20 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
+// Slot of parameter p in the scale table: inside each block of 32 parameters the order is
+// transposed (p % 8, p / 8 % 4) so that a converter warp's K-quarter groups read the 4
+// parameters they need at one step from 64 contiguous bytes (one shared-memory wavefront).
+__host__ __device__ __forceinline__ int64_t tab_slot(int64_t p) {
+  return (p & ~int64_t(31)) | ((p & 7) << 2) | ((p >> 3) & 3);
+}
+
 __device__ __forceinline__ uint64_t to_biased(double x) {
   return (uint64_t)__double2ll_rn(x) + kBias;
 }
+
+// profiling only (debug 9): per-K-block timestamps of CTA 0, see tools/ozaki_timeline.py
+constexpr int kTraceBlocks = 96;
+__device__ long long g_oz_trace[8][kTraceBlocks];
 
 struct Params {
   // A: the sample block.  RM: A is (M x K) row-major (rows = samples, K = parameters, the
@@ -201,7 +212,8 @@ struct Params {
   int64_t ldc;
   int accumulate;
   double* slab;            // nch > 1: [nch][M][N] partial results
-  int debug;               // profiling only: 1 = skip digitising, 2 = skip MMAs, 3 = both, 4 = skip the sample-block loads too
+  int debug;               // profiling only, low bits: 1 = skip digitising, 2 = skip MMAs,
+                           // 3 = both, 4 = skip the sample-block loads too; +8 = trace CTA 0
 };
 
 template <bool RM, typename TA>
@@ -237,10 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < RSTAGES; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], kConvWarps);
+      mbar_init(&rempty[s], kConvWarps / 2);  // one converter group per K-block
     }
     for (int d = 0; d < DSTAGES; ++d) {
-      mbar_init(&conv[d], kConvWarps);
+      mbar_init(&conv[d], kConvWarps / 2);
       mbar_init(&dempty[d], 1);
     }
     for (int b = 0; b < BSTAGES; ++b) {
@@ -285,8 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % RSTAGES;
           mbar_sleep_wait(&rempty[s], ((g / RSTAGES) & 1) ^ 1);
+          if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks) g_oz_trace[0][g] = clock64();
           const int k0 = (int)(kb * BK);
-          if (p.debug == 4) {  // profiling: no sample-block traffic at all
+          if ((p.debug & 7) == 4) {  // profiling: no sample-block traffic at all
             mbar_arrive(&rfull[s]);
             continue;
           }
@@ -320,23 +333,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ===== MMA issuer: the whole warp walks the schedule (descriptors stay warp-uniform), one
-    // elected lane issues =====
+  } else if (warp == 1 || warp == 3) {
+    // ===== MMA issuers: warps 1 and 3 take alternate K-blocks =====
+    // tcgen05.mma issue blocks while the tensor pipe is busy, so a single issuing thread would
+    // expose its barrier waits between K-blocks.  Two warps alternate: one waits for its
+    // K-block's operands while the other issues; a token passed through named barriers 1/2
+    // keeps the issue order (a unit's accumulate = 0 MMAs come first).  Integer accumulation
+    // is exact, so which warp issued a K-block does not affect the result.
+    const int me = warp == 1 ? 0 : 1;
+    int64_t total = 0;  // K-blocks of this CTA over all its units
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int64_t m0, kb0, kb1;
+      int nb, kc;
+      decode(u, m0, nb, kc, kb0, kb1);
+      total += kb1 - kb0;
+    }
     uint32_t g = 0, t = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
       int64_t m0, kb0, kb1;
       int nb, kc;
       decode(u, m0, nb, kc, kb0, kb1);
-      mbar_sleep_wait(tempty, (t & 1) ^ 1);
-      tc_fence_after();
       for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        if ((int)(g & 1) != me) continue;
         const int d = g % DSTAGES, bs = g % BSTAGES;
         mbar_sleep_wait(&bfull[bs], (g / BSTAGES) & 1);
         mbar_sleep_wait(&conv[d], (g / DSTAGES) & 1);
+        if (kb == kb0) mbar_sleep_wait(tempty, (t & 1) ^ 1);  // epilogue drained the TMEM
+        if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks && lane == 0)
+          g_oz_trace[1][g] = clock64();
+        if (g > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + me) : "memory");  // token in
+        if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks && lane == 0)
+          g_oz_trace[2][g] = clock64();
         tc_fence_after();
-        if (elect_one()) {
-          if (p.debug != 2 && p.debug != 3) {
+        if (lane == 0) {
+          if ((p.debug & 7) != 2 && (p.debug & 7) != 3) {
             const uint32_t abase = smem_u32(a_dig(d)), bbase = smem_u32(b_dig(bs));
             // 11 MMAs: digit a of the sample block against the thin digits b <= min(6, 7 - a),
             // written to the level blocks D_(a+b) (TMEM columns 64 (a+b) ...).  Digit 1 goes
@@ -366,43 +396,94 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          // commits track this thread's MMAs; the tensor pipe executes in issue order, so the
+          // other warp's earlier K-blocks are complete as well
           mma_commit(&dempty[d]);
           mma_commit(&bempty[bs]);
+          if (kb + 1 == kb1) mma_commit(tfull);
+          if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks) g_oz_trace[3][g] = clock64();
         }
         __syncwarp();
+        if ((int64_t)g + 1 < total) asm volatile("bar.arrive %0, 64;\n" ::"r"(2 - me) : "memory");
       }
-      if (elect_one()) mma_commit(tfull);
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===== converters + epilogue =====
-    // converter warp cw owns tile rows 8 (cw % 16) .. +7; lane = r8 + 8 q: row r8, K quarter q
+    // Two groups of 8 warps take alternate K-blocks (each has two K-blocks of time per block).
+    // Group warp wi owns tile rows 16 wi + r8 and 16 wi + 8 + r8, lane = r8 + 8 q: K quarter q
     // (8 consecutive K values) - quarter-warps read 8 rows of one K range (conflict-free under
     // the 128-byte swizzle) and a warp's digit stores cover 8 full 32-byte rows.
     const int cw = warp - 4;
+    const int cg = cw >> 3, wi = cw & 7;
     const int q = lane >> 3;
-    const int row = 8 * cw + (lane & 7);
+    const int rowA = 16 * wi + (lane & 7), rowB = rowA + 8;
     const int quad = warp & 3;                // TMEM lane quadrant of this warp (epilogue)
     const int ecol = 16 * (cw >> 2);          // epilogue column group
     const int erow = quad * 32 + lane;
+    auto convert8 = [&](int s, int row, double mu_r, double inv_r, uint64_t (&y)[8]) {
+      if (RM) {
+        // (mu, 2^(54-e)) of K index 8 q + i sits in table slot 4 i + q
+        const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + q;
+        if (F32) {
+          const unsigned char* base = a_raw(s) + row * 128;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float4 f = *reinterpret_cast<const float4*>(
+                base + (((2 * q + c) ^ (row & 7)) << 4));
+            const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const double2 m = mi[4 * (4 * c + e)];
+              y[4 * c + e] = to_biased(((double)fv[e] - m.x) * m.y);
+            }
+          }
+        } else {
+          const unsigned char* base = a_raw(s) + (q >> 1) * 16384 + row * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double2 v = *reinterpret_cast<const double2*>(
+                base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
+            const double2 m0v = mi[4 * (2 * c)], m1v = mi[4 * (2 * c + 1)];
+            y[2 * c] = to_biased((v.x - m0v.x) * m0v.y);
+            y[2 * c + 1] = to_biased((v.y - m1v.x) * m1v.y);
+          }
+        }
+      } else {
+        const TA* base = reinterpret_cast<const TA*>(a_raw(s)) + (8 * q) * BM + row;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = to_biased(((double)base[i * BM] - mu_r) * inv_r);
+      }
+    };
+    auto store8 = [&](int d, int row, const uint32_t (&w)[ND][2]) {
+      unsigned char* dst =
+          a_dig(d) + row * BK + ((((q >> 1) ^ ((row >> 2) & 1))) << 4) + ((q & 1) << 3);
+#pragma unroll
+      for (int a = 0; a < ND; ++a)
+        *reinterpret_cast<uint2*>(dst + a * BM * BK) = make_uint2(w[a][0], w[a][1]);
+    };
     uint32_t g = 0, t = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
       int64_t m0, kb0, kb1;
       int nb, kc;
       decode(u, m0, nb, kc, kb0, kb1);
-      double mu_r = 0.0, inv_r = 0.0;
+      double muA = 0.0, invA = 0.0, muB = 0.0, invB = 0.0;
       if (!RM) {
-        const int64_t pm = m0 + row;
-        if (pm < p.M) {
-          mu_r = p.mu_inv[2 * pm];
-          inv_r = p.mu_inv[2 * pm + 1];
+        if (m0 + rowA < p.M) {
+          muA = p.mu_inv[2 * tab_slot(m0 + rowA)];
+          invA = p.mu_inv[2 * tab_slot(m0 + rowA) + 1];
+        }
+        if (m0 + rowB < p.M) {
+          muB = p.mu_inv[2 * tab_slot(m0 + rowB)];
+          invB = p.mu_inv[2 * tab_slot(m0 + rowB) + 1];
         }
       }
       for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        if ((int)(g & 1) != cg) continue;
         const int s = g % RSTAGES, d = g % DSTAGES;
         mbar_wait(&rfull[s], (g / RSTAGES) & 1);
-        uint64_t y[8];
-        if (p.debug == 1 || p.debug == 3 || p.debug == 4) {
+        const bool tr = p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks && lane == 0 && wi == 0;
+        if (tr) g_oz_trace[4][g] = clock64();
+        if ((p.debug & 7) == 1 || (p.debug & 7) == 3 || (p.debug & 7) == 4) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&rempty[s]);
           mbar_wait(&dempty[d], ((g / DSTAGES) & 1) ^ 1);
@@ -410,57 +491,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&conv[d]);
           continue;
         }
-        if (RM) {
-          const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + 8 * q;
-          if (F32) {
-            const unsigned char* base = a_raw(s) + row * 128;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const float4 f = *reinterpret_cast<const float4*>(
-                  base + (((2 * q + c) ^ (row & 7)) << 4));
-              const float fv[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const double2 m = mi[4 * c + e];
-                y[4 * c + e] = to_biased(((double)fv[e] - m.x) * m.y);
-              }
-            }
-          } else {
-            const unsigned char* base = a_raw(s) + (q >> 1) * 16384 + row * 128;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const double2 v = *reinterpret_cast<const double2*>(
-                  base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
-              const double2 m0v = mi[2 * c], m1v = mi[2 * c + 1];
-              y[2 * c] = to_biased((v.x - m0v.x) * m0v.y);
-              y[2 * c + 1] = to_biased((v.y - m1v.x) * m1v.y);
-            }
-          }
-        } else {
-          const TA* base = reinterpret_cast<const TA*>(a_raw(s)) + (8 * q) * BM + row;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) y[i] = to_biased(((double)base[i * BM] - mu_r) * inv_r);
-        }
+        uint64_t yA[8], yB[8];
+        convert8(s, rowA, muA, invA, yA);
+        convert8(s, rowB, muB, invB, yB);
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[s]);  // raw tile consumed (values are in registers)
-        uint32_t w[ND][2];
-        pack_digits8(y, w);
+        uint32_t wA[ND][2], wB[ND][2];
+        pack_digits8(yA, wA);
+        pack_digits8(yB, wB);
+        if (tr) g_oz_trace[5][g] = clock64();
         mbar_wait(&dempty[d], ((g / DSTAGES) & 1) ^ 1);  // MMA done with this digit slot
-        unsigned char* dst =
-            a_dig(d) + row * BK + ((((q >> 1) ^ ((row >> 2) & 1))) << 4) + ((q & 1) << 3);
-#pragma unroll
-        for (int a = 0; a < ND; ++a)
-          *reinterpret_cast<uint2*>(dst + a * BM * BK) = make_uint2(w[a][0], w[a][1]);
+        if (tr) g_oz_trace[6][g] = clock64();
+        store8(d, rowA, wA);
+        store8(d, rowB, wB);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[d]);
+        if (tr) g_oz_trace[7][g] = clock64();
       }
       // ---- epilogue: D_s (s = 0..7) -> FP64 ----
       mbar_sleep_wait(tfull, t & 1);
       tc_fence_after();
       const int64_t gm = m0 + erow;
       double rowfac = 1.0;
-      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[2 * gm + 1];
+      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[2 * tab_slot(gm) + 1];
       double acc[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = 0.0;
@@ -543,8 +597,29 @@ __global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
       frexp(__longlong_as_double((long long)cmax[p]), &e);  // max < 2^e (0 -> e = 0)
       inv = ldexp(1.0, 54 - e);
     }
-    mu_inv[2 * p] = m;
-    mu_inv[2 * p + 1] = inv;
+    mu_inv[2 * tab_slot(p)] = m;
+    mu_inv[2 * tab_slot(p) + 1] = inv;
+  }
+}
+
+// Same table from column extrema: max_n |fl(O_np - mu_p)| = max(|fl(max_p - mu_p)|,
+// |fl(min_p - mu_p)|) exactly, since rounding is monotone.
+__global__ void mu_inv_minmax_kernel(const double* __restrict__ cmin,
+                                     const double* __restrict__ cmax,
+                                     const double* __restrict__ mu, int64_t cols, int64_t cols_pad,
+                                     double* __restrict__ mu_inv) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cols_pad;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    double m = 0.0, inv = 0.0;
+    if (p < cols) {
+      m = mu ? mu[p] : 0.0;
+      const double big = fmax(fabs(cmax[p] - m), fabs(cmin[p] - m));
+      int e = 0;
+      frexp(isfinite(big) ? big : 0.0, &e);
+      inv = ldexp(1.0, 54 - e);
+    }
+    mu_inv[2 * tab_slot(p)] = m;
+    mu_inv[2 * tab_slot(p) + 1] = inv;
   }
 }
 
@@ -555,21 +630,24 @@ __device__ __forceinline__ double thin_value(const double* B, int64_t ldb, int64
   const double b = B[k * ldb + j];
   if (!mu_inv) return b;
   // 2^54 / inv exactly, from the exponent field of the power of two inv (no division)
-  const long long ebits = __double_as_longlong(mu_inv[2 * k + 1]) >> 52;
+  const long long ebits = __double_as_longlong(mu_inv[2 * tab_slot(k) + 1]) >> 52;
   return b * __longlong_as_double((long long)(2046 + 54 - ebits) << 52);
 }
 
+// Thread layout of both thin-operand kernels: block = 64 columns x 4 groups of 4 consecutive K
+// rows (16 rows per pass), lane-fast over the K groups so each warp reads 8 rows x 4 columns
+// (full 32-byte sectors) and writes 4 rows x 8 K-groups of 4-byte digit words (full sectors).
 __global__ void __launch_bounds__(256)
     thin_colmax_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
                        const double* __restrict__ mu_inv, unsigned long long* __restrict__ out) {
-  // block: 4 k-lanes x 64 columns over 128 rows of K
   const int j = threadIdx.x & 63, kl = threadIdx.x >> 6;
   const int64_t jj = (int64_t)blockIdx.y * 64 + j;
   double best = 0.0;
   if (jj < N) {
-    const int64_t k1 = min(K, (int64_t)(blockIdx.x + 1) * 128);
-    for (int64_t k = (int64_t)blockIdx.x * 128 + kl; k < k1; k += 4) {
-      if (mu_inv && mu_inv[2 * k + 1] == 0.0) continue;
+    const int64_t k1 = min(K, (int64_t)(blockIdx.x + 1) * 256);
+#pragma unroll 4
+    for (int64_t k = (int64_t)blockIdx.x * 256 + kl; k < k1; k += 4) {
+      if (mu_inv && mu_inv[2 * tab_slot(k) + 1] == 0.0) continue;
       best = fmax(best, fabs(thin_value(B, ldb, k, jj, mu_inv)));
     }
   }
@@ -588,39 +666,52 @@ __global__ void __launch_bounds__(256)
                        int64_t kpad, const double* __restrict__ mu_inv,
                        const unsigned long long* __restrict__ cmax, int extra_exp,
                        int8_t* __restrict__ Bd, double* __restrict__ colfac) {
-  // block tile: 32 k x 64 columns of one 64-column block nb = blockIdx.y
-  __shared__ __align__(16) uint8_t tile[ND][64][32 + 16];
-  const int nb = blockIdx.y;
-  const int64_t k0 = (int64_t)blockIdx.x * 32;
-  const int j = threadIdx.x & 63, kq = threadIdx.x >> 6;  // 4 k-lanes
+  // thread: column jl (of 32) and K group kg (of 8, 4 rows each); block covers 32 K x 32 columns
+  const int kg = threadIdx.x & 7, jl = threadIdx.x >> 3;
+  const int nb = blockIdx.y >> 1;
+  const int j = (blockIdx.y & 1) * 32 + jl;
   const int64_t jj = (int64_t)nb * 64 + j;
+  const int64_t k0 = (int64_t)blockIdx.x * 32 + 4 * kg;
   double inv = 0.0;
-  int e = 0;
   if (jj < N) {
+    int e = 0;
     frexp(__longlong_as_double((long long)cmax[jj]), &e);
     inv = ldexp(1.0, 54 - e);
-    if (blockIdx.x == 0 && kq == 0) colfac[jj] = ldexp(1.0, e - 54 - extra_exp);
-  } else if (blockIdx.x == 0 && kq == 0) {
+    if (blockIdx.x == 0 && kg == 0) colfac[jj] = ldexp(1.0, e - 54 - extra_exp);
+  } else if (blockIdx.x == 0 && kg == 0) {
     colfac[jj] = 0.0;
   }
-  for (int kk = kq; kk < 32; kk += 4) {
-    const int64_t k = k0 + kk;
-    double x = 0.0;
-    if (jj < N && k < K && !(mu_inv && mu_inv[2 * k + 1] == 0.0))
-      x = thin_value(B, ldb, k, jj, mu_inv) * inv;
-    const uint64_t y = to_biased(x);
+  uint64_t y[4];
 #pragma unroll
-    for (int a = 0; a < ND; ++a) tile[a][j][kk] = (uint8_t)((y >> (8 * (6 - a))) & 0xFF) ^ 0x80;
+  for (int i = 0; i < 4; ++i) {
+    const int64_t k = k0 + i;
+    double x = 0.0;
+    if (jj < N && k < K && !(mu_inv && mu_inv[2 * tab_slot(k) + 1] == 0.0))
+      x = thin_value(B, ldb, k, jj, mu_inv) * inv;
+    y[i] = to_biased(x);
   }
-  __syncthreads();
-  // write out: 7 x 64 rows x 32 bytes, 16 bytes per thread-step
-  for (int idx = threadIdx.x; idx < ND * 64 * 2; idx += blockDim.x) {
-    const int half = idx & 1, rr = idx >> 1, a = rr / 64, jr = rr % 64;
-    const int64_t kk0 = k0 + 16 * half;
-    if (kk0 >= kpad) continue;
-    const uint4 v = *reinterpret_cast<const uint4*>(&tile[a][jr][16 * half]);
-    *reinterpret_cast<uint4*>(Bd + ((int64_t)(nb * ND + a) * 64 + jr) * kpad + kk0) = v;
+  uint32_t w[ND];
+  {
+    const uint32_t l0 = (uint32_t)y[0], l1 = (uint32_t)y[1], l2 = (uint32_t)y[2], l3 = (uint32_t)y[3];
+    const uint32_t h0 = (uint32_t)(y[0] >> 32), h1 = (uint32_t)(y[1] >> 32);
+    const uint32_t h2 = (uint32_t)(y[2] >> 32), h3 = (uint32_t)(y[3] >> 32);
+    uint32_t u0 = __byte_perm(l0, l1, 0x5140), u1 = __byte_perm(l0, l1, 0x7362);
+    uint32_t v0 = __byte_perm(l2, l3, 0x5140), v1 = __byte_perm(l2, l3, 0x7362);
+    w[6] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
+    w[5] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
+    w[4] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
+    w[3] = __byte_perm(u1, v1, 0x7632) ^ 0x80808080u;
+    u0 = __byte_perm(h0, h1, 0x5140);
+    u1 = __byte_perm(h0, h1, 0x7362);
+    v0 = __byte_perm(h2, h3, 0x5140);
+    v1 = __byte_perm(h2, h3, 0x7362);
+    w[2] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
+    w[1] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
+    w[0] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
   }
+#pragma unroll
+  for (int a = 0; a < ND; ++a)
+    *reinterpret_cast<uint32_t*>(Bd + ((int64_t)(nb * ND + a) * 64 + j) * kpad + k0) = w[a];
 }
 
 bool make_map_i8(CUtensorMap* map, const int8_t* ptr, int64_t inner, int64_t outer) {
@@ -667,6 +758,10 @@ cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorM
 }  // namespace oz
 
 // ---- host side ---------------------------------------------------------------------------------
+cudaError_t ozaki_trace(long long* host, size_t n) {
+  return cudaMemcpyFromSymbol(host, oz::g_oz_trace, std::min(n, sizeof(oz::g_oz_trace)));
+}
+
 int64_t ozaki_scale_len(int64_t cols) { return ((cols + oz::BK - 1) / oz::BK) * oz::BK; }
 
 cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
@@ -687,6 +782,15 @@ cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int
   oz::mu_inv_kernel<<<(int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0, st>>>(
       cmax, mu, cols, cpad, mu_inv);
   ctx.kernel_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t ozaki_scales_minmax(Context& ctx, const double* cmin, const double* cmax,
+                                const double* mu, int64_t cols, double* mu_inv, cudaStream_t st) {
+  const int64_t cpad = ozaki_scale_len(cols);
+  oz::mu_inv_minmax_kernel<<<(int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0,
+                             st>>>(cmin, cmax, mu, cols, cpad, mu_inv);
+  ctx.kernel_launches += 1;
   return cudaGetLastError();
 }
 
@@ -725,9 +829,9 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   // RM (v = Ohat^T q): the thin operand's rows are parameters -> carries the column scales
   const double* bmu = RMm ? mu_inv : nullptr;
   {
-    thin_colmax_kernel<<<dim3((unsigned)((K + 127) / 128), nblk), 256, 0, st>>>(a.B, a.ldb, K, N,
+    thin_colmax_kernel<<<dim3((unsigned)((K + 255) / 256), nblk), 256, 0, st>>>(a.B, a.ldb, K, N,
                                                                                bmu, cmax);
-    thin_digits_kernel<<<dim3((unsigned)((kpad + 31) / 32), nblk), 256, 0, st>>>(
+    thin_digits_kernel<<<dim3((unsigned)(kpad / 32), 2 * nblk), 256, 0, st>>>(
         a.B, a.ldb, K, N, kpad, bmu, cmax, RMm ? 54 : 0, Bd, colfac);
     ctx.kernel_launches += 2;
   }

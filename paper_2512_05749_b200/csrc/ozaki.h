@@ -11,13 +11,21 @@ namespace wssr {
 // Length (in {mu, scale} pairs) of the per-parameter scale table for `cols` parameters.
 int64_t ozaki_scale_len(int64_t cols);
 
-// Per-parameter table mu_inv[p] = {mu_p, 2^(54 - e_p)}, e_p the exponent bound of
+// Per-parameter table {mu_p, 2^(54 - e_p)} (stored in a block-transposed slot order, see
+// tab_slot in ozaki.cu), e_p the exponent bound of
 // max_n |O_np - mu_p| over the (rows x cols, ld lda) sample block; pads to ozaki_scale_len.
 cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
                          int64_t cols, const double* mu, double* mu_inv, cudaStream_t st);
 
+// The same table from per-column extrema of the sample block (fused into assemble's pass).
+cudaError_t ozaki_scales_minmax(Context& ctx, const double* cmin, const double* cmax,
+                                const double* mu, int64_t cols, double* mu_inv, cudaStream_t st);
+
 // Same GemmArgs contract as gemm() for the two sample-block layouts (shift = mu is taken from
 // mu_inv); false when the operands do not suit the TMA/tensor-core path.
+// profiling only: CTA 0's per-K-block timestamps of the last debug-9 launch
+cudaError_t ozaki_trace(long long* host, size_t bytes);
+
 bool ozaki_supported(Layout L, const GemmArgs& a, bool f32);
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
                        cudaStream_t st);

@@ -50,7 +50,7 @@ class EstimatorBundle:
     """
 
     __slots__ = ("loss", "raw_loss", "l_vector", "gradient", "_samples", "_mu", "_scale",
-                 "_fro2", "_gradient_exact", "_o_cache", "_n_global")
+                 "_fro2", "_gradient_exact", "_o_cache", "_n_global", "_scale_table")
 
     def __init__(self, loss, raw_loss, o_matrix, l_vector, gradient):
         o = _arrays.to_tensor(o_matrix)
@@ -64,9 +64,11 @@ class EstimatorBundle:
                    samples.shape[0])
 
     @classmethod
-    def _assembled(cls, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, n_global):
+    def _assembled(cls, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, n_global,
+                   scale_table=None):
         self = cls.__new__(cls)
         self._init(loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, True, n_global)
+        object.__setattr__(self, "_scale_table", scale_table)
         return self
 
     def _init(self, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, exact,
@@ -83,6 +85,7 @@ class EstimatorBundle:
         set_(self, "_gradient_exact", exact)
         set_(self, "_o_cache", None)
         set_(self, "_n_global", n_global)
+        set_(self, "_scale_table", None)
 
     def __setattr__(self, name, value):
         raise AttributeError("EstimatorBundle is immutable")
@@ -152,7 +155,10 @@ def assemble(batch, clip_n_std=5.0):
     mu = torch.empty(p, dtype=torch.float64, device=dev)
     lvec = torch.empty(n, dtype=torch.float64, device=dev)
     grad = torch.empty(p, dtype=torch.float64, device=dev)
-    out = _lib.AssembleOut(mu=mu.data_ptr(), l_vector=lvec.data_ptr(), gradient=grad.data_ptr())
+    # per-parameter scales of the int8 tensor-core O-passes, from the same column pass
+    table = torch.empty(_lib.scale_table_len(p), dtype=torch.float64, device=dev)
+    out = _lib.AssembleOut(mu=mu.data_ptr(), l_vector=lvec.data_ptr(), gradient=grad.data_ptr(),
+                           scale_table=table.data_ptr())
     entry = "wssr_assemble_f32" if derivs.dtype == torch.float32 else "wssr_assemble_f64"
     if derivs.dtype == torch.float32 and (derivs.stride(0) % 4 or derivs.data_ptr() % 16):
         derivs = _pad_rows_f32(derivs)
@@ -160,7 +166,7 @@ def assemble(batch, clip_n_std=5.0):
              _lib.ptr(energies), float(clip_n_std), ctypes.byref(out))
     scale = 1.0 / np.sqrt(out.n_global)
     return EstimatorBundle._assembled(out.loss, out.raw_loss, derivs, mu, scale, out.fro2, lvec,
-                                      grad, int(out.n_global))
+                                      grad, int(out.n_global), table)
 
 
 def _pad_rows_f32(x):

@@ -162,7 +162,8 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     sigma = torch.empty(k, dtype=torch.float64, device=dev)
 
     from .svdengine import _ohat_struct
-    o = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2, hist, 1.0)
+    o = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2, hist, 1.0,
+                     bundle._scale_table)
     lvec = bundle.l_vector.contiguous()
     grad = bundle.gradient if bundle._gradient_exact else None
     ext = None

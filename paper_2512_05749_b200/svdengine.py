@@ -60,8 +60,12 @@ class SsiReport:
     warm_started: bool
 
 
-def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0.0):
-    """wssr_ohat_f64 for Ohat^T = [hist_scale*hist ; scale*(samples - mu)] (sample-major)."""
+def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0.0,
+                 scale_table=None):
+    """wssr_ohat_f64 for Ohat^T = [hist_scale*hist ; scale*(samples - mu)] (sample-major).
+
+    scale_table: the bundle's per-parameter table from assemble (same mu), or None.
+    """
     p = int(samples.shape[1])
     o = _lib.OhatF64()
     o.n_params = p
@@ -79,6 +83,7 @@ def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0
     o.samples_scale = float(scale)
     o.samples_fro2 = float(fro2)
     o.samples_f32 = int(samples.dtype == torch.float32)
+    o.samples_scale_table = scale_table.data_ptr() if scale_table is not None else None
     return o
 
 

@@ -142,3 +142,25 @@ def test_ozaki_is_deterministic():
                  _lib.ptr(B), 64, _lib.ptr(C), 64, 1.0)
         outs.append(C)
     assert torch.equal(outs[0], outs[1])
+
+
+def test_assemble_scale_table_matches_on_demand():
+    """The table fused into assemble's column pass equals the one computed on demand: the step's
+    outputs are bitwise identical either way."""
+    from paper_2512_05749_b200 import estimators, optimizers, synthetic
+
+    cfg = synthetic.config("c0", N=512, P=8192, k=16, L=32, delta=0.5, lam=1e-3)
+    wl = synthetic.HostWorkload.from_config(cfg, 3)
+    o, e = wl.next()
+    b = estimators.assemble(estimators.SampleBatch((None,) * o.shape[0], e, o))
+    assert b._scale_table is not None
+    st = optimizers.WssrState.initial(cfg["P"], rank_init=cfg["k"], delta=cfg["delta"],
+                                      sigma_floor=cfg["lam"])
+    theta = torch.zeros(cfg["P"], dtype=torch.float64, device="cuda")
+    _, st, _ = optimizers.wssr_step(theta, b, 1.0, st)          # dense first step
+    outs = []
+    for table in (b._scale_table, None):
+        object.__setattr__(b, "_scale_table", table)
+        th, _, d = optimizers.wssr_step(theta, b, 1.0, st)
+        outs.append(th)
+    assert torch.equal(outs[0], outs[1])

@@ -1,10 +1,14 @@
-# Round profile: launch list of one bench step + one ncu --set full capture of each O-pass GEMM
-# kernel (v = Ohat^T q: gemm_tma_kernel<1,...>, u = Ohat v: gemm_tma_kernel<0,128,...>) + colstats.
+# Round profile: launch list of one bench step + one ncu --set full capture of each O-pass kernel
+# (v = Ohat^T q: ozaki_gemm_kernel<true,double>, u = Ohat v: ozaki_gemm_kernel<false,double>)
+# and the assemble column pass.  Run under gpurun from the repo root.
 set -x
-ARGS="--steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+ARGS="--steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 python bench.py $ARGS > gpurun_out/plain_prof.log 2>&1 || exit 1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Layout.1, .int.128, .int.64, .int.64" -s 4 -c 1 \
+# ozaki_gemm_kernel launches alternate v = Ohat^T q (row-major pass) and u = Ohat v
+ncu --set full --clock-control none --import-source on -k regex:ozaki_gemm_kernel -s 8 -c 1 \
     -o gpurun_out/prof_k4 python bench.py $ARGS > gpurun_out/ncu_k4.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Layout.0, .int.128, .int.64" -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:ozaki_gemm_kernel -s 9 -c 1 \
     -o gpurun_out/prof_k5 python bench.py $ARGS > gpurun_out/ncu_k5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:colstats -s 3 -c 1 \
+    -o gpurun_out/prof_cs python bench.py $ARGS > gpurun_out/ncu_cs.log 2>&1
 echo done
