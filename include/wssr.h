@@ -96,10 +96,12 @@ int64_t wssr_kernel_launches(const wssr_ctx* ctx);
 
 /* GEMM path of the O-passes:
  *   0 = auto: large sample blocks on the int8 tensor cores (exact digit products, ozaki.cu),
- *       the rest on FP64 DMMA with the TMA + mbarrier pipeline;
+ *       digitised once per step into HBM when the planes fit, else on the fly; the rest on
+ *       FP64 DMMA with the TMA + mbarrier pipeline;
  *   1 = FP64 DMMA with the cp.async pipeline only;
  *   2 = FP64 DMMA only (TMA where operands allow it);
- *   3 = int8 tensor-core path for every sample block it supports (tests). */
+ *   3 = int8 tensor-core path for every sample block it supports (tests);
+ *   4 = as 3 with on-the-fly digitising only (tests). */
 int wssr_set_gemm_path(wssr_ctx* ctx, int path);
 
 /* bench instrumentation: per-phase CUDA-event timing of the O-passes.

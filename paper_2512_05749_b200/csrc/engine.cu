@@ -397,8 +397,34 @@ struct Ohat {
   // (shared by copies)
   const double* scale_tab = nullptr;
   mutable std::shared_ptr<Buf> oz_scale;
+  // the pre-digitised sample block (in the context's plane buffer), built on first use
+  struct Planes {
+    const int8_t* ptr = nullptr;
+  };
+  mutable std::shared_ptr<Planes> oz_planes;
   int64_t cols() const { return r + n; }
 };
+
+// The context's digit-plane buffer, grown on demand while HBM allows (keeps 2 GiB free);
+// false: digitise on the fly instead.
+bool ensure_planes(Context& ctx, size_t bytes) {
+  if (bytes <= ctx.oz_planes_cap) return true;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  const size_t margin = (size_t)2 << 30;
+  if (free_b + ctx.oz_planes_cap < bytes + margin) return false;
+  WSSR_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (ctx.oz_planes) cudaFree(ctx.oz_planes);
+  ctx.oz_planes = nullptr;
+  ctx.oz_planes_cap = 0;
+  if (cudaMalloc(reinterpret_cast<void**>(&ctx.oz_planes), bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ctx.oz_planes = nullptr;
+    return false;
+  }
+  ctx.oz_planes_cap = bytes;
+  return true;
+}
 
 // O-pass GEMMs over the sample block in its storage type
 void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t N, int64_t K,
@@ -414,7 +440,20 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       }
       tab = *o.oz_scale;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream));
+    const int8_t* planes = nullptr;
+    if (ctx.oz_pre == 0) {
+      if (!o.oz_planes) {
+        o.oz_planes = std::make_shared<Ohat::Planes>();
+        const size_t bytes = (size_t)7 * o.n * ozaki_plane_pitch(o.P);
+        if (ensure_planes(ctx, bytes)) {
+          WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, ctx.oz_planes,
+                                   ctx.stream));
+          o.oz_planes->ptr = ctx.oz_planes;
+        }
+      }
+      planes = o.oz_planes->ptr;
+    }
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes));
     return;
   }
   if (o.f32) {
@@ -1190,9 +1229,10 @@ int wssr_ctx_create(int device, wssr_ctx** out) {
 void wssr_ctx_destroy(wssr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
-  if (ctx->c.splitk || ctx->c.oz_ws) cudaDeviceSynchronize();
+  if (ctx->c.splitk || ctx->c.oz_ws || ctx->c.oz_planes) cudaDeviceSynchronize();
   if (ctx->c.splitk) cudaFree(ctx->c.splitk);
   if (ctx->c.oz_ws) cudaFree(ctx->c.oz_ws);
+  if (ctx->c.oz_planes) cudaFree(ctx->c.oz_planes);
   delete ctx->c.comm;
   delete ctx;
 }
@@ -1208,10 +1248,11 @@ int wssr_set_stream(wssr_ctx* ctx, void* stream) {
 int64_t wssr_kernel_launches(const wssr_ctx* ctx) { return ctx ? ctx->c.kernel_launches : 0; }
 
 int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
-  if (!ctx || path < 0 || path > 3) return WSSR_ERR_VALUE;
+  if (!ctx || path < 0 || path > 4) return WSSR_ERR_VALUE;
   ctx->c.disable_tma = path == 1;
-  ctx->c.ozaki = path == 0 || path == 3;
-  ctx->c.oz_min_elems = path == 3 ? 0.0 : 4194304.0;
+  ctx->c.ozaki = path == 0 || path >= 3;
+  ctx->c.oz_min_elems = path >= 3 ? 0.0 : 4194304.0;
+  ctx->c.oz_pre = path == 4 ? 1 : 0;
   return WSSR_OK;
 }
 
@@ -1469,7 +1510,14 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
     const int64_t params = L == Layout::RM ? k : m, samples = L == Layout::RM ? m : k;
     Buf scale((size_t)2 * ozaki_scale_len(params), cx.stream);
     WSSR_CUDA(ozaki_scales(cx, a, a_f32 != 0, lda, samples, params, shift, scale, cx.stream));
-    WSSR_CUDA(ozaki_gemm(cx, L, g, a_f32 != 0, scale, cx.stream));
+    Buf planes;
+    if (cx.oz_pre == 0) {
+      planes = Buf(((size_t)7 * samples * ozaki_plane_pitch(params) + 7) / 8, cx.stream);
+      WSSR_CUDA(ozaki_digitize(cx, a, a_f32 != 0, lda, samples, params, scale,
+                               reinterpret_cast<int8_t*>(planes.p), cx.stream));
+    }
+    WSSR_CUDA(ozaki_gemm(cx, L, g, a_f32 != 0, scale, cx.stream,
+                         reinterpret_cast<const int8_t*>(planes.p)));
     sync(cx);
   });
 }

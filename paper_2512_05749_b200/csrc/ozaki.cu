@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -171,6 +172,35 @@ __device__ __forceinline__ bool elect_one() {
 
 // mbarrier wait that suspends the thread in hardware until the phase flips (single-thread
 // producer / MMA roles: no issue slots burnt spinning)
+#ifdef WSSR_OZ_WATCHDOG
+// debugging build: a wait that has not completed after ~2^28 polls reports where and traps
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_watch(uint64_t* bar, uint32_t parity) {
+  for (long long i = 0; !mbar_try(bar, parity); ++i) {
+    if (i == (1ll << 20)) {
+      printf("WATCHDOG block %d warp %d lane %d bar smem+%u parity %u\n", blockIdx.x,
+             threadIdx.x >> 5, threadIdx.x & 31, smem_u32(bar) & 0xFFFFF, parity);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  mbar_watch(bar, parity);
+}
+#define mbar_wait mbar_watch
+#else
 __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -182,6 +212,7 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) 
       "r"(parity)
       : "memory");
 }
+#endif
 
 // Slot of parameter p in the scale table: inside each block of 32 parameters the order is
 // transposed (p % 8, p / 8 % 4) so that a converter warp's K-quarter groups read the 4
@@ -353,12 +384,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       int64_t m0, kb0, kb1;
       int nb, kc;
       decode(u, m0, nb, kc, kb0, kb1);
+      // both issuers observe every tempty phase in order (a warp that skipped a unit would
+      // otherwise see a stale parity two phases ahead): the epilogue of unit t-1 has drained
+      // the TMEM before any K-block of unit t is issued
+      mbar_sleep_wait(tempty, (t & 1) ^ 1);
       for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
         if ((int)(g & 1) != me) continue;
         const int d = g % DSTAGES, bs = g % BSTAGES;
         mbar_sleep_wait(&bfull[bs], (g / BSTAGES) & 1);
         mbar_sleep_wait(&conv[d], (g / DSTAGES) & 1);
-        if (kb == kb0) mbar_sleep_wait(tempty, (t & 1) ^ 1);  // epilogue drained the TMEM
         if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks && lane == 0)
           g_oz_trace[1][g] = clock64();
         if (g > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + me) : "memory");  // token in
@@ -441,9 +475,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const unsigned char* base = a_raw(s) + (q >> 1) * 16384 + row * 128;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const double2 v = *reinterpret_cast<const double2*>(
-                base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
+            const int mode = p.debug & 7;  // profiling: 5 = loads only, 6 = arithmetic only
+            const double2 v = mode == 6 ? make_double2(row * 1e-3, c * 1e-3)
+                                        : *reinterpret_cast<const double2*>(
+                                              base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
             const double2 m0v = mi[4 * (2 * c)], m1v = mi[4 * (2 * c + 1)];
+            if (mode == 5) {
+              y[2 * c] = __double_as_longlong(v.x) ^ __double_as_longlong(m0v.y);
+              y[2 * c + 1] = __double_as_longlong(v.y) ^ __double_as_longlong(m1v.y);
+              continue;
+            }
             y[2 * c] = to_biased((v.x - m0v.x) * m0v.y);
             y[2 * c + 1] = to_biased((v.y - m1v.x) * m1v.y);
           }
@@ -556,6 +597,314 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem)
                  : "memory");
+  }
+}
+
+// ---- pre-digitised variant ---------------------------------------------------------------------
+// When the step's digit planes fit in HBM they are written once per step (digitize_kernel, with
+// no tensor-core work running: FP64 SIMT arithmetic shares the SM's math datapath with the
+// int8 MMAs and runs ~2.5x slower beside them), and every O-pass streams them with TMA straight
+// into the MMA operands: planes [7][N][Ppad] int8, parameter-contiguous.  The u = Ohat v pass
+// reads the same planes as an MN-major operand (parameters along M), so one layout serves both.
+constexpr int PBK = 32;                // K per stage (kind::i8 MMA-K steps of 32 bytes)
+constexpr int PA_DIG = ND * BM * PBK;  // 28 KB
+constexpr int PB_DIG = BROWS * PBK;    // 14 KB
+constexpr int PSTAGES = 5;             // sample-digit ring (deep: the tiles stream from HBM)
+constexpr int PBSTAGES = 5;            // thin-operand digit ring
+constexpr int kPreThreads = 256;       // warps 0,2 producers; 1,3 MMA issuers; 4-7 epilogue
+constexpr size_t kPreSmem = (size_t)PA_DIG * PSTAGES + (size_t)PB_DIG * PBSTAGES + 256 + 1024;
+
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t addr) {
+  // K-major, SWIZZLE_64B: rows of 64 B, 8-row groups 512 B apart (SBO); layout type 4
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | (32ull << 32) | (1ull << 46) |
+         (4ull << 61);
+}
+
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr) {
+  // MN-major, SWIZZLE_128B: 128 int8 along M per 128-byte row, 8-row atoms of 1 KB along K (SBO)
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool RM>
+__global__ void __launch_bounds__(kPreThreads, 1)
+    ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* bring = smem + (size_t)PA_DIG * PSTAGES;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(bring + (size_t)PB_DIG * PBSTAGES);
+  uint64_t* aempty = afull + PSTAGES;
+  uint64_t* bfull = aempty + PSTAGES;
+  uint64_t* bempty = bfull + PBSTAGES;
+  uint64_t* tfull = bempty + PBSTAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto a_dig = [&](int s) { return smem + (size_t)s * PA_DIG; };
+  auto b_dig = [&](int s) { return bring + (size_t)s * PB_DIG; };
+
+  if (tid == 0) {
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < PBSTAGES; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t units = (int64_t)p.mtiles * p.nblk * p.nch;
+  auto decode = [&](int64_t u, int64_t& m0, int& nb, int& kc, int64_t& kb0, int64_t& kb1) {
+    m0 = (u % p.mtiles) * BM;
+    const int64_t rest = u / p.mtiles;
+    nb = (int)(rest % p.nblk);
+    kc = (int)(rest / p.nblk);
+    kb0 = p.kblocks * kc / p.nch;
+    kb1 = p.kblocks * (kc + 1) / p.nch;
+  };
+
+  if (warp == 0 || warp == 2) {
+    // ===== TMA producers: warp 0 the sample digits, warp 2 the thin-operand digits =====
+    if (lane == 0) {
+      const bool A = warp == 0;
+      prefetch_tmap(A ? &tmA : &tmB);
+      uint32_t g = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t m0, kb0, kb1;
+        int nb, kc;
+        decode(u, m0, nb, kc, kb0, kb1);
+        for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+          const int k0 = (int)(kb * PBK);
+          if (A) {
+            const int s = g % PSTAGES;
+            mbar_sleep_wait(&aempty[s], ((g / PSTAGES) & 1) ^ 1);
+            if ((p.debug & 7) == 5) {  // profiling: no sample-digit traffic
+              mbar_arrive(&afull[s]);
+              continue;
+            }
+            mbar_arrive_expect_tx(&afull[s], PA_DIG);
+            if (RM)
+              tma_load_3d(a_dig(s), &tmA, k0, (int)m0, 0, &afull[s]);  // [7][128 n][64 p]
+            else
+              tma_load_3d(a_dig(s), &tmA, (int)m0, k0, 0, &afull[s]);  // [7][64 n][128 p]
+          } else {
+            const int b = g % PBSTAGES;
+            mbar_sleep_wait(&bempty[b], ((g / PBSTAGES) & 1) ^ 1);
+            if ((p.debug & 7) == 6) {  // profiling: no thin-digit traffic
+              mbar_arrive(&bfull[b]);
+              continue;
+            }
+            mbar_arrive_expect_tx(&bfull[b], PB_DIG);
+            tma_load_2d(b_dig(b), &tmB, k0, nb * BROWS, &bfull[b]);
+            tma_load_2d(b_dig(b) + 224 * PBK, &tmB, k0, nb * BROWS + 224, &bfull[b]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 3) {
+    // ===== MMA issuers taking alternate K-blocks (see ozaki_gemm_kernel) =====
+    const int me = warp == 1 ? 0 : 1;
+    int64_t total = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int64_t m0, kb0, kb1;
+      int nb, kc;
+      decode(u, m0, nb, kc, kb0, kb1);
+      total += kb1 - kb0;
+    }
+    const uint32_t amajor = RM ? 0u : (1u << 15);
+    auto adesc_of = [&](uint32_t addr) {
+      return RM ? (PBK == 64 ? smem_desc_sw64(addr) : smem_desc_sw32(addr))
+                : smem_desc_mn_sw128(addr);
+    };
+    uint32_t g = 0, t = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      int64_t m0, kb0, kb1;
+      int nb, kc;
+      decode(u, m0, nb, kc, kb0, kb1);
+      mbar_sleep_wait(tempty, (t & 1) ^ 1);  // every phase, in order (see ozaki_gemm_kernel)
+      for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        if ((int)(g & 1) != me) continue;
+        const int s = g % PSTAGES, bs = g % PBSTAGES;
+        mbar_sleep_wait(&bfull[bs], (g / PBSTAGES) & 1);
+        mbar_sleep_wait(&afull[s], (g / PSTAGES) & 1);
+        if (g > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + me) : "memory");  // token in
+        tc_fence_after();
+        if (lane == 0 && (p.debug & 7) == 7) {  // profiling: no MMAs
+          mma_commit(&aempty[s]);
+          mma_commit(&bempty[bs]);
+          if (kb + 1 == kb1) mma_commit(tfull);
+        } else if (lane == 0) {
+          // two MMA-K steps per stage: K-major operands advance 32 bytes inside the 64-byte
+          // swizzled rows; the MN-major sample digits advance 32 rows (4 KB)
+#pragma unroll
+          for (int kk = 0; kk < PBK / 32; ++kk) {
+            const uint32_t abase = smem_u32(a_dig(s)) + (RM ? 32u * kk : 4096u * kk);
+            const uint32_t bbase = smem_u32(b_dig(bs)) + 32u * kk;
+            const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
+            auto bdesc = [&](int row) {
+              return PBK == 64 ? smem_desc_sw64(bbase + row * PBK) : smem_desc_sw32(bbase + row * PBK);
+            };
+            const uint64_t ad1 = adesc_of(abase + 1 * BM * PBK);
+            const uint64_t ad0 = adesc_of(abase);
+            mma_i8(tmem + 64, ad1, bdesc(0), idesc_i8(256) | amajor, first);
+            mma_i8(tmem + 320, ad1, bdesc(256), idesc_i8(192) | amajor, first);
+            mma_i8(tmem + 0, ad0, bdesc(0), idesc_i8(64) | amajor, first);
+            mma_i8(tmem + 64, ad0, bdesc(64), idesc_i8(256) | amajor, 1u);
+            mma_i8(tmem + 320, ad0, bdesc(320), idesc_i8(128) | amajor, 1u);
+#pragma unroll
+            for (int a = 2; a < ND; ++a) {
+              const uint64_t adesc = adesc_of(abase + a * BM * PBK);
+              int col = NB * a, brow = 0, left = NB * (NL - a);
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                if (left > 0) {
+                  const int n = left > 256 ? 256 : left;
+                  mma_i8(tmem + col, adesc, bdesc(brow), idesc_i8(n) | amajor, 1u);
+                  col += n;
+                  brow += n;
+                  left -= n;
+                }
+              }
+            }
+          }
+          mma_commit(&aempty[s]);
+          mma_commit(&bempty[bs]);
+          if (kb + 1 == kb1) mma_commit(tfull);
+        }
+        __syncwarp();
+        if ((int64_t)g + 1 < total) asm volatile("bar.arrive %0, 64;\n" ::"r"(2 - me) : "memory");
+      }
+    }
+  } else {
+    // ===== epilogue: warps 4-7, TMEM lane quadrant = warp % 4, all 64 columns =====
+    const int quad = warp & 3;
+    const int erow = quad * 32 + lane;
+    uint32_t t = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      int64_t m0, kb0, kb1;
+      int nb, kc;
+      decode(u, m0, nb, kc, kb0, kb1);
+      mbar_sleep_wait(tfull, t & 1);
+      tc_fence_after();
+      const int64_t gm = m0 + erow;
+      double rowfac = 1.0;
+      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[2 * tab_slot(gm) + 1];
+      double out[NB];
+#pragma unroll
+      for (int jc = 0; jc < NB / 16; ++jc) {
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll
+        for (int sd = 0; sd < NL; ++sd) {
+          uint32_t r[16];
+          tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + NB * sd + 16 * jc, r);
+          tmem_ld_wait();
+          const double wgt = __longlong_as_double((long long)(1023 + 96 - 8 * sd) << 52);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)r[j], wgt, acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[16 * jc + j] = acc[j];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      if (gm < p.M) {
+        const int64_t gj0 = (int64_t)nb * NB;
+        const double rf = p.alpha * rowfac;
+        if (p.nch > 1) {
+          double* dst = p.slab + ((int64_t)kc * p.M + gm) * p.N;
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            if (gj0 + j < p.N) dst[gj0 + j] = rf * p.colfac[gj0 + j] * out[j];
+        } else {
+          double* dst = p.C + gm * p.ldc;
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            if (gj0 + j < p.N) {
+              const double v = rf * p.colfac[gj0 + j] * out[j];
+              dst[gj0 + j] = p.accumulate ? dst[gj0 + j] + v : v;
+            }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem)
+                 : "memory");
+  }
+}
+
+// planes[a][n][p] (int8, pitch ppad) = digit a (most significant first) of
+// X_np = rint((O_np - mu_p) 2^(54 - e_p)); parameters past `cols` get zero digits.
+template <typename TA>
+__global__ void __launch_bounds__(256)
+    digitize_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                    int64_t ppad, const double* __restrict__ mu_inv, int8_t* __restrict__ planes) {
+  const int64_t quads = ppad / 4;
+  const int64_t plane = rows * ppad;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * quads;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = idx / quads, p0 = (idx % quads) * 4;
+    uint64_t y[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t pp = p0 + i;
+      double x = 0.0;
+      if (pp < cols) {
+        const double m = mu_inv[2 * tab_slot(pp)], inv = mu_inv[2 * tab_slot(pp) + 1];
+        x = ((double)A[n * lda + pp] - m) * inv;
+      }
+      y[i] = to_biased(x);
+    }
+    const uint32_t l0 = (uint32_t)y[0], l1 = (uint32_t)y[1], l2 = (uint32_t)y[2], l3 = (uint32_t)y[3];
+    const uint32_t h0 = (uint32_t)(y[0] >> 32), h1 = (uint32_t)(y[1] >> 32);
+    const uint32_t h2 = (uint32_t)(y[2] >> 32), h3 = (uint32_t)(y[3] >> 32);
+    uint32_t u0 = __byte_perm(l0, l1, 0x5140), u1 = __byte_perm(l0, l1, 0x7362);
+    uint32_t v0 = __byte_perm(l2, l3, 0x5140), v1 = __byte_perm(l2, l3, 0x7362);
+    uint32_t w[ND];
+    w[6] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
+    w[5] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
+    w[4] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
+    w[3] = __byte_perm(u1, v1, 0x7632) ^ 0x80808080u;
+    u0 = __byte_perm(h0, h1, 0x5140);
+    u1 = __byte_perm(h0, h1, 0x7362);
+    v0 = __byte_perm(h2, h3, 0x5140);
+    v1 = __byte_perm(h2, h3, 0x7362);
+    w[2] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
+    w[1] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
+    w[0] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
+    int8_t* dst = planes + n * ppad + p0;
+#pragma unroll
+    for (int a = 0; a < ND; ++a) *reinterpret_cast<uint32_t*>(dst + a * plane) = w[a];
   }
 }
 
@@ -714,15 +1063,17 @@ __global__ void __launch_bounds__(256)
     *reinterpret_cast<uint32_t*>(Bd + ((int64_t)(nb * ND + a) * 64 + j) * kpad + k0) = w[a];
 }
 
-bool make_map_i8(CUtensorMap* map, const int8_t* ptr, int64_t inner, int64_t outer) {
+bool make_map_i8(CUtensorMap* map, const int8_t* ptr, int64_t inner, int64_t outer,
+                 int kbox = BK) {
   auto fn = tma_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   cuuint64_t strides[1] = {(cuuint64_t)inner};
-  cuuint32_t box[2] = {(cuuint32_t)BK, 224u};
+  cuuint32_t box[2] = {(cuuint32_t)kbox, 224u};
   cuuint32_t es[2] = {1u, 1u};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(ptr), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            kbox == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -753,6 +1104,37 @@ cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorM
   }
   ozaki_gemm_kernel<RM, TA><<<grid, kThreads, kSmem, st>>>(tA, tB, tS, p);
   return cudaGetLastError();
+}
+
+template <bool RM>
+cudaError_t launch_pre(const CUtensorMap& tA, const CUtensorMap& tB, const Params& p, int grid,
+                       cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ozaki_pre_kernel<RM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kPreSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  ozaki_pre_kernel<RM><<<grid, kPreThreads, kPreSmem, st>>>(tA, tB, p);
+  return cudaGetLastError();
+}
+
+// 3-D map over the digit planes [7][rows][ppad] int8
+bool make_map_planes(CUtensorMap* map, const int8_t* planes, int64_t ppad, int64_t rows, bool rm) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)ppad, (cuuint64_t)rows, (cuuint64_t)ND};
+  cuuint64_t strides[2] = {(cuuint64_t)ppad, (cuuint64_t)(ppad * rows)};
+  cuuint32_t box[3] = {rm ? (cuuint32_t)PBK : (cuuint32_t)BM, rm ? (cuuint32_t)BM : (cuuint32_t)PBK,
+                       (cuuint32_t)ND};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            rm ? (PBK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B)
+               : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace oz
@@ -801,15 +1183,39 @@ bool ozaki_supported(Layout L, const GemmArgs& a, bool f32) {
          a.N <= 4096 && !a.partial && !a.Cin && (L == Layout::RM || L == Layout::CM);
 }
 
+int64_t ozaki_plane_pitch(int64_t cols) {
+  static const int extra = [] {
+    const char* e = std::getenv("WSSR_OZ_PITCH_PAD");  // debugging only
+    return e ? std::atoi(e) : 0;
+  }();
+  return ((cols + 127) / 128) * 128 + 128 * extra;
+}
+
+cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
+                           int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st) {
+  const int64_t ppad = ozaki_plane_pitch(cols);
+  const int64_t work = rows * (ppad / 4);
+  const int grid = (int)std::min<int64_t>((work + 255) / 256, 16 * ctx.num_sms);
+  if (f32)
+    oz::digitize_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A), lda, rows,
+                                                     cols, ppad, mu_inv, planes);
+  else
+    oz::digitize_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(A), lda, rows,
+                                                      cols, ppad, mu_inv, planes);
+  ctx.kernel_launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
-                       cudaStream_t st) {
+                       cudaStream_t st, const int8_t* planes) {
   using namespace oz;
   const bool RMm = L == Layout::RM;
   const int64_t M = a.M, N = a.N, K = a.K;
   if (M == 0 || N == 0) return cudaSuccess;
   const int nblk = (int)((N + NB - 1) / NB);
-  const int64_t kpad = ((K + BK - 1) / BK) * BK;
-  const int64_t kblocks = kpad / BK;
+  const int kstep = planes ? PBK : BK;  // K per pipeline stage
+  const int64_t kpad = ((K + kstep - 1) / kstep) * kstep;
+  const int64_t kblocks = kpad / kstep;
   const int mtiles = (int)((M + BM - 1) / BM);
   // thin-operand digits + factors (workspace owned by the context)
   const size_t dig_bytes = (size_t)nblk * BROWS * kpad;
@@ -853,6 +1259,11 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
       if (eff >= 0.92 && units >= ctx.num_sms) break;
     }
     nch = best;
+    static const int force_nch = [] {
+      const char* e = std::getenv("WSSR_OZ_NCH");  // profiling / debugging only
+      return e ? std::atoi(e) : 0;
+    }();
+    if (force_nch > 0) nch = (int)std::min<int64_t>(std::max<int64_t>(force_nch, nch), kblocks);
   }
   Params p{};
   p.M = M;
@@ -884,22 +1295,38 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   std::memset(&tS, 0, sizeof(tS));
   const int es = f32 ? 4 : 8;
   bool ok;
-  if (RMm) {
+  if (planes) {
+    // pre-digitised planes [7][samples][ppad]: samples = M (RM) or K (CM)
+    const int64_t samples = RMm ? M : K;
+    const int64_t ppad = ozaki_plane_pitch(RMm ? K : M);
+    ok = make_map_planes(&tA, planes, ppad, samples, RMm) &&
+         make_map_i8(&tB, Bd, kpad, (int64_t)nblk * BROWS, PBK);
+    if (!ok) return cudaErrorInvalidValue;
+    const int64_t units = (int64_t)mtiles * nblk * nch;
+    const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
+    e = RMm ? launch_pre<true>(tA, tB, p, grid, st) : launch_pre<false>(tA, tB, p, grid, st);
+    ctx.kernel_launches += 1;
+    ctx.gemm_launches += 1;
+  } else if (RMm) {
     ok = make_map_2d(&tA, a.A, K, M, a.lda, BM, es) &&
          make_map_1d(&tS, mu_inv, 2 * kpad, 2 * BK);
   } else {
     ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
   }
-  ok = ok && make_map_i8(&tB, Bd, kpad, (int64_t)nblk * BROWS);
-  if (!ok) return cudaErrorInvalidValue;
-  const int64_t units = (int64_t)mtiles * nblk * nch;
-  const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
-  if (RMm)
-    e = f32 ? launch<true, float>(tA, tB, tS, p, grid, st) : launch<true, double>(tA, tB, tS, p, grid, st);
-  else
-    e = f32 ? launch<false, float>(tA, tB, tS, p, grid, st) : launch<false, double>(tA, tB, tS, p, grid, st);
-  ctx.kernel_launches += 1;
-  ctx.gemm_launches += 1;
+  if (!planes) {
+    ok = ok && make_map_i8(&tB, Bd, kpad, (int64_t)nblk * BROWS);
+    if (!ok) return cudaErrorInvalidValue;
+    const int64_t units = (int64_t)mtiles * nblk * nch;
+    const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
+    if (RMm)
+      e = f32 ? launch<true, float>(tA, tB, tS, p, grid, st)
+              : launch<true, double>(tA, tB, tS, p, grid, st);
+    else
+      e = f32 ? launch<false, float>(tA, tB, tS, p, grid, st)
+              : launch<false, double>(tA, tB, tS, p, grid, st);
+    ctx.kernel_launches += 1;
+    ctx.gemm_launches += 1;
+  }
   if (e != cudaSuccess || nch == 1) return e;
   const int64_t total = M * N;
   const int rb = (int)std::min<int64_t>((total + 255) / 256, 16 * ctx.num_sms);

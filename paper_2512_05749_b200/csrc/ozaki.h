@@ -27,7 +27,15 @@ cudaError_t ozaki_scales_minmax(Context& ctx, const double* cmin, const double* 
 cudaError_t ozaki_trace(long long* host, size_t bytes);
 
 bool ozaki_supported(Layout L, const GemmArgs& a, bool f32);
+// planes: the step's pre-digitised sample block (ozaki_digitize) or nullptr (digitise on the fly)
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
-                       cudaStream_t st);
+                       cudaStream_t st, const int8_t* planes = nullptr);
+
+// Digit planes [7][rows][ozaki_plane_pitch(cols)] int8 of the centred, scaled sample block
+// (rows = samples, cols = parameters, row-major with pitch lda); written once per step and
+// streamed by both O-passes.
+int64_t ozaki_plane_pitch(int64_t cols);
+cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
+                           int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st);
 
 }  // namespace wssr

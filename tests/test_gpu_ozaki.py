@@ -14,6 +14,22 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+_PATH = [3]
+
+
+@pytest.fixture(params=[3, 4], ids=["predigitised", "on_the_fly"], autouse=True)
+def digit_path(request):
+    """Run every test on both variants: digit planes written once per step (gemm path 3) and
+    digitised inside the GEMM (path 4)."""
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    _PATH[0] = request.param
+    ctx.lib.wssr_set_gemm_path(ctx.handle, request.param)
+    yield request.param
+    ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
+
+
 def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift=True):
     from paper_2512_05749_b200 import _lib
 
@@ -59,7 +75,7 @@ def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift
                     ctx.call("wssr_gemm_f64", layout, M, N, K, _lib.ptr(A), lda, _lib.ptr(shift),
                              _lib.ptr(B), ldb, _lib.ptr(C), N + pad, 0.5, 0, 1024)
             finally:
-                ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
+                ctx.lib.wssr_set_gemm_path(ctx.handle, _PATH[0])
         out[name] = C
     Xl = X.cpu().numpy().astype(np.longdouble)
     Bl = B[:, :N].cpu().numpy().astype(np.longdouble)

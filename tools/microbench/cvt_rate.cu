@@ -41,6 +41,24 @@ __global__ void k_magic(double* in, long long* out, int iters) {
   }
   if (acc == 42) out[0] = acc;
 }
+// converter-like: 16 independent elements per thread, DADD -> DMUL -> F2I -> +bias
+__global__ void k_conv16(double* in, long long* out, int iters, int use_f2i) {
+  double x[16]; unsigned long long acc = 0;
+  for (int i = 0; i < 16; ++i) x[i] = in[(threadIdx.x + i) & 4095] + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double t = (x[i] - 0.25) * 1024.0;
+      unsigned long long y;
+      if (use_f2i) y = (unsigned long long)__double2ll_rn(t) + 0x0080808080808080ull;
+      else y = (unsigned long long)(__double_as_longlong(t + 6755399441055744.0) - 0x4338000000000000ll) + 0x0080808080808080ull;
+      acc ^= y;
+      x[i] += 1.0;
+    }
+  }
+  if (acc == 42) out[0] = acc;
+}
+
 int main() {
   double* in; long long* out; cudaMalloc(&in, 4096 * 8); cudaMalloc(&out, 8); cudaMemset(in, 0, 4096 * 8);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -59,5 +77,17 @@ int main() {
     printf("%s: %.1f Gop/s  = %.1f per clk per SM @1.9GHz\n", kind == 0 ? "F2I.S64.F64 (+DADD)" : kind == 1 ? "DADD+DMUL" : "magic int round",
            ops / (ms * 1e6), ops / (ms * 1e-3) / sms / 1.9e9);
   }
+  for (int use = 0; use < 2; ++use)
+    for (int warps : {8, 16, 32}) {
+      cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        k_conv16<<<sms, 32 * warps>>>(in, out, 1024, use);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+      }
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      const double el = (double)sms * 32 * warps * 1024 * 16;
+      printf("conv16 %s warps/SM=%d: %.1f elements/clk/SM\n", use ? "F2I  " : "magic", warps, el / (ms * 1e-3) / sms / 1.9e9);
+    }
   return 0;
 }

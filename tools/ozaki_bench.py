@@ -17,9 +17,9 @@ def bench(layout, M, N, K, f32=False, reps=10):
     B = torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g)
     C = torch.empty(M, N, dtype=torch.float64, device="cuda")
     res = {}
-    for name in ("ozaki", "dmma"):
+    for name in ("ozaki", "ozaki_fly", "dmma"):
         def run():
-            if name == "ozaki":
+            if name.startswith("ozaki"):
                 ctx.call("wssr_debug_ozaki_gemm", layout, M, N, K, _lib.ptr(A), params, int(f32),
                          _lib.ptr(mu), _lib.ptr(B), N, _lib.ptr(C), N, 1.0)
             elif f32:
@@ -28,7 +28,7 @@ def bench(layout, M, N, K, f32=False, reps=10):
             else:
                 ctx.call("wssr_gemm_f64", layout, M, N, K, _lib.ptr(A), params, _lib.ptr(mu),
                          _lib.ptr(B), N, _lib.ptr(C), N, 1.0, 0, 1024)
-        ctx.lib.wssr_set_gemm_path(ctx.handle, 0 if name == "ozaki" else 2)
+        ctx.lib.wssr_set_gemm_path(ctx.handle, {"ozaki": 0, "ozaki_fly": 4, "dmma": 2}[name])
         for _ in range(2):
             run()
         torch.cuda.synchronize()
@@ -43,7 +43,7 @@ def bench(layout, M, N, K, f32=False, reps=10):
     ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
     gb = samples * params * A.element_size() / 1e9
     print(f"layout={layout} M={M} N={N} K={K} f32={f32}: ozaki {res['ozaki']:.3f} ms "
-          f"({gb / res['ozaki']:.2f} TB/s incl. scales)  dmma {res['dmma']:.3f} ms "
+          f"(pre-digitised, incl. scales + digitise) on-the-fly {res['ozaki_fly']:.3f} ms  dmma {res['dmma']:.3f} ms "
           f"({2 * M * N * K / res['dmma'] / 1e9:.1f} TF/s)", flush=True)
 
 
