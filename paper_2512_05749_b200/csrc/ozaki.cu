@@ -132,6 +132,32 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ uint64_t smem_desc_mn_sw32(uint32_t addr) {
+  // MN-major, SWIZZLE_32B: 32 int8 along M per 32-byte row, 8-row K atoms of 256 B (SBO), the
+  // four 32-wide M blocks 1 KB apart (LBO); layout type 6
+  return (uint64_t)((addr >> 4) & 0x3FFF) | (64ull << 16) | (16ull << 32) | (1ull << 46) |
+         (6ull << 61);
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+
 // Biased integers Y = X + kBias -> digit planes: plane a holds byte (6 - a) of every Y (most
 // significant digit first), XOR 0x80 = the signed digit.
 // 8 biased integers -> 7 digit planes x 8 bytes (2 words each)
@@ -357,10 +383,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
           const int b = g % BSTAGES;
           mbar_sleep_wait(&bempty[b], ((g / BSTAGES) & 1) ^ 1);
-          const int k0 = (int)(kb * BK);
           mbar_arrive_expect_tx(&bfull[b], B_DIG);
-          tma_load_2d(b_dig(b), &tmB, k0, nb * BROWS, &bfull[b]);
-          tma_load_2d(b_dig(b) + 224 * BK, &tmB, k0, nb * BROWS + 224, &bfull[b]);
+          const int bblk = (int)(nb * p.kblocks + kb);
+          tma_load_3d(b_dig(b), &tmB, 0, 0, bblk, &bfull[b]);
+          tma_load_3d(b_dig(b) + 224 * BK, &tmB, 0, 224, bblk, &bfull[b]);
         }
       }
     }
@@ -626,15 +652,6 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr) {
          (2ull << 61);
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
-      "{%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-
 template <bool RM>
 __global__ void __launch_bounds__(kPreThreads, 1)
     ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -707,10 +724,10 @@ __global__ void __launch_bounds__(kPreThreads, 1)
               continue;
             }
             mbar_arrive_expect_tx(&afull[s], PA_DIG);
-            if (RM)
-              tma_load_3d(a_dig(s), &tmA, k0, (int)m0, 0, &afull[s]);  // [7][128 n][64 p]
-            else
-              tma_load_3d(a_dig(s), &tmA, (int)m0, k0, 0, &afull[s]);  // [7][64 n][128 p]
+            if (RM)  // [7][128 n][32 p]: one 4 KB run per plane
+              tma_load_4d(a_dig(s), &tmA, 0, (int)m0, (int)kb, 0, &afull[s]);
+            else     // [7][4 p-blocks][32 n][32 p]: four 1 KB runs per plane
+              tma_load_4d(a_dig(s), &tmA, 0, k0, (int)(m0 / 32), 0, &afull[s]);
           } else {
             const int b = g % PBSTAGES;
             mbar_sleep_wait(&bempty[b], ((g / PBSTAGES) & 1) ^ 1);
@@ -719,8 +736,9 @@ __global__ void __launch_bounds__(kPreThreads, 1)
               continue;
             }
             mbar_arrive_expect_tx(&bfull[b], PB_DIG);
-            tma_load_2d(b_dig(b), &tmB, k0, nb * BROWS, &bfull[b]);
-            tma_load_2d(b_dig(b) + 224 * PBK, &tmB, k0, nb * BROWS + 224, &bfull[b]);
+            const int bblk = (int)(nb * p.kblocks + kb);
+            tma_load_3d(b_dig(b), &tmB, 0, 0, bblk, &bfull[b]);
+            tma_load_3d(b_dig(b) + 224 * PBK, &tmB, 0, 224, bblk, &bfull[b]);
           }
         }
       }
@@ -737,8 +755,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
     }
     const uint32_t amajor = RM ? 0u : (1u << 15);
     auto adesc_of = [&](uint32_t addr) {
-      return RM ? (PBK == 64 ? smem_desc_sw64(addr) : smem_desc_sw32(addr))
-                : smem_desc_mn_sw128(addr);
+      return RM ? smem_desc_sw32(addr) : smem_desc_mn_sw32(addr);
     };
     uint32_t g = 0, t = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
@@ -762,7 +779,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
           // swizzled rows; the MN-major sample digits advance 32 rows (4 KB)
 #pragma unroll
           for (int kk = 0; kk < PBK / 32; ++kk) {
-            const uint32_t abase = smem_u32(a_dig(s)) + (RM ? 32u * kk : 4096u * kk);
+            const uint32_t abase = smem_u32(a_dig(s));
             const uint32_t bbase = smem_u32(b_dig(bs)) + 32u * kk;
             const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
             auto bdesc = [&](int row) {
@@ -863,17 +880,22 @@ __global__ void __launch_bounds__(kPreThreads, 1)
   }
 }
 
-// planes[a][n][p] (int8, pitch ppad) = digit a (most significant first) of
-// X_np = rint((O_np - mu_p) 2^(54 - e_p)); parameters past `cols` get zero digits.
+// Blocked digit planes: digit a (most significant first) of X_np = rint((O_np - mu_p) 2^(54 - e_p))
+// at planes[((a * ppad / 32 + p / 32) * rows + n) * 32 + p % 32] - a K-block of either O-pass is
+// then one or four contiguous runs per plane.  Parameters past `cols` get zero digits.
 template <typename TA>
 __global__ void __launch_bounds__(256)
     digitize_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
                     int64_t ppad, const double* __restrict__ mu_inv, int8_t* __restrict__ planes) {
-  const int64_t quads = ppad / 4;
+  const int64_t pblocks = ppad / 32;
   const int64_t plane = rows * ppad;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * quads;
+  const int64_t total = pblocks * rows * 8;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t n = idx / quads, p0 = (idx % quads) * 4;
+    // thread = (p block, row n, quad of 4 parameters): a warp writes 4 rows x 32 bytes contiguous
+    const int q8 = (int)(idx & 7);
+    const int64_t n = (idx >> 3) % rows, pb = (idx >> 3) / rows;
+    const int64_t p0 = pb * 32 + 4 * q8;
     uint64_t y[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -902,7 +924,7 @@ __global__ void __launch_bounds__(256)
     w[2] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
     w[1] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
     w[0] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
-    int8_t* dst = planes + n * ppad + p0;
+    int8_t* dst = planes + (pb * rows + n) * 32 + 4 * q8;
 #pragma unroll
     for (int a = 0; a < ND; ++a) *reinterpret_cast<uint32_t*>(dst + a * plane) = w[a];
   }
@@ -1009,7 +1031,8 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// digits: Bd[(nb*7 + a)*64 + jj][k] (K contiguous, kpad columns), colfac[nb*64 + jj]
+// digits, blocked by 32 K: Bd[nb][k / 32][a * 64 + j][k % 32] (every K-block's 448 x 32-byte
+// tile is one contiguous 14 KB run), colfac[nb*64 + jj]
 __global__ void __launch_bounds__(256)
     thin_digits_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
                        int64_t kpad, const double* __restrict__ mu_inv,
@@ -1060,21 +1083,8 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int a = 0; a < ND; ++a)
-    *reinterpret_cast<uint32_t*>(Bd + ((int64_t)(nb * ND + a) * 64 + j) * kpad + k0) = w[a];
-}
-
-bool make_map_i8(CUtensorMap* map, const int8_t* ptr, int64_t inner, int64_t outer,
-                 int kbox = BK) {
-  auto fn = tma_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)inner};
-  cuuint32_t box[2] = {(cuuint32_t)kbox, 224u};
-  cuuint32_t es[2] = {1u, 1u};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(ptr), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            kbox == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    *reinterpret_cast<uint32_t*>(
+        Bd + (((int64_t)nb * (kpad / 32) + blockIdx.x) * BROWS + a * 64 + j) * 32 + 4 * kg) = w[a];
 }
 
 // (K x M) row-major sample block, box = 128 parameters x 32 samples, no swizzle
@@ -1121,19 +1131,30 @@ cudaError_t launch_pre(const CUtensorMap& tA, const CUtensorMap& tB, const Param
   return cudaGetLastError();
 }
 
-// 3-D map over the digit planes [7][rows][ppad] int8
+// 4-D map over the blocked digit planes [7][ppad / 32][rows][32] int8
 bool make_map_planes(CUtensorMap* map, const int8_t* planes, int64_t ppad, int64_t rows, bool rm) {
   auto fn = tma_encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)ppad, (cuuint64_t)rows, (cuuint64_t)ND};
-  cuuint64_t strides[2] = {(cuuint64_t)ppad, (cuuint64_t)(ppad * rows)};
-  cuuint32_t box[3] = {rm ? (cuuint32_t)PBK : (cuuint32_t)BM, rm ? (cuuint32_t)BM : (cuuint32_t)PBK,
+  cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)(ppad / 32), (cuuint64_t)ND};
+  cuuint64_t strides[3] = {32, (cuuint64_t)(32 * rows), (cuuint64_t)(ppad * rows)};
+  cuuint32_t box[4] = {32, rm ? (cuuint32_t)BM : 32u, rm ? 1u : (cuuint32_t)(BM / 32),
                        (cuuint32_t)ND};
+  cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D map over the blocked thin-operand digits [nblk * kblocks][448][32]
+bool make_map_thin(CUtensorMap* map, const int8_t* bd, int64_t blocks) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)BROWS, (cuuint64_t)blocks};
+  cuuint64_t strides[2] = {32, (cuuint64_t)(32 * BROWS)};
+  cuuint32_t box[3] = {32, 224u, 1u};
   cuuint32_t es[3] = {1u, 1u, 1u};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            rm ? (PBK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B)
-               : CU_TENSOR_MAP_SWIZZLE_128B,
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(bd), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1194,7 +1215,7 @@ int64_t ozaki_plane_pitch(int64_t cols) {
 cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
                            int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st) {
   const int64_t ppad = ozaki_plane_pitch(cols);
-  const int64_t work = rows * (ppad / 4);
+  const int64_t work = rows * (ppad / 4);  // threads: one per 4 parameters of a row
   const int grid = (int)std::min<int64_t>((work + 255) / 256, 16 * ctx.num_sms);
   if (f32)
     oz::digitize_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A), lda, rows,
@@ -1300,7 +1321,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     const int64_t samples = RMm ? M : K;
     const int64_t ppad = ozaki_plane_pitch(RMm ? K : M);
     ok = make_map_planes(&tA, planes, ppad, samples, RMm) &&
-         make_map_i8(&tB, Bd, kpad, (int64_t)nblk * BROWS, PBK);
+         make_map_thin(&tB, Bd, (int64_t)nblk * kblocks);
     if (!ok) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nblk * nch;
     const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
@@ -1314,7 +1335,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
   }
   if (!planes) {
-    ok = ok && make_map_i8(&tB, Bd, kpad, (int64_t)nblk * BROWS);
+    ok = ok && make_map_thin(&tB, Bd, (int64_t)nblk * kblocks);
     if (!ok) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nblk * nch;
     const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
