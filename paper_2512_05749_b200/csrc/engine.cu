@@ -444,7 +444,7 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
     if (ctx.oz_pre == 0) {
       if (!o.oz_planes) {
         o.oz_planes = std::make_shared<Ohat::Planes>();
-        const size_t bytes = (size_t)7 * o.n * ozaki_plane_pitch(o.P);
+        const size_t bytes = ozaki_planes_bytes(o.n, o.P);
         if (ensure_planes(ctx, bytes)) {
           WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, ctx.oz_planes,
                                    ctx.stream));
@@ -1512,7 +1512,7 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
     WSSR_CUDA(ozaki_scales(cx, a, a_f32 != 0, lda, samples, params, shift, scale, cx.stream));
     Buf planes;
     if (cx.oz_pre == 0) {
-      planes = Buf(((size_t)7 * samples * ozaki_plane_pitch(params) + 7) / 8, cx.stream);
+      planes = Buf((ozaki_planes_bytes(samples, params) + 7) / 8, cx.stream);
       WSSR_CUDA(ozaki_digitize(cx, a, a_f32 != 0, lda, samples, params, scale,
                                reinterpret_cast<int8_t*>(planes.p), cx.stream));
     }

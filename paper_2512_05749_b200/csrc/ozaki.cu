@@ -148,6 +148,17 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// plain bulk copy global -> shared (contiguous bytes, no tensor map; the data are stored
+// pre-swizzled so they land in the MMA's canonical layout)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, uint64_t* bar) {
   asm volatile(
@@ -269,6 +280,9 @@ struct Params {
   int64_t ldc;
   int accumulate;
   double* slab;            // nch > 1: [nch][M][N] partial results
+  const int8_t* planes;    // pre-digitised: blocked, pre-swizzled planes [7][pblocks][prows][32]
+  int64_t prows, pblocks;
+  const int8_t* bd;        // blocked, pre-swizzled thin digits [nblk * kblocks][448][32]
   int debug;               // profiling only, low bits: 1 = skip digitising, 2 = skip MMAs,
                            // 3 = both, 4 = skip the sample-block loads too; +8 = trace CTA 0
 };
@@ -374,7 +388,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     // ===== TMA producer: thin-operand digit tiles =====
     if (lane == 0) {
-      prefetch_tmap(&tmB);
       uint32_t g = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t m0, kb0, kb1;
@@ -384,9 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int b = g % BSTAGES;
           mbar_sleep_wait(&bempty[b], ((g / BSTAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&bfull[b], B_DIG);
-          const int bblk = (int)(nb * p.kblocks + kb);
-          tma_load_3d(b_dig(b), &tmB, 0, 0, bblk, &bfull[b]);
-          tma_load_3d(b_dig(b) + 224 * BK, &tmB, 0, 224, bblk, &bfull[b]);
+          bulk_load(b_dig(b), p.bd + (nb * p.kblocks + kb) * (int64_t)B_DIG, B_DIG, &bfull[b]);
         }
       }
     }
@@ -654,8 +665,7 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr) {
 
 template <bool RM>
 __global__ void __launch_bounds__(kPreThreads, 1)
-    ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, const Params p) {
+    ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA, const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* bring = smem + (size_t)PA_DIG * PSTAGES;
@@ -708,7 +718,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
     // ===== TMA producers: warp 0 the sample digits, warp 2 the thin-operand digits =====
     if (lane == 0) {
       const bool A = warp == 0;
-      prefetch_tmap(A ? &tmA : &tmB);
+      if (A) prefetch_tmap(&tmA);
       uint32_t g = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t m0, kb0, kb1;
@@ -724,10 +734,11 @@ __global__ void __launch_bounds__(kPreThreads, 1)
               continue;
             }
             mbar_arrive_expect_tx(&afull[s], PA_DIG);
+            // 128-byte rows over the pre-swizzled planes, no TMA swizzle
             if (RM)  // [7][128 n][32 p]: one 4 KB run per plane
-              tma_load_4d(a_dig(s), &tmA, 0, (int)m0, (int)kb, 0, &afull[s]);
+              tma_load_4d(a_dig(s), &tmA, 0, (int)(m0 / 4), (int)kb, 0, &afull[s]);
             else     // [7][4 p-blocks][32 n][32 p]: four 1 KB runs per plane
-              tma_load_4d(a_dig(s), &tmA, 0, k0, (int)(m0 / 32), 0, &afull[s]);
+              tma_load_4d(a_dig(s), &tmA, 0, k0 / 4, (int)(m0 / 32), 0, &afull[s]);
           } else {
             const int b = g % PBSTAGES;
             mbar_sleep_wait(&bempty[b], ((g / PBSTAGES) & 1) ^ 1);
@@ -736,9 +747,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
               continue;
             }
             mbar_arrive_expect_tx(&bfull[b], PB_DIG);
-            const int bblk = (int)(nb * p.kblocks + kb);
-            tma_load_3d(b_dig(b), &tmB, 0, 0, bblk, &bfull[b]);
-            tma_load_3d(b_dig(b) + 224 * PBK, &tmB, 0, 224, bblk, &bfull[b]);
+            bulk_load(b_dig(b), p.bd + (nb * p.kblocks + kb) * (int64_t)PB_DIG, PB_DIG, &bfull[b]);
           }
         }
       }
@@ -881,14 +890,17 @@ __global__ void __launch_bounds__(kPreThreads, 1)
 }
 
 // Blocked digit planes: digit a (most significant first) of X_np = rint((O_np - mu_p) 2^(54 - e_p))
-// at planes[((a * ppad / 32 + p / 32) * rows + n) * 32 + p % 32] - a K-block of either O-pass is
-// then one or four contiguous runs per plane.  Parameters past `cols` get zero digits.
+// at planes[((a * ppad / 32 + p / 32) * prows + n) * 32 + (p % 32 ^ 16 [bit 2 of n])] - a K-block
+// of either O-pass is then one (v pass) or four (u pass) contiguous runs per plane, stored
+// pre-swizzled (32-byte swizzle) so bulk copies land in the MMA operand layout.  Parameters past
+// `cols` get zero digits; rows past `rows` (up to prows) are left untouched (never used).
 template <typename TA>
 __global__ void __launch_bounds__(256)
-    digitize_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
-                    int64_t ppad, const double* __restrict__ mu_inv, int8_t* __restrict__ planes) {
+    digitize_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t prows,
+                    int64_t cols, int64_t ppad, const double* __restrict__ mu_inv,
+                    int8_t* __restrict__ planes) {
   const int64_t pblocks = ppad / 32;
-  const int64_t plane = rows * ppad;
+  const int64_t plane = prows * ppad;
   const int64_t total = pblocks * rows * 8;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -924,7 +936,7 @@ __global__ void __launch_bounds__(256)
     w[2] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
     w[1] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
     w[0] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
-    int8_t* dst = planes + (pb * rows + n) * 32 + 4 * q8;
+    int8_t* dst = planes + (pb * prows + n) * 32 + ((4 * q8) ^ (((n >> 2) & 1) << 4));
 #pragma unroll
     for (int a = 0; a < ND; ++a) *reinterpret_cast<uint32_t*>(dst + a * plane) = w[a];
   }
@@ -1032,7 +1044,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // digits, blocked by 32 K: Bd[nb][k / 32][a * 64 + j][k % 32] (every K-block's 448 x 32-byte
-// tile is one contiguous 14 KB run), colfac[nb*64 + jj]
+// tile is one contiguous 14 KB run), stored pre-swizzled (32-byte swizzle: the 16-byte half of
+// row r is flipped when bit 2 of r is set) so a plain bulk copy lands in the MMA layout;
+// colfac[nb*64 + jj]
 __global__ void __launch_bounds__(256)
     thin_digits_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
                        int64_t kpad, const double* __restrict__ mu_inv,
@@ -1084,7 +1098,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int a = 0; a < ND; ++a)
     *reinterpret_cast<uint32_t*>(
-        Bd + (((int64_t)nb * (kpad / 32) + blockIdx.x) * BROWS + a * 64 + j) * 32 + 4 * kg) = w[a];
+        Bd + (((int64_t)nb * (kpad / 32) + blockIdx.x) * BROWS + a * 64 + j) * 32 +
+        ((4 * kg) ^ ((((a * 64 + j) >> 2) & 1) << 4))) = w[a];
 }
 
 // (K x M) row-major sample block, box = 128 parameters x 32 samples, no swizzle
@@ -1117,8 +1132,7 @@ cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorM
 }
 
 template <bool RM>
-cudaError_t launch_pre(const CUtensorMap& tA, const CUtensorMap& tB, const Params& p, int grid,
-                       cudaStream_t st) {
+cudaError_t launch_pre(const CUtensorMap& tA, const Params& p, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(ozaki_pre_kernel<RM>,
@@ -1127,34 +1141,22 @@ cudaError_t launch_pre(const CUtensorMap& tA, const CUtensorMap& tB, const Param
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  ozaki_pre_kernel<RM><<<grid, kPreThreads, kPreSmem, st>>>(tA, tB, p);
+  ozaki_pre_kernel<RM><<<grid, kPreThreads, kPreSmem, st>>>(tA, p);
   return cudaGetLastError();
 }
 
-// 4-D map over the blocked digit planes [7][ppad / 32][rows][32] int8
-bool make_map_planes(CUtensorMap* map, const int8_t* planes, int64_t ppad, int64_t rows, bool rm) {
+// 4-D map over the blocked, pre-swizzled digit planes viewed as 128-byte rows:
+// {128 B (4 sample rows), prows / 4, ppad / 32 parameter blocks, 7 planes}, no TMA swizzle
+bool make_map_planes(CUtensorMap* map, const int8_t* planes, int64_t prows, int64_t pblocks,
+                     bool rm) {
   auto fn = tma_encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)(ppad / 32), (cuuint64_t)ND};
-  cuuint64_t strides[3] = {32, (cuuint64_t)(32 * rows), (cuuint64_t)(ppad * rows)};
-  cuuint32_t box[4] = {32, rm ? (cuuint32_t)BM : 32u, rm ? 1u : (cuuint32_t)(BM / 32),
-                       (cuuint32_t)ND};
+  cuuint64_t dims[4] = {128, (cuuint64_t)(prows / 4), (cuuint64_t)pblocks, (cuuint64_t)ND};
+  cuuint64_t strides[3] = {128, (cuuint64_t)(32 * prows), (cuuint64_t)(32 * prows * pblocks)};
+  cuuint32_t box[4] = {128, rm ? 32u : 8u, rm ? 1u : 4u, (cuuint32_t)ND};
   cuuint32_t es[4] = {1u, 1u, 1u, 1u};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// 3-D map over the blocked thin-operand digits [nblk * kblocks][448][32]
-bool make_map_thin(CUtensorMap* map, const int8_t* bd, int64_t blocks) {
-  auto fn = tma_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {32, (cuuint64_t)BROWS, (cuuint64_t)blocks};
-  cuuint64_t strides[2] = {32, (cuuint64_t)(32 * BROWS)};
-  cuuint32_t box[3] = {32, 224u, 1u};
-  cuuint32_t es[3] = {1u, 1u, 1u};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(bd), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1204,25 +1206,23 @@ bool ozaki_supported(Layout L, const GemmArgs& a, bool f32) {
          a.N <= 4096 && !a.partial && !a.Cin && (L == Layout::RM || L == Layout::CM);
 }
 
-int64_t ozaki_plane_pitch(int64_t cols) {
-  static const int extra = [] {
-    const char* e = std::getenv("WSSR_OZ_PITCH_PAD");  // debugging only
-    return e ? std::atoi(e) : 0;
-  }();
-  return ((cols + 127) / 128) * 128 + 128 * extra;
+int64_t ozaki_plane_pitch(int64_t cols) { return ((cols + 127) / 128) * 128; }
+int64_t ozaki_plane_rows(int64_t rows) { return ((rows + 127) / 128) * 128; }
+size_t ozaki_planes_bytes(int64_t rows, int64_t cols) {
+  return (size_t)oz::ND * ozaki_plane_rows(rows) * ozaki_plane_pitch(cols);
 }
 
 cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
                            int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st) {
-  const int64_t ppad = ozaki_plane_pitch(cols);
+  const int64_t ppad = ozaki_plane_pitch(cols), prows = ozaki_plane_rows(rows);
   const int64_t work = rows * (ppad / 4);  // threads: one per 4 parameters of a row
   const int grid = (int)std::min<int64_t>((work + 255) / 256, 16 * ctx.num_sms);
   if (f32)
     oz::digitize_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A), lda, rows,
-                                                     cols, ppad, mu_inv, planes);
+                                                     prows, cols, ppad, mu_inv, planes);
   else
     oz::digitize_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(A), lda, rows,
-                                                      cols, ppad, mu_inv, planes);
+                                                      prows, cols, ppad, mu_inv, planes);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
 }
@@ -1301,6 +1301,12 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   p.ldc = a.ldc;
   p.accumulate = a.accumulate;
   p.slab = nullptr;
+  p.bd = Bd;
+  p.planes = planes;
+  if (planes) {
+    p.prows = ozaki_plane_rows(RMm ? M : K);
+    p.pblocks = ozaki_plane_pitch(RMm ? K : M) / 32;
+  }
   {
     static const int dbg = [] {
       const char* e = std::getenv("WSSR_OZ_DEBUG");
@@ -1317,15 +1323,10 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   const int es = f32 ? 4 : 8;
   bool ok;
   if (planes) {
-    // pre-digitised planes [7][samples][ppad]: samples = M (RM) or K (CM)
-    const int64_t samples = RMm ? M : K;
-    const int64_t ppad = ozaki_plane_pitch(RMm ? K : M);
-    ok = make_map_planes(&tA, planes, ppad, samples, RMm) &&
-         make_map_thin(&tB, Bd, (int64_t)nblk * kblocks);
-    if (!ok) return cudaErrorInvalidValue;
+    if (!make_map_planes(&tA, planes, p.prows, p.pblocks, RMm)) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nblk * nch;
     const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
-    e = RMm ? launch_pre<true>(tA, tB, p, grid, st) : launch_pre<false>(tA, tB, p, grid, st);
+    e = RMm ? launch_pre<true>(tA, p, grid, st) : launch_pre<false>(tA, p, grid, st);
     ctx.kernel_launches += 1;
     ctx.gemm_launches += 1;
   } else if (RMm) {
@@ -1335,7 +1336,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
   }
   if (!planes) {
-    ok = ok && make_map_thin(&tB, Bd, (int64_t)nblk * kblocks);
+    std::memset(&tB, 0, sizeof(tB));  // thin digits arrive by plain bulk copies
     if (!ok) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nblk * nch;
     const int grid = (int)std::min<int64_t>(units, ctx.num_sms);

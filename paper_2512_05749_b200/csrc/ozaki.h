@@ -35,6 +35,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
 // (rows = samples, cols = parameters, row-major with pitch lda); written once per step and
 // streamed by both O-passes.
 int64_t ozaki_plane_pitch(int64_t cols);
+size_t ozaki_planes_bytes(int64_t rows, int64_t cols);
 cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
                            int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st);
 

@@ -49,7 +49,10 @@ def bench(layout, M, N, K, f32=False, reps=10):
 
 if __name__ == "__main__":
     if "--one" in sys.argv:
-        bench(1, 4096, 64, 131072, reps=3)
+        if sys.argv[-1] == "0":
+            bench(0, 131072, 64, 4096, reps=3)
+        else:
+            bench(1, 4096, 64, 131072, reps=3)
         sys.exit(0)
     bench(1, 4096, 64, 131072)
     bench(0, 131072, 64, 4096)
