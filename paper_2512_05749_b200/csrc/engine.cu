@@ -441,19 +441,27 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       tab = *o.oz_scale;
     }
     const int8_t* planes = nullptr;
+    int8_t* store = nullptr;
     if (ctx.oz_pre == 0) {
       if (!o.oz_planes) {
         o.oz_planes = std::make_shared<Ohat::Planes>();
         const size_t bytes = ozaki_planes_bytes(o.n, o.P);
         if (ensure_planes(ctx, bytes)) {
-          WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, ctx.oz_planes,
-                                   ctx.stream));
+          if (layout == Layout::RM) {
+            // the first pass (v = Ohat^T q) digitises on the fly and writes the planes
+            store = ctx.oz_planes;
+          } else {
+            WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, ctx.oz_planes,
+                                     ctx.stream));
+            planes = ctx.oz_planes;
+          }
           o.oz_planes->ptr = ctx.oz_planes;
         }
+      } else {
+        planes = o.oz_planes->ptr;
       }
-      planes = o.oz_planes->ptr;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store));
     return;
   }
   if (o.f32) {

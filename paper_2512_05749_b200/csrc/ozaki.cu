@@ -283,6 +283,7 @@ struct Params {
   const int8_t* planes;    // pre-digitised: blocked, pre-swizzled planes [7][pblocks][prows][32]
   int64_t prows, pblocks;
   const int8_t* bd;        // blocked, pre-swizzled thin digits [nblk * kblocks][448][32]
+  int8_t* store;           // on-the-fly v pass: also write the digit planes (layout as `planes`)
   int debug;               // profiling only, low bits: 1 = skip digitising, 2 = skip MMAs,
                            // 3 = both, 4 = skip the sample-block loads too; +8 = trace CTA 0
 };
@@ -436,6 +437,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks && lane == 0)
           g_oz_trace[2][g] = clock64();
         tc_fence_after();
+        const bool stored = RM && p.store && nb == 0;
+        if (lane == 0 && stored) {
+          // the digit tile in shared memory already has the planes' pre-swizzled layout:
+          // one 4 KB bulk store per plane (async; its shared-memory reads are awaited before
+          // this stage's slot is released below)
+          const int64_t pstride = p.pblocks * p.prows * 32;
+#pragma unroll
+          for (int a = 0; a < ND; ++a)
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 4096;\n" ::"l"(
+                    p.store + a * pstride + (kb * p.prows + m0) * 32),
+                "r"(smem_u32(a_dig(d) + a * BM * BK))
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
         if (lane == 0) {
           if ((p.debug & 7) != 2 && (p.debug & 7) != 3) {
             const uint32_t abase = smem_u32(a_dig(d)), bbase = smem_u32(b_dig(bs));
@@ -469,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // commits track this thread's MMAs; the tensor pipe executes in issue order, so the
           // other warp's earlier K-blocks are complete as well
+          if (stored) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
           mma_commit(&dempty[d]);
           mma_commit(&bempty[bs]);
           if (kb + 1 == kb1) mma_commit(tfull);
@@ -628,6 +645,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if ((warp == 1 || warp == 3) && lane == 0 && RM && p.store)
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // digit planes written
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -1228,7 +1247,7 @@ cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, i
 }
 
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
-                       cudaStream_t st, const int8_t* planes) {
+                       cudaStream_t st, const int8_t* planes, int8_t* store) {
   using namespace oz;
   const bool RMm = L == Layout::RM;
   const int64_t M = a.M, N = a.N, K = a.K;
@@ -1303,7 +1322,8 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   p.slab = nullptr;
   p.bd = Bd;
   p.planes = planes;
-  if (planes) {
+  p.store = (!planes && RMm) ? store : nullptr;
+  if (planes || p.store) {
     p.prows = ozaki_plane_rows(RMm ? M : K);
     p.pblocks = ozaki_plane_pitch(RMm ? K : M) / 32;
   }

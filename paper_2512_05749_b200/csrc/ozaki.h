@@ -27,9 +27,11 @@ cudaError_t ozaki_scales_minmax(Context& ctx, const double* cmin, const double* 
 cudaError_t ozaki_trace(long long* host, size_t bytes);
 
 bool ozaki_supported(Layout L, const GemmArgs& a, bool f32);
-// planes: the step's pre-digitised sample block (ozaki_digitize) or nullptr (digitise on the fly)
+// planes: the step's pre-digitised sample block (ozaki_digitize) or nullptr (digitise on the
+// fly); store: with planes == nullptr and the row-major (v) layout, also write the digit planes
+// the on-the-fly pass produces (same layout as ozaki_digitize), so later passes can stream them.
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
-                       cudaStream_t st, const int8_t* planes = nullptr);
+                       cudaStream_t st, const int8_t* planes = nullptr, int8_t* store = nullptr);
 
 // Digit planes [7][rows][ozaki_plane_pitch(cols)] int8 of the centred, scaled sample block
 // (rows = samples, cols = parameters, row-major with pitch lda); written once per step and

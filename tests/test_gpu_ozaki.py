@@ -180,3 +180,32 @@ def test_assemble_scale_table_matches_on_demand():
         th, _, d = optimizers.wssr_step(theta, b, 1.0, st)
         outs.append(th)
     assert torch.equal(outs[0], outs[1])
+
+
+def test_step_paths_agree():
+    """A WSSR step with the planes written by the first on-the-fly pass (path 3), digitised
+    inside every pass (path 4) and on FP64 DMMA (path 2) agree to rounding level."""
+    from paper_2512_05749_b200 import _lib, estimators, optimizers, synthetic
+
+    ctx = _lib.context()
+    cfg = synthetic.config("c0", N=480, P=12288, k=24, L=32, delta=0.5, lam=1e-3)
+    wl = synthetic.HostWorkload.from_config(cfg, 9)
+    o, e = wl.next()
+    b = estimators.assemble(estimators.SampleBatch((None,) * o.shape[0], e, o))
+    st0 = optimizers.WssrState.initial(cfg["P"], rank_init=cfg["k"], delta=cfg["delta"],
+                                       sigma_floor=cfg["lam"])
+    theta = torch.zeros(cfg["P"], dtype=torch.float64, device="cuda")
+    _, st, _ = optimizers.wssr_step(theta, b, 1.0, st0)
+    o, e = wl.next()
+    b = estimators.assemble(estimators.SampleBatch((None,) * o.shape[0], e, o))
+    outs = {}
+    for path in (3, 4, 2):
+        ctx.lib.wssr_set_gemm_path(ctx.handle, path)
+        th, st1, d = optimizers.wssr_step(theta, b, 1.0, st)
+        outs[path] = (th, optimizers.sigma_of(st1), d.ssi.iterations_used)
+    ctx.lib.wssr_set_gemm_path(ctx.handle, _PATH[0])
+    for path in (3, 4):
+        th, sg, it = outs[path]
+        assert it == outs[2][2]
+        assert ((th - outs[2][0]).norm() / outs[2][0].norm()).item() < 1e-12
+        assert ((sg - outs[2][1]).norm() / outs[2][1].norm()).item() < 1e-12
