@@ -247,7 +247,18 @@ double read_scalar(Context& ctx, const double* dev) {
 void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int* status) {
   const size_t smem = sizeof(double) * chol_scratch_doubles(k);
   if (k <= 64) {
-    chol_inv_reg64_kernel<<<1, 256, 0, ctx.stream>>>(G, k, R, Rinv, status, kCholPivotRel);
+    // dynamic shared memory enables the near-identity series path (second CholeskyQR2 pass)
+    const int series_smem = ctx.chol_series ? (int)(2 * 64 * 65 * sizeof(double)) : 0;
+    static bool attr = false;
+    if (!attr) {
+      WSSR_CUDA(cudaFuncSetAttribute(chol_inv_reg64_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(2 * 64 * 65 * sizeof(double))));
+      attr = true;
+    }
+    chol_inv_reg64_kernel<<<1, 256, series_smem, ctx.stream>>>(G, k, R, Rinv, status,
+                                                                 kCholPivotRel,
+                                                                 ctx.chol_series ? 1 : 0);
   } else if (smem <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {

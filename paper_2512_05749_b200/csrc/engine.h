@@ -37,6 +37,7 @@ struct Context {
   bool disable_tma = false;  // force the cp.async GEMM path (tests / A-B comparisons)
   bool ozaki = true;         // O-passes on the int8 tensor cores (exact digit products)
   double oz_min_elems = 4194304.0;  // smallest sample block (elements) sent to that path
+  bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
   int oz_pre = 0;            // digit planes: 0 = pre-digitise when they fit, 1 = on the fly only
   int8_t* oz_planes = nullptr;  // the step's pre-digitised sample block (reused across steps)
   size_t oz_planes_cap = 0;     // bytes

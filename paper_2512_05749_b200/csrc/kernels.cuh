@@ -406,6 +406,107 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     }
 }
 
+constexpr double kCholSeriesMax = 1e-5;  // ||G - I||_max below which the series path is taken
+
+// Series Cholesky + inverse of a near-identity k x k Gram (k <= 64), one CTA of 256 threads.
+// w holds the thread's 4 x 4 slice of G (rows ty + 16 a, columns tx + 16 b, identity-padded).
+// buf: 2 x 64 x 65 doubles of shared memory.
+__device__ __noinline__ void chol_series(const double (&w)[4][4], double em, int k,
+                                         double* __restrict__ R, double* __restrict__ Rinv,
+                                         double* buf) {
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  constexpr int LD = 65;
+  double* X = buf;
+  double* Y = buf + 64 * LD;
+  // number of corrections / Neumann terms so that em^(n) < 1e-18
+  const double lg = log10(fmax(em, 1e-300));
+  const int terms = em == 0.0 ? 0 : (int)ceil(-18.0 / lg);  // em < 1e-5 -> at most 4
+  double e[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      e[a][b] = w[a][b] - (i == c ? 1.0 : 0.0);
+      X[i * LD + c] = i < c ? e[a][b] : (i == c ? 0.5 * e[a][b] : 0.0);
+    }
+  __syncthreads();
+  for (int it = 0; it < terms; ++it) {  // X <- U(E - X^T X)
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int m = 0; m < 64; ++m) {
+      double xa[4], xb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xa[a] = X[m * LD + ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) xb[b] = X[m * LD + tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(xa[a], xb[b], acc[a][b]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = ty + 16 * a, c = tx + 16 * b;
+        const double v = e[a][b] - acc[a][b];
+        X[i * LD + c] = i < c ? v : (i == c ? 0.5 * v : 0.0);
+      }
+    __syncthreads();
+  }
+  // Y = sum_j (-X)^j by Horner: Y <- I - X Y, terms + 1 times
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      Y[i * LD + c] = (i == c) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  for (int it = 0; it <= terms; ++it) {
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int m = 0; m < 64; ++m) {
+      double xa[4], yb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xa[a] = X[(ty + 16 * a) * LD + m];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) yb[b] = Y[m * LD + tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(xa[a], yb[b], acc[a][b]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = ty + 16 * a, c = tx + 16 * b;
+        Y[i * LD + c] = (i == c ? 1.0 : 0.0) - acc[a][b];
+      }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      if (i < k && c < k) {
+        R[i * k + c] = i <= c ? (i == c ? 1.0 : 0.0) + X[i * LD + c] : 0.0;
+        Rinv[i * k + c] = i <= c ? Y[i * LD + c] : 0.0;
+      }
+    }
+}
+
 // k <= 64: register-resident variant.  The matrix is padded to 64 x 64 with an identity tail;
 // thread (ty, tx) of the 16 x 16 grid owns rows {ty + 16 a} x columns {tx + 16 b}, a, b < 4, of
 // both L (lower part of W) and X = L^-1, in registers.  Per column j: the owners of column j of L
@@ -416,7 +517,8 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
                                                              double* __restrict__ R,
                                                              double* __restrict__ Rinv,
                                                              int* __restrict__ status,
-                                                             double pivot_rel) {
+                                                             double pivot_rel, int use_series) {
+  extern __shared__ double series_buf[];  // 2 x 64 x 65 doubles when use_series
   __shared__ double colL[64], rowX[64], dg[64];
   __shared__ double s_sq, s_inv, s_tr, s_gmax;
   __shared__ int s_fail;
@@ -432,6 +534,35 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
     }
   if (tid < 64) dg[tid] = tid < k ? G[tid * k + tid] : 1.0;
   __syncthreads();
+  {
+    // Near-identity Gram (the second pass of CholeskyQR2): R = I + X with X upper triangular,
+    // X + X^T + X^T X = E = G - I, solved by X <- U(E - X^T X) (U: strict upper part plus half
+    // the diagonal), and R^-1 = sum_j (-X)^j.  Each iteration gains one order of ||E||, so a
+    // handful of 64 x 64 products replace the 64-step dependent Cholesky sweep.
+    double em = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = ty + 16 * a, c = tx + 16 * b;
+        em = fmax(em, fabs(w[a][b] - (i == c ? 1.0 : 0.0)));
+      }
+    __shared__ double red_em[8];
+    em = warp_max(em);
+    if ((tid & 31) == 0) red_em[tid >> 5] = em;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < 8 ? red_em[tid] : 0.0;
+      v = warp_max(v);
+      if (tid == 0) red_em[0] = v;
+    }
+    __syncthreads();
+    em = red_em[0];
+    if (use_series && em < kCholSeriesMax) {
+      chol_series(w, em, k, R, Rinv, series_buf);
+      return;
+    }
+  }
   if (tid == 0) {
     double gm = 0.0, tr = 0.0;
     for (int j = 0; j < k; ++j) {

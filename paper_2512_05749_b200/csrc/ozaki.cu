@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
           if (A) {
             const int s = g % PSTAGES;
             mbar_sleep_wait(&aempty[s], ((g / PSTAGES) & 1) ^ 1);
+            if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks) g_oz_trace[5][g] = clock64();
             if ((p.debug & 7) == 5) {  // profiling: no sample-digit traffic
               mbar_arrive(&afull[s]);
               continue;
@@ -761,6 +762,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
           } else {
             const int b = g % PBSTAGES;
             mbar_sleep_wait(&bempty[b], ((g / PBSTAGES) & 1) ^ 1);
+            if (p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks) g_oz_trace[6][g] = clock64();
             if ((p.debug & 7) == 6) {  // profiling: no thin-digit traffic
               mbar_arrive(&bfull[b]);
               continue;
@@ -794,9 +796,14 @@ __global__ void __launch_bounds__(kPreThreads, 1)
       for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
         if ((int)(g & 1) != me) continue;
         const int s = g % PSTAGES, bs = g % PBSTAGES;
+        const bool tr = p.debug >= 8 && blockIdx.x == 0 && g < kTraceBlocks && lane == 0;
+        if (tr) g_oz_trace[0][g] = clock64();
         mbar_sleep_wait(&bfull[bs], (g / PBSTAGES) & 1);
+        if (tr) g_oz_trace[1][g] = clock64();
         mbar_sleep_wait(&afull[s], (g / PSTAGES) & 1);
+        if (tr) g_oz_trace[2][g] = clock64();
         if (g > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + me) : "memory");  // token in
+        if (tr) g_oz_trace[3][g] = clock64();
         tc_fence_after();
         if (lane == 0 && (p.debug & 7) == 7) {  // profiling: no MMAs
           mma_commit(&aempty[s]);
@@ -839,6 +846,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
           mma_commit(&aempty[s]);
           mma_commit(&bempty[bs]);
           if (kb + 1 == kb1) mma_commit(tfull);
+          if (tr) g_oz_trace[4][g] = clock64();
         }
         __syncwarp();
         if ((int64_t)g + 1 < total) asm volatile("bar.arrive %0, 64;\n" ::"r"(2 - me) : "memory");

@@ -61,3 +61,20 @@ def test_maxeig_clustered_top():
     a = (q * ev) @ q.T
     lam, _, _ = _small(1, a)
     assert abs(lam[0, 0] - 1.0) < 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 5, 32, 64])
+@pytest.mark.parametrize("eps", [0.0, 1e-15, 1e-10, 3e-6])
+def test_cholesky_near_identity_series(k, eps):
+    """Near-identity Grams (the second CholeskyQR2 pass) take the series path: R and R^-1 agree
+    with the Cholesky factor to rounding level and R^T R reproduces G."""
+    rng = np.random.default_rng(int(k * 1000 + eps * 1e15) % 2**32)
+    e = rng.standard_normal((k, k)) * eps
+    g = np.eye(k) + (e + e.T) / 2
+    r, rinv, st = _small(0, g)
+    assert st == (0, 0)
+    ref = np.linalg.cholesky(g).T
+    np.testing.assert_allclose(r, ref, rtol=0, atol=4e-16)
+    np.testing.assert_allclose(r.T @ r, g, rtol=0, atol=4e-16)
+    np.testing.assert_allclose(rinv @ r, np.eye(k), rtol=0, atol=4e-16)
+    assert np.all(np.tril(rinv, -1) == 0.0) and np.all(np.tril(r, -1) == 0.0)

@@ -11,6 +11,10 @@ from paper_2512_05749_b200 import _lib
 
 layout = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 ctx = _lib.context()
+if os.environ.get("OZ_PRE", "0") == "1":
+    ctx.lib.wssr_set_gemm_path(ctx.handle, 3)
+else:
+    ctx.lib.wssr_set_gemm_path(ctx.handle, 4)
 if layout == 1:
     M, N, K = 4096, 64, 131072
 else:
@@ -25,11 +29,14 @@ for _ in range(2):
              _lib.ptr(B), N, _lib.ptr(C), N, 1.0)
 tr = np.zeros((8, 96), dtype=np.int64)
 ctx.call("wssr_debug_ozaki_trace", ctypes.c_void_p(tr.ctypes.data), tr.size)
-names = ["raw TMA issue", "mma waits done", "mma token", "mma issued", "conv rfull ok",
-         "conv computed", "conv dempty ok", "conv arrived"]
+PRE = os.environ.get("OZ_PRE", "0") == "1"
+names = (["raw TMA issue", "mma waits done", "mma token", "mma issued", "conv rfull ok",
+          "conv computed", "conv dempty ok", "conv arrived"] if not PRE else
+         ["mma start", "bfull ok", "afull ok", "token ok", "issued", "A TMA issue", "B TMA issue",
+          "-"])
 t0 = tr[0][0]
 print("g   " + " ".join(f"{n[:13]:>13s}" for n in names))
 for g in range(10, 40):
     print(f"{g:3d} " + " ".join(f"{(tr[i][g] - t0) if tr[i][g] else -1:13d}" for i in range(8)))
-d = np.diff(tr[3][10:90])
+d = np.diff(tr[4 if PRE else 3][10:90])
 print("MMA issued-to-issued per K-block: mean", d.mean(), "median", np.median(d))
