@@ -62,7 +62,7 @@ constexpr int kColStatsWarps = 8;
 // VEC columns per lane (VEC = 2: 16-byte loads, a warp streams 512 contiguous bytes per row);
 // UNROLL rows in flight per lane so each SM keeps >= 64 KB of loads outstanding.
 template <typename T, int VEC, int UNROLL>
-__global__ void __launch_bounds__(32 * kColStatsWarps, 3)
+__global__ void __launch_bounds__(32 * kColStatsWarps, 2)
     colstats_kernel(const T* __restrict__ O, int64_t n, int64_t p, int64_t ld,
                     const double* __restrict__ lraw, double* __restrict__ mu,
                     double* __restrict__ m2, double* __restrict__ gsum,
@@ -75,15 +75,18 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
   for (int v = 0; v < VEC; ++v) act[v] = col0 + v < p;
   const int64_t rows_per = (n + kColStatsWarps - 1) / kColStatsWarps;
   const int64_t r0 = min(n, (int64_t)w * rows_per), r1 = min(n, r0 + rows_per);
-  double K[VEC], s1[VEC], s2[VEC], sl[VEC], mn[VEC], mx[VEC];
+  // samples stay in their storage type until used (FP32: half the registers, so twice the rows
+  // in flight); extrema are exact in that type
+  double K[VEC], s1[VEC], s2[VEC], sl[VEC];
+  T mn[VEC], mx[VEC];
   double lsum = 0.0;
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
     K[v] = s1[v] = s2[v] = sl[v] = 0.0;
-    mn[v] = 1.0 / 0.0;
-    mx[v] = -1.0 / 0.0;
+    mn[v] = (T)(1.0 / 0.0);
+    mx[v] = (T)(-1.0 / 0.0);
   }
-  auto load = [&](int64_t r, double (&x)[VEC]) {
+  auto load = [&](int64_t r, T (&x)[VEC]) {
     if constexpr (sizeof(T) == 8 && VEC == 2) {
       if (act[VEC - 1]) {
         const double2 y = __ldg(reinterpret_cast<const double2*>(O + r * ld + col0));
@@ -102,16 +105,17 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
       }
     }
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) x[v] = act[v] ? (double)__ldg(O + r * ld + col0 + v) : 0.0;
+    for (int v = 0; v < VEC; ++v) x[v] = act[v] ? __ldg(O + r * ld + col0 + v) : (T)0;
   };
   if (r1 > r0) {
-    double x0[VEC];
+    T x0[VEC];
     load(r0, x0);
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) K[v] = act[v] ? x0[v] : 0.0;
+    for (int v = 0; v < VEC; ++v) K[v] = act[v] ? (double)x0[v] : 0.0;
     int64_t r = r0;
     for (; r + UNROLL <= r1; r += UNROLL) {
-      double x[UNROLL][VEC], l[UNROLL];
+      T x[UNROLL][VEC];
+      double l[UNROLL];
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         load(r + u, x[u]);
@@ -122,23 +126,23 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
         lsum += l[u];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
-          const double d = act[v] ? x[u][v] - K[v] : 0.0;
+          const double d = act[v] ? (double)x[u][v] - K[v] : 0.0;
           s1[v] += d;
           s2[v] = fma(d, d, s2[v]);
           sl[v] = fma(d, l[u], sl[v]);
-          mn[v] = x[u][v] < mn[v] ? x[u][v] : mn[v];  // (no NaN propagation: 3 instructions)
+          mn[v] = x[u][v] < mn[v] ? x[u][v] : mn[v];  // (no NaN propagation)
           mx[v] = x[u][v] > mx[v] ? x[u][v] : mx[v];
         }
       }
     }
     for (; r < r1; ++r) {
-      double x[VEC];
+      T x[VEC];
       load(r, x);
       const double l = __ldg(lraw + r);
       lsum += l;
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
-        const double d = act[v] ? x[v] - K[v] : 0.0;
+        const double d = act[v] ? (double)x[v] - K[v] : 0.0;
         s1[v] += d;
         s2[v] = fma(d, d, s2[v]);
         sl[v] = fma(d, l, sl[v]);
@@ -196,8 +200,8 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 3)
     __syncthreads();
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      sh[w][0][lane * VEC + v] = mn[v];
-      sh[w][1][lane * VEC + v] = mx[v];
+      sh[w][0][lane * VEC + v] = (double)mn[v];
+      sh[w][1][lane * VEC + v] = (double)mx[v];
     }
     __syncthreads();
     for (int c = threadIdx.x; c < 32 * VEC; c += blockDim.x) {
