@@ -347,11 +347,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   const int64_t units = (int64_t)p.mtiles * p.nblk * p.nch;
+  // unit -> (64-column block fastest, then row tile, then K chunk): the column blocks of one row
+  // tile run on neighbouring CTAs at the same time, so the second reads the tile from L2
   auto decode = [&](int64_t u, int64_t& m0, int& nb, int& kc, int64_t& kb0, int64_t& kb1) {
-    m0 = (u % p.mtiles) * BM;
-    const int64_t rest = u / p.mtiles;
-    nb = (int)(rest % p.nblk);
-    kc = (int)(rest / p.nblk);
+    nb = (int)(u % p.nblk);
+    const int64_t rest = u / p.nblk;
+    m0 = (rest % p.mtiles) * BM;
+    kc = (int)(rest / p.mtiles);
     kb0 = p.kblocks * kc / p.nch;
     kb1 = p.kblocks * (kc + 1) / p.nch;
   };
@@ -724,11 +726,13 @@ __global__ void __launch_bounds__(kPreThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   const int64_t units = (int64_t)p.mtiles * p.nblk * p.nch;
+  // unit -> (64-column block fastest, then row tile, then K chunk): the column blocks of one row
+  // tile run on neighbouring CTAs at the same time, so the second reads the tile from L2
   auto decode = [&](int64_t u, int64_t& m0, int& nb, int& kc, int64_t& kb0, int64_t& kb1) {
-    m0 = (u % p.mtiles) * BM;
-    const int64_t rest = u / p.mtiles;
-    nb = (int)(rest % p.nblk);
-    kc = (int)(rest / p.nblk);
+    nb = (int)(u % p.nblk);
+    const int64_t rest = u / p.nblk;
+    m0 = (rest % p.mtiles) * BM;
+    kc = (int)(rest / p.mtiles);
     kb0 = p.kblocks * kc / p.nch;
     kb1 = p.kblocks * (kc + 1) / p.nch;
   };
