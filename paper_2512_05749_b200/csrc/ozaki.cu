@@ -1054,15 +1054,35 @@ __device__ __forceinline__ double thin_value(const double* B, int64_t ldb, int64
 __global__ void __launch_bounds__(256)
     thin_colmax_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
                        const double* __restrict__ mu_inv, unsigned long long* __restrict__ out) {
+  // block: 64 columns of one 64-column block x 4 row lanes, 128 rows; 8 independent rows in
+  // flight per thread
   const int j = threadIdx.x & 63, kl = threadIdx.x >> 6;
   const int64_t jj = (int64_t)blockIdx.y * 64 + j;
   double best = 0.0;
   if (jj < N) {
-    const int64_t k1 = min(K, (int64_t)(blockIdx.x + 1) * 256);
-#pragma unroll 4
-    for (int64_t k = (int64_t)blockIdx.x * 256 + kl; k < k1; k += 4) {
-      if (mu_inv && mu_inv[2 * tab_slot(k) + 1] == 0.0) continue;
-      best = fmax(best, fabs(thin_value(B, ldb, k, jj, mu_inv)));
+    const int64_t k0 = (int64_t)blockIdx.x * 128 + kl;
+#pragma unroll
+    for (int u = 0; u < 32; u += 8) {
+      double v[8], mul[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t k = k0 + 4 * (u + i);
+        v[i] = 0.0;
+        mul[i] = 1.0;
+        if (k < K) {
+          v[i] = __ldg(B + k * ldb + jj);
+          if (mu_inv) {
+            const double inv = __ldg(mu_inv + 2 * tab_slot(k) + 1);
+            // 2^54 / inv from the exponent field (0 for padding columns: inv == 0)
+            mul[i] = inv == 0.0 ? 0.0
+                                : __longlong_as_double(
+                                      (long long)(2046 + 54 - (__double_as_longlong(inv) >> 52))
+                                      << 52);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) best = fmax(best, fabs(v[i] * mul[i]));
     }
   }
   __shared__ double red[4][64];
@@ -1287,7 +1307,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   // RM (v = Ohat^T q): the thin operand's rows are parameters -> carries the column scales
   const double* bmu = RMm ? mu_inv : nullptr;
   {
-    thin_colmax_kernel<<<dim3((unsigned)((K + 255) / 256), nblk), 256, 0, st>>>(a.B, a.ldb, K, N,
+    thin_colmax_kernel<<<dim3((unsigned)((K + 127) / 128), nblk), 256, 0, st>>>(a.B, a.ldb, K, N,
                                                                                bmu, cmax);
     thin_digits_kernel<<<dim3((unsigned)(kpad / 32), 2 * nblk), 256, 0, st>>>(
         a.B, a.ldb, K, N, kpad, bmu, cmax, RMm ? 54 : 0, Bd, colfac);
