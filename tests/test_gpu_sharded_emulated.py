@@ -139,3 +139,31 @@ def test_emulated_allreduce_sums_in_rank_order():
     with EmulatedGroup(3) as grp:
         for out in grp.run(body):
             np.testing.assert_array_equal(out, 6.0)
+
+
+@pytest.mark.parametrize("path", [3, 4], ids=["int8_planes", "int8_on_the_fly"])
+def test_sharded_int8_o_passes(golden, path):
+    """The int8 tensor-core O-passes under row sharding (per-rank scale tables and digit planes,
+    allreduced u): 2 emulated ranks reproduce the single-rank step on the same path."""
+    from paper_2512_05749_b200 import _lib
+    from paper_2512_05749_b200.distributed import EmulatedGroup, row_shard
+    from _runs import fixture_config
+
+    g = golden("hist_T4.npz")
+    n = fixture_config("hist_T4.npz", g)[0]["N"]
+    ctx = _lib.context()
+    ctx.lib.wssr_set_gemm_path(ctx.handle, path)
+    try:
+        single = device_run("hist_T4.npz", g)
+        with EmulatedGroup(2) as grp:
+            for c in grp.contexts:
+                c.lib.wssr_set_gemm_path(c.handle, path)
+            sharded = grp.run(lambda r, w: device_run("hist_T4.npz", g, rows=row_shard(n, r, w)))
+    finally:
+        ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
+    _check_run(single, g, "hist_T4 single int8")
+    for runs in sharded:
+        for a, b in zip(single, runs):
+            assert a["r_eff"] == b["r_eff"] and a["iterations"] == b["iterations"]
+            assert rel(b["update"], a["update"]) < 1e-11
+            assert rel(b["sigma"], a["sigma"]) < 1e-11
