@@ -78,3 +78,23 @@ def test_cholesky_near_identity_series(k, eps):
     np.testing.assert_allclose(r.T @ r, g, rtol=0, atol=4e-16)
     np.testing.assert_allclose(rinv @ r, np.eye(k), rtol=0, atol=4e-16)
     assert np.all(np.tril(rinv, -1) == 0.0) and np.all(np.tril(r, -1) == 0.0)
+
+
+@pytest.mark.parametrize("rows,k", [(20000, 64), (9001, 37), (50000, 8)])
+def test_tall_skinny_qr(rows, k):
+    """CholeskyQR2 on the tall-skinny kernels (symmetric Gram, triangular products) reproduces
+    the Householder QR: orthonormal Q, R with a nonnegative diagonal, A = Q R."""
+    from paper_2512_05749_b200 import linalg
+
+    g = torch.Generator(device="cuda").manual_seed(rows + k)
+    a = torch.randn(rows, k, dtype=torch.float64, device="cuda", generator=g)
+    a = a * torch.logspace(-3, 3, k, dtype=torch.float64, device="cuda")
+    q, r = linalg.qr_orthonormalize(a)
+    eye = torch.eye(k, dtype=torch.float64, device="cuda")
+    assert (q.t() @ q - eye).abs().max().item() < 1e-13
+    assert ((q @ r - a).norm() / a.norm()).item() < 1e-14
+    q2, r2 = torch.linalg.qr(a)
+    s = torch.sign(torch.diagonal(r2))
+    r2 = r2 * s[:, None]
+    assert ((r - r2).norm() / r2.norm()).item() < 1e-12
+    assert torch.all(torch.tril(r, -1) == 0)
