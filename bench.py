@@ -254,7 +254,7 @@ def run_ours(args, rank, world, local_rank):
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
     launches = ctx.kernel_launches() - launches0
-    phases = [ctx.phase_stats(i) for i in range(3)]
+    phases = [ctx.phase_stats(i) for i in range(8)]
     ctx.set_timing(False)
     step_ms = sum(x.elapsed_time(y) for x, y in intervals)
     t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
@@ -308,6 +308,11 @@ def run_ours(args, rank, world, local_rank):
                    "gbs": ph["bytes"] / (ph["ms"] * 1e-3) / 1e9 if ph["ms"] else None,
                    "launches": ph["launches"]}
             for name, ph in zip(["v=OhatT_q", "u=Ohat_v", "assemble_colstats"], phases)},
+        "step_budget_ms": dict(
+            **{name: phases[i]["ms"] / args.steps for i, name in enumerate(
+                ["v_passes", "u_passes", "assemble_colstats", "cholqr2_Pxk",
+                 "ssi_quotient_residual", "drift", "precond_and_refresh", "qr_v_and_sort"])},
+            other=ms_per_step - sum(ph["ms"] for ph in phases) / args.steps),
         "step": {
             "flops_alg": flops_alg, "bytes_alg": bytes_alg, "ssi_iterations": m_avg,
             "t_roof_ms": bytes_alg / (hbm_peak * 1e9 * world) * 1e3,

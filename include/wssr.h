@@ -83,6 +83,9 @@ typedef struct wssr_ohat_f64 {
                           {mu_p, 2^(54 - e_p)} table of the int8 tensor-core O-passes, as written
                           by assemble (wssr_assemble_out.scale_table); NULL: computed on demand
                           with one extra read of the sample block. */
+  const double* samples_fro2_dev; /* optional: when samples_fro2 < 0, the device value of the
+                          sample block's ||.||_F^2 (wssr_assemble_out.fro2_dev); read at the first
+                          host synchronisation of the step instead of up front. */
 } wssr_ohat_f64;
 
 /* --- context ------------------------------------------------------------------------------ */
@@ -142,6 +145,13 @@ typedef struct wssr_assemble_out {
   int64_t n_global;
   double* scale_table; /* optional [2 * roundup(P, 32)]: per-parameter scales of the int8
                           tensor-core O-passes, from the same column pass (this rank's rows) */
+  /* optional deferred host outputs (single rank): when `deferred` (pinned host memory, 5
+     doubles) is non-NULL the call returns without waiting for the device; {loss, raw_loss,
+     e_mean, e_std, fro2} land there in stream order (valid once the stream reaches this point)
+     and the host fields above are left unset.  fro2_dev (device, 1 double) then receives fro2
+     for wssr_ohat_f64.samples_fro2_dev, so a following wssr_step never waits on assemble. */
+  double* deferred;
+  double* fro2_dev;
 } wssr_assemble_out;
 int wssr_assemble_f64(wssr_ctx* ctx, const double* derivs, int64_t n, int64_t p, int64_t ld,
                       const double* energies, double clip_n_std, wssr_assemble_out* out);
@@ -255,6 +265,19 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
 /* profiling hook: per-K-block timestamps (SM clock) of CTA 0 of the last int8 O-pass launched
  * with WSSR_OZ_DEBUG=9, 8 rows x 96 K-blocks (producer, MMA issuers, converter group leaders). */
 int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
+
+/* engine option: 1 (default) runs the Grams and k x k products of P x k blocks with k = 32 or 64
+ * (CholeskyQR2, Rayleigh quotient and residual, drift) on the tall-skinny kernels
+ * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
+int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
+
+/* test hook: one tall-skinny kernel, row-major operands with ld = k (k = 32 or 64).
+ * op 0: out = A^T A (k x k); op 1: out = A^T B; op 2: out (rows x k) = A (alpha M) with M upper
+ * triangular; op 3: out = A (alpha M); op 4: out = Cin + A (alpha M);
+ * op 5: out[0] = ||Cin + A (alpha M)||_F^2; op 6: out (k) = alpha A^T x, x = cin (rows). */
+int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const double* a,
+                          const double* b, const double* m, const double* cin, double alpha,
+                          double* out);
 
 /* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
 int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,

@@ -32,7 +32,7 @@ class OhatF64(ctypes.Structure):
         ("hist", _vp), ("hist_rank", _i64), ("hist_ld", _i64), ("hist_scale", _dbl),
         ("samples", _vp), ("n_samples", _i64), ("samples_ld", _i64), ("mu", _vp),
         ("samples_scale", _dbl), ("samples_fro2", _dbl), ("samples_f32", _i64),
-        ("samples_scale_table", _vp),
+        ("samples_scale_table", _vp), ("samples_fro2_dev", _vp),
     ]
 
 
@@ -41,6 +41,7 @@ class AssembleOut(ctypes.Structure):
         ("mu", _vp), ("l_vector", _vp), ("gradient", _vp),
         ("loss", _dbl), ("raw_loss", _dbl), ("e_mean", _dbl), ("e_std", _dbl),
         ("fro2", _dbl), ("n_global", _i64), ("scale_table", _vp),
+        ("deferred", _vp), ("fro2_dev", _vp),
     ]
 
 
@@ -85,6 +86,9 @@ SIGNATURES = {
     "wssr_kernel_launches": (_i64, [_vp]),
     "wssr_set_gemm_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_set_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_debug_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp,
+                                             _dbl, _vp]),
     "wssr_phase_stats": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_dbl),
                                         ctypes.POINTER(_i64), ctypes.POINTER(_dbl),
                                         ctypes.POINTER(_dbl)]),

@@ -18,6 +18,7 @@
 #include "ozaki.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "tallskinny.h"
 
 struct wssr_ctx {
   wssr::Context c;
@@ -192,8 +193,53 @@ void gemm_rm_add(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A,
 // Gram G (k x k) = A^T A, A rows x k (lda); allreduced over ranks when rows are sharded.
 void gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* G,
           bool distributed) {
-  gemm_cm(ctx, k, k, rows, A, lda, nullptr, A, lda, G, k, 1.0, false);
+  if (ctx.tallskinny && ts_supported(k)) {
+    WSSR_CUDA(ts_gram(ctx, rows, k, A, lda, G));
+  } else {
+    gemm_cm(ctx, k, k, rows, A, lda, nullptr, A, lda, G, k, 1.0, false);
+  }
   if (distributed) allreduce(ctx, G, (size_t)(k * k));
+}
+
+// C (k x k) = A^T B for rows x k blocks
+void cross(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, const double* B,
+           int64_t ldb, double* C) {
+  if (ctx.tallskinny && ts_supported(k)) {
+    WSSR_CUDA(ts_cross(ctx, rows, k, A, lda, B, ldb, C));
+  } else {
+    gemm_cm(ctx, k, k, rows, A, lda, nullptr, B, ldb, C, k, 1.0, false);
+  }
+}
+
+// out[j] = sum_i A[i][j] x[i] (A rows x n): the k-vectors of the preconditioner / state refresh
+void gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, int64_t lda, const double* x,
+            double* out) {
+  if (ctx.tallskinny) {
+    WSSR_CUDA(ts_gemv_t(ctx, rows, n, A, lda, x, 1.0, out));
+  } else {
+    gemm_cm(ctx, n, 1, rows, A, lda, nullptr, x, 1, out, 1, 1.0, false);
+  }
+}
+
+// Y = A M for a rows x k block A and a k x k M (upper: M upper triangular, e.g. R^-1)
+void mul_small(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+               const double* M, bool upper, double* Y, int64_t ldy) {
+  if (ctx.tallskinny && ts_mul_supported(k, A, lda, Y, ldy)) {
+    WSSR_CUDA(ts_mul(ctx, rows, k, A, lda, M, upper, 1.0, Y, ldy));
+  } else {
+    gemm_rm(ctx, rows, k, k, A, lda, nullptr, M, k, Y, ldy, 1.0, false);
+  }
+}
+
+// Y = Cin - A M
+void sub_mul_small(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                   const double* M, const double* Cin, int64_t ldcin, double* Y, int64_t ldy) {
+  if (ctx.tallskinny && ts_mul_supported(k, A, lda, Y, ldy) &&
+      ts_mul_supported(k, Cin, ldcin, Y, ldy)) {
+    WSSR_CUDA(ts_mul_add(ctx, rows, k, A, lda, M, -1.0, Cin, ldcin, Y, ldy));
+  } else {
+    gemm_rm_add(ctx, rows, k, k, A, lda, M, k, Cin, ldcin, Y, ldy, -1.0);
+  }
 }
 
 // ---- small helpers -------------------------------------------------------------------------
@@ -281,17 +327,20 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
 // and checked by the caller; no host synchronisation.
 void cholqr2(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* Q,
              int64_t ldq, double* R, int* status, bool distributed) {
+  PhaseTimer tm(ctx, rows >= 65536 ? 3 : 7, 8.0 * rows * k * k, 4.0 * 8.0 * rows * k);
   Buf G((size_t)k * k, ctx.stream), R1((size_t)k * k, ctx.stream), R1i((size_t)k * k, ctx.stream),
       R2((size_t)k * k, ctx.stream), R2i((size_t)k * k, ctx.stream),
       T((size_t)rows * k, ctx.stream);
   gram(ctx, rows, k, A, lda, G, distributed);
   chol_inv(ctx, G, (int)k, R1, R1i, status);
-  gemm_rm(ctx, rows, k, k, A, lda, nullptr, R1i, k, T, k, 1.0, false);
+  mul_small(ctx, rows, k, A, lda, R1i, true, T, k);
   gram(ctx, rows, k, T, k, G, distributed);
   chol_inv(ctx, G, (int)k, R2, R2i, status);
-  gemm_rm(ctx, rows, k, k, T, k, nullptr, R2i, k, Q, ldq, 1.0, false);
-  triu_mul_kernel<<<blocks_for(k * k, 256, 1 << 20), 256, 0, ctx.stream>>>(R2, R1, (int)k, R);
-  post_launch(ctx);
+  mul_small(ctx, rows, k, T, k, R2i, true, Q, ldq);
+  if (R) {  // R = R2 R1 (only the callers that read R ask for it)
+    triu_mul_kernel<<<blocks_for(k * k, 256, 1 << 20), 256, 0, ctx.stream>>>(R2, R1, (int)k, R);
+    post_launch(ctx);
+  }
 }
 
 __global__ void set_entry_kernel(double* p, double v) { *p = v; }
@@ -390,7 +439,8 @@ void qr(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, dou
   if (hst[0] == 0) return;
   if (distributed)
     throw Fail{WSSR_ERR_UNSUPPORTED, "rank-deficient block under row sharding"};
-  cgs2_patch(ctx, rows, k, A, lda, Q, ldq, R, fro);
+  Buf Rscratch(R ? 0 : (size_t)k * k, ctx.stream);
+  cgs2_patch(ctx, rows, k, A, lda, Q, ldq, R ? R : (double*)Rscratch, fro);
 }
 
 // ---- the stacked matrix Ohat (optimizers.py:321-324) as a virtual two-block operator ----------
@@ -541,6 +591,24 @@ double ohat_fro2(Context& ctx, const Ohat& o, double samples_fro2, bool hist_own
   return total;
 }
 
+// ||Ohat||_F^2: a host part plus, when assemble deferred its scalars, a device part read back at
+// the first host synchronisation of the SSI (so the step never waits on assemble).
+struct Fro2 {
+  double host = 0.0;
+  const double* dev = nullptr;
+  double dev_scale = 1.0;
+  double dev_val = 0.0;
+  bool enqueued = false;
+  void enqueue(Context& ctx) {
+    if (dev && !enqueued) {
+      d2h(ctx, &dev_val, dev, sizeof(double));
+      enqueued = true;
+    }
+  }
+  // valid after a stream sync that follows enqueue()
+  double value() const { return dev ? host + dev_scale * dev_val : host; }
+};
+
 // ---- ssi_svd (svdengine.py:88-158) ------------------------------------------------------------
 struct SsiResult {
   int64_t k_pos = 0, r_eff = 0, iterations = 0;
@@ -553,7 +621,7 @@ struct SsiResult {
 // U_out (P x k, ldU) gets the re-orthonormalised left vectors (first k_pos columns), sigma_out
 // the sorted values.  fro2 is the global ||Ohat||_F^2.
 SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
-                   const double* u_init, int64_t ld_init, double tol, double fro2, bool final_res,
+                   const double* u_init, int64_t ld_init, double tol, Fro2& fro2_in, bool final_res,
                    bool careful, double* U_out, int64_t ldU, double* sigma_out, double r_reg,
                    int* status) {
   const int64_t P = o.P, cols = o.cols();
@@ -561,20 +629,19 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   cudaStream_t st = ctx.stream;
   Buf q((size_t)P * k, st), ua((size_t)P * k, st), ub((size_t)P * k, st);
   Buf va((size_t)std::max<int64_t>(cols, 1) * k, st), vb((size_t)std::max<int64_t>(cols, 1) * k, st);
-  Buf Rk((size_t)k * k, st), quot((size_t)k * k, st), scal(4, st);
+  Buf quot((size_t)k * k, st), scal(4, st);
   double* u = ua;
   double* w = ub;
   double* v = va;
   double* v2 = vb;
 
-  qr(ctx, P, k, u_init, ld_init, q, k, Rk, status, careful, false);  // svdengine.py:130
+  qr(ctx, P, k, u_init, ld_init, q, k, nullptr, status, careful, false);  // svdengine.py:130
   apply_OT(ctx, o, q, k, k, v, k);
   apply_O(ctx, o, v, k, k, u, k);
   SsiResult res;
   int64_t it = 0;
-  Buf tmp((size_t)P * k, st);
   while (true) {  // svdengine.py:132-142
-    qr(ctx, P, k, u, k, q, k, Rk, status, careful, false);
+    qr(ctx, P, k, u, k, q, k, nullptr, status, careful, false);
     ++it;
     if (it >= max_iters && !final_res) {
       res.residual = std::numeric_limits<double>::quiet_NaN();  // look-ahead skipped
@@ -583,14 +650,26 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
     // look-ahead pass: w = Ohat Ohat^T q is also the next iteration's u (svdengine.py:137)
     apply_OT(ctx, o, q, k, k, v2, k);
     apply_O(ctx, o, v2, k, k, w, k);
-    gemm_cm(ctx, k, k, P, q, k, nullptr, w, k, quot, k, 1.0, false);  // quotient = q^T w
-    gemm_rm_add(ctx, P, k, k, q, k, quot, k, w, k, tmp, k, -1.0);  // w - q quotient
-    sumsq_matrix(ctx, tmp, P, k, k, scal);
-    small_norms_kernel<<<1, 256, 0, st>>>(nullptr, nullptr, 0, quot, (int)k, scal + 1);
-    post_launch(ctx);
+    {
+      PhaseTimer tm(ctx, 4, 0.0, 0.0);
+      cross(ctx, P, k, q, k, w, k, quot);  // quotient = q^T w
+      if (ctx.tallskinny && ts_mul_supported(k, q, k, w, k)) {
+        // ||w - q quotient||_F^2 straight from registers (nothing written)
+        WSSR_CUDA(ts_mul_add_sumsq(ctx, P, k, q, k, quot, -1.0, w, k, scal));
+      } else {
+        Buf tmp((size_t)P * k, st);
+        gemm_rm_add(ctx, P, k, k, q, k, quot, k, w, k, tmp, k, -1.0);  // w - q quotient
+        sumsq_matrix(ctx, tmp, P, k, k, scal);
+      }
+      small_norms_kernel<<<1, 256, 0, st>>>(nullptr, nullptr, 0, quot, (int)k, scal + 1);
+      post_launch(ctx);
+    }
     double h[3];
     d2h(ctx, h, scal, 3 * sizeof(double));
+    fro2_in.enqueue(ctx);
     sync(ctx);
+    const double fro2 = fro2_in.value();
+    if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
     const double residual = std::sqrt(h[0]) / fro2;
     const double mixing = h[2] / fro2;
     res.residual = residual;
@@ -609,8 +688,10 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
                                                        sigma_out, ints.i32());
   post_launch(ctx);
   int hi[2];
+  std::vector<int64_t> hord(k);
   d2h(ctx, hi, ints, sizeof(hi));
   d2h(ctx, &res.sigma0, sigma_out, sizeof(double));
+  d2h(ctx, hord.data(), res.order, sizeof(int64_t) * k);
   sync(ctx);
   res.k_pos = hi[0];
   res.r_eff = hi[1];
@@ -620,9 +701,6 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   // U = QR(u[:, order[:k]]) and V = q_v[:, order] (svdengine.py:151-152).  When the order is
   // the identity the QR is exactly the one already computed at the top of the last iteration
   // (q = QR(u), same inputs, same deterministic kernels), so it is reused.
-  std::vector<int64_t> hord(k);
-  d2h(ctx, hord.data(), res.order, sizeof(int64_t) * k);
-  sync(ctx);
   bool identity = kp == k;
   for (int64_t j = 0; j < kp && identity; ++j) identity = hord[j] == j;
   if (identity) {
@@ -632,8 +710,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
     gather_cols_kernel<<<blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
         u, k, P, res.order.i64(), (int)kp, uperm, kp);
     post_launch(ctx);
-    Buf Rf((size_t)kp * kp, st);
-    qr(ctx, P, kp, uperm, kp, U_out, ldU, Rf, status, careful, false);
+    qr(ctx, P, kp, uperm, kp, U_out, ldU, nullptr, status, careful, false);
   }
   res.qv = Buf((size_t)std::max<int64_t>(cols, 1) * k, st);
   if (cols > 0) {
@@ -664,6 +741,10 @@ auto with_fallback(Context& ctx, int64_t flags, F&& body) -> decltype(body(false
 
 // ---- largest eigenvalue of a small symmetric matrix ---------------------------------------
 void maxeig(Context& ctx, const double* A, int k, double* out_dev) {
+  if (k <= 64) {
+    maxeig64_kernel<<<1, 1024, 0, ctx.stream>>>(A, k, out_dev);
+    return;
+  }
   const size_t smem = sizeof(double) * ((size_t)k * (k + 1) + 4 * (size_t)k);
   if (smem <= 200 * 1024) {
     static bool attr = false;
@@ -687,13 +768,16 @@ std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, in
   if (r == 0) return {0.0, 0.0};
   cudaStream_t st = ctx.stream;
   Buf C((size_t)r * r, st), X((size_t)rows * r, st), GX((size_t)r * r, st), out(3, st);
-  small_norms_kernel<<<1, 256, 0, st>>>(s1, s2, (int)r, nullptr, 0, out);
-  post_launch(ctx);
-  gemm_cm(ctx, r, r, rows, u1, ld1, nullptr, u2, ld2, C, r, 1.0, false);  // u1^T u2
-  gemm_rm_add(ctx, rows, r, r, u1, ld1, C, r, u2, ld2, X, r, -1.0);  // u2 - u1 (u1^T u2)
-  gemm_cm(ctx, r, r, rows, X, r, nullptr, X, r, GX, r, 1.0, false);
-  maxeig(ctx, GX, (int)r, out + 2);
-  post_launch(ctx);
+  {
+    PhaseTimer tm(ctx, 5, 0.0, 0.0);
+    small_norms_kernel<<<1, 256, 0, st>>>(s1, s2, (int)r, nullptr, 0, out);
+    post_launch(ctx);
+    cross(ctx, rows, r, u1, ld1, u2, ld2, C);                  // u1^T u2
+    sub_mul_small(ctx, rows, r, u1, ld1, C, u2, ld2, X, r);    // u2 - u1 (u1^T u2)
+    gram(ctx, rows, r, X, r, GX, false);
+    maxeig(ctx, GX, (int)r, out + 2);
+    post_launch(ctx);
+  }
   double h[3];
   d2h(ctx, h, out, sizeof(h));
   sync(ctx);
@@ -838,6 +922,16 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     reduce_final_kernel<<<1, 256, 0, st>>>(part, nbb, 1.0 / n_global, fro);
     post_launch(ctx);
   }
+  if (out->deferred && !dist) {
+    // stream-ordered host scalars; the caller synchronises before reading them
+    if (out->fro2_dev)
+      WSSR_CUDA(cudaMemcpyAsync(out->fro2_dev, fro, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    d2h(ctx, out->deferred, scal, 4 * sizeof(double));
+    d2h(ctx, out->deferred + 4, fro, sizeof(double));
+    out->loss = out->raw_loss = out->e_mean = out->e_std = out->fro2 =
+        std::numeric_limits<double>::quiet_NaN();
+    return;
+  }
   double hs[4];
   d2h(ctx, hs, scal, sizeof(hs));
   d2h(ctx, &out->fro2, fro, sizeof(double));
@@ -939,8 +1033,16 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   double samples_fro2 = oh.samples_fro2 >= 0.0 ? oh.samples_fro2 * (sq_new * sq_new) : -1.0;
   Ohat ofull = o;  // the history block is replicated: every rank adds its norm
   ofull.r = oh.hist_rank;
-  const double fro2 = ohat_fro2(ctx, ofull, samples_fro2, true);
-  if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+  Fro2 fro2;
+  if (samples_fro2 < 0.0 && oh.samples_fro2_dev && !dist) {
+    fro2.host = ohat_fro2(ctx, ofull, 0.0, true);  // history part; samples part still on device
+    fro2.dev = oh.samples_fro2_dev;
+    fro2.dev_scale = sq_new * sq_new;
+  } else {
+    fro2.host = ohat_fro2(ctx, ofull, samples_fro2, true);
+    if (fro2.host == 0.0)
+      throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+  }
 
   // lhat = [sqrt(delta) lbar, sqrt(1-delta) L]  (optimizers.py:324)
   Buf lhat((size_t)std::max<int64_t>(cols, 1), st);
@@ -1005,7 +1107,9 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
 
   // preconditioned update (optimizers.py:361-364)
   Buf c(r_eff, st);
-  gemm_cm(ctx, r_eff, 1, P, out->u_next, out->ld_u, nullptr, gbar, 1, c, 1, 1.0, false);
+  {
+  PhaseTimer tm(ctx, 6, 0.0, 0.0);
+  gemv_t(ctx, P, r_eff, out->u_next, out->ld_u, gbar, c);
   const double floor = in->sigma_floor * (in->sigma_floor_relative ? top_sq : 1.0);
   {
     const int threads = 256;
@@ -1016,6 +1120,21 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
     post_launch(ctx);
   }
 
+  // state refresh (optimizers.py:376-383): obar = U sigma, lbar = V[:r] lhat
+  {
+    dim3 grid((unsigned)((P + 31) / 32), (unsigned)((r_eff + 31) / 32));
+    transpose_scale_kernel<<<grid, dim3(32, 8), 0, st>>>(out->u_next, out->ld_u, P, (int)r_eff,
+                                                         out->sigma, out->obar_next_t,
+                                                         out->ld_obar);
+    post_launch(ctx);
+  }
+  if (cols > 0) {
+    gemv_t(ctx, cols, r_eff, sr.qv, k, lhat, out->lbar_next);
+  } else {
+    WSSR_CUDA(cudaMemsetAsync(out->lbar_next, 0, sizeof(double) * r_eff, st));
+  }
+  }
+  if (dist) allreduce(ctx, out->lbar_next, r_eff);
   // drift telemetry against the previous factors (optimizers.py:366-374)
   double sd = 0.0, pd = 0.0;
   if (in->r_prev > 0) {
@@ -1029,20 +1148,6 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
     pd = d.second;
   }
 
-  // state refresh (optimizers.py:376-383): obar = U sigma, lbar = V[:r] lhat
-  {
-    dim3 grid((unsigned)((P + 31) / 32), (unsigned)((r_eff + 31) / 32));
-    transpose_scale_kernel<<<grid, dim3(32, 8), 0, st>>>(out->u_next, out->ld_u, P, (int)r_eff,
-                                                         out->sigma, out->obar_next_t,
-                                                         out->ld_obar);
-    post_launch(ctx);
-  }
-  if (cols > 0) {
-    gemm_cm(ctx, r_eff, 1, cols, sr.qv, k, nullptr, lhat, 1, out->lbar_next, 1, 1.0, false);
-  } else {
-    WSSR_CUDA(cudaMemsetAsync(out->lbar_next, 0, sizeof(double) * r_eff, st));
-  }
-  if (dist) allreduce(ctx, out->lbar_next, r_eff);
   sync(ctx);
 
   out->r_eff = r_eff;
@@ -1275,6 +1380,32 @@ int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
   return WSSR_OK;
 }
 
+int wssr_set_tallskinny(wssr_ctx* ctx, int enabled) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  ctx->c.tallskinny = enabled != 0;
+  return WSSR_OK;
+}
+
+int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const double* a,
+                          const double* b, const double* m, const double* cin, double alpha,
+                          double* out) {
+  return guarded(ctx, [&] {
+    Context& c = ctx->c;
+    if (!ts_supported(k) || rows < 0) throw Fail{WSSR_ERR_VALUE, "tall-skinny: k must be 32 or 64"};
+    switch (op) {
+      case 0: WSSR_CUDA(ts_gram(c, rows, k, a, k, out)); break;
+      case 1: WSSR_CUDA(ts_cross(c, rows, k, a, k, b, k, out)); break;
+      case 2:
+      case 3: WSSR_CUDA(ts_mul(c, rows, k, a, k, m, op == 2, alpha, out, k)); break;
+      case 4: WSSR_CUDA(ts_mul_add(c, rows, k, a, k, m, alpha, cin, k, out, k)); break;
+      case 5: WSSR_CUDA(ts_mul_add_sumsq(c, rows, k, a, k, m, alpha, cin, k, out)); break;
+      case 6: WSSR_CUDA(ts_gemv_t(c, rows, k, a, k, cin, alpha, out)); break;
+      default: throw Fail{WSSR_ERR_VALUE, "tall-skinny: unknown op"};
+    }
+    sync(c);
+  });
+}
+
 int wssr_set_timing(wssr_ctx* ctx, int enabled) {
   if (!ctx) return WSSR_ERR_VALUE;
   ctx->c.timing = enabled != 0;
@@ -1435,8 +1566,10 @@ int wssr_ssi_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, int64_t rank, int
     o.f32 = ohat->samples_f32 != 0;
     o.scale_tab = ohat->samples_scale_table;
     if (max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
-    const double fro2 = ohat_fro2(c, o, ohat->samples_fro2, true);
-    if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+    Fro2 fro2;
+    fro2.host = ohat_fro2(c, o, ohat->samples_fro2, true);
+    if (fro2.host == 0.0)
+      throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
     SsiResult sr = with_fallback(c, flags, [&](bool careful, int* status) {
       return ssi_core(c, o, rank, max_iters, u_init, ld_init, residual_tol, fro2,
                       (flags & WSSR_FLAG_FINAL_RESIDUAL) != 0, careful, out->u, out->ld_u,

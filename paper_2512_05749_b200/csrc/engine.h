@@ -38,6 +38,7 @@ struct Context {
   bool ozaki = true;         // O-passes on the int8 tensor cores (exact digit products)
   double oz_min_elems = 4194304.0;  // smallest sample block (elements) sent to that path
   bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
+  bool tallskinny = true;    // k = 32/64 Grams and products of P x k blocks: tallskinny.cu
   int oz_pre = 0;            // digit planes: 0 = pre-digitise when they fit, 1 = on the fly only
   int8_t* oz_planes = nullptr;  // the step's pre-digitised sample block (reused across steps)
   size_t oz_planes_cap = 0;     // bytes
@@ -45,7 +46,9 @@ struct Context {
   size_t oz_ws_cap = 0;      // doubles
 
   // optional per-phase timing of the O-passes (CUDA events on the launching stream)
-  static constexpr int kPhases = 3;  // 0: v = Ohat^T q, 1: u = Ohat v, 2: assemble column pass
+  // 0: v = Ohat^T q, 1: u = Ohat v, 2: assemble column pass, 3: CholeskyQR2 of P x k blocks,
+  // 4: SSI quotient + residual, 5: drift, 6: preconditioner + state refresh, 7: QR(v) + sort
+  static constexpr int kPhases = 8;
   bool timing = false;
   struct PendingEvent {
     int phase;
@@ -54,10 +57,10 @@ struct Context {
   };
   std::vector<PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
-  double phase_ms[kPhases] = {0, 0, 0};
-  double phase_flops[kPhases] = {0, 0, 0};
-  double phase_bytes[kPhases] = {0, 0, 0};
-  int64_t phase_count[kPhases] = {0, 0, 0};
+  double phase_ms[kPhases] = {};
+  double phase_flops[kPhases] = {};
+  double phase_bytes[kPhases] = {};
+  int64_t phase_count[kPhases] = {};
 
   double* splitk_buffer(size_t n);
   int world() const { return comm ? comm->world : 1; }

@@ -415,7 +415,7 @@ constexpr double kCholSeriesMax = 1e-5;  // ||G - I||_max below which the series
 // Series Cholesky + inverse of a near-identity k x k Gram (k <= 64), one CTA of 256 threads.
 // w holds the thread's 4 x 4 slice of G (rows ty + 16 a, columns tx + 16 b, identity-padded).
 // buf: 2 x 64 x 65 doubles of shared memory.
-__device__ __noinline__ void chol_series(const double (&w)[4][4], double em, int k,
+__device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, int k,
                                          double* __restrict__ R, double* __restrict__ Rinv,
                                          double* buf) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -521,7 +521,8 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
                                                              double* __restrict__ R,
                                                              double* __restrict__ Rinv,
                                                              int* __restrict__ status,
-                                                             double pivot_rel, int use_series) {
+                                                             double pivot_rel, int use_series,
+                                                             long long* prof = nullptr) {
   extern __shared__ double series_buf[];  // 2 x 64 x 65 doubles when use_series
   __shared__ double colL[64], rowX[64], dg[64];
   __shared__ double s_sq, s_inv, s_tr, s_gmax;
@@ -600,7 +601,9 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
   // Published vectors carry exact zeros where an update must not land, so the rank-1 updates
   // below are branch-free: colL[i] = L[i][j] for i > j (0 for i <= j, the diagonal stays in its
   // owner's register), rowX[c] = X[j][c] for c <= j (0 above).
+  if (prof && tid == 0) prof[0] = clock64();
   for (int j = 0; j < 64; ++j) {
+    if (prof && tid == 0 && j == 10) prof[10] = clock64();
     if (s_fail) break;
     const double inv = s_inv, sq = s_sq;
     const int jt = j & 15, ja = j >> 4;
@@ -636,7 +639,9 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
         rowX[c] = v;
       }
     }
+    if (prof && tid == 0 && j == 10) prof[11] = clock64();
     __syncthreads();
+    if (prof && tid == 0 && j == 10) prof[12] = clock64();
     double li[4], lc[4], xr[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) li[a] = colL[ty + 16 * a];
@@ -652,6 +657,7 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
         w[a][b] = fma(-li[a], lc[b], w[a][b]);  // only j < c, i touched (else a factor is 0)
         x[a][b] = fma(-li[a], xr[b], x[a][b]);  // only i > j, c <= j touched
       }
+    if (prof && tid == 0 && j == 10) prof[13] = clock64();
     // next pivot W[j+1][j+1] lives with thread (ty, tx) = ((j+1) & 15, (j+1) & 15)
     const int jn = j + 1;
     if (jn < 64 && ty == (jn & 15) && tx == (jn & 15)) {
@@ -669,8 +675,11 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
         s_sq = d * y;
       }
     }
+    if (prof && ty == 11 && tx == 11 && j == 10) prof[14] = clock64();
     __syncthreads();
+    if (prof && tid == 0 && j == 10) prof[15] = clock64();
   }
+  if (prof && tid == 0) prof[1] = clock64();
   if (s_fail) {
     if (tid == 0) atomicCAS(status, 0, s_fail);
     return;
@@ -968,6 +977,165 @@ __device__ void maxeig_body(const double* __restrict__ Ain, int k, double* A, do
     __syncthreads();
   }
   if (tid == 0) *out = 0.5 * (s_lo + s_hi);
+}
+
+// k <= 64: the same Householder tridiagonalisation + Sturm multisection, laid out for latency.
+// Warp 0 forms each reflector (v, beta) from the column in shared memory; the matvec and the
+// rank-2 update give every thread 4 x 16 entries (row t / 4, columns t % 4 + 4 i) so no step needs
+// more than a 2-level shuffle; barriers are cheap (~30 cycles), long shuffle chains are not.
+// The Sturm counts use the three-term recurrence of det(T_i - x I) (one dependent FMA per row,
+// power-of-two rescaling every 8 rows) on T scaled to unit Gershgorin radius, instead of the
+// pivot recurrence with a reciprocal per row.
+__global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict__ Ain, int k,
+                                                        double* __restrict__ out,
+                                                        long long* prof = nullptr) {
+  constexpr int LD = 65;
+  __shared__ double A[64 * LD];
+  __shared__ double v[64], p[64], dg[64], od[64], e2[64];
+  __shared__ double s_beta, s_kc, s_lo, s_hi, s_scale;
+  __shared__ int s_skip, s_best;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row = tid >> 4, qq = tid & 15;  // 64 rows x 16 column lanes
+  if (prof && tid == 0) prof[1] = clock64();
+  for (int e = tid; e < k * k; e += 1024) {
+    const int r = e / k, c = e % k;
+    A[r * LD + c] = 0.5 * (Ain[r * k + c] + Ain[c * k + r]);
+  }
+  __syncthreads();
+  for (int j = 0; j + 2 < k; ++j) {
+    const int n = k - j - 1;
+    if (warp == 0) {
+      const int i0 = lane, i1 = lane + 32;
+      const double x0v = i0 < n ? A[(j + 1 + i0) * LD + j] : 0.0;
+      const double x1v = i1 < n ? A[(j + 1 + i1) * LD + j] : 0.0;
+      const double xnorm2 = warp_sum(fma(x0v, x0v, x1v * x1v));
+      const double x0 = __shfl_sync(0xffffffffu, x0v, 0);
+      const double xn = sqrt(xnorm2);
+      const double alpha = x0 >= 0.0 ? -xn : xn;
+      const double vtv = 2.0 * xn * (xn + fabs(x0));
+      if (i0 < n) v[i0] = x0v - (i0 == 0 ? alpha : 0.0);
+      if (i1 < n) v[i1] = x1v;
+      if (lane == 0) {
+        dg[j] = A[j * LD + j];
+        od[j] = (vtv > 0.0) ? alpha : x0;
+        s_skip = !(vtv > 0.0);
+        s_beta = (vtv > 0.0) ? 2.0 * fast_rcp(vtv) : 0.0;
+      }
+    }
+    __syncthreads();
+    if (s_skip) {  // column already reduced (uniform); barrier before s_skip is rewritten
+      __syncthreads();
+      continue;
+    }
+    const double beta = s_beta;
+    // p = beta A' v: row `row`, columns qq + 4 i
+    double q = 0.0;
+    if (row < n) {
+      const double* ar = A + (j + 1 + row) * LD + (j + 1);
+      double qa = 0.0, qb = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; i += 2) {  // fixed trip count: every load issued up front
+        const int c0 = qq + 16 * i, c1 = c0 + 16;
+        if (c0 < n) qa = fma(ar[c0], v[c0], qa);
+        if (c1 < n) qb = fma(ar[c1], v[c1], qb);
+      }
+      q = qa + qb;
+    }
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (qq == 0 && row < n) p[row] = beta * q;
+    __syncthreads();
+    if (warp == 0) {
+      const int i0 = lane, i1 = lane + 32;
+      const double t = fma(i0 < n ? v[i0] : 0.0, i0 < n ? p[i0] : 0.0,
+                           (i1 < n ? v[i1] : 0.0) * (i1 < n ? p[i1] : 0.0));
+      const double vp = warp_sum(t);
+      if (lane == 0) s_kc = 0.5 * beta * vp;
+    }
+    __syncthreads();
+    // A' -= v w^T + w v^T,  w = p - Kc v
+    if (row < n) {
+      const double kc = s_kc;
+      const double vr = v[row], wr = p[row] - kc * vr;
+      double* ar = A + (j + 1 + row) * LD + (j + 1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = qq + 16 * i;
+        if (c < n) {
+          const double vc = v[c], wc = p[c] - kc * vc;
+          ar[c] -= vr * wc + wr * vc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (prof && tid == 0) prof[0] = clock64();
+  if (tid == 0) {
+    if (k >= 2) {
+      dg[k - 2] = A[(k - 2) * LD + (k - 2)];
+      od[k - 2] = A[(k - 1) * LD + (k - 2)];
+    }
+    dg[k - 1] = A[(k - 1) * LD + (k - 1)];
+    double lo = 1.0 / 0.0, hi = -1.0 / 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double r = (i > 0 ? fabs(od[i - 1]) : 0.0) + (i + 1 < k ? fabs(od[i]) : 0.0);
+      lo = fmin(lo, dg[i] - r);
+      hi = fmax(hi, dg[i] + r);
+    }
+    const double m = fmax(fabs(lo), fabs(hi));
+    // power-of-two scale to unit Gershgorin radius (exact)
+    int ex = 0;
+    frexp(m, &ex);
+    s_scale = (m > 0.0 && isfinite(m)) ? ldexp(1.0, -ex) : 1.0;
+    s_lo = lo * s_scale;
+    s_hi = hi * s_scale;
+  }
+  __syncthreads();
+  const double sc = s_scale;
+  if (tid < k) {
+    dg[tid] *= sc;
+    e2[tid] = tid > 0 ? (od[tid - 1] * sc) * (od[tid - 1] * sc) : 0.0;
+  }
+  __syncthreads();
+  for (int round = 0; round < 12; ++round) {
+    const double lo = s_lo, hi = s_hi;
+    if (!(hi - lo > 2e-16 * fmax(fabs(hi), fabs(lo)))) break;
+    const double x = lo + (hi - lo) * (double)(tid + 1) / 1025.0;
+    // q_i = (a_i - x) q_{i-1} - e_i^2 q_{i-2}; eigenvalues below x = sign changes (a zero takes
+    // the sign opposite to its predecessor, i.e. the pivot q_i / q_{i-1} counts as negative)
+    double q1 = 1.0, q2 = 0.0;
+    int sprev = 1, cnt = 0;
+    for (int i = 0; i < k; ++i) {
+      const double qn = fma(dg[i] - x, q1, -e2[i] * q2);
+      const int sn = qn > 0.0 ? 1 : (qn < 0.0 ? -1 : -sprev);
+      cnt += sn != sprev;
+      sprev = sn;
+      q2 = q1;
+      q1 = qn;
+      if ((i & 7) == 7) {  // rescale by a power of two (exact) to stay in range
+        const int e = (__double2hiint(q1) >> 20) & 0x7ff;
+        if (e > 0 && e < 0x7ff) {
+          const double f = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
+          q1 *= f;
+          q2 *= f;
+        }
+      }
+    }
+    const int above = cnt == k;  // x > lambda_max
+    if (tid == 0) s_best = 1024;
+    __syncthreads();
+    if (above) atomicMin(&s_best, tid);
+    __syncthreads();
+    if (tid == 0) {
+      const int b = s_best;
+      const double step = (hi - lo) / 1025.0;
+      s_lo = lo + step * (double)b;
+      s_hi = (b < 1024) ? lo + step * (double)(b + 1) : hi;
+    }
+    __syncthreads();
+    if (prof && tid == 0) prof[2 + round] = clock64();
+  }
+  if (tid == 0) *out = 0.5 * (s_lo + s_hi) / sc;
 }
 
 __global__ void maxeig_smem_kernel(const double* Ain, int k, double* out) {

@@ -1,0 +1,401 @@
+// Tall-skinny FP64 kernels for the P x k blocks of the SSI loop (k = 32 or 64, rows = P up to
+// 10^6): the Grams and triangular products of CholeskyQR2 (qr_orthonormalize, linalg.py:29-61),
+// the Rayleigh quotient q^T w and the residual ||w - q (q^T w)||_F (svdengine.py:137-139), and the
+// drift block u2 - u1 (u1^T u2) (svdengine.py:217-221).
+//
+// These operands are 67 MB at c1 (10 us of HBM) and the products are 2 P k^2 FLOP (29 us of
+// DMMA at the measured 37 TF/s), so the generic TMA tile GEMM - built for the N x P sample block -
+// wastes most of its time on split-K slabs, a 64 x 64 output tile per CTA and full (not
+// triangular / symmetric) products.  Here every warp streams its own rows straight into DMMA
+// fragments (no shared-memory staging of the tall operand: each fragment load is a full 32-byte
+// sector per row), and:
+//   * Grams compute only the upper 8 x 8 tiles (36 of 64 at k = 64): the A and B fragments of
+//     A^T A are the same register, so one load per column block feeds every tile of a k-step;
+//   * products with the triangular CholeskyQR2 factors R^-1 skip the zero tiles (72 of 128 DMMAs
+//     per 8 rows);
+//   * the residual ||W - A M||_F^2 is reduced in registers and never written;
+//   * per-CTA partials are summed in a fixed order (bitwise repeatable, like every reduction in
+//     this library).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "engine.h"
+#include "tallskinny.h"
+
+namespace wssr {
+namespace ts {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kRowStep = 16;  // rows per warp iteration (4 DMMA k-steps of the Grams)
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+
+// ---- Gram / cross-Gram: slabs[cta] (KC x KC, upper tiles only when SYM) ------------------------
+// SYM: C = A^T A, every warp owns all NB(NB+1)/2 upper tiles and a contiguous row range.
+// !SYM: C = A^T B, warps pair up: warp w owns the column blocks [h NB/2, (h+1) NB/2), h = w & 1,
+// of the row range of pair w >> 1.
+// Fragments (mma.m8n8k4.f64, lane = 4 g + t): a = A^T[8bi + g][r0 + t] = A[r0 + t][8bi + g],
+// b = B[r0 + t][8bj + g]; c[e] = C[8bi + g][8bj + 2t + e].
+template <int KC, bool SYM>
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                int64_t ldb, int64_t rows, int64_t rows_per_cta, double* __restrict__ slabs) {
+  constexpr int NB = KC / 8;
+  constexpr int NJ = SYM ? NB : NB / 2;  // column blocks per warp
+  constexpr int U = kRowStep / 4;
+  constexpr int GROUPS = SYM ? kWarps : kWarps / 2;  // row groups per CTA
+  __shared__ __align__(16) double red[NB * NB * 64];
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  const int grp = SYM ? warp : warp >> 1;
+  const int jb0 = SYM ? 0 : (warp & 1) * NJ;
+
+  const int64_t cta_r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t cta_r1 = min(rows, cta_r0 + rows_per_cta);
+  const int64_t per_grp = (rows_per_cta / GROUPS + kRowStep - 1) / kRowStep * kRowStep;
+  const int64_t r_begin = cta_r0 + grp * per_grp;
+  const int64_t r_end = min(cta_r1, r_begin + per_grp);
+
+  double acc[NB][NJ][2];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kRowStep) {
+    double fa[U][NB], fb[U][NJ];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + 4 * u + t;
+      const bool ok = r < r_end;
+      const double* pa = A + (ok ? r : 0) * lda + g;
+      const double* pb = B + (ok ? r : 0) * ldb + g + 8 * jb0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) fa[u][b] = ok ? pa[8 * b] : 0.0;
+      if (!SYM) {
+#pragma unroll
+        for (int b = 0; b < NJ; ++b) fb[u][b] = ok ? pb[8 * b] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          if (SYM && j < i) continue;
+          dmma884(acc[i][j], fa[u][i], SYM ? fa[u][j] : fb[u][j]);
+        }
+  }
+
+  // CTA reduction over the row groups, in group order (deterministic)
+  for (int gi = 0; gi < GROUPS; ++gi) {
+    if (grp == gi) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          if (SYM && j < i) continue;
+          double2* slot = reinterpret_cast<double2*>(red + ((i * NB + jb0 + j) * 64 + 2 * lane));
+          if (gi == 0) {
+            *slot = make_double2(acc[i][j][0], acc[i][j][1]);
+          } else {
+            double2 v = *slot;
+            v.x += acc[i][j][0];
+            v.y += acc[i][j][1];
+            *slot = v;
+          }
+        }
+    }
+    __syncthreads();
+  }
+  // slab in matrix layout: C[8bi + g][8bj + 2t + e] (lower tiles left unwritten when SYM)
+  double* slab = slabs + (size_t)blockIdx.x * KC * KC;
+  for (int idx = threadIdx.x; idx < NB * NB * 32; idx += kThreads) {
+    const int tile = idx >> 5, l = idx & 31;
+    const int bi = tile / NB, bj = tile % NB;
+    if (SYM && bj < bi) continue;
+    const double2 v = *reinterpret_cast<const double2*>(red + tile * 64 + 2 * l);
+    *reinterpret_cast<double2*>(slab + (8 * bi + (l >> 2)) * KC + 8 * bj + 2 * (l & 3)) = v;
+  }
+}
+
+// C[i][j] = sum over slabs in slab order; SYM mirrors the upper tiles.  Block: 32 consecutive
+// entries x 8 slab groups.
+template <int KC, bool SYM>
+__global__ void __launch_bounds__(256)
+    gram_finish_kernel(const double* __restrict__ slabs, int nslab, double* __restrict__ C,
+                       int64_t ldc) {
+  __shared__ double part[8][33];
+  const int jj = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + jj;  // entry (row-major KC x KC)
+  const int i = e / KC, j = e % KC;
+  const int src = (SYM && (j >> 3) < (i >> 3)) ? j * KC + i : e;
+  double s = 0.0;
+  for (int c = sg; c < nslab; c += 8) s += slabs[(size_t)c * KC * KC + src];
+  part[sg][jj] = s;
+  __syncthreads();
+  if (sg == 0) {
+    double tot = part[0][jj];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) tot += part[q][jj];
+    C[(int64_t)i * ldc + j] = tot;
+  }
+}
+
+// ---- row-block products: Y = A M, Y = Cin + A M, or ||Cin + A M||_F^2 -------------------------
+// M (KC x KC) is staged once per CTA in fragment order: Ms[jp][bn][lane] = {M[8jp + 2t][8bn + g],
+// M[8jp + 2t + 1][8bn + g]}; the k-slots of DMMA step 2jp (2jp + 1) are the columns 8jp + 2t
+// (8jp + 2t + 1), so each lane fetches its A pair with one 16-byte load.  TRI: M upper
+// triangular, the tiles (jp > bn) are skipped.  Every warp takes 16-row blocks.
+enum Mode : int { kStore = 0, kAddStore = 1, kAddSumsq = 2 };
+
+template <int KC, bool TRI, int MODE>
+__global__ void __launch_bounds__(kThreads, KC == 64 ? 1 : 2)
+    mul_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ M,
+               int64_t ldm, double alpha, const double* __restrict__ Cin, int64_t ldcin,
+               double* __restrict__ Y, int64_t ldy, int64_t rows, double* __restrict__ partial) {
+  constexpr int NB = KC / 8;
+  __shared__ __align__(16) double2 Ms[NB * NB * 32];
+  __shared__ double scratch[32];
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  for (int idx = threadIdx.x; idx < NB * NB * 32; idx += kThreads) {
+    const int l = idx & 31, bn = (idx >> 5) % NB, jp = (idx >> 5) / NB;
+    const int gg = l >> 2, tt = l & 3;
+    const int r = 8 * jp + 2 * tt, c = 8 * bn + gg;
+    Ms[idx] = make_double2(alpha * M[r * ldm + c], alpha * M[(r + 1) * ldm + c]);
+  }
+  __syncthreads();
+
+  double ss = 0.0;
+  const int64_t nblk = (rows + 15) / 16;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t blk = gw; blk < nblk; blk += nw) {
+    const int64_t r0 = blk * 16;
+    double2 a[2][NB];
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb) {
+      const int64_t r = r0 + 8 * mb + g;
+      const bool ok = r < rows;
+      const double* pa = A + (ok ? r : 0) * lda + 2 * t;
+#pragma unroll
+      for (int jp = 0; jp < NB; ++jp) a[mb][jp] = ok ? ld2(pa + 8 * jp) : make_double2(0.0, 0.0);
+    }
+    double acc[2][NB][2];
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int bn = 0; bn < NB; ++bn) acc[mb][bn][0] = acc[mb][bn][1] = 0.0;
+#pragma unroll
+    for (int bn = 0; bn < NB; ++bn)
+#pragma unroll
+      for (int jp = 0; jp < NB; ++jp) {
+        if (TRI && jp > bn) continue;
+        const double2 m = Ms[(jp * NB + bn) * 32 + lane];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+          dmma884(acc[mb][bn], a[mb][jp].x, m.x);
+          dmma884(acc[mb][bn], a[mb][jp].y, m.y);
+        }
+      }
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb) {
+      const int64_t r = r0 + 8 * mb + g;
+      if (r >= rows) continue;
+#pragma unroll
+      for (int bn = 0; bn < NB; ++bn) {
+        double2 y = make_double2(acc[mb][bn][0], acc[mb][bn][1]);
+        if (MODE != kStore) {
+          const double2 c = ld2(Cin + r * ldcin + 8 * bn + 2 * t);
+          y.x = c.x + y.x;
+          y.y = c.y + y.y;
+        }
+        if (MODE == kAddSumsq) {
+          ss = fma(y.x, y.x, ss);
+          ss = fma(y.y, y.y, ss);
+        } else {
+          *reinterpret_cast<double2*>(Y + r * ldy + 8 * bn + 2 * t) = y;
+        }
+      }
+    }
+  }
+  if (MODE == kAddSumsq) {
+    ss = block_sum(ss, scratch);
+    if (threadIdx.x == 0) partial[blockIdx.x] = ss;
+  }
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partials, int n,
+                                    double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ---- transposed GEMV: out[j] = alpha sum_i A[i][j] x[i] (the k-vectors U^T gbar and V^T lhat,
+// optimizers.py:361, 380).  Block: columns [blockIdx.y * CW, + CW) x (256 / CW) row lanes over a
+// contiguous row range; partials[blockIdx.x][j] summed in block order by the finish kernel.
+__global__ void __launch_bounds__(256)
+    gemv_t_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ x,
+                  int64_t rows, int n, int cw, int64_t rows_per_block,
+                  double* __restrict__ partial) {
+  __shared__ double red[256];
+  const int c = threadIdx.x % cw, rl = threadIdx.x / cw, lanes = 256 / cw;
+  const int j = blockIdx.y * cw + c;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  double s0 = 0.0, s1 = 0.0;
+  if (j < n) {
+    int64_t r = r0 + rl;
+    for (; r + lanes < r1; r += 2 * lanes) {
+      s0 = fma(A[r * lda + j], x[r], s0);
+      s1 = fma(A[(r + lanes) * lda + j], x[r + lanes], s1);
+    }
+    if (r < r1) s0 = fma(A[r * lda + j], x[r], s0);
+  }
+  red[threadIdx.x] = s0 + s1;
+  __syncthreads();
+  if (rl == 0 && j < n) {
+    double t = red[c];
+    for (int q = 1; q < lanes; ++q) t += red[q * cw + c];
+    partial[(size_t)blockIdx.x * n + j] = t;
+  }
+}
+
+__global__ void gemv_t_finish_kernel(const double* __restrict__ partial, int nblk, int n,
+                                     double alpha, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double t = 0.0;
+  for (int b = 0; b < nblk; ++b) t += partial[(size_t)b * n + j];
+  out[j] = alpha * t;
+}
+
+template <int KC, bool SYM>
+cudaError_t gram_launch(Context& ctx, int64_t rows, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double* C, int64_t ldc) {
+  const int64_t min_rows = 64;  // keep every CTA's share at least a few row steps
+  int grid = (int)std::min<int64_t>(ctx.num_sms, std::max<int64_t>(1, rows / min_rows));
+  int64_t rpc = (rows + grid - 1) / grid;
+  rpc = (rpc + kRowStep - 1) / kRowStep * kRowStep;
+  grid = (int)((rows + rpc - 1) / rpc);
+  if (grid < 1) grid = 1;
+  double* slabs = ctx.splitk_buffer((size_t)grid * KC * KC);
+  if (!slabs) return cudaErrorMemoryAllocation;
+  gram_kernel<KC, SYM><<<grid, kThreads, 0, ctx.stream>>>(A, lda, B, ldb, rows, rpc, slabs);
+  gram_finish_kernel<KC, SYM><<<KC * KC / 32, 256, 0, ctx.stream>>>(slabs, grid, C, ldc);
+  ctx.kernel_launches += 2;
+  return cudaGetLastError();
+}
+
+template <int KC, bool TRI, int MODE>
+cudaError_t mul_launch(Context& ctx, int64_t rows, const double* A, int64_t lda, const double* M,
+                       int64_t ldm, double alpha, const double* Cin, int64_t ldcin, double* Y,
+                       int64_t ldy, double* out) {
+  const int64_t nblk = (rows + 15) / 16;
+  int grid = (int)std::min<int64_t>(2 * ctx.num_sms, std::max<int64_t>(1, (nblk + 3) / 4));
+  double* partial = nullptr;
+  if (MODE == kAddSumsq) {
+    partial = ctx.splitk_buffer((size_t)grid);
+    if (!partial) return cudaErrorMemoryAllocation;
+  }
+  mul_kernel<KC, TRI, MODE><<<grid, kThreads, 0, ctx.stream>>>(A, lda, M, ldm, alpha, Cin, ldcin,
+                                                                Y, ldy, rows, partial);
+  ctx.kernel_launches += 1;
+  if (MODE == kAddSumsq) {
+    sum_partials_kernel<<<1, 256, 0, ctx.stream>>>(partial, grid, out);
+    ctx.kernel_launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+bool aligned16(const void* p, int64_t ld) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld & 1) == 0;
+}
+
+}  // namespace ts
+
+bool ts_supported(int64_t k) { return k == 32 || k == 64; }
+
+cudaError_t ts_gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, int64_t lda,
+                      const double* x, double alpha, double* out) {
+  if (n <= 0) return cudaSuccess;
+  if (rows <= 0) return cudaMemsetAsync(out, 0, sizeof(double) * n, ctx.stream);
+  const int cw = n >= 256 ? 256 : (n > 128 ? 256 : (n > 64 ? 128 : (n > 32 ? 64 : 32)));
+  const int ycols = (int)((n + cw - 1) / cw);
+  const int64_t lanes = 256 / cw;
+  int nblk = (int)std::min<int64_t>(2 * ctx.num_sms, std::max<int64_t>(1, rows / (8 * lanes)));
+  const int64_t rpb = (rows + nblk - 1) / nblk;
+  nblk = (int)((rows + rpb - 1) / rpb);
+  double* partial = ctx.splitk_buffer((size_t)nblk * n);
+  if (!partial) return cudaErrorMemoryAllocation;
+  ts::gemv_t_kernel<<<dim3(nblk, ycols), 256, 0, ctx.stream>>>(A, lda, x, rows, (int)n, cw, rpb,
+                                                              partial);
+  ts::gemv_t_finish_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx.stream>>>(
+      partial, nblk, (int)n, alpha, out);
+  ctx.kernel_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t ts_gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                    double* G) {
+  if (rows <= 0) return cudaMemsetAsync(G, 0, sizeof(double) * k * k, ctx.stream);
+  if (k == 64) return ts::gram_launch<64, true>(ctx, rows, A, lda, A, lda, G, k);
+  return ts::gram_launch<32, true>(ctx, rows, A, lda, A, lda, G, k);
+}
+
+cudaError_t ts_cross(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* C) {
+  if (rows <= 0) return cudaMemsetAsync(C, 0, sizeof(double) * k * k, ctx.stream);
+  if (k == 64) return ts::gram_launch<64, false>(ctx, rows, A, lda, B, ldb, C, k);
+  return ts::gram_launch<32, false>(ctx, rows, A, lda, B, ldb, C, k);
+}
+
+bool ts_mul_supported(int64_t k, const double* A, int64_t lda, const double* Y, int64_t ldy) {
+  return ts_supported(k) && ts::aligned16(A, lda) && ts::aligned16(Y, ldy);
+}
+
+cudaError_t ts_mul(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                   const double* M, bool upper, double alpha, double* Y, int64_t ldy) {
+  if (rows <= 0) return cudaSuccess;
+  if (k == 64)
+    return upper ? ts::mul_launch<64, true, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr, 0,
+                                                        Y, ldy, nullptr)
+                 : ts::mul_launch<64, false, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr,
+                                                         0, Y, ldy, nullptr);
+  return upper ? ts::mul_launch<32, true, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr, 0, Y,
+                                                      ldy, nullptr)
+               : ts::mul_launch<32, false, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr, 0,
+                                                       Y, ldy, nullptr);
+}
+
+cudaError_t ts_mul_add(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                       const double* M, double alpha, const double* Cin, int64_t ldcin, double* Y,
+                       int64_t ldy) {
+  if (rows <= 0) return cudaSuccess;
+  if (k == 64)
+    return ts::mul_launch<64, false, ts::kAddStore>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin, Y,
+                                                    ldy, nullptr);
+  return ts::mul_launch<32, false, ts::kAddStore>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin, Y,
+                                                  ldy, nullptr);
+}
+
+cudaError_t ts_mul_add_sumsq(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                             const double* M, double alpha, const double* Cin, int64_t ldcin,
+                             double* out) {
+  if (rows <= 0) return cudaMemsetAsync(out, 0, sizeof(double), ctx.stream);
+  if (k == 64)
+    return ts::mul_launch<64, false, ts::kAddSumsq>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin,
+                                                    nullptr, 0, out);
+  return ts::mul_launch<32, false, ts::kAddSumsq>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin,
+                                                  nullptr, 0, out);
+}
+
+}  // namespace wssr

@@ -49,8 +49,9 @@ class EstimatorBundle:
     the reference's test helpers (test_optimizers.py:27-34).
     """
 
-    __slots__ = ("loss", "raw_loss", "l_vector", "gradient", "_samples", "_mu", "_scale",
-                 "_fro2", "_gradient_exact", "_o_cache", "_n_global", "_scale_table")
+    __slots__ = ("_loss", "_raw_loss", "l_vector", "gradient", "_samples", "_mu", "_scale",
+                 "_fro2_val", "_gradient_exact", "_o_cache", "_n_global", "_scale_table",
+                 "_deferred")
 
     def __init__(self, loss, raw_loss, o_matrix, l_vector, gradient):
         o = _arrays.to_tensor(o_matrix)
@@ -65,23 +66,28 @@ class EstimatorBundle:
 
     @classmethod
     def _assembled(cls, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, n_global,
-                   scale_table=None):
+                   scale_table=None, deferred=None):
+        """deferred: (event, pinned host [loss, raw_loss, e_mean, e_std, fro2], device fro2) -
+        the scalars of an assemble that returned without waiting for the device; they resolve on
+        first access (the optimizer step takes fro2 from the device copy and never waits)."""
         self = cls.__new__(cls)
         self._init(loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, True, n_global)
         object.__setattr__(self, "_scale_table", scale_table)
+        object.__setattr__(self, "_deferred", deferred)
         return self
 
     def _init(self, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, exact,
               n_global):
         set_ = object.__setattr__
-        set_(self, "loss", loss)
-        set_(self, "raw_loss", raw_loss)
+        set_(self, "_loss", loss)
+        set_(self, "_raw_loss", raw_loss)
         set_(self, "l_vector", l_vector)
         set_(self, "gradient", gradient)
         set_(self, "_samples", samples)
         set_(self, "_mu", mu)
         set_(self, "_scale", scale)
-        set_(self, "_fro2", fro2)
+        set_(self, "_fro2_val", fro2)
+        set_(self, "_deferred", None)
         set_(self, "_gradient_exact", exact)
         set_(self, "_o_cache", None)
         set_(self, "_n_global", n_global)
@@ -89,6 +95,46 @@ class EstimatorBundle:
 
     def __setattr__(self, name, value):
         raise AttributeError("EstimatorBundle is immutable")
+
+    def _resolve(self):
+        d = self._deferred
+        if d is not None:
+            event, host, _ = d
+            event.synchronize()
+            vals = host.tolist()
+            set_ = object.__setattr__
+            set_(self, "_loss", float(vals[0]))
+            set_(self, "_raw_loss", float(vals[1]))
+            set_(self, "_fro2_val", float(vals[4]))
+            set_(self, "_deferred", None)
+
+    @property
+    def loss(self) -> float:
+        """mean of the clipped local energies (estimators.py:92)"""
+        self._resolve()
+        return self._loss
+
+    @property
+    def raw_loss(self) -> float:
+        """mean of the raw local energies (estimators.py:89)"""
+        self._resolve()
+        return self._raw_loss
+
+    @property
+    def _fro2(self) -> float:
+        """||o_matrix||_F^2 (host value; waits for a deferred assemble)"""
+        self._resolve()
+        return self._fro2_val
+
+    def _fro2_args(self):
+        """(host fro2 or -1, device fro2 or None) for the engine, without waiting"""
+        d = self._deferred
+        if d is not None:
+            if d[0].query():
+                self._resolve()
+            else:
+                return -1.0, d[2]
+        return self._fro2_val, None
 
     @property
     def o_matrix(self) -> torch.Tensor:
@@ -157,16 +203,28 @@ def assemble(batch, clip_n_std=5.0):
     grad = torch.empty(p, dtype=torch.float64, device=dev)
     # per-parameter scales of the int8 tensor-core O-passes, from the same column pass
     table = torch.empty(_lib.scale_table_len(p), dtype=torch.float64, device=dev)
+    # single rank: the host scalars arrive asynchronously (no wait on the column pass, so the
+    # optimizer step that follows is enqueued while the device is still busy)
+    defer = int(getattr(ctx, "world", 1)) == 1
+    host = torch.empty(5, dtype=torch.float64, pin_memory=True) if defer else None
+    fro2_dev = torch.empty(1, dtype=torch.float64, device=dev) if defer else None
     out = _lib.AssembleOut(mu=mu.data_ptr(), l_vector=lvec.data_ptr(), gradient=grad.data_ptr(),
-                           scale_table=table.data_ptr())
+                           scale_table=table.data_ptr(),
+                           deferred=host.data_ptr() if defer else None,
+                           fro2_dev=fro2_dev.data_ptr() if defer else None)
     entry = "wssr_assemble_f32" if derivs.dtype == torch.float32 else "wssr_assemble_f64"
     if derivs.dtype == torch.float32 and (derivs.stride(0) % 4 or derivs.data_ptr() % 16):
         derivs = _pad_rows_f32(derivs)
     ctx.call(entry, _lib.ptr(derivs), n, p, _arrays.ld(derivs),
              _lib.ptr(energies), float(clip_n_std), ctypes.byref(out))
     scale = 1.0 / np.sqrt(out.n_global)
+    deferred = None
+    if defer:
+        event = torch.cuda.Event()
+        event.record(torch.cuda.current_stream(dev))
+        deferred = (event, host, fro2_dev)
     return EstimatorBundle._assembled(out.loss, out.raw_loss, derivs, mu, scale, out.fro2, lvec,
-                                      grad, int(out.n_global), table)
+                                      grad, int(out.n_global), table, deferred)
 
 
 def _pad_rows_f32(x):

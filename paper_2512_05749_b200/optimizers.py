@@ -162,8 +162,9 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     sigma = torch.empty(k, dtype=torch.float64, device=dev)
 
     from .svdengine import _ohat_struct
-    o = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2, hist, 1.0,
-                     bundle._scale_table)
+    fro2_host, fro2_dev = bundle._fro2_args()
+    o = _ohat_struct(samples, bundle._mu, bundle._scale, fro2_host, hist, 1.0,
+                     bundle._scale_table, fro2_dev)
     lvec = bundle.l_vector.contiguous()
     grad = bundle.gradient if bundle._gradient_exact else None
     ext = None

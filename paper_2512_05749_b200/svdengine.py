@@ -61,7 +61,7 @@ class SsiReport:
 
 
 def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0.0,
-                 scale_table=None):
+                 scale_table=None, fro2_dev=None):
     """wssr_ohat_f64 for Ohat^T = [hist_scale*hist ; scale*(samples - mu)] (sample-major).
 
     scale_table: the bundle's per-parameter table from assemble (same mu), or None.
@@ -84,6 +84,9 @@ def _ohat_struct(samples, mu=None, scale=1.0, fro2=-1.0, hist=None, hist_scale=0
     o.samples_fro2 = float(fro2)
     o.samples_f32 = int(samples.dtype == torch.float32)
     o.samples_scale_table = scale_table.data_ptr() if scale_table is not None else None
+    # fro2 < 0 with fro2_dev: the value is still on its way from assemble (read by the engine at
+    # its first host synchronisation)
+    o.samples_fro2_dev = fro2_dev.data_ptr() if (fro2 < 0 and fro2_dev is not None) else None
     return o
 
 
