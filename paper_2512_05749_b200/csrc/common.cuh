@@ -13,9 +13,46 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace wssr {
 
 constexpr int kWarp = 32;
+
+// Programmatic dependent launch.  Every kernel of this library is launched with
+// programmaticStreamSerialization, so its CTAs may be scheduled while the previous kernel in the
+// stream drains; each kernel therefore starts with pdl_wait() (griddepcontrol.wait), which
+// returns once the previous grid has completed and its memory is visible.  What overlaps is the
+// launch latency and CTA rasterisation of kernel i+1 with the tail of kernel i (~2-3 us per
+// boundary, over ~120 launches per WSSR step).  WSSR_NO_PDL=1 launches plainly.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("WSSR_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 

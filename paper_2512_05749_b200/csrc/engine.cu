@@ -246,7 +246,7 @@ void sub_mul_small(Context& ctx, int64_t rows, int64_t k, const double* A, int64
 void copy2d(Context& ctx, const double* in, int64_t ldi, int64_t rows, int64_t cols, double scale,
             double* out, int64_t ldo) {
   if (rows <= 0 || cols <= 0) return;
-  copy2d_kernel<<<blocks_for(rows * cols, 256, 8 * ctx.num_sms), 256, 0, ctx.stream>>>(
+  launch_pdl(copy2d_kernel, blocks_for(rows * cols, 256, 8 * ctx.num_sms), 256, 0, ctx.stream, 
       in, ldi, rows, cols, scale, out, ldo);
   post_launch(ctx);
 }
@@ -262,9 +262,9 @@ void sumsq_matrix(Context& ctx, const double* x, int64_t rows, int64_t cols, int
   const int64_t rpb = (rows + nblk - 1) / nblk;
   const int nb = (int)((rows + rpb - 1) / rpb);
   Buf part(nb, ctx.stream);
-  matrix_sumsq_partials_kernel<<<nb, 256, 0, ctx.stream>>>(x, rows, cols, ld, rpb, part);
+  launch_pdl(matrix_sumsq_partials_kernel, nb, 256, 0, ctx.stream, x, rows, cols, ld, rpb, part);
   post_launch(ctx);
-  reduce_final_kernel<<<1, 256, 0, ctx.stream>>>(part, nb, scale, out_dev);
+  launch_pdl(reduce_final_kernel, 1, 256, 0, ctx.stream, part, nb, scale, out_dev);
   post_launch(ctx);
 }
 
@@ -274,10 +274,10 @@ void row_norms(Context& ctx, const double* x, int64_t rows, int64_t cols, int64_
   const int64_t chunk = 8192;
   const int nb = (int)std::max<int64_t>(1, (cols + chunk - 1) / chunk);
   Buf part((size_t)rows * nb, ctx.stream);
-  row_sumsq_partials_kernel<<<dim3(nb, (unsigned)rows), 256, 0, ctx.stream>>>(x, cols, ld, chunk,
+  launch_pdl(row_sumsq_partials_kernel, dim3(nb, (unsigned)rows), 256, 0, ctx.stream, x, cols, ld, chunk,
                                                                                part);
   post_launch(ctx);
-  row_norms_final_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, ctx.stream>>>(part, nb,
+  launch_pdl(row_norms_final_kernel, (unsigned)((rows + 127) / 128), 128, 0, ctx.stream, part, nb,
                                                                                 (int)rows, out, 1);
   post_launch(ctx);
 }
@@ -302,9 +302,9 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
                                      (int)(2 * 64 * 65 * sizeof(double))));
       attr = true;
     }
-    chol_inv_reg64_kernel<<<1, 256, series_smem, ctx.stream>>>(G, k, R, Rinv, status,
+    launch_pdl(chol_inv_reg64_kernel, 1, 256, series_smem, ctx.stream, G, k, R, Rinv, status,
                                                                  kCholPivotRel,
-                                                                 ctx.chol_series ? 1 : 0);
+                                                                 ctx.chol_series ? 1 : 0, nullptr);
   } else if (smem <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {
@@ -312,10 +312,10 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    chol_inv_smem_kernel<<<1, 256, smem, ctx.stream>>>(G, k, R, Rinv, status, kCholPivotRel);
+    launch_pdl(chol_inv_smem_kernel, 1, 256, smem, ctx.stream, G, k, R, Rinv, status, kCholPivotRel);
   } else {
     Buf W(chol_scratch_doubles(k), ctx.stream);
-    chol_inv_gmem_kernel<<<1, 256, 0, ctx.stream>>>(G, k, W, R, Rinv, status, kCholPivotRel);
+    launch_pdl(chol_inv_gmem_kernel, 1, 256, 0, ctx.stream, G, k, W, R, Rinv, status, kCholPivotRel);
   }
   post_launch(ctx);
 }
@@ -338,13 +338,15 @@ void cholqr2(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda
   chol_inv(ctx, G, (int)k, R2, R2i, status);
   mul_small(ctx, rows, k, T, k, R2i, true, Q, ldq);
   if (R) {  // R = R2 R1 (only the callers that read R ask for it)
-    triu_mul_kernel<<<blocks_for(k * k, 256, 1 << 20), 256, 0, ctx.stream>>>(R2, R1, (int)k, R);
+    launch_pdl(triu_mul_kernel, blocks_for(k * k, 256, 1 << 20), 256, 0, ctx.stream, R2, R1, (int)k, R);
     post_launch(ctx);
   }
 }
 
-__global__ void set_entry_kernel(double* p, double v) { *p = v; }
+__global__ void set_entry_kernel(double* p, double v) {
+  pdl_wait(); *p = v; }
 __global__ void add_col_kernel(double* R, int64_t ldr, int64_t col, const double* c, int64_t n) {
+  pdl_wait();
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) R[i * ldr + col] += c[i];
 }
 
@@ -361,7 +363,7 @@ void cgs2_patch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t 
       if (j == 0) break;
       gemm_cm(ctx, j, 1, rows, Q, ldq, nullptr, v, ldv, coeff, 1, 1.0, false);
       if (into_r) {
-        add_col_kernel<<<1, 256, 0, ctx.stream>>>(R, k, j, coeff, j);
+        launch_pdl(add_col_kernel, 1, 256, 0, ctx.stream, R, k, j, coeff, j);
         post_launch(ctx);
       }
       gemm_rm(ctx, rows, 1, j, Q, ldq, nullptr, coeff, 1, v, ldv, -1.0, true);
@@ -375,7 +377,7 @@ void cgs2_patch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t 
     const double norm = std::sqrt(read_scalar(ctx, scal));
     if (norm > tol) {
       copy2d(ctx, qj, ldq, rows, 1, 1.0 / norm, qj, ldq);
-      set_entry_kernel<<<1, 1, 0, ctx.stream>>>(R + j * k + j, norm);
+      launch_pdl(set_entry_kernel, 1, 1, 0, ctx.stream, R + j * k + j, norm);
       post_launch(ctx);
       continue;
     }
@@ -385,7 +387,7 @@ void cgs2_patch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t 
     bool done = false;
     for (int64_t i = 0; i < rows && !done; ++i) {
       WSSR_CUDA(cudaMemset2DAsync(qj, sizeof(double) * ldq, 0, sizeof(double), rows, ctx.stream));
-      set_entry_kernel<<<1, 1, 0, ctx.stream>>>(qj + i * ldq, 1.0);
+      launch_pdl(set_entry_kernel, 1, 1, 0, ctx.stream, qj + i * ldq, 1.0);
       post_launch(ctx);
       project_out(j, qj, ldq, false);
       sumsq_matrix(ctx, qj, rows, 1, ldq, scal);
@@ -402,7 +404,7 @@ void cgs2_patch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t 
       if (best < 0 || best_norm <= 0.0)
         throw Fail{WSSR_ERR_ZERO_MATRIX, "no canonical direction available for deficiency patch"};
       WSSR_CUDA(cudaMemset2DAsync(qj, sizeof(double) * ldq, 0, sizeof(double), rows, ctx.stream));
-      set_entry_kernel<<<1, 1, 0, ctx.stream>>>(qj + best * ldq, 1.0);
+      launch_pdl(set_entry_kernel, 1, 1, 0, ctx.stream, qj + best * ldq, 1.0);
       post_launch(ctx);
       project_out(j, qj, ldq, false);
       copy2d(ctx, qj, ldq, rows, 1, 1.0 / best_norm, qj, ldq);
@@ -661,7 +663,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
         gemm_rm_add(ctx, P, k, k, q, k, quot, k, w, k, tmp, k, -1.0);  // w - q quotient
         sumsq_matrix(ctx, tmp, P, k, k, scal);
       }
-      small_norms_kernel<<<1, 256, 0, st>>>(nullptr, nullptr, 0, quot, (int)k, scal + 1);
+      launch_pdl(small_norms_kernel, 1, 256, 0, st, nullptr, nullptr, 0, quot, (int)k, scal + 1);
       post_launch(ctx);
     }
     double h[3];
@@ -684,7 +686,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   qr(ctx, cols, k, v, k, qv_raw, k, Rv, status, careful, dist);
   res.order = Buf(k, st);
   Buf ints(1, st);
-  sort_sigma_kernel<<<1, 256, sizeof(double) * k, st>>>(Rv, (int)k, r_reg, res.order.i64(),
+  launch_pdl(sort_sigma_kernel, 1, 256, sizeof(double) * k, st, Rv, (int)k, r_reg, res.order.i64(),
                                                        sigma_out, ints.i32());
   post_launch(ctx);
   int hi[2];
@@ -707,14 +709,14 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
     copy2d(ctx, q, k, P, k, 1.0, U_out, ldU);
   } else {
     Buf uperm((size_t)P * kp, st);
-    gather_cols_kernel<<<blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
+    launch_pdl(gather_cols_kernel, blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st, 
         u, k, P, res.order.i64(), (int)kp, uperm, kp);
     post_launch(ctx);
     qr(ctx, P, kp, uperm, kp, U_out, ldU, nullptr, status, careful, false);
   }
   res.qv = Buf((size_t)std::max<int64_t>(cols, 1) * k, st);
   if (cols > 0) {
-    gather_cols_kernel<<<blocks_for(cols * kp, 256, 16 * ctx.num_sms), 256, 0, st>>>(
+    launch_pdl(gather_cols_kernel, blocks_for(cols * kp, 256, 16 * ctx.num_sms), 256, 0, st, 
         qv_raw, k, cols, res.order.i64(), (int)kp, res.qv, k);
     post_launch(ctx);
   }
@@ -742,7 +744,7 @@ auto with_fallback(Context& ctx, int64_t flags, F&& body) -> decltype(body(false
 // ---- largest eigenvalue of a small symmetric matrix ---------------------------------------
 void maxeig(Context& ctx, const double* A, int k, double* out_dev) {
   if (k <= 64) {
-    maxeig64_kernel<<<1, 1024, 0, ctx.stream>>>(A, k, out_dev);
+    launch_pdl(maxeig64_kernel, 1, 1024, 0, ctx.stream, A, k, out_dev, nullptr);
     return;
   }
   const size_t smem = sizeof(double) * ((size_t)k * (k + 1) + 4 * (size_t)k);
@@ -753,10 +755,10 @@ void maxeig(Context& ctx, const double* A, int k, double* out_dev) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    maxeig_smem_kernel<<<1, 256, smem, ctx.stream>>>(A, k, out_dev);
+    launch_pdl(maxeig_smem_kernel, 1, 256, smem, ctx.stream, A, k, out_dev);
   } else {
     Buf W((size_t)k * (k + 1) + 4 * (size_t)k, ctx.stream);
-    maxeig_gmem_kernel<<<1, 256, 0, ctx.stream>>>(A, k, W, out_dev);
+    launch_pdl(maxeig_gmem_kernel, 1, 256, 0, ctx.stream, A, k, W, out_dev);
   }
 }
 
@@ -770,7 +772,7 @@ std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, in
   Buf C((size_t)r * r, st), X((size_t)rows * r, st), GX((size_t)r * r, st), out(3, st);
   {
     PhaseTimer tm(ctx, 5, 0.0, 0.0);
-    small_norms_kernel<<<1, 256, 0, st>>>(s1, s2, (int)r, nullptr, 0, out);
+    launch_pdl(small_norms_kernel, 1, 256, 0, st, s1, s2, (int)r, nullptr, 0, out);
     post_launch(ctx);
     cross(ctx, rows, r, u1, ld1, u2, ld2, C);                  // u1^T u2
     sub_mul_small(ctx, rows, r, u1, ld1, C, u2, ld2, X, r);    // u2 - u1 (u1^T u2)
@@ -793,6 +795,7 @@ __global__ void merge_rank_stats_kernel(int64_t p, double n_local, double n_glob
                                         const double* mu_loc, const double* m2_loc,
                                         const double* g_loc, double lsum_loc, const double* mu,
                                         double* m2_out, double* g_out) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double d = mu_loc[i] - mu[i];
@@ -801,6 +804,7 @@ __global__ void merge_rank_stats_kernel(int64_t p, double n_local, double n_glob
   }
 }
 __global__ void scale_kernel(int64_t n, double a, const double* x, double* y) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = a * x[i];
@@ -846,7 +850,7 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     allreduce(ctx, e_all, (size_t)n_global);
     E = e_all;
   }
-  energy_stats_kernel<<<1, 1024, 0, st>>>(E, n_global, n_std, clip, scale, l_all, lraw_all, scal);
+  launch_pdl(energy_stats_kernel, 1, 1024, 0, st, E, n_global, n_std, clip, scale, l_all, lraw_all, scal);
   post_launch(ctx);
   WSSR_CUDA(cudaMemcpyAsync(out->l_vector, l_all + offset, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, st));
@@ -865,13 +869,13 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     PhaseTimer tm(ctx, 2, 4.0 * n * p, (double)sizeof(T) * n * p);
     const bool al16 = (reinterpret_cast<uintptr_t>(derivs) & 15) == 0;
     if (sizeof(T) == 8 && ld % 2 == 0 && al16) {
-      colstats_kernel<T, 2, 8><<<(unsigned)((p + 63) / 64), 32 * kColStatsWarps, 0, st>>>(
+      launch_pdl(colstats_kernel<T, 2, 8>, (unsigned)((p + 63) / 64), 32 * kColStatsWarps, 0, st, 
           derivs, n, p, ld, lraw, out->mu, m2, gsum, cmin, cmax);
     } else if (sizeof(T) == 4 && ld % 4 == 0 && al16) {
-      colstats_kernel<T, 4, 8><<<(unsigned)((p + 127) / 128), 32 * kColStatsWarps, 0, st>>>(
+      launch_pdl(colstats_kernel<T, 4, 8>, (unsigned)((p + 127) / 128), 32 * kColStatsWarps, 0, st, 
           derivs, n, p, ld, lraw, out->mu, m2, gsum, cmin, cmax);
     } else {
-      colstats_kernel<T, 1, 8><<<(unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st>>>(
+      launch_pdl(colstats_kernel<T, 1, 8>, (unsigned)((p + 31) / 32), 32 * kColStatsWarps, 0, st, 
           derivs, n, p, ld, lraw, out->mu, m2, gsum, cmin, cmax);
     }
     post_launch(ctx);
@@ -884,16 +888,16 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     // mu = sum_r n_r mu_r / N ; M2 = sum_r [M2_r + n_r (mu_r - mu)^2] ; G likewise
     Buf mu_loc(p, st), mu(p, st), lsum(1, st);
     WSSR_CUDA(cudaMemcpyAsync(mu_loc, out->mu, sizeof(double) * p, cudaMemcpyDeviceToDevice, st));
-    scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, (double)n, mu_loc, mu);
+    launch_pdl(scale_kernel, blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st, p, (double)n, mu_loc, mu);
     post_launch(ctx);
     allreduce(ctx, mu, p);
-    scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, 1.0 / n_global, mu, mu);
+    launch_pdl(scale_kernel, blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st, p, 1.0 / n_global, mu, mu);
     post_launch(ctx);
     Buf parts(1, st);
-    reduce_final_kernel<<<1, 256, 0, st>>>(lraw, (int)n, 1.0, lsum);
+    launch_pdl(reduce_final_kernel, 1, 256, 0, st, lraw, (int)n, 1.0, lsum);
     post_launch(ctx);
     const double lsum_h = read_scalar(ctx, lsum);
-    merge_rank_stats_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(
+    launch_pdl(merge_rank_stats_kernel, blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st, 
         p, (double)n, (double)n_global, mu_loc, m2, gsum, lsum_h, mu, m2, gsum);
     post_launch(ctx);
     allreduce(ctx, m2, p);
@@ -908,7 +912,7 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     }
   }
   // gradient = 2 * o_matrix @ l_vector = 2 * gsum / N   (estimators.py:93)
-  scale_kernel<<<blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st>>>(p, 2.0 / n_global, gsum,
+  launch_pdl(scale_kernel, blocks_for(p, 256, 8 * ctx.num_sms), 256, 0, st, p, 2.0 / n_global, gsum,
                                                                      out->gradient);
   post_launch(ctx);
   Buf fro(1, st);
@@ -917,9 +921,9 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     const int64_t chunk = (p + nb - 1) / nb;
     const int nbb = (int)((p + chunk - 1) / chunk);
     Buf part(nbb, st);
-    reduce_partials_kernel<<<nbb, 256, 0, st>>>(m2, p, chunk, 0, part);
+    launch_pdl(reduce_partials_kernel, nbb, 256, 0, st, m2, p, chunk, 0, part);
     post_launch(ctx);
-    reduce_final_kernel<<<1, 256, 0, st>>>(part, nbb, 1.0 / n_global, fro);
+    launch_pdl(reduce_final_kernel, 1, 256, 0, st, part, nbb, 1.0 / n_global, fro);
     post_launch(ctx);
   }
   if (out->deferred && !dist) {
@@ -952,7 +956,7 @@ constexpr int64_t kDenseSvdMax = 512;
 void transpose(Context& ctx, const double* in, int64_t ldi, int64_t rows, int64_t cols,
                const double* shift, double scale, double* out, int64_t ldo) {
   dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
-  transpose_shift_kernel<<<grid, dim3(32, 8), 0, ctx.stream>>>(in, ldi, rows, cols, shift, scale,
+  launch_pdl(transpose_shift_kernel, grid, dim3(32, 8), 0, ctx.stream, in, ldi, rows, cols, shift, scale,
                                                                out, ldo);
   post_launch(ctx);
 }
@@ -977,9 +981,9 @@ void dense_svd(Context& ctx, int64_t m, int64_t n, const double* A, int64_t lda,
   Buf W((size_t)q * q, st), V((size_t)q * q, st), Us((size_t)q * q, st), Vs((size_t)q * q, st),
       sw(1, st);
   copy2d(ctx, R, q, q, q, 1.0, W, q);
-  jacobi_svd_kernel<<<1, 1024, 0, st>>>(W, V, (int)q, (int)q, 60, sw.i32());
+  launch_pdl(jacobi_svd_kernel, 1, 1024, 0, st, W, V, (int)q, (int)q, 60, sw.i32());
   post_launch(ctx);
-  svd_finalize_kernel<<<1, 1024, 2 * sizeof(double) * q, st>>>(W, V, (int)q, (int)q, S, Us, Vs,
+  launch_pdl(svd_finalize_kernel, 1, 1024, 2 * sizeof(double) * q, st, W, V, (int)q, (int)q, S, Us, Vs,
                                                               (int)q);
   post_launch(ctx);
   if (m >= n) {
@@ -1089,7 +1093,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   Buf gbar(P, st);
   if (in->gradient) {
     // bundle.gradient = 2 o_matrix l_vector, exact for bundles assembled by this library
-    scale_kernel<<<blocks_for(P, 256, 8 * ctx.num_sms), 256, 0, st>>>(
+    launch_pdl(scale_kernel, blocks_for(P, 256, 8 * ctx.num_sms), 256, 0, st, 
         P, 0.5 * sq_new * sq_new, in->gradient, gbar);
     post_launch(ctx);
   } else {
@@ -1114,7 +1118,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   {
     const int threads = 256;
     const int blocks = blocks_for(P * 32, threads, 16 * ctx.num_sms);
-    precond_update_kernel<<<blocks, threads, sizeof(double) * 2 * r_eff, st>>>(
+    launch_pdl(precond_update_kernel, blocks, threads, sizeof(double) * 2 * r_eff, st, 
         out->u_next, out->ld_u, P, (int)r_eff, c, out->sigma, gbar, 1.0 / floor, in->theta,
         in->eta, out->theta_next, out->update);
     post_launch(ctx);
@@ -1123,7 +1127,7 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   // state refresh (optimizers.py:376-383): obar = U sigma, lbar = V[:r] lhat
   {
     dim3 grid((unsigned)((P + 31) / 32), (unsigned)((r_eff + 31) / 32));
-    transpose_scale_kernel<<<grid, dim3(32, 8), 0, st>>>(out->u_next, out->ld_u, P, (int)r_eff,
+    launch_pdl(transpose_scale_kernel, grid, dim3(32, 8), 0, st, out->u_next, out->ld_u, P, (int)r_eff,
                                                          out->sigma, out->obar_next_t,
                                                          out->ld_obar);
     post_launch(ctx);
@@ -1209,6 +1213,7 @@ struct EmuSumArgs {
   const double* src[8];
 };
 __global__ void emu_sum_kernel(EmuSumArgs a, int world, size_t n, double* out) {
+  pdl_wait();
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     double s = a.src[0][i];
@@ -1272,7 +1277,7 @@ struct EmuComm : Comm {
       }
       EmuSumArgs a{};
       for (int r = 0; r < world; ++r) a.src[r] = g->bufs[r];
-      emu_sum_kernel<<<256, 256, 0, st>>>(a, world, n, g->scratch);
+      launch_pdl(emu_sum_kernel, 256, 256, 0, st, a, world, n, g->scratch);
       e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) g->abort();
     }
@@ -1289,6 +1294,7 @@ struct EmuComm : Comm {
 
 namespace wssr {
 __global__ void dmma_peak_kernel(double* out, int iters) {
+  pdl_wait();
   double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
   double c[8][2];
 #pragma unroll
@@ -1436,9 +1442,9 @@ int wssr_dmma_peak_probe(wssr_ctx* ctx, double* tflops) {
     cudaEvent_t a, b;
     WSSR_CUDA(cudaEventCreate(&a));
     WSSR_CUDA(cudaEventCreate(&b));
-    dmma_peak_kernel<<<blocks, threads, 0, ctx->c.stream>>>(sink, iters);
+    launch_pdl(dmma_peak_kernel, blocks, threads, 0, ctx->c.stream, sink, iters);
     WSSR_CUDA(cudaEventRecord(a, ctx->c.stream));
-    dmma_peak_kernel<<<blocks, threads, 0, ctx->c.stream>>>(sink, iters);
+    launch_pdl(dmma_peak_kernel, blocks, threads, 0, ctx->c.stream, sink, iters);
     WSSR_CUDA(cudaEventRecord(b, ctx->c.stream));
     WSSR_CUDA(cudaEventSynchronize(b));
     float ms = 0.f;

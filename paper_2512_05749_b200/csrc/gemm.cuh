@@ -89,6 +89,7 @@ __device__ __forceinline__ void load_chunk(double* dst, const double* base, cons
 template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int VA, int VB>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
     gemm_dmma_kernel(const GemmArgs args) {
+  pdl_wait();
   using Cfg = GemmCfg<L, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   constexpr bool CM = Cfg::kCM;
   constexpr int NT = Cfg::kThreads;
@@ -277,6 +278,7 @@ static __global__ void __launch_bounds__(256)
     splitk_reduce_few_kernel(const double* __restrict__ partial, int S, int64_t M, int64_t N,
                              double* __restrict__ C, int64_t ldc, double alpha, int accumulate,
                              const double* __restrict__ Cin, int64_t ldcin) {
+  pdl_wait();
   const int64_t total = M * N;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -297,6 +299,7 @@ static __global__ void __launch_bounds__(256)
     splitk_reduce_kernel(const double* __restrict__ partial, int S, int64_t M, int64_t N,
                          double* __restrict__ C, int64_t ldc, double alpha, int accumulate,
                          const double* __restrict__ Cin, int64_t ldcin) {
+  pdl_wait();
   __shared__ double red[8][33];
   const int64_t total = M * N;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

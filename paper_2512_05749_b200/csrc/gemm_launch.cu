@@ -69,7 +69,7 @@ cudaError_t launch_one(const GemmArgs& a, int splits, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((a.N + BN - 1) / BN), (unsigned)splits);
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(a);
+  launch_pdl(kern, grid, Cfg::kThreads, Cfg::kSmemBytes, st, a);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -137,11 +137,11 @@ struct TmaTile {
     if (PERSIST) {
       const int64_t units = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * splits;
       const int64_t cap = (int64_t)num_sms() * ctas_per_sm();
-      kern<<<(unsigned)std::min(units, cap), Cfg::kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tS, a);
+      launch_pdl(kern, (unsigned)std::min(units, cap), Cfg::kThreads, Cfg::kSmemBytes, st, tA, tB, tS, a);
     } else {
       dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((a.N + BN - 1) / BN),
                 (unsigned)splits);
-      kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(tA, tB, tS, a);
+      launch_pdl(kern, grid, Cfg::kThreads, Cfg::kSmemBytes, st, tA, tB, tS, a);
     }
     ++g_launches;
     return cudaGetLastError();
@@ -256,11 +256,11 @@ cudaError_t run_tile(Context& ctx, GemmArgs a, bool va2, bool vb2, int max_split
   const int64_t total = a.M * a.N;
   if (s <= 8) {
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 16LL * ctx.num_sms);
-    splitk_reduce_few_kernel<<<std::max(blocks, 1), 256, 0, st>>>(part, s, a.M, a.N, C, ldc, alpha,
+    launch_pdl(splitk_reduce_few_kernel, std::max(blocks, 1), 256, 0, st, part, s, a.M, a.N, C, ldc, alpha,
                                                                   acc, a.Cin, a.ldcin);
   } else {
     int blocks = (int)std::min<int64_t>((total + 31) / 32, 8LL * ctx.num_sms);
-    splitk_reduce_kernel<<<std::max(blocks, 1), 256, 0, st>>>(part, s, a.M, a.N, C, ldc, alpha,
+    launch_pdl(splitk_reduce_kernel, std::max(blocks, 1), 256, 0, st, part, s, a.M, a.N, C, ldc, alpha,
                                                               acc, a.Cin, a.ldcin);
   }
   ++g_launches;

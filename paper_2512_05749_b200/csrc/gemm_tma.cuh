@@ -105,6 +105,7 @@ template <Layout L, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES
 __global__ void __launch_bounds__(32 * (WARPS_M * WARPS_N + 1))
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmS, const GemmArgs args) {
+  pdl_wait();
   using Cfg = TmaCfg<L, BM, BN, BK, WARPS_M, WARPS_N, STAGES, TA>;
   constexpr bool CM = Cfg::kCM;
   constexpr bool F32 = Cfg::kF32;

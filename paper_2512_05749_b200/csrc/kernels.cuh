@@ -14,6 +14,7 @@ namespace wssr {
 __global__ void energy_stats_kernel(const double* __restrict__ E, int64_t n, double n_std,
                                     int clip_enabled, double scale, double* __restrict__ l_scaled,
                                     double* __restrict__ l_raw, double* __restrict__ scal_out) {
+  pdl_wait();
   __shared__ double scratch[32];
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += E[i];
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 2)
                     const double* __restrict__ lraw, double* __restrict__ mu,
                     double* __restrict__ m2, double* __restrict__ gsum,
                     double* __restrict__ cmin, double* __restrict__ cmax) {
+  pdl_wait();
   __shared__ double sh[kColStatsWarps][5][32 * VEC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t col0 = (int64_t)blockIdx.x * (32 * VEC) + (int64_t)lane * VEC;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(32 * kColStatsWarps, 2)
 // ---------------------------------------------------------------------------------------------
 __global__ void reduce_partials_kernel(const double* __restrict__ x, int64_t n, int64_t chunk,
                                        int op, double* __restrict__ partials) {
+  pdl_wait();
   __shared__ double scratch[32];
   const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(n, b0 + chunk);
   double s = 0.0;
@@ -236,6 +239,7 @@ __global__ void reduce_partials_kernel(const double* __restrict__ x, int64_t n, 
 }
 __global__ void reduce_final_kernel(const double* __restrict__ partials, int nparts, double scale,
                                     double* __restrict__ out) {
+  pdl_wait();
   __shared__ double scratch[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partials[i];
@@ -248,6 +252,7 @@ __global__ void reduce_final_kernel(const double* __restrict__ partials, int npa
 // (optimizers.py:370), where rows are P = 10^5..10^6 long.
 __global__ void row_sumsq_partials_kernel(const double* __restrict__ x, int64_t cols, int64_t ld,
                                           int64_t chunk, double* __restrict__ partial) {
+  pdl_wait();
   __shared__ double scratch[32];
   const int64_t r = blockIdx.y, b = blockIdx.x;
   const double* row = x + r * ld;
@@ -265,6 +270,7 @@ __global__ void row_sumsq_partials_kernel(const double* __restrict__ x, int64_t 
 }
 __global__ void row_norms_final_kernel(const double* __restrict__ partial, int nb, int rows,
                                        double* __restrict__ out, int sqrt_out) {
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   double s = 0.0;
@@ -277,6 +283,7 @@ __global__ void row_norms_final_kernel(const double* __restrict__ partial, int n
 __global__ void matrix_sumsq_partials_kernel(const double* __restrict__ x, int64_t rows,
                                              int64_t cols, int64_t ld, int64_t rows_per_block,
                                              double* __restrict__ partials) {
+  pdl_wait();
   __shared__ double scratch[32];
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block, r1 = min(rows, r0 + rows_per_block);
   double s0 = 0.0, s1 = 0.0;
@@ -523,6 +530,7 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
                                                              int* __restrict__ status,
                                                              double pivot_rel, int use_series,
                                                              long long* prof = nullptr) {
+  pdl_wait();
   extern __shared__ double series_buf[];  // 2 x 64 x 65 doubles when use_series
   __shared__ double colL[64], rowX[64], dg[64];
   __shared__ double s_sq, s_inv, s_tr, s_gmax;
@@ -704,6 +712,7 @@ __host__ __device__ inline size_t chol_scratch_doubles(int k) {
 __global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int k, double* R,
                                                             double* Rinv, int* status,
                                                             double pivot_rel) {
+  pdl_wait();
   extern __shared__ __align__(16) double smem[];
   double* W = smem;
   double* X = W + (size_t)k * (k + 1);
@@ -712,6 +721,7 @@ __global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int
 __global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int k, double* ws,
                                                             double* R, double* Rinv, int* status,
                                                             double pivot_rel) {
+  pdl_wait();
   double* W = ws;
   double* X = W + (size_t)k * (k + 1);
   chol_inv_body(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
@@ -720,6 +730,7 @@ __global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int
 // C = A * B for k x k upper-triangular A, B (row-major, ld k).
 __global__ void triu_mul_kernel(const double* __restrict__ A, const double* __restrict__ B, int k,
                                 double* __restrict__ C) {
+  pdl_wait();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
   const int r = e / k, c = e % k;
@@ -736,6 +747,7 @@ __global__ void triu_mul_kernel(const double* __restrict__ A, const double* __re
 __global__ void sort_sigma_kernel(const double* __restrict__ Rv, int k, double r_reg,
                                   int64_t* __restrict__ order_out, double* __restrict__ sigma_out,
                                   int* __restrict__ ints_out) {
+  pdl_wait();
   extern __shared__ double sd[];
   for (int i = threadIdx.x; i < k; i += blockDim.x) sd[i] = Rv[i * k + i];
   __syncthreads();
@@ -774,6 +786,7 @@ __global__ void sort_sigma_kernel(const double* __restrict__ Rv, int k, double r
 __global__ void gather_cols_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows,
                                    const int64_t* __restrict__ order, int kk,
                                    double* __restrict__ out, int64_t ldo) {
+  pdl_wait();
   const int64_t total = rows * kk;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -786,6 +799,7 @@ __global__ void gather_cols_kernel(const double* __restrict__ in, int64_t ldi, i
 // strided 2-D copy (rows x cols), optional scale
 __global__ void copy2d_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows,
                               int64_t cols, double scale, double* __restrict__ out, int64_t ldo) {
+  pdl_wait();
   const int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -799,6 +813,7 @@ __global__ void copy2d_kernel(const double* __restrict__ in, int64_t ldi, int64_
 __global__ void transpose_scale_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows,
                                        int cols, const double* __restrict__ colscale,
                                        double* __restrict__ out, int64_t ldo) {
+  pdl_wait();
   __shared__ double tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
@@ -819,6 +834,7 @@ __global__ void transpose_scale_kernel(const double* __restrict__ in, int64_t ld
 // y[i] = a*x[i] + b*y[i]
 __global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, double b,
                              double* __restrict__ y) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = a * x[i] + (b == 0.0 ? 0.0 : b * y[i]);
@@ -836,6 +852,7 @@ __global__ void precond_update_kernel(const double* __restrict__ U, int64_t ldu,
                                       const double* __restrict__ theta, double eta,
                                       double* __restrict__ theta_out,
                                       double* __restrict__ update_out) {
+  pdl_wait();
   extern __shared__ double sc[];  // [2r]: c/sigma^2, c
   for (int j = threadIdx.x; j < r; j += blockDim.x) {
     const double s = sigma[j];
@@ -989,6 +1006,7 @@ __device__ void maxeig_body(const double* __restrict__ Ain, int k, double* A, do
 __global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict__ Ain, int k,
                                                         double* __restrict__ out,
                                                         long long* prof = nullptr) {
+  pdl_wait();
   constexpr int LD = 65;
   __shared__ double A[64 * LD];
   __shared__ double v[64], p[64], dg[64], od[64], e2[64];
@@ -1139,10 +1157,12 @@ __global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict
 }
 
 __global__ void maxeig_smem_kernel(const double* Ain, int k, double* out) {
+  pdl_wait();
   extern __shared__ __align__(16) double smem[];
   maxeig_body(Ain, k, smem, smem + (size_t)k * (k + 1), out);
 }
 __global__ void maxeig_gmem_kernel(const double* Ain, int k, double* W, double* out) {
+  pdl_wait();
   maxeig_body(Ain, k, W, W + (size_t)k * (k + 1), out);
 }
 
@@ -1160,6 +1180,7 @@ __device__ __forceinline__ int rr_index(int pos, int round, int kk) {
 
 __global__ void jacobi_svd_kernel(double* __restrict__ W, double* __restrict__ V, int n, int ld,
                                   int max_sweeps, int* __restrict__ sweeps_out) {
+  pdl_wait();
   __shared__ int s_rot;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int nn = n + (n & 1);
@@ -1214,6 +1235,7 @@ __global__ void jacobi_svd_kernel(double* __restrict__ W, double* __restrict__ V
 __global__ void svd_finalize_kernel(const double* __restrict__ W, const double* __restrict__ V,
                                     int n, int ld, double* __restrict__ sigma,
                                     double* __restrict__ Us, double* __restrict__ Vs, int lds) {
+  pdl_wait();
   extern __shared__ double sn[];  // [n] norms, then [n] order (as double)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < n; j += nw) {
@@ -1244,6 +1266,7 @@ __global__ void svd_finalize_kernel(const double* __restrict__ W, const double* 
 __global__ void transpose_shift_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows,
                                        int64_t cols, const double* __restrict__ shift,
                                        double scale, double* __restrict__ out, int64_t ldo) {
+  pdl_wait();
   __shared__ double tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -1264,6 +1287,7 @@ __global__ void transpose_shift_kernel(const double* __restrict__ in, int64_t ld
 __global__ void small_norms_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                    int r, const double* __restrict__ Q, int k,
                                    double* __restrict__ out) {
+  pdl_wait();
   __shared__ double scratch[32];
   double s = 0.0;
   if (a) {

@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmS, const Params p) {
+  pdl_wait();
   constexpr bool F32 = sizeof(TA) == 4;
   constexpr int A_BYTES = BM * BK * (int)sizeof(TA);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -687,6 +688,7 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr) {
 template <bool RM>
 __global__ void __launch_bounds__(kPreThreads, 1)
     ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA, const Params p) {
+  pdl_wait();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* bring = smem + (size_t)PA_DIG * PSTAGES;
@@ -930,6 +932,7 @@ __global__ void __launch_bounds__(256)
     digitize_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t prows,
                     int64_t cols, int64_t ppad, const double* __restrict__ mu_inv,
                     int8_t* __restrict__ planes) {
+  pdl_wait();
   const int64_t pblocks = ppad / 32;
   const int64_t plane = prows * ppad;
   const int64_t total = pblocks * rows * 8;
@@ -980,6 +983,7 @@ template <typename TA, bool RM>
 __global__ void __launch_bounds__(256)
     colmax_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
                   const double* __restrict__ mu, unsigned long long* __restrict__ out) {
+  pdl_wait();
   // element (sample n, parameter p) at A[n * lda + p] in both layouts (row-major sample block)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= cols) return;
@@ -1002,6 +1006,7 @@ __global__ void __launch_bounds__(256)
 __global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
                               const double* __restrict__ mu, int64_t cols, int64_t cols_pad,
                               double* __restrict__ mu_inv) {
+  pdl_wait();
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cols_pad;
        p += (int64_t)gridDim.x * blockDim.x) {
     double m = 0.0, inv = 0.0;
@@ -1022,6 +1027,7 @@ __global__ void mu_inv_minmax_kernel(const double* __restrict__ cmin,
                                      const double* __restrict__ cmax,
                                      const double* __restrict__ mu, int64_t cols, int64_t cols_pad,
                                      double* __restrict__ mu_inv) {
+  pdl_wait();
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cols_pad;
        p += (int64_t)gridDim.x * blockDim.x) {
     double m = 0.0, inv = 0.0;
@@ -1054,6 +1060,7 @@ __device__ __forceinline__ double thin_value(const double* B, int64_t ldb, int64
 __global__ void __launch_bounds__(256)
     thin_colmax_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
                        const double* __restrict__ mu_inv, unsigned long long* __restrict__ out) {
+  pdl_wait();
   // block: 64 columns of one 64-column block x 4 row lanes, 128 rows; 8 independent rows in
   // flight per thread
   const int j = threadIdx.x & 63, kl = threadIdx.x >> 6;
@@ -1103,6 +1110,7 @@ __global__ void __launch_bounds__(256)
                        int64_t kpad, const double* __restrict__ mu_inv,
                        const unsigned long long* __restrict__ cmax, int extra_exp,
                        int8_t* __restrict__ Bd, double* __restrict__ colfac) {
+  pdl_wait();
   // thread: column jl (of 32) and K group kg (of 8, 4 rows each); block covers 32 K x 32 columns
   const int kg = threadIdx.x & 7, jl = threadIdx.x >> 3;
   const int nb = blockIdx.y >> 1;
@@ -1178,7 +1186,7 @@ cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorM
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  ozaki_gemm_kernel<RM, TA><<<grid, kThreads, kSmem, st>>>(tA, tB, tS, p);
+  launch_pdl(ozaki_gemm_kernel<RM, TA>, grid, kThreads, kSmem, st, tA, tB, tS, p);
   return cudaGetLastError();
 }
 
@@ -1192,7 +1200,7 @@ cudaError_t launch_pre(const CUtensorMap& tA, const Params& p, int grid, cudaStr
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  ozaki_pre_kernel<RM><<<grid, kPreThreads, kPreSmem, st>>>(tA, p);
+  launch_pdl(ozaki_pre_kernel<RM>, grid, kPreThreads, kPreSmem, st, tA, p);
   return cudaGetLastError();
 }
 
@@ -1230,12 +1238,12 @@ cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int
   const int gx = (int)((cols + 255) / 256);
   const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(rows / 64, (8 * ctx.num_sms + gx - 1) / gx));
   if (f32)
-    oz::colmax_kernel<float, true><<<dim3(gx, gy), 256, 0, st>>>(
+    launch_pdl(oz::colmax_kernel<float, true>, dim3(gx, gy), 256, 0, st, 
         static_cast<const float*>(A), lda, rows, cols, mu, cmax);
   else
-    oz::colmax_kernel<double, true><<<dim3(gx, gy), 256, 0, st>>>(
+    launch_pdl(oz::colmax_kernel<double, true>, dim3(gx, gy), 256, 0, st, 
         static_cast<const double*>(A), lda, rows, cols, mu, cmax);
-  oz::mu_inv_kernel<<<(int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0, st>>>(
+  launch_pdl(oz::mu_inv_kernel, (int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0, st, 
       cmax, mu, cols, cpad, mu_inv);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
@@ -1244,8 +1252,7 @@ cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int
 cudaError_t ozaki_scales_minmax(Context& ctx, const double* cmin, const double* cmax,
                                 const double* mu, int64_t cols, double* mu_inv, cudaStream_t st) {
   const int64_t cpad = ozaki_scale_len(cols);
-  oz::mu_inv_minmax_kernel<<<(int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0,
-                             st>>>(cmin, cmax, mu, cols, cpad, mu_inv);
+  launch_pdl(oz::mu_inv_minmax_kernel, (int)std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms), 256, 0, st, cmin, cmax, mu, cols, cpad, mu_inv);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
 }
@@ -1269,10 +1276,10 @@ cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, i
   const int64_t work = rows * (ppad / 4);  // threads: one per 4 parameters of a row
   const int grid = (int)std::min<int64_t>((work + 255) / 256, 16 * ctx.num_sms);
   if (f32)
-    oz::digitize_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A), lda, rows,
+    launch_pdl(oz::digitize_kernel<float>, grid, 256, 0, st, static_cast<const float*>(A), lda, rows,
                                                      prows, cols, ppad, mu_inv, planes);
   else
-    oz::digitize_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(A), lda, rows,
+    launch_pdl(oz::digitize_kernel<double>, grid, 256, 0, st, static_cast<const double*>(A), lda, rows,
                                                       prows, cols, ppad, mu_inv, planes);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
@@ -1307,9 +1314,9 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   // RM (v = Ohat^T q): the thin operand's rows are parameters -> carries the column scales
   const double* bmu = RMm ? mu_inv : nullptr;
   {
-    thin_colmax_kernel<<<dim3((unsigned)((K + 127) / 128), nblk), 256, 0, st>>>(a.B, a.ldb, K, N,
+    launch_pdl(thin_colmax_kernel, dim3((unsigned)((K + 127) / 128), nblk), 256, 0, st, a.B, a.ldb, K, N,
                                                                                bmu, cmax);
-    thin_digits_kernel<<<dim3((unsigned)(kpad / 32), 2 * nblk), 256, 0, st>>>(
+    launch_pdl(thin_digits_kernel, dim3((unsigned)(kpad / 32), 2 * nblk), 256, 0, st, 
         a.B, a.ldb, K, N, kpad, bmu, cmax, RMm ? 54 : 0, Bd, colfac);
     ctx.kernel_launches += 2;
   }
@@ -1405,11 +1412,10 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   const int64_t total = M * N;
   const int rb = (int)std::min<int64_t>((total + 255) / 256, 16 * ctx.num_sms);
   if (nch <= 8)
-    splitk_reduce_few_kernel<<<rb, 256, 0, st>>>(p.slab, nch, M, N, a.C, a.ldc, 1.0, a.accumulate,
+    launch_pdl(splitk_reduce_few_kernel, rb, 256, 0, st, p.slab, nch, M, N, a.C, a.ldc, 1.0, a.accumulate,
                                                 nullptr, 0);
   else
-    splitk_reduce_kernel<<<(int)std::min<int64_t>((total + 31) / 32, 16 * ctx.num_sms), 256, 0,
-                           st>>>(p.slab, nch, M, N, a.C, a.ldc, 1.0, a.accumulate, nullptr, 0);
+    launch_pdl(splitk_reduce_kernel, (int)std::min<int64_t>((total + 31) / 32, 16 * ctx.num_sms), 256, 0, st, p.slab, nch, M, N, a.C, a.ldc, 1.0, a.accumulate, nullptr, 0);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
 }

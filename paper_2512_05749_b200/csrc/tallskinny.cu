@@ -46,6 +46,7 @@ template <int KC, bool SYM>
 __global__ void __launch_bounds__(kThreads, 1)
     gram_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                 int64_t ldb, int64_t rows, int64_t rows_per_cta, double* __restrict__ slabs) {
+  pdl_wait();
   constexpr int NB = KC / 8;
   constexpr int NJ = SYM ? NB : NB / 2;  // column blocks per warp
   constexpr int U = kRowStep / 4;
@@ -131,6 +132,7 @@ template <int KC, bool SYM>
 __global__ void __launch_bounds__(256)
     gram_finish_kernel(const double* __restrict__ slabs, int nslab, double* __restrict__ C,
                        int64_t ldc) {
+  pdl_wait();
   __shared__ double part[8][33];
   const int jj = threadIdx.x & 31, sg = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + jj;  // entry (row-major KC x KC)
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, KC == 64 ? 1 : 2)
     mul_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ M,
                int64_t ldm, double alpha, const double* __restrict__ Cin, int64_t ldcin,
                double* __restrict__ Y, int64_t ldy, int64_t rows, double* __restrict__ partial) {
+  pdl_wait();
   constexpr int NB = KC / 8;
   __shared__ __align__(16) double2 Ms[NB * NB * 32];
   __shared__ double scratch[32];
@@ -232,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, KC == 64 ? 1 : 2)
 
 __global__ void sum_partials_kernel(const double* __restrict__ partials, int n,
                                     double* __restrict__ out) {
+  pdl_wait();
   __shared__ double scratch[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
@@ -246,6 +250,7 @@ __global__ void __launch_bounds__(256)
     gemv_t_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ x,
                   int64_t rows, int n, int cw, int64_t rows_per_block,
                   double* __restrict__ partial) {
+  pdl_wait();
   __shared__ double red[256];
   const int c = threadIdx.x % cw, rl = threadIdx.x / cw, lanes = 256 / cw;
   const int j = blockIdx.y * cw + c;
@@ -271,6 +276,7 @@ __global__ void __launch_bounds__(256)
 
 __global__ void gemv_t_finish_kernel(const double* __restrict__ partial, int nblk, int n,
                                      double alpha, double* __restrict__ out) {
+  pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   double t = 0.0;
@@ -289,8 +295,8 @@ cudaError_t gram_launch(Context& ctx, int64_t rows, const double* A, int64_t lda
   if (grid < 1) grid = 1;
   double* slabs = ctx.splitk_buffer((size_t)grid * KC * KC);
   if (!slabs) return cudaErrorMemoryAllocation;
-  gram_kernel<KC, SYM><<<grid, kThreads, 0, ctx.stream>>>(A, lda, B, ldb, rows, rpc, slabs);
-  gram_finish_kernel<KC, SYM><<<KC * KC / 32, 256, 0, ctx.stream>>>(slabs, grid, C, ldc);
+  launch_pdl(gram_kernel<KC, SYM>, grid, kThreads, 0, ctx.stream, A, lda, B, ldb, rows, rpc, slabs);
+  launch_pdl(gram_finish_kernel<KC, SYM>, KC * KC / 32, 256, 0, ctx.stream, slabs, grid, C, ldc);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
 }
@@ -306,11 +312,11 @@ cudaError_t mul_launch(Context& ctx, int64_t rows, const double* A, int64_t lda,
     partial = ctx.splitk_buffer((size_t)grid);
     if (!partial) return cudaErrorMemoryAllocation;
   }
-  mul_kernel<KC, TRI, MODE><<<grid, kThreads, 0, ctx.stream>>>(A, lda, M, ldm, alpha, Cin, ldcin,
+  launch_pdl(mul_kernel<KC, TRI, MODE>, grid, kThreads, 0, ctx.stream, A, lda, M, ldm, alpha, Cin, ldcin,
                                                                 Y, ldy, rows, partial);
   ctx.kernel_launches += 1;
   if (MODE == kAddSumsq) {
-    sum_partials_kernel<<<1, 256, 0, ctx.stream>>>(partial, grid, out);
+    launch_pdl(sum_partials_kernel, 1, 256, 0, ctx.stream, partial, grid, out);
     ctx.kernel_launches += 1;
   }
   return cudaGetLastError();
@@ -336,9 +342,9 @@ cudaError_t ts_gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, in
   nblk = (int)((rows + rpb - 1) / rpb);
   double* partial = ctx.splitk_buffer((size_t)nblk * n);
   if (!partial) return cudaErrorMemoryAllocation;
-  ts::gemv_t_kernel<<<dim3(nblk, ycols), 256, 0, ctx.stream>>>(A, lda, x, rows, (int)n, cw, rpb,
+  launch_pdl(ts::gemv_t_kernel, dim3(nblk, ycols), 256, 0, ctx.stream, A, lda, x, rows, (int)n, cw, rpb,
                                                               partial);
-  ts::gemv_t_finish_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx.stream>>>(
+  launch_pdl(ts::gemv_t_finish_kernel, (unsigned)((n + 127) / 128), 128, 0, ctx.stream, 
       partial, nblk, (int)n, alpha, out);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
