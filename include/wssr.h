@@ -233,6 +233,12 @@ typedef struct wssr_step_out {
   /* host outputs */
   int64_t r_eff, k_pos, iterations, next_r_max, binding;
   double residual, sigma_drift, projector_drift;
+  /* optional: pinned host memory for {sigma_drift, projector_drift}.  With an auxiliary stream set
+     (wssr_set_aux_stream) and a single rank, the drift telemetry (optimizers.py:366-374) runs on
+     that stream after the step's own work and its two values land here in aux-stream order;
+     the host fields above then read NaN and the call does not wait for them.  Without an aux
+     stream the values are written here too (synchronously). */
+  double* drift_host;
 } wssr_step_out;
 int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
 
@@ -270,6 +276,11 @@ int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
  * (CholeskyQR2, Rayleigh quotient and residual, drift) on the tall-skinny kernels
  * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
+
+/* auxiliary CUDA stream for the asynchronous drift telemetry of wssr_step_f64 (NULL: none).  The
+ * caller keeps the step's inputs/outputs alive until that stream passes the step (e.g. torch's
+ * record_stream). */
+int wssr_set_aux_stream(wssr_ctx* ctx, void* cuda_stream);
 
 /* test hook: one tall-skinny kernel, row-major operands with ld = k (k = 32 or 64).
  * op 0: out = A^T A (k x k); op 1: out = A^T B; op 2: out (rows x k) = A (alpha M) with M upper

@@ -73,6 +73,7 @@ class StepOut(ctypes.Structure):
         ("r_eff", _i64), ("k_pos", _i64), ("iterations", _i64), ("next_r_max", _i64),
         ("binding", _i64),
         ("residual", _dbl), ("sigma_drift", _dbl), ("projector_drift", _dbl),
+        ("drift_host", _vp),
     ]
 
 
@@ -87,6 +88,7 @@ SIGNATURES = {
     "wssr_set_gemm_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_set_aux_stream": (ctypes.c_int, [_vp, _vp]),
     "wssr_debug_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp,
                                              _dbl, _vp]),
     "wssr_phase_stats": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_dbl),
@@ -176,6 +178,16 @@ class Context:
         self.device = int(device)
         self.rank = 0
         self.world = 1
+        self._aux = None
+
+    def aux_stream(self):
+        """Side stream for the step's asynchronous drift telemetry (created on first use)."""
+        import torch
+
+        if self._aux is None:
+            self._aux = torch.cuda.Stream(device=self.device)
+            self.lib.wssr_set_aux_stream(self.handle, _vp(self._aux.cuda_stream))
+        return self._aux
 
     def __del__(self):
         try:

@@ -763,31 +763,48 @@ void maxeig(Context& ctx, const double* A, int k, double* out_dev) {
 }
 
 // ---- subspace_drift (svdengine.py:199-226) ----------------------------------------------------
+// {sigma_drift, projector_drift} from {||s1 - s2||, -, lambda_max}: sqrt and the 1e-12 -> 0 rule
+// (svdengine.py:222-225)
+__global__ void drift_finalize_kernel(const double* __restrict__ in, double* __restrict__ out) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    double sd = in[0];
+    double pd = sqrt(fmax(in[2], 0.0));
+    out[0] = sd < 1e-12 ? 0.0 : sd;
+    out[1] = pd < 1e-12 ? 0.0 : pd;
+  }
+}
+
+// Enqueue the drift on ctx.stream; out2 (device, 2 doubles) = {sigma_drift, projector_drift}.
+void drift_enqueue(Context& ctx, int64_t rows, const double* u1, int64_t ld1, const double* s1,
+                   int64_t r, const double* u2, int64_t ld2, const double* s2, double* out2) {
+  cudaStream_t st = ctx.stream;
+  Buf C((size_t)r * r, st), X((size_t)rows * r, st), GX((size_t)r * r, st), out(3, st);
+  launch_pdl(small_norms_kernel, 1, 256, 0, st, s1, s2, (int)r, nullptr, 0, out);
+  post_launch(ctx);
+  cross(ctx, rows, r, u1, ld1, u2, ld2, C);                  // u1^T u2
+  sub_mul_small(ctx, rows, r, u1, ld1, C, u2, ld2, X, r);    // u2 - u1 (u1^T u2)
+  gram(ctx, rows, r, X, r, GX, false);
+  maxeig(ctx, GX, (int)r, out + 2);
+  post_launch(ctx);
+  launch_pdl(drift_finalize_kernel, 1, 32, 0, st, (const double*)out, out2);
+  post_launch(ctx);
+}
+
 std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, int64_t ld1,
                                 const double* s1, int64_t r1, const double* u2, int64_t ld2,
                                 const double* s2, int64_t r2) {
   const int64_t r = std::min(r1, r2);
   if (r == 0) return {0.0, 0.0};
-  cudaStream_t st = ctx.stream;
-  Buf C((size_t)r * r, st), X((size_t)rows * r, st), GX((size_t)r * r, st), out(3, st);
+  Buf out2(2, ctx.stream);
   {
     PhaseTimer tm(ctx, 5, 0.0, 0.0);
-    launch_pdl(small_norms_kernel, 1, 256, 0, st, s1, s2, (int)r, nullptr, 0, out);
-    post_launch(ctx);
-    cross(ctx, rows, r, u1, ld1, u2, ld2, C);                  // u1^T u2
-    sub_mul_small(ctx, rows, r, u1, ld1, C, u2, ld2, X, r);    // u2 - u1 (u1^T u2)
-    gram(ctx, rows, r, X, r, GX, false);
-    maxeig(ctx, GX, (int)r, out + 2);
-    post_launch(ctx);
+    drift_enqueue(ctx, rows, u1, ld1, s1, r, u2, ld2, s2, out2);
   }
-  double h[3];
-  d2h(ctx, h, out, sizeof(h));
+  double h[2];
+  d2h(ctx, h, out2, sizeof(h));
   sync(ctx);
-  double sd = h[0];
-  double pd = std::sqrt(std::max(h[2], 0.0));
-  if (sd < kDriftZero) sd = 0.0;
-  if (pd < kDriftZero) pd = 0.0;
-  return {sd, pd};
+  return {h[0], h[1]};
 }
 
 // ---- estimators.assemble (estimators.py:74-100) --------------------------------------------
@@ -1141,8 +1158,38 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   if (dist) allreduce(ctx, out->lbar_next, r_eff);
   // drift telemetry against the previous factors (optimizers.py:366-374)
   double sd = 0.0, pd = 0.0;
-  if (in->r_prev > 0) {
-    const int64_t r_hist = oh.hist_rank;
+  const int64_t r_hist = oh.hist_rank;
+  const int64_t r_drift = in->r_prev > 0 ? std::min(std::min(r_hist, in->r_prev), r_eff) : 0;
+  if (r_drift > 0 && out->drift_host && ctx.aux && !dist) {
+    // asynchronous: the drift runs on the auxiliary stream (after everything above) while the
+    // caller moves on; {sigma_drift, projector_drift} land in out->drift_host in aux-stream order
+    if (!ctx.aux_event) WSSR_CUDA(cudaEventCreateWithFlags(&ctx.aux_event, cudaEventDisableTiming));
+    WSSR_CUDA(cudaEventRecord(ctx.aux_event, st));
+    WSSR_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.aux_event, 0));
+    // the aux stream gets its own slab buffer (the main stream's is reused by the next step)
+    cudaStream_t main_stream = ctx.stream;
+    std::swap(ctx.splitk, ctx.aux_splitk);
+    std::swap(ctx.splitk_cap, ctx.aux_splitk_cap);
+    ctx.stream = ctx.aux;
+    auto restore = [&] {
+      ctx.stream = main_stream;
+      std::swap(ctx.splitk, ctx.aux_splitk);
+      std::swap(ctx.splitk_cap, ctx.aux_splitk_cap);
+    };
+    try {
+      Buf sprev(r_hist, ctx.aux), out2(2, ctx.aux);
+      PhaseTimer tm(ctx, 5, 0.0, 0.0);  // events on the aux stream
+      row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
+      drift_enqueue(ctx, P, in->u_prev, in->ld_prev, sprev, r_drift, out->u_next, out->ld_u,
+                    out->sigma, out2);
+      d2h(ctx, out->drift_host, out2, 2 * sizeof(double));
+    } catch (...) {
+      restore();
+      throw;
+    }
+    restore();
+    sd = pd = std::numeric_limits<double>::quiet_NaN();
+  } else if (in->r_prev > 0) {
     Buf sprev(std::max<int64_t>(r_hist, 1), st);
     if (r_hist > 0) row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
     const int64_t r1 = std::min(r_hist, in->r_prev);
@@ -1150,6 +1197,10 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
                    r_eff);
     sd = d.first;
     pd = d.second;
+  }
+  if (out->drift_host && !std::isnan(sd)) {
+    out->drift_host[0] = sd;
+    out->drift_host[1] = pd;
   }
 
   sync(ctx);
@@ -1360,6 +1411,9 @@ void wssr_ctx_destroy(wssr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   if (ctx->c.splitk || ctx->c.oz_ws || ctx->c.oz_planes) cudaDeviceSynchronize();
+  if (ctx->c.aux) cudaStreamSynchronize(ctx->c.aux);
+  if (ctx->c.aux_event) cudaEventDestroy(ctx->c.aux_event);
+  if (ctx->c.aux_splitk) cudaFree(ctx->c.aux_splitk);
   if (ctx->c.splitk) cudaFree(ctx->c.splitk);
   if (ctx->c.oz_ws) cudaFree(ctx->c.oz_ws);
   if (ctx->c.oz_planes) cudaFree(ctx->c.oz_planes);
@@ -1410,6 +1464,12 @@ int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const 
     }
     sync(c);
   });
+}
+
+int wssr_set_aux_stream(wssr_ctx* ctx, void* stream) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  ctx->c.aux = static_cast<cudaStream_t>(stream);
+  return WSSR_OK;
 }
 
 int wssr_set_timing(wssr_ctx* ctx, int enabled) {

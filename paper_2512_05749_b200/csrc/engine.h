@@ -39,6 +39,10 @@ struct Context {
   double oz_min_elems = 4194304.0;  // smallest sample block (elements) sent to that path
   bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
   bool tallskinny = true;    // k = 32/64 Grams and products of P x k blocks: tallskinny.cu
+  cudaStream_t aux = nullptr;      // optional: asynchronous drift telemetry (wssr_set_aux_stream)
+  cudaEvent_t aux_event = nullptr;
+  double* aux_splitk = nullptr;    // the aux stream's own split-K / slab buffer
+  size_t aux_splitk_cap = 0;
   int oz_pre = 0;            // digit planes: 0 = pre-digitise when they fit, 1 = on the fly only
   int8_t* oz_planes = nullptr;  // the step's pre-digitised sample block (reused across steps)
   size_t oz_planes_cap = 0;     // bytes

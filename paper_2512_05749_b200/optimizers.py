@@ -86,15 +86,60 @@ class WssrState:
                    sigma_floor_relative=sigma_floor_relative, r_reg=r_reg, eps_grow=eps_grow)
 
 
-@dataclass(frozen=True)
 class WssrDiagnostics:
-    """Per-step telemetry mirrored into the trace file (optimizers.py:250-258)."""
+    """Per-step telemetry mirrored into the trace file (optimizers.py:250-258).
 
-    ssi: SsiReport
-    effective_rank: int
-    r_max: int
-    sigma_drift: float
-    projector_drift: float
+    Same fields as the reference's frozen dataclass.  The two drift values of a single-rank
+    step are computed on a side stream after the step's own work; they resolve (waiting for
+    that stream) on first access, so a caller that never reads them never waits.
+    """
+
+    __slots__ = ("ssi", "effective_rank", "r_max", "_drift", "_pending")
+
+    def __init__(self, ssi, effective_rank, r_max, sigma_drift, projector_drift):
+        set_ = object.__setattr__
+        set_(self, "ssi", ssi)
+        set_(self, "effective_rank", effective_rank)
+        set_(self, "r_max", r_max)
+        set_(self, "_drift", (float(sigma_drift), float(projector_drift)))
+        set_(self, "_pending", None)
+
+    @classmethod
+    def _deferred(cls, ssi, effective_rank, r_max, event, host):
+        self = cls(ssi, effective_rank, r_max, float("nan"), float("nan"))
+        object.__setattr__(self, "_pending", (event, host))
+        return self
+
+    def _resolve(self):
+        if self._pending is not None:
+            event, host = self._pending
+            event.synchronize()
+            object.__setattr__(self, "_drift", tuple(float(x) for x in host.tolist()))
+            object.__setattr__(self, "_pending", None)
+        return self._drift
+
+    @property
+    def sigma_drift(self) -> float:
+        return self._resolve()[0]
+
+    @property
+    def projector_drift(self) -> float:
+        return self._resolve()[1]
+
+    def __setattr__(self, name, value):
+        raise AttributeError("WssrDiagnostics is immutable")
+
+    def __eq__(self, other):
+        if not isinstance(other, WssrDiagnostics):
+            return NotImplemented
+        return (self.ssi, self.effective_rank, self.r_max, self.sigma_drift,
+                self.projector_drift) == (other.ssi, other.effective_rank, other.r_max,
+                                          other.sigma_drift, other.projector_drift)
+
+    def __repr__(self):
+        return (f"WssrDiagnostics(ssi={self.ssi!r}, effective_rank={self.effective_rank!r}, "
+                f"r_max={self.r_max!r}, sigma_drift={self.sigma_drift!r}, "
+                f"projector_drift={self.projector_drift!r})")
 
 
 def _per_step_seed(rng_seed, step):
@@ -227,8 +272,20 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         u_next=u_next.data_ptr(), ld_u=k, obar_next_t=obar_t.data_ptr(), ld_obar=m,
         lbar_next=lbar_next.data_ptr(), sigma=sigma.data_ptr(),
     )
+    aux = ctx.aux_stream() if int(getattr(ctx, "world", 1)) == 1 and hasattr(ctx, "aux_stream") \
+        else None
+    drift_host = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    sout.drift_host = drift_host.data_ptr()
     ctx.call("wssr_step_f64", ctypes.byref(sin), ctypes.byref(sout))
     r_eff = int(sout.r_eff)
+    deferred = aux is not None and math.isnan(sout.projector_drift)
+    if deferred:
+        # the drift kernels still read these on the side stream
+        event = torch.cuda.Event()
+        event.record(aux)
+        for t in (u_prev, hist, u_next, sigma):
+            if t is not None and t.numel() > 0 and t.is_cuda:
+                t.record_stream(aux)
     state_next = replace(
         state,
         obar=obar_t[:r_eff].t(),
@@ -239,9 +296,12 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     )
     report = SsiReport(iterations_used=int(sout.iterations),
                        subspace_residual=float(sout.residual), warm_started=not dense)
-    diag = WssrDiagnostics(ssi=report, effective_rank=r_eff, r_max=int(state.r_max),
-                           sigma_drift=float(sout.sigma_drift),
-                           projector_drift=float(sout.projector_drift))
+    if deferred:
+        diag = WssrDiagnostics._deferred(report, r_eff, int(state.r_max), event, drift_host)
+    else:
+        diag = WssrDiagnostics(ssi=report, effective_rank=r_eff, r_max=int(state.r_max),
+                               sigma_drift=float(sout.sigma_drift),
+                               projector_drift=float(sout.projector_drift))
     if return_update:
         return theta_next, state_next, diag, update
     return theta_next, state_next, diag
