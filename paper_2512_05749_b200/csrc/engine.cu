@@ -41,7 +41,6 @@ struct Fail {
 constexpr double kDeficientColumnRel = 1e-12;  // linalg.py:16 DEFICIENT_COLUMN_REL
 constexpr double kZeroMatrixNorm = 1e-300;     // linalg.py:15 ZERO_MATRIX_NORM
 constexpr double kCholPivotRel = 1e-13;        // CholeskyQR2 safety margin (see kernels.cuh)
-constexpr double kDriftZero = 1e-12;           // svdengine.py:222-225
 
 double* Context::splitk_buffer(size_t n) {
   if (n > splitk_cap) {
@@ -151,7 +150,12 @@ struct PhaseTimer {
 };
 // fold finished event pairs into the per-phase totals (call after a stream sync)
 void collect_timing(Context& ctx) {
+  std::vector<Context::PendingEvent> later;  // pairs on the aux stream that have not finished
   for (auto& pe : ctx.pending) {
+    if (cudaEventQuery(pe.b) == cudaErrorNotReady) {
+      later.push_back(pe);
+      continue;
+    }
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, pe.a, pe.b) == cudaSuccess) {
       ctx.phase_ms[pe.phase] += ms;
@@ -162,7 +166,8 @@ void collect_timing(Context& ctx) {
     ctx.event_pool.push_back(pe.a);
     ctx.event_pool.push_back(pe.b);
   }
-  ctx.pending.clear();
+  cudaGetLastError();  // clear cudaErrorNotReady
+  ctx.pending.swap(later);
 }
 
 // ---- GEMM wrappers ------------------------------------------------------------------------
@@ -294,7 +299,7 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
   const size_t smem = sizeof(double) * chol_scratch_doubles(k);
   if (k <= 64) {
     // dynamic shared memory enables the near-identity series path (second CholeskyQR2 pass)
-    const int series_smem = ctx.chol_series ? (int)(2 * 64 * 65 * sizeof(double)) : 0;
+    const int series_smem = (int)(2 * 64 * 65 * sizeof(double));  // series path / blocked sweep
     static bool attr = false;
     if (!attr) {
       WSSR_CUDA(cudaFuncSetAttribute(chol_inv_reg64_kernel,
@@ -1485,6 +1490,10 @@ int wssr_set_timing(wssr_ctx* ctx, int enabled) {
 int wssr_phase_stats(wssr_ctx* ctx, int phase, double* ms, int64_t* launches, double* flops,
                      double* bytes) {
   if (!ctx || phase < 0 || phase >= Context::kPhases) return WSSR_ERR_VALUE;
+  if (!ctx->c.pending.empty()) {
+    cudaDeviceSynchronize();
+    collect_timing(ctx->c);
+  }
   *ms = ctx->c.phase_ms[phase];
   *launches = ctx->c.phase_count[phase];
   *flops = ctx->c.phase_flops[phase];

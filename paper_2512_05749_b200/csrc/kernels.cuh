@@ -518,12 +518,10 @@ __device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, 
     }
 }
 
-// k <= 64: register-resident variant.  The matrix is padded to 64 x 64 with an identity tail;
-// thread (ty, tx) of the 16 x 16 grid owns rows {ty + 16 a} x columns {tx + 16 b}, a, b < 4, of
-// both L (lower part of W) and X = L^-1, in registers.  Per column j: the owners of column j of L
-// and of row j of X publish them (scaled) through shared memory, one barrier, every thread
-// applies its 16 + 16 rank-1 updates, the owner of the next pivot precomputes sqrt and 1/sqrt,
-// one barrier.  ~60 instructions per thread per column instead of strided shared-memory loops.
+// k <= 64: the matrix is padded to 64 x 64 with an identity tail and loaded in a 16 x 16 thread
+// grid (thread (ty, tx) holds rows {ty + 16 a} x columns {tx + 16 b}); a near-identity Gram
+// takes the series path, any other the blocked sweep below (same pivot tests and status codes as
+// the generic chol_inv_body).
 __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __restrict__ G, int k,
                                                              double* __restrict__ R,
                                                              double* __restrict__ Rinv,
@@ -532,18 +530,17 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
                                                              long long* prof = nullptr) {
   pdl_wait();
   extern __shared__ double series_buf[];  // 2 x 64 x 65 doubles when use_series
-  __shared__ double colL[64], rowX[64], dg[64];
-  __shared__ double s_sq, s_inv, s_tr, s_gmax;
+  __shared__ double dg[64];
+  __shared__ double s_tr, s_gmax;
   __shared__ int s_fail;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double w[4][4], x[4][4];
+  double w[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int i = ty + 16 * a, c = tx + 16 * b;
       w[a][b] = (i < k && c < k) ? G[i * k + c] : (i == c ? 1.0 : 0.0);
-      x[a][b] = (i == c) ? 1.0 : 0.0;
     }
   if (tid < 64) dg[tid] = tid < k ? G[tid * k + tid] : 1.0;
   __syncthreads();
@@ -576,26 +573,31 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
       return;
     }
   }
+  // ---- blocked right-looking Cholesky (8-column panels) + blocked triangular inverse ----------
+  // Warp 0 factorises each 64 x 8 panel in registers (pivot by shuffle, one rsqrt per column);
+  // all 256 threads then apply the panel's rank-8 update to the trailing block.  The inverse
+  // X = L^-1 is formed by 8x8 blocks: the 8 diagonal blocks in parallel (one warp each), then
+  // block rows i = 1..7 with X_ij = -X_ii sum_{m=j}^{i-1} L_im X_mj.  Shared memory: L and X,
+  // 64 x 65 doubles each (the series path's buffer).
+  constexpr int LD = 65;
+  double* Ls = series_buf;
+  double* Xs = series_buf + 64 * LD;
+  __shared__ double s_invd[64];
+  __shared__ double T[64 * 8];  // block-row scratch: T_ij rows (8 per block) x 8
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) Ls[(ty + 16 * a) * LD + tx + 16 * b] = w[a][b];
   if (tid == 0) {
     double gm = 0.0, tr = 0.0;
-    for (int j = 0; j < k; ++j) {
-      gm = fmax(gm, dg[j]);
-      tr += dg[j];
+    for (int jj = 0; jj < k; ++jj) {
+      gm = fmax(gm, dg[jj]);
+      tr += dg[jj];
     }
     s_gmax = gm;
     s_tr = tr;
-    s_fail = 0;
-    const double d = dg[0];
-    const double defic = 1.0000001e-24 * tr;
-    if (!(gm > 0.0) || !(gm < 1.0 / 0.0)) {
-      s_fail = -1;
-    } else if (!(d > pivot_rel * dg[0]) || !(d > defic)) {
-      s_fail = 1;
-    } else {
-      const double y = fast_rsqrt(d);
-      s_inv = y;
-      s_sq = d * y;
-    }
+    s_fail = (!(gm > 0.0) || !(gm < 1.0 / 0.0)) ? -1 : 0;
   }
   __syncthreads();
   if (s_fail < 0) {
@@ -605,104 +607,134 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
     }
     return;
   }
-  const double deficient_sq = 1.0000001e-24 * s_tr;
-  // Published vectors carry exact zeros where an update must not land, so the rank-1 updates
-  // below are branch-free: colL[i] = L[i][j] for i > j (0 for i <= j, the diagonal stays in its
-  // owner's register), rowX[c] = X[j][c] for c <= j (0 above).
-  if (prof && tid == 0) prof[0] = clock64();
-  for (int j = 0; j < 64; ++j) {
-    if (prof && tid == 0 && j == 10) prof[10] = clock64();
-    if (s_fail) break;
-    const double inv = s_inv, sq = s_sq;
-    const int jt = j & 15, ja = j >> 4;
-    if (tx == jt) {
+  const double defic = 1.0000001e-24 * s_tr;
+  for (int p = 0; p < 8; ++p) {
+    const int c0 = 8 * p;
+    if (warp == 0) {
+      double pv[2][8];
+      const int r0 = c0 + lane, r1 = c0 + lane + 32;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = ty + 16 * a;
-        double v = 0.0;
+      for (int jj = 0; jj < 8; ++jj) {
+        pv[0][jj] = r0 < 64 ? Ls[r0 * LD + c0 + jj] : 0.0;
+        pv[1][jj] = r1 < 64 ? Ls[r1 * LD + c0 + jj] : 0.0;
+      }
+      int fail = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (b == ja) {
-            const double sc = w[a][b] * inv;
-            v = (i > j) ? sc : 0.0;
-            w[a][b] = (i > j) ? sc : ((i == j) ? sq : w[a][b]);
-          }
+      for (int jj = 0; jj < 8; ++jj) {
+        const int cj = c0 + jj;
+        const double d = __shfl_sync(0xffffffffu, pv[0][jj], jj);
+        if (cj < k && (!(d > pivot_rel * dg[cj]) || !(d > defic))) {
+          fail = cj + 1;
+          break;
         }
-        colL[i] = v;
-      }
-    }
-    if (ty == jt) {
+        const double y = fast_rsqrt(d), sq = d * y;
+        // column jj of L (rows above the pivot are not part of L)
+        pv[0][jj] = lane > jj ? pv[0][jj] * y : (lane == jj ? sq : 0.0);
+        pv[1][jj] = pv[1][jj] * y;
+        if (lane == 0) s_invd[cj] = y;
+        // rank-1 update of the panel's remaining columns: L[r][jj] L[c0 + jn][jj]
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int c = tx + 16 * b;
-        double v = 0.0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          if (a == ja) {
-            const double sc = x[a][b] * inv;
-            x[a][b] = sc;
-            v = (c <= j) ? sc : 0.0;
-          }
+        for (int jn = jj + 1; jn < 8; ++jn) {
+          const double lc = __shfl_sync(0xffffffffu, pv[0][jj], jn);
+          pv[0][jn] = fma(-pv[0][jj], lc, pv[0][jn]);
+          pv[1][jn] = fma(-pv[1][jj], lc, pv[1][jn]);
         }
-        rowX[c] = v;
       }
-    }
-    if (prof && tid == 0 && j == 10) prof[11] = clock64();
-    __syncthreads();
-    if (prof && tid == 0 && j == 10) prof[12] = clock64();
-    double li[4], lc[4], xr[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) li[a] = colL[ty + 16 * a];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      lc[b] = colL[tx + 16 * b];
-      xr[b] = rowX[tx + 16 * b];
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        w[a][b] = fma(-li[a], lc[b], w[a][b]);  // only j < c, i touched (else a factor is 0)
-        x[a][b] = fma(-li[a], xr[b], x[a][b]);  // only i > j, c <= j touched
-      }
-    if (prof && tid == 0 && j == 10) prof[13] = clock64();
-    // next pivot W[j+1][j+1] lives with thread (ty, tx) = ((j+1) & 15, (j+1) & 15)
-    const int jn = j + 1;
-    if (jn < 64 && ty == (jn & 15) && tx == (jn & 15)) {
-      const int an = jn >> 4;
-      double d = 0.0;
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-        if (a == an) d = w[a][a];
-      if (!(d > pivot_rel * dg[jn]) || !(d > deficient_sq)) {
-        if (jn < k) s_fail = jn + 1;
-        else { s_sq = 1.0; s_inv = 1.0; }  // padded identity tail
+      if (fail) {
+        if (lane == 0) s_fail = fail;
       } else {
-        const double y = fast_rsqrt(d);
-        s_inv = y;
-        s_sq = d * y;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          if (r0 < 64) Ls[r0 * LD + c0 + jj] = pv[0][jj];
+          if (r1 < 64) Ls[r1 * LD + c0 + jj] = pv[1][jj];
+        }
       }
     }
-    if (prof && ty == 11 && tx == 11 && j == 10) prof[14] = clock64();
     __syncthreads();
-    if (prof && tid == 0 && j == 10) prof[15] = clock64();
-  }
-  if (prof && tid == 0) prof[1] = clock64();
-  if (s_fail) {
-    if (tid == 0) atomicCAS(status, 0, s_fail);
-    return;
-  }
-  // R = L^T, Rinv = X^T
+    if (s_fail) {
+      if (tid == 0) atomicCAS(status, 0, s_fail);
+      return;
+    }
+    // trailing update W[r][c] -= sum_jj L[r][c0+jj] L[c][c0+jj], r, c >= c0 + 8 (full square)
+    const int t0 = c0 + 8, m = 64 - t0;
+    if (m > 0) {
+      const int rl = tid >> 2, cg = tid & 3;
+      if (rl < m) {
+        const int r = t0 + rl;
+        double lr[8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+        for (int jj = 0; jj < 8; ++jj) lr[jj] = Ls[r * LD + c0 + jj];
+        for (int cl = cg; cl < m; cl += 8) {  // two columns per pass: independent chains
+          const int c = t0 + cl, c2 = c + 4;
+          const bool two = cl + 4 < m;
+          double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = ty + 16 * a, c = tx + 16 * b;
-      if (i < k && c < k) {
-        R[c * k + i] = (c <= i) ? w[a][b] : 0.0;
-        Rinv[c * k + i] = (c <= i) ? x[a][b] : 0.0;
+          for (int jj = 0; jj < 8; jj += 2) {
+            a0 = fma(lr[jj], Ls[c * LD + c0 + jj], a0);
+            a1 = fma(lr[jj + 1], Ls[c * LD + c0 + jj + 1], a1);
+            if (two) {
+              b0 = fma(lr[jj], Ls[c2 * LD + c0 + jj], b0);
+              b1 = fma(lr[jj + 1], Ls[c2 * LD + c0 + jj + 1], b1);
+            }
+          }
+          Ls[r * LD + c] -= a0 + a1;
+          if (two) Ls[r * LD + c2] -= b0 + b1;
+        }
       }
     }
+    __syncthreads();
+  }
+  // ---- X = L^-1: diagonal blocks (warp w inverts block w; lane c < 8 owns column c) ---------
+  {
+    const int b0 = 8 * warp;
+    if (lane < 8) {
+      const int c = lane;
+      double xc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double acc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int mm = 0; mm < i; ++mm) acc = fma(-Ls[(b0 + i) * LD + b0 + mm], xc[mm], acc);
+        xc[i] = i < c ? 0.0 : acc * s_invd[b0 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Xs[(b0 + i) * LD + b0 + c] = xc[i];
+    }
+  }
+  __syncthreads();
+  // block rows i = 1..7: T_ij = sum_{m=j}^{i-1} L_im X_mj, then X_ij = -X_ii T_ij (j < i)
+  for (int bi = 1; bi < 8; ++bi) {
+    const int r0 = 8 * bi, ncol = 8 * bi;  // columns 0 .. 8 bi - 1 of block row bi
+    // T (8 rows x ncol columns): thread per entry
+    for (int e = tid; e < 8 * ncol; e += 256) {
+      const int rr = e / ncol, cc = e % ncol;  // cc in block bj = cc / 8
+      const int mstart = cc & ~7;  // a multiple of 8, as is r0: whole 8-blocks of the sum
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* lrow = Ls + (r0 + rr) * LD;
+      for (int mm = mstart; mm < r0; mm += 4) {  // 4 independent chains
+        a0 = fma(lrow[mm], Xs[mm * LD + cc], a0);
+        a1 = fma(lrow[mm + 1], Xs[(mm + 1) * LD + cc], a1);
+        a2 = fma(lrow[mm + 2], Xs[(mm + 2) * LD + cc], a2);
+        a3 = fma(lrow[mm + 3], Xs[(mm + 3) * LD + cc], a3);
+      }
+      T[rr * 64 + cc] = (a0 + a1) + (a2 + a3);
+    }
+    __syncthreads();
+    for (int e = tid; e < 8 * ncol; e += 256) {
+      const int rr = e / ncol, cc = e % ncol;
+      double acc = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < 8; ++mm) acc = fma(Xs[(r0 + rr) * LD + r0 + mm], T[mm * 64 + cc], acc);
+      Xs[(r0 + rr) * LD + cc] = -acc;
+    }
+    __syncthreads();
+  }
+  // R = L^T, Rinv = X^T (upper triangular), k x k
+  for (int e = tid; e < k * k; e += 256) {
+    const int r = e / k, c = e % k;  // output row r, column c
+    R[e] = (c >= r) ? Ls[c * LD + r] : 0.0;
+    Rinv[e] = (c >= r) ? Xs[c * LD + r] : 0.0;
+  }
 }
 
 __host__ __device__ inline size_t chol_scratch_doubles(int k) {
