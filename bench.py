@@ -257,7 +257,11 @@ def run_ours(args, rank, world, local_rank):
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
     launches = ctx.kernel_launches() - launches0
-    phases = [ctx.phase_stats(i) for i in range(8)]
+    phases = [ctx.phase_stats(i) for i in range(16)]
+    if os.environ.get("WSSR_FINE_PHASES") == "1":  # profiling: CholeskyQR2 pieces, us per call
+        print(json.dumps({n: round(1e3 * phases[i]["ms"] / max(phases[i]["launches"], 1), 1)
+                          for i, n in zip(range(8, 14), ["gram1", "chol1", "trmm1", "gram2",
+                                                         "chol2", "trmm2"])}), file=sys.stderr)
     ctx.set_timing(False)
     step_ms = sum(x.elapsed_time(y) for x, y in intervals)
     t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
@@ -315,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
             **{name: phases[i]["ms"] / args.steps for i, name in enumerate(
                 ["v_passes", "u_passes", "assemble_colstats", "cholqr2_Pxk",
                  "ssi_quotient_residual", "drift", "precond_and_refresh", "qr_v_and_sort"])},
-            other=ms_per_step - sum(ph["ms"] for ph in phases) / args.steps),
+            other=ms_per_step - sum(ph["ms"] for ph in phases[:8]) / args.steps),
         "step": {
             "flops_alg": flops_alg, "bytes_alg": bytes_alg, "ssi_iterations": m_avg,
             "t_roof_ms": bytes_alg / (hbm_peak * 1e9 * world) * 1e3,

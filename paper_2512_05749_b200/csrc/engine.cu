@@ -136,7 +136,7 @@ struct PhaseTimer {
   double flops, bytes;
   cudaEvent_t a = nullptr;
   PhaseTimer(Context& c, int ph, double f, double b) : ctx(c), phase(ph), flops(f), bytes(b) {
-    if (ctx.timing) {
+    if (ctx.timing && ph >= 0) {
       a = take_event(ctx);
       WSSR_CUDA(cudaEventRecord(a, ctx.stream));
     }
@@ -336,12 +336,14 @@ void cholqr2(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda
   Buf G((size_t)k * k, ctx.stream), R1((size_t)k * k, ctx.stream), R1i((size_t)k * k, ctx.stream),
       R2((size_t)k * k, ctx.stream), R2i((size_t)k * k, ctx.stream),
       T((size_t)rows * k, ctx.stream);
-  gram(ctx, rows, k, A, lda, G, distributed);
-  chol_inv(ctx, G, (int)k, R1, R1i, status);
-  mul_small(ctx, rows, k, A, lda, R1i, true, T, k);
-  gram(ctx, rows, k, T, k, G, distributed);
-  chol_inv(ctx, G, (int)k, R2, R2i, status);
-  mul_small(ctx, rows, k, T, k, R2i, true, Q, ldq);
+  const bool fine = ctx.fine_phases && ctx.timing;
+  auto sub = [&](int ph) { return std::make_unique<PhaseTimer>(ctx, fine ? ph : -1, 0.0, 0.0); };
+  { auto t = sub(8); gram(ctx, rows, k, A, lda, G, distributed); }
+  { auto t = sub(9); chol_inv(ctx, G, (int)k, R1, R1i, status); }
+  { auto t = sub(10); mul_small(ctx, rows, k, A, lda, R1i, true, T, k); }
+  { auto t = sub(11); gram(ctx, rows, k, T, k, G, distributed); }
+  { auto t = sub(12); chol_inv(ctx, G, (int)k, R2, R2i, status); }
+  { auto t = sub(13); mul_small(ctx, rows, k, T, k, R2i, true, Q, ldq); }
   if (R) {  // R = R2 R1 (only the callers that read R ask for it)
     launch_pdl(triu_mul_kernel, blocks_for(k * k, 256, 1 << 20), 256, 0, ctx.stream, R2, R1, (int)k, R);
     post_launch(ctx);
@@ -1457,6 +1459,11 @@ int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const 
   return guarded(ctx, [&] {
     Context& c = ctx->c;
     if (!ts_supported(k) || rows < 0) throw Fail{WSSR_ERR_VALUE, "tall-skinny: k must be 32 or 64"};
+    static const int reps = [] {
+      const char* e = std::getenv("WSSR_DEBUG_REPS");  // profiling: back-to-back launches
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    for (int rep = 0; rep < reps; ++rep)
     switch (op) {
       case 0: WSSR_CUDA(ts_gram(c, rows, k, a, k, out)); break;
       case 1: WSSR_CUDA(ts_cross(c, rows, k, a, k, b, k, out)); break;
@@ -1480,6 +1487,10 @@ int wssr_set_aux_stream(wssr_ctx* ctx, void* stream) {
 int wssr_set_timing(wssr_ctx* ctx, int enabled) {
   if (!ctx) return WSSR_ERR_VALUE;
   ctx->c.timing = enabled != 0;
+  {
+    const char* e = std::getenv("WSSR_FINE_PHASES");  // profiling only
+    ctx->c.fine_phases = e && e[0] == '1';
+  }
   for (int i = 0; i < Context::kPhases; ++i) {
     ctx->c.phase_ms[i] = ctx->c.phase_flops[i] = ctx->c.phase_bytes[i] = 0.0;
     ctx->c.phase_count[i] = 0;

@@ -52,7 +52,10 @@ struct Context {
   // optional per-phase timing of the O-passes (CUDA events on the launching stream)
   // 0: v = Ohat^T q, 1: u = Ohat v, 2: assemble column pass, 3: CholeskyQR2 of P x k blocks,
   // 4: SSI quotient + residual, 5: drift, 6: preconditioner + state refresh, 7: QR(v) + sort
-  static constexpr int kPhases = 8;
+  // 8-15 (WSSR_FINE_PHASES=1, profiling): CholeskyQR2 pieces - Gram 1, chol 1, TRMM 1, Gram 2,
+  // chol 2, TRMM 2, triu product, other
+  static constexpr int kPhases = 16;
+  bool fine_phases = false;
   bool timing = false;
   struct PendingEvent {
     int phase;

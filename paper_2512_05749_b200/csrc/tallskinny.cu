@@ -68,10 +68,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += kRowStep) {
-    double fa[U][NB], fb[U][NJ];
+  // two-stage register pipeline: the fragments of the next 8 rows are in flight while the DMMAs
+  // of the current 8 run (a load stall would otherwise open every iteration)
+  constexpr int H = U / 2;  // k-steps per stage
+  auto load = [&](int64_t r0, double (&fa)[H][NB], double (&fb)[H][NJ]) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < H; ++u) {
       const int64_t r = r0 + 4 * u + t;
       const bool ok = r < r_end;
       const double* pa = A + (ok ? r : 0) * lda + g;
@@ -83,8 +85,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int b = 0; b < NJ; ++b) fb[u][b] = ok ? pb[8 * b] : 0.0;
       }
     }
+  };
+  auto compute = [&](const double (&fa)[H][NB], const double (&fb)[H][NJ]) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < H; ++u)
 #pragma unroll
       for (int i = 0; i < NB; ++i)
 #pragma unroll
@@ -92,6 +96,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (SYM && j < i) continue;
           dmma884(acc[i][j], fa[u][i], SYM ? fa[u][j] : fb[u][j]);
         }
+  };
+  double fa0[H][NB], fb0[H][NJ], fa1[H][NB], fb1[H][NJ];
+  load(r_begin, fa0, fb0);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kRowStep) {
+    load(r0 + 4 * H, fa1, fb1);
+    compute(fa0, fb0);
+    load(r0 + kRowStep, fa0, fb0);
+    compute(fa1, fb1);
   }
 
   // CTA reduction over the row groups, in group order (deterministic)
@@ -129,23 +141,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 // C[i][j] = sum over slabs in slab order; SYM mirrors the upper tiles.  Block: 32 consecutive
 // entries x 8 slab groups.
 template <int KC, bool SYM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     gram_finish_kernel(const double* __restrict__ slabs, int nslab, double* __restrict__ C,
                        int64_t ldc) {
   pdl_wait();
-  __shared__ double part[8][33];
+  __shared__ double part[16][33];
   const int jj = threadIdx.x & 31, sg = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + jj;  // entry (row-major KC x KC)
   const int i = e / KC, j = e % KC;
   const int src = (SYM && (j >> 3) < (i >> 3)) ? j * KC + i : e;
-  double s = 0.0;
-  for (int c = sg; c < nslab; c += 8) s += slabs[(size_t)c * KC * KC + src];
-  part[sg][jj] = s;
+  double s0 = 0.0, s1 = 0.0;
+  int c = sg;
+  for (; c + 16 < nslab; c += 32) {
+    s0 += slabs[(size_t)c * KC * KC + src];
+    s1 += slabs[(size_t)(c + 16) * KC * KC + src];
+  }
+  if (c < nslab) s0 += slabs[(size_t)c * KC * KC + src];
+  part[sg][jj] = s0 + s1;
   __syncthreads();
   if (sg == 0) {
     double tot = part[0][jj];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) tot += part[q][jj];
+    for (int q = 1; q < 16; ++q) tot += part[q][jj];
     C[(int64_t)i * ldc + j] = tot;
   }
 }
@@ -158,7 +175,7 @@ __global__ void __launch_bounds__(256)
 enum Mode : int { kStore = 0, kAddStore = 1, kAddSumsq = 2 };
 
 template <int KC, bool TRI, int MODE>
-__global__ void __launch_bounds__(kThreads, KC == 64 ? 1 : 2)
+__global__ void __launch_bounds__(kThreads, 1)
     mul_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ M,
                int64_t ldm, double alpha, const double* __restrict__ Cin, int64_t ldcin,
                double* __restrict__ Y, int64_t ldy, int64_t rows, double* __restrict__ partial) {
@@ -178,17 +195,26 @@ __global__ void __launch_bounds__(kThreads, KC == 64 ? 1 : 2)
   double ss = 0.0;
   const int64_t nblk = (rows + 15) / 16;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t blk = gw; blk < nblk; blk += nw) {
-    const int64_t r0 = blk * 16;
-    double2 a[2][NB];
+  // the next block's A fragments are loaded while this block's DMMAs run
+  auto load = [&](int64_t blk, double2 (&a)[2][NB]) {
 #pragma unroll
     for (int mb = 0; mb < 2; ++mb) {
-      const int64_t r = r0 + 8 * mb + g;
-      const bool ok = r < rows;
+      const int64_t r = blk * 16 + 8 * mb + g;
+      const bool ok = blk < nblk && r < rows;
       const double* pa = A + (ok ? r : 0) * lda + 2 * t;
 #pragma unroll
       for (int jp = 0; jp < NB; ++jp) a[mb][jp] = ok ? ld2(pa + 8 * jp) : make_double2(0.0, 0.0);
     }
+  };
+  double2 a[2][NB], an[2][NB];
+  load(gw, an);
+  for (int64_t blk = gw; blk < nblk; blk += nw) {
+    const int64_t r0 = blk * 16;
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int jp = 0; jp < NB; ++jp) a[mb][jp] = an[mb][jp];
+    load(blk + nw, an);
     double acc[2][NB][2];
 #pragma unroll
     for (int mb = 0; mb < 2; ++mb)
@@ -256,16 +282,16 @@ __global__ void __launch_bounds__(256)
   const int j = blockIdx.y * cw + c;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = min(rows, r0 + rows_per_block);
-  double s0 = 0.0, s1 = 0.0;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (j < n) {
     int64_t r = r0 + rl;
-    for (; r + lanes < r1; r += 2 * lanes) {
-      s0 = fma(A[r * lda + j], x[r], s0);
-      s1 = fma(A[(r + lanes) * lda + j], x[r + lanes], s1);
+    for (; r + 7 * lanes < r1; r += 8 * lanes) {  // 8 independent loads in flight per thread
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[q] = fma(A[(r + q * lanes) * lda + j], x[r + q * lanes], s[q]);
     }
-    if (r < r1) s0 = fma(A[r * lda + j], x[r], s0);
+    for (; r < r1; r += lanes) s[0] = fma(A[r * lda + j], x[r], s[0]);
   }
-  red[threadIdx.x] = s0 + s1;
+  red[threadIdx.x] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
   __syncthreads();
   if (rl == 0 && j < n) {
     double t = red[c];
@@ -274,14 +300,17 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void gemv_t_finish_kernel(const double* __restrict__ partial, int nblk, int n,
-                                     double alpha, double* __restrict__ out) {
+// out[j] = alpha sum_b partial[b][j]: one block per output, fixed-order block reduction
+__global__ void __launch_bounds__(128)
+    gemv_t_finish_kernel(const double* __restrict__ partial, int nblk, int n, double alpha,
+                         double* __restrict__ out) {
   pdl_wait();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+  __shared__ double scratch[32];
+  const int j = blockIdx.x;
   double t = 0.0;
-  for (int b = 0; b < nblk; ++b) t += partial[(size_t)b * n + j];
-  out[j] = alpha * t;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) t += partial[(size_t)b * n + j];
+  t = block_sum(t, scratch);
+  if (threadIdx.x == 0) out[j] = alpha * t;
 }
 
 template <int KC, bool SYM>
@@ -296,7 +325,7 @@ cudaError_t gram_launch(Context& ctx, int64_t rows, const double* A, int64_t lda
   double* slabs = ctx.splitk_buffer((size_t)grid * KC * KC);
   if (!slabs) return cudaErrorMemoryAllocation;
   launch_pdl(gram_kernel<KC, SYM>, grid, kThreads, 0, ctx.stream, A, lda, B, ldb, rows, rpc, slabs);
-  launch_pdl(gram_finish_kernel<KC, SYM>, KC * KC / 32, 256, 0, ctx.stream, slabs, grid, C, ldc);
+  launch_pdl(gram_finish_kernel<KC, SYM>, KC * KC / 32, 512, 0, ctx.stream, slabs, grid, C, ldc);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
 }
@@ -337,14 +366,14 @@ cudaError_t ts_gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, in
   const int cw = n >= 256 ? 256 : (n > 128 ? 256 : (n > 64 ? 128 : (n > 32 ? 64 : 32)));
   const int ycols = (int)((n + cw - 1) / cw);
   const int64_t lanes = 256 / cw;
-  int nblk = (int)std::min<int64_t>(2 * ctx.num_sms, std::max<int64_t>(1, rows / (8 * lanes)));
+  int nblk = (int)std::min<int64_t>(4 * ctx.num_sms, std::max<int64_t>(1, rows / (16 * lanes)));
   const int64_t rpb = (rows + nblk - 1) / nblk;
   nblk = (int)((rows + rpb - 1) / rpb);
   double* partial = ctx.splitk_buffer((size_t)nblk * n);
   if (!partial) return cudaErrorMemoryAllocation;
   launch_pdl(ts::gemv_t_kernel, dim3(nblk, ycols), 256, 0, ctx.stream, A, lda, x, rows, (int)n, cw, rpb,
                                                               partial);
-  launch_pdl(ts::gemv_t_finish_kernel, (unsigned)((n + 127) / 128), 128, 0, ctx.stream, 
+  launch_pdl(ts::gemv_t_finish_kernel, (unsigned)n, 128, 0, ctx.stream, 
       partial, nblk, (int)n, alpha, out);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
