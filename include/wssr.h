@@ -120,6 +120,8 @@ int wssr_dmma_peak_probe(wssr_ctx* ctx, double* tflops);
 /* 128-byte ncclUniqueId produced on rank 0 and broadcast by the caller (torch.distributed). */
 int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]);
 int wssr_nccl_attach(wssr_ctx* ctx, const unsigned char id[128], int rank, int world);
+/* (world == 1 builds a 1-rank communicator: the engine stays unsharded and wssr_allreduce_f64
+ * then exercises the NCCL transport itself.) */
 
 /* Thread-emulated communicator for testing the sharded engine on one GPU: `world` host threads,
  * each with its own context and stream, attach to one group; collectives synchronise on the host

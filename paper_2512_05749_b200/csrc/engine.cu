@@ -1223,8 +1223,13 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
 }
 
 // ---- NCCL (dlopen'd so the library has no link-time NCCL dependency) ------------------------
-typedef int (*nccl_get_id_fn)(void*);
-typedef int (*nccl_init_rank_fn)(void**, int, const void*, int);
+// ncclUniqueId is a 128-byte struct that ncclCommInitRank takes BY VALUE (nccl.h):
+//   ncclResult_t ncclCommInitRank(ncclComm_t*, int nranks, ncclUniqueId commId, int rank);
+struct NcclUniqueId {
+  char internal[128];
+};
+typedef int (*nccl_get_id_fn)(NcclUniqueId*);
+typedef int (*nccl_init_rank_fn)(void**, int, NcclUniqueId, int);
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*nccl_destroy_fn)(void*);
 
@@ -1538,7 +1543,9 @@ int wssr_dmma_peak_probe(wssr_ctx* ctx, double* tflops) {
 int wssr_nccl_unique_id(wssr_ctx* ctx, unsigned char out_id[128]) {
   return guarded(ctx, [&] {
     if (!g_nccl.load()) throw Fail{WSSR_ERR_NCCL, "libnccl.so.2 not loadable"};
-    if (g_nccl.get_id(out_id) != 0) throw Fail{WSSR_ERR_NCCL, "ncclGetUniqueId failed"};
+    NcclUniqueId uid;
+    if (g_nccl.get_id(&uid) != 0) throw Fail{WSSR_ERR_NCCL, "ncclGetUniqueId failed"};
+    std::memcpy(out_id, uid.internal, sizeof(uid.internal));
   });
 }
 
@@ -1547,12 +1554,15 @@ int wssr_nccl_attach(wssr_ctx* ctx, const unsigned char id[128], int rank, int w
     if (world < 1 || rank < 0 || rank >= world) throw Fail{WSSR_ERR_VALUE, "bad rank/world"};
     delete ctx->c.comm;
     ctx->c.comm = nullptr;
-    if (world == 1) return;
+    // world == 1 builds a 1-rank communicator: the engine treats it as unsharded (world() == 1)
+    // and wssr_allreduce_f64 exercises the transport
     if (!g_nccl.load()) throw Fail{WSSR_ERR_NCCL, "libnccl.so.2 not loadable"};
     auto* cm = new NcclComm();
     cm->rank = rank;
     cm->world = world;
-    if (g_nccl.init_rank(&cm->comm, world, id, rank) != 0) {
+    NcclUniqueId uid;
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    if (g_nccl.init_rank(&cm->comm, world, uid, rank) != 0) {
       delete cm;
       throw Fail{WSSR_ERR_NCCL, "ncclCommInitRank failed"};
     }
@@ -1598,7 +1608,11 @@ int wssr_emu_attach(wssr_ctx* ctx, void* group, int rank) {
 int wssr_allreduce_f64(wssr_ctx* ctx, double* buf, int64_t n) {
   return guarded(ctx, [&] {
     if (n < 0 || (n > 0 && !buf)) throw Fail{WSSR_ERR_VALUE, "bad buffer"};
-    if (ctx->c.world() > 1 && n > 0) allreduce(ctx->c, buf, (size_t)n);
+    if (n == 0 || !ctx->c.comm) return;
+    // also with a 1-rank communicator (a self-test of the transport)
+    if (ctx->c.comm->allreduce_sum(buf, (size_t)n, ctx->c.stream) != cudaSuccess)
+      throw Fail{WSSR_ERR_NCCL, "allreduce failed"};
+    sync(ctx->c);
   });
 }
 
