@@ -470,6 +470,7 @@ struct Ohat {
   // the pre-digitised sample block (in the context's plane buffer), built on first use
   struct Planes {
     const int8_t* ptr = nullptr;
+    int64_t rows = 0;  // planes cover samples [0, rows); the rest is digitised on the fly
   };
   mutable std::shared_ptr<Planes> oz_planes;
   int64_t cols() const { return r + n; }
@@ -496,6 +497,30 @@ bool ensure_planes(Context& ctx, size_t bytes) {
   return true;
 }
 
+// Samples whose digit planes the step keeps (a multiple of 128, or all of them): every sample
+// when the planes fit next to the step's workspace (16 P x k blocks + 2 GiB), else as many as
+// HBM allows (c2/c3: the 7-byte planes of 16384 x 2^20 samples are 120 GB), 0 below 1024.
+int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
+  const size_t full = ozaki_planes_bytes(o.n, o.P);
+  const size_t margin = ((size_t)2 << 30) + (size_t)16 * o.P * std::max<int64_t>(k, 1) * 8;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const size_t have = free_b + ctx.oz_planes_cap;
+  const size_t avail = have > margin ? have - margin : 0;
+  // testing only: cap the planes at WSSR_OZ_PLANE_ROWS samples (exercises the split passes)
+  const char* cap_env = std::getenv("WSSR_OZ_PLANE_ROWS");
+  const int64_t cap = cap_env ? std::max<int64_t>(0, std::atoll(cap_env)) / 128 * 128 : -1;
+  if (full <= avail && (cap < 0 || cap >= o.n)) return ensure_planes(ctx, full) ? o.n : 0;
+  int64_t rows = (int64_t)(avail / ozaki_planes_bytes(128, o.P)) * 128;
+  if (cap >= 0) rows = std::min(rows, cap);
+  else if (rows < 1024) return 0;
+  if (rows <= 0) return 0;
+  return ensure_planes(ctx, ozaki_planes_bytes(rows, o.P)) ? rows : 0;
+}
+
 // O-pass GEMMs over the sample block in its storage type
 void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t N, int64_t K,
                   const double* B, int64_t ldb, double* C, int64_t ldc, double alpha) {
@@ -512,26 +537,50 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
     }
     const int8_t* planes = nullptr;
     int8_t* store = nullptr;
+    int64_t n_pl = 0;  // samples covered by planes (or by the store of this first pass)
     if (ctx.oz_pre == 0) {
       if (!o.oz_planes) {
         o.oz_planes = std::make_shared<Ohat::Planes>();
-        const size_t bytes = ozaki_planes_bytes(o.n, o.P);
-        if (ensure_planes(ctx, bytes)) {
+        n_pl = plan_plane_rows(ctx, o, N);
+        if (n_pl > 0) {
           if (layout == Layout::RM) {
             // the first pass (v = Ohat^T q) digitises on the fly and writes the planes
             store = ctx.oz_planes;
           } else {
-            WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, ctx.oz_planes,
+            WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, n_pl, o.P, tab, ctx.oz_planes,
                                      ctx.stream));
             planes = ctx.oz_planes;
           }
           o.oz_planes->ptr = ctx.oz_planes;
+          o.oz_planes->rows = n_pl;
         }
-      } else {
+      } else if (o.oz_planes->ptr) {
         planes = o.oz_planes->ptr;
+        n_pl = o.oz_planes->rows;
       }
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store));
+    if (n_pl == 0 || n_pl >= o.n) {
+      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store));
+      return;
+    }
+    // planes for samples [0, n_pl), on-the-fly digits for the rest
+    const size_t es = o.f32 ? 4 : 8;
+    const double* tail = reinterpret_cast<const double*>(
+        reinterpret_cast<const char*>(o.samp) + (size_t)n_pl * o.lds * es);
+    GemmArgs a1 = a, a2 = a;
+    a2.A = tail;
+    if (layout == Layout::RM) {  // M = samples: disjoint rows of C
+      a1.M = n_pl;
+      a2.M = o.n - n_pl;
+      a2.C = C + n_pl * ldc;
+    } else {                     // K = samples: the second part accumulates
+      a1.K = n_pl;
+      a2.K = o.n - n_pl;
+      a2.B = B + n_pl * ldb;
+      a2.accumulate = 1;
+    }
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a2, o.f32, tab, ctx.stream, nullptr, nullptr));
     return;
   }
   if (o.f32) {
