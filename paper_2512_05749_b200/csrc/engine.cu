@@ -518,7 +518,11 @@ int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
   if (cap >= 0) rows = std::min(rows, cap);
   else if (rows < 1024) return 0;
   if (rows <= 0) return 0;
-  return ensure_planes(ctx, ozaki_planes_bytes(rows, o.P)) ? rows : 0;
+  const bool ok = ensure_planes(ctx, ozaki_planes_bytes(rows, o.P));
+  if (std::getenv("WSSR_VERBOSE"))
+    std::fprintf(stderr, "[wssr] digit planes for %lld of %lld samples (%s; free %.1f GB)\n",
+                 (long long)rows, (long long)o.n, ok ? "ok" : "alloc failed", free_b / 1e9);
+  return ok ? rows : 0;
 }
 
 // O-pass GEMMs over the sample block in its storage type

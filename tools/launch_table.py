@@ -1,5 +1,6 @@
-"""Print the per-launch list (and per-kernel totals) of an ncu --metrics gpu__time_duration.sum
-CSV log: python tools/launch_table.py gpurun_out/launches.csv [last_n]"""
+"""Per-kernel totals of an ncu --metrics gpu__time_duration.sum CSV log, over the last WSSR step
+(from its energy_stats launch) and over the whole run; optionally the last N launches.
+python tools/launch_table.py gpurun_out/launches.csv [last_n]"""
 import collections
 import csv
 import sys
@@ -13,14 +14,28 @@ last = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 if last:
     for i, k, v in data[-last:]:
         print(f"{i:>5} {v / 1000:9.1f} us  {k[:90]}")
+def totals(seq, title):
+    tot = collections.defaultdict(lambda: [0.0, 0])
+    for _, k, v in seq:
+        if k.startswith("void at::") or "at::native" in k:
+            continue
+        key = k.split("(")[0][:80]
+        tot[key][0] += v
+        tot[key][1] += 1
+    print(f"---- {title} ----")
+    for k, (v, n) in sorted(tot.items(), key=lambda x: -x[1][0]):
+        print(f"{v / 1000:9.1f} us n={n:4d}  {k}")
+    print(f"sum {sum(v for v, _ in tot.values()) / 1000:.1f} us")
+
+
+starts = [i for i, (_, k, _) in enumerate(data) if "energy_stats" in k]
+if starts:
+    totals(data[starts[-1]:], "last step (cold caches, serialised: compare shares)")
 tot = collections.defaultdict(lambda: [0.0, 0])
-for _, k, v in data:
+for _, k, v in []:
     if k.startswith("void at::") or "at::native" in k:
         continue
     key = k.split("(")[0][:80]
     tot[key][0] += v
     tot[key][1] += 1
-print("---- totals (ours) ----")
-for k, (v, n) in sorted(tot.items(), key=lambda x: -x[1][0]):
-    print(f"{v / 1000:9.1f} us n={n:4d}  {k}")
-print(f"sum {sum(v for v, _ in tot.values()) / 1000:.1f} us")
+totals(data, "whole run (ours)")
