@@ -132,7 +132,7 @@ def _positive_prefix(sigma, limit):
 def exact_truncated_svd(ohat, rank):
     """Dense SVD truncated to the leading triplets, exact zeros dropped (svdengine.py:75-85).
 
-    Device path for min(m, n) <= 512 (linalg.exact_svd); larger problems raise Unsupported.
+    Device path: libwssr's QR + Jacobi for min(m, n) <= 512, cuSOLVER above (linalg.exact_svd).
     """
     from .linalg import exact_svd
 
