@@ -353,8 +353,13 @@ def run_ours(args, rank, world, local_rank):
         O_d = [torch.empty(rows, P, dtype=wl.O.dtype, device=dev) for _ in range(nbuf)]
         E_d = [torch.empty(rows, dtype=torch.float64, device=dev) for _ in range(nbuf)]
         copy_stream = torch.cuda.Stream(dev) if pipelined else stream
+        # the batch is uploaded in row chunks on several copy streams (several copy engines
+        # in flight over PCIe); WSSR_E2E_SPLIT overrides the count
+        nsplit = max(1, int(os.environ.get("WSSR_E2E_SPLIT", "2"))) if pipelined else 1
+        copy_streams = [copy_stream] + [torch.cuda.Stream(dev) for _ in range(nsplit - 1)]
         ready = [torch.cuda.Event() for _ in range(nbuf)]
         freed = [torch.cuda.Event() for _ in range(nbuf)]
+        chunk_done = [torch.cuda.Event() for _ in range(nsplit)]
         del O, E
         torch.cuda.synchronize()
         barrier()
@@ -364,12 +369,20 @@ def run_ours(args, rank, world, local_rank):
 
         def upload(t):
             i = t % nbuf
-            with torch.cuda.stream(copy_stream):
-                if pipelined:
-                    copy_stream.wait_event(freed[i])
-                O_d[i].copy_(O_h[i], non_blocking=True)
-                E_d[i].copy_(E_h[i], non_blocking=True)
-                ready[i].record(copy_stream)
+            bounds = [rows * c // nsplit for c in range(nsplit + 1)]
+            for c, cs in enumerate(copy_streams):
+                with torch.cuda.stream(cs):
+                    if pipelined:
+                        cs.wait_event(freed[i])
+                    O_d[i][bounds[c]:bounds[c + 1]].copy_(O_h[i][bounds[c]:bounds[c + 1]],
+                                                           non_blocking=True)
+                    if c == 0:
+                        E_d[i].copy_(E_h[i], non_blocking=True)
+                    if c > 0:
+                        chunk_done[c].record(cs)
+            for c in range(1, nsplit):
+                copy_stream.wait_event(chunk_done[c])
+            ready[i].record(copy_stream)
 
         for i in range(nbuf):
             freed[i].record(stream)
@@ -396,7 +409,7 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": rows * P * esize + rows * 8,  # O and E; theta once
                "h2d_bytes_once": P * 8,
                "d2h_bytes_per_step": P * 8, "steps": e2e_steps,
-               "pipelined_upload": pipelined,
+               "pipelined_upload": pipelined, "upload_streams": nsplit,
                "path": "estimators.assemble + optimizers.wssr_step on batches uploaded from pinned "
                        "host memory every step (the next batch's upload overlapping the current "
                        "step when two device copies fit); theta' read back to the host every "
