@@ -179,6 +179,24 @@ class Context:
         self.rank = 0
         self.world = 1
         self._aux = None
+        self._pinned = None
+        self._pinned_next = 0
+
+    def pinned_slot(self, n: int):
+        """n float64 of pinned host memory for stream-ordered device->host scalars.  Slots come
+        from a context-owned ring (never handed back to torch's host allocator), so a copy still
+        in flight can never land in memory that was reused for something else; a slot is
+        recycled only 4096 requests later (~2000 steps), long after its copy completed; the
+        holders (bundle scalars, drift telemetry) copy their values out on first read, and
+        wssr_step reads the bundle's as soon as they have landed."""
+        import torch
+
+        if self._pinned is None:
+            self._pinned = torch.empty(4096 * 8, dtype=torch.float64, pin_memory=True)
+        assert n <= 8
+        i = self._pinned_next
+        self._pinned_next = (i + 1) % 4096
+        return self._pinned[8 * i:8 * i + n]
 
     def aux_stream(self):
         """Side stream for the step's asynchronous drift telemetry (created on first use)."""

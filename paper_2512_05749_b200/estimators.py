@@ -206,7 +206,7 @@ def assemble(batch, clip_n_std=5.0):
     # single rank: the host scalars arrive asynchronously (no wait on the column pass, so the
     # optimizer step that follows is enqueued while the device is still busy)
     defer = int(getattr(ctx, "world", 1)) == 1
-    host = torch.empty(5, dtype=torch.float64, pin_memory=True) if defer else None
+    host = ctx.pinned_slot(5) if defer else None
     fro2_dev = torch.empty(1, dtype=torch.float64, device=dev) if defer else None
     out = _lib.AssembleOut(mu=mu.data_ptr(), l_vector=lvec.data_ptr(), gradient=grad.data_ptr(),
                            scale_table=table.data_ptr(),

@@ -274,9 +274,11 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     )
     aux = ctx.aux_stream() if int(getattr(ctx, "world", 1)) == 1 and hasattr(ctx, "aux_stream") \
         else None
-    drift_host = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    drift_host = ctx.pinned_slot(2) if hasattr(ctx, "pinned_slot") else \
+        torch.empty(2, dtype=torch.float64, pin_memory=True)
     sout.drift_host = drift_host.data_ptr()
     ctx.call("wssr_step_f64", ctypes.byref(sin), ctypes.byref(sout))
+    bundle._fro2_args()  # resolves the bundle's deferred scalars if they have landed (no wait)
     r_eff = int(sout.r_eff)
     deferred = aux is not None and math.isnan(sout.projector_drift)
     if deferred:
