@@ -138,6 +138,133 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- 16-warp Gram / cross-Gram (~120 registers: 16 warps per SM hide the DMMA and load
+// latencies that leave the 8-warp kernel above at ~60% of the DMMA pipe).  Warp w = (group
+// G = w % NG, row quarter w / NG).  SYM: group G "folds" row blocks G and NB-1-G, i.e. the tiles
+// (G, j >= G) and (NB-1-G, j >= NB-1-G): NB/2 + ... = 9 tiles at k = 64, every group equal;
+// its fragments are the column blocks G..NB-1.  !SYM: group G owns the column blocks
+// [G NB/NG, (G+1) NB/NG) against all NB row blocks.  The group index is a template parameter
+// (warp-uniform switch) so every fragment / accumulator index stays static.
+constexpr int kGWarps = 16;
+
+template <int KC, bool SYM, int G>
+__device__ __forceinline__ void gram16_group(const double* __restrict__ A, int64_t lda,
+                                             const double* __restrict__ B, int64_t ldb,
+                                             int64_t r_begin, int64_t r_end, int rq, int lane,
+                                             double* red) {
+  constexpr int NB = KC / 8;
+  constexpr int NG = NB / 2;
+  constexpr int RQ = kGWarps / NG;
+  constexpr int CW = NB / NG;  // !SYM: column blocks per group
+  constexpr int I0 = G, I1 = NB - 1 - G;
+  // tile (i, j) -> accumulator slot; -1: not this group's
+  auto slot = [](int i, int j) constexpr -> int {
+    if (SYM) {
+      if (i == I0 && j >= I0) return j - I0;
+      if (i == I1 && j >= I1) return (NB - I0) + (j - I1);
+      return -1;
+    }
+    return (j >= G * CW && j < (G + 1) * CW) ? i * CW + (j - G * CW) : -1;
+  };
+  constexpr int NT = SYM ? (NB - I0) + (NB - I1) : NB * CW;
+  constexpr int FB0 = SYM ? I0 : 0;  // first A fragment block needed
+  const int g = lane >> 2, t = lane & 3;
+  double acc[NT][2];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) acc[q][0] = acc[q][1] = 0.0;
+  constexpr int H = SYM ? 2 : 1;  // k-steps (4 rows each) per pipeline stage (register budget)
+  auto load = [&](int64_t r0, double (&fa)[H][NB], double (&fb)[H][CW]) {
+#pragma unroll
+    for (int u = 0; u < H; ++u) {
+      const int64_t r = r0 + 4 * u + t;
+      const bool ok = r < r_end;
+      const double* pa = A + (ok ? r : 0) * lda + g;
+#pragma unroll
+      for (int b = FB0; b < NB; ++b) fa[u][b] = ok ? pa[8 * b] : 0.0;
+      if (!SYM) {
+        const double* pb = B + (ok ? r : 0) * ldb + g + 8 * G * CW;
+#pragma unroll
+        for (int b = 0; b < CW; ++b) fb[u][b] = ok ? pb[8 * b] : 0.0;
+      }
+    }
+  };
+  auto compute = [&](const double (&fa)[H][NB], const double (&fb)[H][CW]) {
+#pragma unroll
+    for (int u = 0; u < H; ++u)
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int q = slot(i, j);
+          if (q < 0) continue;
+          dmma884(acc[q], fa[u][i], SYM ? fa[u][j] : fb[u][j - G * CW]);
+        }
+  };
+  double fa0[H][NB], fb0[H][CW], fa1[H][NB], fb1[H][CW];
+  const int64_t step = 4 * H;
+  // this warp's rows: quarter rq of [r_begin, r_end), in 2*step-row slices interleaved over the
+  // RQ quarters (equal shares, neighbouring warps stream neighbouring rows)
+  load(r_begin + 2 * step * rq, fa0, fb0);
+  for (int64_t r0 = r_begin + 2 * step * rq; r0 < r_end; r0 += 2 * step * RQ) {
+    load(r0 + step, fa1, fb1);
+    compute(fa0, fb0);
+    load(r0 + 2 * step * RQ, fa0, fb0);
+    compute(fa1, fb1);
+  }
+  // deterministic CTA reduction: row quarters in order, groups in parallel (disjoint tiles)
+  for (int qi = 0; qi < RQ; ++qi) {
+    if (rq == qi) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int q = slot(i, j);
+          if (q < 0) continue;
+          double2* dst = reinterpret_cast<double2*>(red + ((i * NB + j) * 64 + 2 * lane));
+          if (qi == 0) {
+            *dst = make_double2(acc[q][0], acc[q][1]);
+          } else {
+            double2 v = *dst;
+            v.x += acc[q][0];
+            v.y += acc[q][1];
+            *dst = v;
+          }
+        }
+    }
+    __syncthreads();
+  }
+}
+
+template <int KC, bool SYM>
+__global__ void __launch_bounds__(32 * kGWarps, 1)
+    gram16_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                  int64_t ldb, int64_t rows, int64_t rows_per_cta, double* __restrict__ slabs) {
+  pdl_wait();
+  constexpr int NB = KC / 8;
+  constexpr int NG = NB / 2;
+  __shared__ __align__(16) double red[NB * NB * 64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp % NG, rq = warp / NG;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r_end = min(rows, r_begin + rows_per_cta);
+  switch (grp) {  // warp-uniform
+    case 0: gram16_group<KC, SYM, 0>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
+    case 1: gram16_group<KC, SYM, 1>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
+    case 2: if constexpr (NG > 2) gram16_group<KC, SYM, (NG > 2 ? 2 : 0)>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
+    default: if constexpr (NG > 3) gram16_group<KC, SYM, (NG > 3 ? 3 : 0)>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
+  }
+  double* slab = slabs + (size_t)blockIdx.x * KC * KC;
+  for (int idx = threadIdx.x; idx < NB * NB * 32; idx += 32 * kGWarps) {
+    const int tile = idx >> 5, l = idx & 31;
+    const int bi = tile / NB, bj = tile % NB;
+    if (SYM && bj < bi) continue;
+    const double2 v = *reinterpret_cast<const double2*>(red + tile * 64 + 2 * l);
+    *reinterpret_cast<double2*>(slab + (8 * bi + (l >> 2)) * KC + 8 * bj + 2 * (l & 3)) = v;
+  }
+}
+
 // C[i][j] = sum over slabs in slab order; SYM mirrors the upper tiles.  Block: 32 consecutive
 // entries x 8 slab groups.
 template <int KC, bool SYM>
@@ -174,8 +301,12 @@ __global__ void __launch_bounds__(512)
 // triangular, the tiles (jp > bn) are skipped.  Every warp takes 16-row blocks.
 enum Mode : int { kStore = 0, kAddStore = 1, kAddSumsq = 2 };
 
+// MBR 8-row blocks per warp iteration: 1 keeps the kernel near 110 registers, so two CTAs (16
+// warps) share an SM and hide the DMMA / load latencies.
+constexpr int MBR = 1;
+
 template <int KC, bool TRI, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     mul_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ M,
                int64_t ldm, double alpha, const double* __restrict__ Cin, int64_t ldcin,
                double* __restrict__ Y, int64_t ldy, int64_t rows, double* __restrict__ partial) {
@@ -193,31 +324,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   double ss = 0.0;
-  const int64_t nblk = (rows + 15) / 16;
+  const int64_t nblk = (rows + 8 * MBR - 1) / (8 * MBR);
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, nw = (int64_t)gridDim.x * kWarps;
   // the next block's A fragments are loaded while this block's DMMAs run
-  auto load = [&](int64_t blk, double2 (&a)[2][NB]) {
+  auto load = [&](int64_t blk, double2 (&a)[MBR][NB]) {
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb) {
-      const int64_t r = blk * 16 + 8 * mb + g;
+    for (int mb = 0; mb < MBR; ++mb) {
+      const int64_t r = blk * 8 * MBR + 8 * mb + g;
       const bool ok = blk < nblk && r < rows;
       const double* pa = A + (ok ? r : 0) * lda + 2 * t;
 #pragma unroll
       for (int jp = 0; jp < NB; ++jp) a[mb][jp] = ok ? ld2(pa + 8 * jp) : make_double2(0.0, 0.0);
     }
   };
-  double2 a[2][NB], an[2][NB];
+  double2 a[MBR][NB], an[MBR][NB];
   load(gw, an);
   for (int64_t blk = gw; blk < nblk; blk += nw) {
-    const int64_t r0 = blk * 16;
+    const int64_t r0 = blk * 8 * MBR;
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+    for (int mb = 0; mb < MBR; ++mb)
 #pragma unroll
       for (int jp = 0; jp < NB; ++jp) a[mb][jp] = an[mb][jp];
     load(blk + nw, an);
-    double acc[2][NB][2];
+    double acc[MBR][NB][2];
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+    for (int mb = 0; mb < MBR; ++mb)
 #pragma unroll
       for (int bn = 0; bn < NB; ++bn) acc[mb][bn][0] = acc[mb][bn][1] = 0.0;
 #pragma unroll
@@ -227,13 +358,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (TRI && jp > bn) continue;
         const double2 m = Ms[(jp * NB + bn) * 32 + lane];
 #pragma unroll
-        for (int mb = 0; mb < 2; ++mb) {
+        for (int mb = 0; mb < MBR; ++mb) {
           dmma884(acc[mb][bn], a[mb][jp].x, m.x);
           dmma884(acc[mb][bn], a[mb][jp].y, m.y);
         }
       }
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb) {
+    for (int mb = 0; mb < MBR; ++mb) {
       const int64_t r = r0 + 8 * mb + g;
       if (r >= rows) continue;
 #pragma unroll
@@ -324,7 +455,15 @@ cudaError_t gram_launch(Context& ctx, int64_t rows, const double* A, int64_t lda
   if (grid < 1) grid = 1;
   double* slabs = ctx.splitk_buffer((size_t)grid * KC * KC);
   if (!slabs) return cudaErrorMemoryAllocation;
-  launch_pdl(gram_kernel<KC, SYM>, grid, kThreads, 0, ctx.stream, A, lda, B, ldb, rows, rpc, slabs);
+  // symmetric Grams: the 8-warp kernel (one load per column block feeds 36 DMMAs; measured
+  // 29 us at c1 against 35.5 for the 16-warp fold split); cross-Grams: the 16-warp kernel (44 us
+  // against 51)
+  if (SYM)
+    launch_pdl(gram_kernel<KC, SYM>, grid, kThreads, 0, ctx.stream, A, lda, B, ldb, rows, rpc,
+               slabs);
+  else
+    launch_pdl(gram16_kernel<KC, SYM>, grid, 32 * kGWarps, 0, ctx.stream, A, lda, B, ldb, rows,
+               rpc, slabs);
   launch_pdl(gram_finish_kernel<KC, SYM>, KC * KC / 32, 512, 0, ctx.stream, slabs, grid, C, ldc);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
@@ -334,8 +473,8 @@ template <int KC, bool TRI, int MODE>
 cudaError_t mul_launch(Context& ctx, int64_t rows, const double* A, int64_t lda, const double* M,
                        int64_t ldm, double alpha, const double* Cin, int64_t ldcin, double* Y,
                        int64_t ldy, double* out) {
-  const int64_t nblk = (rows + 15) / 16;
-  int grid = (int)std::min<int64_t>(2 * ctx.num_sms, std::max<int64_t>(1, (nblk + 3) / 4));
+  const int64_t nblk = (rows + 8 * MBR - 1) / (8 * MBR);
+  int grid = (int)std::min<int64_t>(2 * ctx.num_sms, std::max<int64_t>(1, (nblk + 7) / 8));
   double* partial = nullptr;
   if (MODE == kAddSumsq) {
     partial = ctx.splitk_buffer((size_t)grid);
