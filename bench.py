@@ -260,8 +260,9 @@ def run_ours(args, rank, world, local_rank):
     phases = [ctx.phase_stats(i) for i in range(16)]
     if os.environ.get("WSSR_FINE_PHASES") == "1":  # profiling: CholeskyQR2 pieces, us per call
         print(json.dumps({n: round(1e3 * phases[i]["ms"] / max(phases[i]["launches"], 1), 1)
-                          for i, n in zip(range(8, 14), ["gram1", "chol1", "trmm1", "gram2",
-                                                         "chol2", "trmm2"])}), file=sys.stderr)
+                          for i, n in zip(range(8, 16), ["gram1", "chol1", "trmm1", "gram2",
+                                                         "chol2", "trmm2", "v_first", "v_pre"])}),
+              file=sys.stderr)
     ctx.set_timing(False)
     step_ms = sum(x.elapsed_time(y) for x, y in intervals)
     t = torch.tensor([step_ms], dtype=torch.float64, device=dev)

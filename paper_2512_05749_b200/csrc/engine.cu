@@ -502,6 +502,13 @@ bool ensure_planes(Context& ctx, size_t bytes) {
 // HBM allows (c2/c3: the 7-byte planes of 16384 x 2^20 samples are 120 GB), 0 below 1024.
 int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
   const size_t full = ozaki_planes_bytes(o.n, o.P);
+  const char* cap_env0 = std::getenv("WSSR_OZ_PLANE_ROWS");
+  // no memory query when the decision is already known: cudaMemGetInfo can stall the host for
+  // milliseconds (it contends with NVML clients), and the stream drains meanwhile
+  if (!cap_env0) {
+    if (full <= ctx.oz_planes_cap) return o.n;
+    if (ctx.plan_n == o.n && ctx.plan_p == o.P && ctx.plan_k == k) return ctx.plan_rows;
+  }
   const size_t margin = ((size_t)2 << 30) + (size_t)16 * o.P * std::max<int64_t>(k, 1) * 8;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
@@ -514,11 +521,13 @@ int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
   const char* cap_env = std::getenv("WSSR_OZ_PLANE_ROWS");
   const int64_t cap = cap_env ? std::max<int64_t>(0, std::atoll(cap_env)) / 128 * 128 : -1;
   if (full <= avail && (cap < 0 || cap >= o.n)) return ensure_planes(ctx, full) ? o.n : 0;
+  ctx.plan_n = o.n, ctx.plan_p = o.P, ctx.plan_k = k, ctx.plan_rows = 0;
   int64_t rows = (int64_t)(avail / ozaki_planes_bytes(128, o.P)) * 128;
   if (cap >= 0) rows = std::min(rows, cap);
   else if (rows < 1024) return 0;
   if (rows <= 0) return 0;
   const bool ok = ensure_planes(ctx, ozaki_planes_bytes(rows, o.P));
+  if (!cap_env) ctx.plan_rows = ok ? rows : 0;
   if (std::getenv("WSSR_VERBOSE"))
     std::fprintf(stderr, "[wssr] digit planes for %lld of %lld samples (%s; free %.1f GB)\n",
                  (long long)rows, (long long)o.n, ok ? "ok" : "alloc failed", free_b / 1e9);
@@ -564,6 +573,10 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       }
     }
     if (n_pl == 0 || n_pl >= o.n) {
+      // profiling (WSSR_FINE_PHASES): 14 = the step's digitising first pass, 15 = the other
+      // row-major (v) passes
+      const int fp = (ctx.fine_phases && layout == Layout::RM) ? (store ? 14 : 15) : -1;
+      PhaseTimer tm(ctx, fp, 0.0, 0.0);
       WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store));
       return;
     }
@@ -661,14 +674,22 @@ struct Fro2 {
   double dev_scale = 1.0;
   double dev_val = 0.0;
   bool enqueued = false;
+  double* stage = nullptr;  // pinned slot the device value is copied into
   void enqueue(Context& ctx) {
     if (dev && !enqueued) {
-      d2h(ctx, &dev_val, dev, sizeof(double));
+      stage = ctx.hbuf + 3;
+      d2h(ctx, stage, dev, sizeof(double));
       enqueued = true;
     }
   }
   // valid after a stream sync that follows enqueue()
-  double value() const { return dev ? host + dev_scale * dev_val : host; }
+  double value() {
+    if (dev && stage) {
+      dev_val = *stage;
+      stage = nullptr;
+    }
+    return dev ? host + dev_scale * dev_val : host;
+  }
 };
 
 // ---- ssi_svd (svdengine.py:88-158) ------------------------------------------------------------
@@ -702,6 +723,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   apply_O(ctx, o, v, k, k, u, k);
   SsiResult res;
   int64_t it = 0;
+  bool deferred_residual = false;
   while (true) {  // svdengine.py:132-142
     qr(ctx, P, k, u, k, q, k, nullptr, status, careful, false);
     ++it;
@@ -726,16 +748,22 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
       launch_pdl(small_norms_kernel, 1, 256, 0, st, nullptr, nullptr, 0, quot, (int)k, scal + 1);
       post_launch(ctx);
     }
-    double h[3];
+    double* h = ctx.hbuf;  // pinned: the copies are asynchronous
     d2h(ctx, h, scal, 3 * sizeof(double));
     fro2_in.enqueue(ctx);
+    if (it >= max_iters) {
+      // the loop ends whatever the residual is: read it at the next synchronisation (the rank
+      // cut) instead of waiting here
+      deferred_residual = true;
+      break;
+    }
     sync(ctx);
     const double fro2 = fro2_in.value();
     if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
     const double residual = std::sqrt(h[0]) / fro2;
     const double mixing = h[2] / fro2;
     res.residual = residual;
-    if (std::max(residual, mixing) < tol || it >= max_iters) break;
+    if (std::max(residual, mixing) < tol) break;
     std::swap(v, v2);
     std::swap(u, w);
   }
@@ -749,12 +777,23 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   launch_pdl(sort_sigma_kernel, 1, 256, sizeof(double) * k, st, Rv, (int)k, r_reg, res.order.i64(),
                                                        sigma_out, ints.i32());
   post_launch(ctx);
-  int hi[2];
-  std::vector<int64_t> hord(k);
-  d2h(ctx, hi, ints, sizeof(hi));
-  d2h(ctx, &res.sigma0, sigma_out, sizeof(double));
-  d2h(ctx, hord.data(), res.order, sizeof(int64_t) * k);
+  // one synchronisation for the counts, the top value, the order (and a deferred residual);
+  // staged through pinned memory so the copies do not each block the host
+  const bool big_k = 16 + k > 4096;
+  std::vector<int64_t> hord_big(big_k ? k : 0);
+  int* hi = reinterpret_cast<int*>(ctx.hbuf + 8);
+  double* hsig0 = ctx.hbuf + 9;
+  int64_t* hord = big_k ? hord_big.data() : reinterpret_cast<int64_t*>(ctx.hbuf + 16);
+  d2h(ctx, hi, ints, 2 * sizeof(int));
+  d2h(ctx, hsig0, sigma_out, sizeof(double));
+  d2h(ctx, hord, res.order, sizeof(int64_t) * k);
   sync(ctx);
+  if (deferred_residual) {
+    const double fro2 = fro2_in.value();
+    if (fro2 == 0.0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+    res.residual = std::sqrt(ctx.hbuf[0]) / fro2;
+  }
+  res.sigma0 = *hsig0;
   res.k_pos = hi[0];
   res.r_eff = hi[1];
   if (res.k_pos == 0)
@@ -791,8 +830,8 @@ auto with_fallback(Context& ctx, int64_t flags, F&& body) -> decltype(body(false
     Buf status(1, ctx.stream);
     WSSR_CUDA(cudaMemsetAsync(status, 0, sizeof(double), ctx.stream));
     auto r = body(false, status.i32());
-    int hs[2];
-    d2h(ctx, hs, status, sizeof(hs));
+    int* hs = reinterpret_cast<int*>(ctx.hbuf + 4);
+    d2h(ctx, hs, status, 2 * sizeof(int));
     sync(ctx);
     if (hs[0] == 0) return r;
   }
@@ -1473,6 +1512,10 @@ int wssr_ctx_create(int device, wssr_ctx** out) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
+  if (cudaMallocHost(reinterpret_cast<void**>(&c->c.hbuf), 4096 * sizeof(double)) != cudaSuccess) {
+    delete c;
+    return WSSR_ERR_CUDA;
+  }
   *out = c;
   return WSSR_OK;
 }
@@ -1482,6 +1525,10 @@ void wssr_ctx_destroy(wssr_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   if (ctx->c.splitk || ctx->c.oz_ws || ctx->c.oz_planes) cudaDeviceSynchronize();
   if (ctx->c.aux) cudaStreamSynchronize(ctx->c.aux);
+  if (ctx->c.hbuf) {
+    cudaDeviceSynchronize();
+    cudaFreeHost(ctx->c.hbuf);
+  }
   if (ctx->c.aux_event) cudaEventDestroy(ctx->c.aux_event);
   if (ctx->c.aux_splitk) cudaFree(ctx->c.aux_splitk);
   if (ctx->c.splitk) cudaFree(ctx->c.splitk);

@@ -39,6 +39,7 @@ struct Context {
   double oz_min_elems = 4194304.0;  // smallest sample block (elements) sent to that path
   bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
   bool tallskinny = true;    // k = 32/64 Grams and products of P x k blocks: tallskinny.cu
+  double* hbuf = nullptr;          // pinned host staging for the step's small readbacks (4096)
   cudaStream_t aux = nullptr;      // optional: asynchronous drift telemetry (wssr_set_aux_stream)
   cudaEvent_t aux_event = nullptr;
   double* aux_splitk = nullptr;    // the aux stream's own split-K / slab buffer
@@ -46,6 +47,7 @@ struct Context {
   int oz_pre = 0;            // digit planes: 0 = pre-digitise when they fit, 1 = on the fly only
   int8_t* oz_planes = nullptr;  // the step's pre-digitised sample block (reused across steps)
   size_t oz_planes_cap = 0;     // bytes
+  int64_t plan_n = -1, plan_p = -1, plan_k = -1, plan_rows = 0;  // last partial-planes decision
   double* oz_ws = nullptr;   // Ozaki thin-operand digits + factors
   size_t oz_ws_cap = 0;      // doubles
 

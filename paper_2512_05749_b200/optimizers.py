@@ -208,6 +208,8 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
 
     from .svdengine import _ohat_struct
     fro2_host, fro2_dev = bundle._fro2_args()
+    if fro2_dev is not None:  # assemble's outputs may still be in flight on another stream
+        torch.cuda.current_stream(dev).wait_event(bundle._deferred[0])
     o = _ohat_struct(samples, bundle._mu, bundle._scale, fro2_host, hist, 1.0,
                      bundle._scale_table, fro2_dev)
     lvec = bundle.l_vector.contiguous()
