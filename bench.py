@@ -366,7 +366,6 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
 
         def upload(t):
             i = t % nbuf
@@ -385,21 +384,29 @@ def run_ours(args, rank, world, local_rank):
                 copy_stream.wait_event(chunk_done[c])
             ready[i].record(copy_stream)
 
-        for i in range(nbuf):
-            freed[i].record(stream)
-        upload(0)
-        th_d = theta_h.to(dev, non_blocking=True)
-        for t in range(e2e_steps):
-            i = t % nbuf
-            stream.wait_event(ready[i])
-            if pipelined and t + 1 < e2e_steps:
-                upload(t + 1)
-            th_d, state, diag = step(O_d[i], E_d[i], state, th_d)
-            freed[i].record(stream)
-            out_h.copy_(th_d, non_blocking=True)
-            if not pipelined and t + 1 < e2e_steps:
-                upload(t + 1)
-        stream.wait_stream(aux)
+        def run_e2e(nsteps, st):
+            for i in range(nbuf):
+                freed[i].record(stream)
+            upload(0)
+            th_d = theta_h.to(dev, non_blocking=True)
+            for t in range(nsteps):
+                i = t % nbuf
+                stream.wait_event(ready[i])
+                if pipelined and t + 1 < nsteps:
+                    upload(t + 1)
+                th_d, st, _ = step(O_d[i], E_d[i], st, th_d)
+                freed[i].record(stream)
+                out_h.copy_(th_d, non_blocking=True)
+                if not pipelined and t + 1 < nsteps:
+                    upload(t + 1)
+            stream.wait_stream(aux)
+            return st
+
+        state = run_e2e(2, state)  # untimed warm-up: first touches of the pinned pages, copy engines
+        torch.cuda.synchronize()
+        barrier()
+        a.record(stream)
+        state = run_e2e(e2e_steps, state)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b)
