@@ -710,7 +710,8 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   const int64_t P = o.P, cols = o.cols();
   const bool dist = ctx.world() > 1;
   cudaStream_t st = ctx.stream;
-  Buf q((size_t)P * k, st), ua((size_t)P * k, st), ub((size_t)P * k, st);
+  Buf qbuf((size_t)P * k, st), ua((size_t)P * k, st), ub((size_t)P * k, st);
+  double* q = qbuf;
   Buf va((size_t)std::max<int64_t>(cols, 1) * k, st), vb((size_t)std::max<int64_t>(cols, 1) * k, st);
   Buf quot((size_t)k * k, st), scal(4, st);
   double* u = ua;
@@ -725,6 +726,9 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   int64_t it = 0;
   bool deferred_residual = false;
   while (true) {  // svdengine.py:132-142
+    // the last iteration's q is the returned U when the order comes out sorted
+    // (svdengine.py:151): write it there directly
+    if (it + 1 == max_iters && ldU == k && U_out) q = U_out;
     qr(ctx, P, k, u, k, q, k, nullptr, status, careful, false);
     ++it;
     if (it >= max_iters && !final_res) {
@@ -805,7 +809,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   bool identity = kp == k;
   for (int64_t j = 0; j < kp && identity; ++j) identity = hord[j] == j;
   if (identity) {
-    copy2d(ctx, q, k, P, k, 1.0, U_out, ldU);
+    if (q != U_out) copy2d(ctx, q, k, P, k, 1.0, U_out, ldU);
   } else {
     Buf uperm((size_t)P * kp, st);
     launch_pdl(gather_cols_kernel, blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st, 
