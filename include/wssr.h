@@ -274,7 +274,7 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
  * with WSSR_OZ_DEBUG=9, 8 rows x 96 K-blocks (producer, MMA issuers, converter group leaders). */
 int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
 
-/* engine option: 1 (default) runs the Grams and k x k products of P x k blocks with k = 32 or 64
+/* engine option: 1 (default) runs the Grams and k x k products of P x k blocks with k = 32, 64, 128
  * (CholeskyQR2, Rayleigh quotient and residual, drift) on the tall-skinny kernels
  * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
@@ -284,7 +284,7 @@ int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
  * record_stream). */
 int wssr_set_aux_stream(wssr_ctx* ctx, void* cuda_stream);
 
-/* test hook: one tall-skinny kernel, row-major operands with ld = k (k = 32 or 64).
+/* test hook: one tall-skinny kernel, row-major operands with ld = k (k = 32, 64 or 128).
  * op 0: out = A^T A (k x k); op 1: out = A^T B; op 2: out (rows x k) = A (alpha M) with M upper
  * triangular; op 3: out = A (alpha M); op 4: out = Cin + A (alpha M);
  * op 5: out[0] = ||Cin + A (alpha M)||_F^2; op 6: out (k) = alpha A^T x, x = cin (rows). */

@@ -1572,7 +1572,7 @@ int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const 
                           double* out) {
   return guarded(ctx, [&] {
     Context& c = ctx->c;
-    if (!ts_supported(k) || rows < 0) throw Fail{WSSR_ERR_VALUE, "tall-skinny: k must be 32 or 64"};
+    if (!ts_supported(k) || rows < 0) throw Fail{WSSR_ERR_VALUE, "tall-skinny: k must be 32, 64 or 128"};
     static const int reps = [] {
       const char* e = std::getenv("WSSR_DEBUG_REPS");  // profiling: back-to-back launches
       return e ? std::max(1, std::atoi(e)) : 1;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "engine.h"
@@ -138,24 +139,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ---- 16-warp Gram / cross-Gram (~120 registers: 16 warps per SM hide the DMMA and load
-// latencies that leave the 8-warp kernel above at ~60% of the DMMA pipe).  Warp w = (group
-// G = w % NG, row quarter w / NG).  SYM: group G "folds" row blocks G and NB-1-G, i.e. the tiles
-// (G, j >= G) and (NB-1-G, j >= NB-1-G): NB/2 + ... = 9 tiles at k = 64, every group equal;
-// its fragments are the column blocks G..NB-1.  !SYM: group G owns the column blocks
-// [G NB/NG, (G+1) NB/NG) against all NB row blocks.  The group index is a template parameter
-// (warp-uniform switch) so every fragment / accumulator index stays static.
-constexpr int kGWarps = 16;
+// ---- grouped Gram / cross-Gram.  Warp w = (group G = w % NG, row quarter w / NG), NG = NB/2
+// groups.  SYM: group G "folds" row blocks G and NB-1-G, i.e. the tiles (G, j >= G) and
+// (NB-1-G, j >= NB-1-G) - NB + 1 tiles, equal for every group; its fragments are the column
+// blocks G..NB-1.  !SYM: group G owns the column blocks [2G, 2G+2) against all NB row blocks.
+// The group index is a template parameter (warp-uniform switch), so every fragment and
+// accumulator index stays static.  k = 32/64: 16 warps (~120 registers: 16 warps per SM hide the
+// DMMA and load latencies); k = 128: 8 warps, one per group, each writing its tiles straight to
+// the CTA's slab.
+template <int KC>
+struct GramCfg {
+  static constexpr int NB = KC / 8;
+  static constexpr int NG = NB / 2;
+  static constexpr int WARPS = KC == 128 ? 8 : 16;
+  static constexpr int RQ = WARPS / NG;  // row quarters
+};
 
 template <int KC, bool SYM, int G>
 __device__ __forceinline__ void gram16_group(const double* __restrict__ A, int64_t lda,
                                              const double* __restrict__ B, int64_t ldb,
                                              int64_t r_begin, int64_t r_end, int rq, int lane,
-                                             double* red) {
-  constexpr int NB = KC / 8;
-  constexpr int NG = NB / 2;
-  constexpr int RQ = kGWarps / NG;
-  constexpr int CW = NB / NG;  // !SYM: column blocks per group
+                                             double* red, double* slab) {
+  using Cfg = GramCfg<KC>;
+  constexpr int NB = Cfg::NB;
+  constexpr int RQ = Cfg::RQ;
+  constexpr int CW = 2;  // !SYM: column blocks per group
   constexpr int I0 = G, I1 = NB - 1 - G;
   // tile (i, j) -> accumulator slot; -1: not this group's
   auto slot = [](int i, int j) constexpr -> int {
@@ -172,7 +180,7 @@ __device__ __forceinline__ void gram16_group(const double* __restrict__ A, int64
   double acc[NT][2];
 #pragma unroll
   for (int q = 0; q < NT; ++q) acc[q][0] = acc[q][1] = 0.0;
-  constexpr int H = SYM ? 2 : 1;  // k-steps (4 rows each) per pipeline stage (register budget)
+  constexpr int H = (SYM && KC <= 64) ? 2 : 1;  // k-steps (4 rows each) per pipeline stage
   auto load = [&](int64_t r0, double (&fa)[H][NB], double (&fb)[H][CW]) {
 #pragma unroll
     for (int u = 0; u < H; ++u) {
@@ -195,8 +203,6 @@ __device__ __forceinline__ void gram16_group(const double* __restrict__ A, int64
       for (int i = 0; i < NB; ++i)
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
-          constexpr int dummy = 0;
-          (void)dummy;
           const int q = slot(i, j);
           if (q < 0) continue;
           dmma884(acc[q], fa[u][i], SYM ? fa[u][j] : fb[u][j - G * CW]);
@@ -204,8 +210,7 @@ __device__ __forceinline__ void gram16_group(const double* __restrict__ A, int64
   };
   double fa0[H][NB], fb0[H][CW], fa1[H][NB], fb1[H][CW];
   const int64_t step = 4 * H;
-  // this warp's rows: quarter rq of [r_begin, r_end), in 2*step-row slices interleaved over the
-  // RQ quarters (equal shares, neighbouring warps stream neighbouring rows)
+  // this warp's rows: 2*step-row slices interleaved over the RQ quarters
   load(r_begin + 2 * step * rq, fa0, fb0);
   for (int64_t r0 = r_begin + 2 * step * rq; r0 < r_end; r0 += 2 * step * RQ) {
     load(r0 + step, fa1, fb1);
@@ -213,55 +218,84 @@ __device__ __forceinline__ void gram16_group(const double* __restrict__ A, int64
     load(r0 + 2 * step * RQ, fa0, fb0);
     compute(fa1, fb1);
   }
-  // deterministic CTA reduction: row quarters in order, groups in parallel (disjoint tiles)
-  for (int qi = 0; qi < RQ; ++qi) {
-    if (rq == qi) {
+  if constexpr (RQ == 1) {
+    // sole owner of its tiles: straight to the slab, C[8i + g][8j + 2t + e]
 #pragma unroll
-      for (int i = 0; i < NB; ++i)
+    for (int i = 0; i < NB; ++i)
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int q = slot(i, j);
-          if (q < 0) continue;
-          double2* dst = reinterpret_cast<double2*>(red + ((i * NB + j) * 64 + 2 * lane));
-          if (qi == 0) {
-            *dst = make_double2(acc[q][0], acc[q][1]);
-          } else {
-            double2 v = *dst;
-            v.x += acc[q][0];
-            v.y += acc[q][1];
-            *dst = v;
+      for (int j = 0; j < NB; ++j) {
+        const int q = slot(i, j);
+        if (q < 0) continue;
+        *reinterpret_cast<double2*>(slab + (8 * i + g) * KC + 8 * j + 2 * t) =
+            make_double2(acc[q][0], acc[q][1]);
+      }
+  } else {
+    // deterministic CTA reduction: row quarters in order, groups in parallel (disjoint tiles)
+    for (int qi = 0; qi < RQ; ++qi) {
+      if (rq == qi) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            const int q = slot(i, j);
+            if (q < 0) continue;
+            double2* dst = reinterpret_cast<double2*>(red + ((i * NB + j) * 64 + 2 * lane));
+            if (qi == 0) {
+              *dst = make_double2(acc[q][0], acc[q][1]);
+            } else {
+              double2 v = *dst;
+              v.x += acc[q][0];
+              v.y += acc[q][1];
+              *dst = v;
+            }
           }
-        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
 template <int KC, bool SYM>
-__global__ void __launch_bounds__(32 * kGWarps, 1)
+__global__ void __launch_bounds__(32 * GramCfg<KC>::WARPS, 1)
     gram16_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                   int64_t ldb, int64_t rows, int64_t rows_per_cta, double* __restrict__ slabs) {
   pdl_wait();
-  constexpr int NB = KC / 8;
-  constexpr int NG = NB / 2;
-  __shared__ __align__(16) double red[NB * NB * 64];
+  using Cfg = GramCfg<KC>;
+  constexpr int NB = Cfg::NB;
+  constexpr int NG = Cfg::NG;
+  constexpr int NRED = Cfg::RQ > 1 ? NB * NB * 64 : 2;
+  __shared__ __align__(16) double red[NRED];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = warp % NG, rq = warp / NG;
   const int64_t r_begin = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t r_end = min(rows, r_begin + rows_per_cta);
-  switch (grp) {  // warp-uniform
-    case 0: gram16_group<KC, SYM, 0>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
-    case 1: gram16_group<KC, SYM, 1>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
-    case 2: if constexpr (NG > 2) gram16_group<KC, SYM, (NG > 2 ? 2 : 0)>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
-    default: if constexpr (NG > 3) gram16_group<KC, SYM, (NG > 3 ? 3 : 0)>(A, lda, B, ldb, r_begin, r_end, rq, lane, red); break;
-  }
   double* slab = slabs + (size_t)blockIdx.x * KC * KC;
-  for (int idx = threadIdx.x; idx < NB * NB * 32; idx += 32 * kGWarps) {
-    const int tile = idx >> 5, l = idx & 31;
-    const int bi = tile / NB, bj = tile % NB;
-    if (SYM && bj < bi) continue;
-    const double2 v = *reinterpret_cast<const double2*>(red + tile * 64 + 2 * l);
-    *reinterpret_cast<double2*>(slab + (8 * bi + (l >> 2)) * KC + 8 * bj + 2 * (l & 3)) = v;
+#define WSSR_GRAM_CASE(c)                                                                     \
+  case c:                                                                                      \
+    if constexpr (NG > c)                                                                      \
+      gram16_group<KC, SYM, (NG > c ? c : 0)>(A, lda, B, ldb, r_begin, r_end, rq, lane, red,   \
+                                              slab);                                            \
+    break;
+  switch (grp) {  // warp-uniform
+    WSSR_GRAM_CASE(0)
+    WSSR_GRAM_CASE(1)
+    WSSR_GRAM_CASE(2)
+    WSSR_GRAM_CASE(3)
+    WSSR_GRAM_CASE(4)
+    WSSR_GRAM_CASE(5)
+    WSSR_GRAM_CASE(6)
+    WSSR_GRAM_CASE(7)
+    default: break;
+  }
+#undef WSSR_GRAM_CASE
+  if constexpr (Cfg::RQ > 1) {
+    for (int idx = threadIdx.x; idx < NB * NB * 32; idx += 32 * Cfg::WARPS) {
+      const int tile = idx >> 5, l = idx & 31;
+      const int bi = tile / NB, bj = tile % NB;
+      if (SYM && bj < bi) continue;
+      const double2 v = *reinterpret_cast<const double2*>(red + tile * 64 + 2 * l);
+      *reinterpret_cast<double2*>(slab + (8 * bi + (l >> 2)) * KC + 8 * bj + 2 * (l & 3)) = v;
+    }
   }
 }
 
@@ -306,13 +340,13 @@ enum Mode : int { kStore = 0, kAddStore = 1, kAddSumsq = 2 };
 constexpr int MBR = 1;
 
 template <int KC, bool TRI, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, KC == 128 ? 1 : 2)
     mul_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ M,
                int64_t ldm, double alpha, const double* __restrict__ Cin, int64_t ldcin,
                double* __restrict__ Y, int64_t ldy, int64_t rows, double* __restrict__ partial) {
   pdl_wait();
   constexpr int NB = KC / 8;
-  __shared__ __align__(16) double2 Ms[NB * NB * 32];
+  extern __shared__ __align__(16) double2 Ms[];  // NB * NB * 32 (KC^2 doubles)
   __shared__ double scratch[32];
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
   for (int idx = threadIdx.x; idx < NB * NB * 32; idx += kThreads) {
@@ -458,12 +492,12 @@ cudaError_t gram_launch(Context& ctx, int64_t rows, const double* A, int64_t lda
   // symmetric Grams: the 8-warp kernel (one load per column block feeds 36 DMMAs; measured
   // 29 us at c1 against 35.5 for the 16-warp fold split); cross-Grams: the 16-warp kernel (44 us
   // against 51)
-  if (SYM)
+  if constexpr (SYM && KC <= 64)
     launch_pdl(gram_kernel<KC, SYM>, grid, kThreads, 0, ctx.stream, A, lda, B, ldb, rows, rpc,
                slabs);
   else
-    launch_pdl(gram16_kernel<KC, SYM>, grid, 32 * kGWarps, 0, ctx.stream, A, lda, B, ldb, rows,
-               rpc, slabs);
+    launch_pdl(gram16_kernel<KC, SYM>, grid, 32 * GramCfg<KC>::WARPS, 0, ctx.stream, A, lda, B,
+               ldb, rows, rpc, slabs);
   launch_pdl(gram_finish_kernel<KC, SYM>, KC * KC / 32, 512, 0, ctx.stream, slabs, grid, C, ldc);
   ctx.kernel_launches += 2;
   return cudaGetLastError();
@@ -480,8 +514,16 @@ cudaError_t mul_launch(Context& ctx, int64_t rows, const double* A, int64_t lda,
     partial = ctx.splitk_buffer((size_t)grid);
     if (!partial) return cudaErrorMemoryAllocation;
   }
-  launch_pdl(mul_kernel<KC, TRI, MODE>, grid, kThreads, 0, ctx.stream, A, lda, M, ldm, alpha, Cin, ldcin,
-                                                                Y, ldy, rows, partial);
+  constexpr int smem = KC * KC * 8;  // R^-1 / M in fragment order
+  static bool attr = false;  // one per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(mul_kernel<KC, TRI, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  launch_pdl(mul_kernel<KC, TRI, MODE>, grid, kThreads, smem, ctx.stream, A, lda, M, ldm, alpha,
+             Cin, ldcin, Y, ldy, rows, partial);
   ctx.kernel_launches += 1;
   if (MODE == kAddSumsq) {
     launch_pdl(sum_partials_kernel, 1, 256, 0, ctx.stream, partial, grid, out);
@@ -496,7 +538,7 @@ bool aligned16(const void* p, int64_t ld) {
 
 }  // namespace ts
 
-bool ts_supported(int64_t k) { return k == 32 || k == 64; }
+bool ts_supported(int64_t k) { return k == 32 || k == 64 || k == 128; }
 
 cudaError_t ts_gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, int64_t lda,
                       const double* x, double alpha, double* out) {
@@ -521,6 +563,7 @@ cudaError_t ts_gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, in
 cudaError_t ts_gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                     double* G) {
   if (rows <= 0) return cudaMemsetAsync(G, 0, sizeof(double) * k * k, ctx.stream);
+  if (k == 128) return ts::gram_launch<128, true>(ctx, rows, A, lda, A, lda, G, k);
   if (k == 64) return ts::gram_launch<64, true>(ctx, rows, A, lda, A, lda, G, k);
   return ts::gram_launch<32, true>(ctx, rows, A, lda, A, lda, G, k);
 }
@@ -528,6 +571,7 @@ cudaError_t ts_gram(Context& ctx, int64_t rows, int64_t k, const double* A, int6
 cudaError_t ts_cross(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double* C) {
   if (rows <= 0) return cudaMemsetAsync(C, 0, sizeof(double) * k * k, ctx.stream);
+  if (k == 128) return ts::gram_launch<128, false>(ctx, rows, A, lda, B, ldb, C, k);
   if (k == 64) return ts::gram_launch<64, false>(ctx, rows, A, lda, B, ldb, C, k);
   return ts::gram_launch<32, false>(ctx, rows, A, lda, B, ldb, C, k);
 }
@@ -536,40 +580,48 @@ bool ts_mul_supported(int64_t k, const double* A, int64_t lda, const double* Y, 
   return ts_supported(k) && ts::aligned16(A, lda) && ts::aligned16(Y, ldy);
 }
 
+namespace {
+// k (32 / 64 / 128) and triangularity as template arguments
+template <int MODE>
+cudaError_t mul_dispatch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
+                         const double* M, bool upper, double alpha, const double* Cin,
+                         int64_t ldcin, double* Y, int64_t ldy, double* out) {
+  auto go = [&](auto kc, auto tri) {
+    return ts::mul_launch<decltype(kc)::value, decltype(tri)::value, MODE>(
+        ctx, rows, A, lda, M, k, alpha, Cin, ldcin, Y, ldy, out);
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  using K32 = std::integral_constant<int, 32>;
+  using K64 = std::integral_constant<int, 64>;
+  using K128 = std::integral_constant<int, 128>;
+  if (k == 128) return upper ? go(K128{}, T{}) : go(K128{}, F{});
+  if (k == 64) return upper ? go(K64{}, T{}) : go(K64{}, F{});
+  return upper ? go(K32{}, T{}) : go(K32{}, F{});
+}
+}  // namespace
+
 cudaError_t ts_mul(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                    const double* M, bool upper, double alpha, double* Y, int64_t ldy) {
   if (rows <= 0) return cudaSuccess;
-  if (k == 64)
-    return upper ? ts::mul_launch<64, true, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr, 0,
-                                                        Y, ldy, nullptr)
-                 : ts::mul_launch<64, false, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr,
-                                                         0, Y, ldy, nullptr);
-  return upper ? ts::mul_launch<32, true, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr, 0, Y,
-                                                      ldy, nullptr)
-               : ts::mul_launch<32, false, ts::kStore>(ctx, rows, A, lda, M, k, alpha, nullptr, 0,
-                                                       Y, ldy, nullptr);
+  return mul_dispatch<ts::kStore>(ctx, rows, k, A, lda, M, upper, alpha, nullptr, 0, Y, ldy,
+                                  nullptr);
 }
 
 cudaError_t ts_mul_add(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                        const double* M, double alpha, const double* Cin, int64_t ldcin, double* Y,
                        int64_t ldy) {
   if (rows <= 0) return cudaSuccess;
-  if (k == 64)
-    return ts::mul_launch<64, false, ts::kAddStore>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin, Y,
-                                                    ldy, nullptr);
-  return ts::mul_launch<32, false, ts::kAddStore>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin, Y,
-                                                  ldy, nullptr);
+  return mul_dispatch<ts::kAddStore>(ctx, rows, k, A, lda, M, false, alpha, Cin, ldcin, Y, ldy,
+                                     nullptr);
 }
 
 cudaError_t ts_mul_add_sumsq(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                              const double* M, double alpha, const double* Cin, int64_t ldcin,
                              double* out) {
   if (rows <= 0) return cudaMemsetAsync(out, 0, sizeof(double), ctx.stream);
-  if (k == 64)
-    return ts::mul_launch<64, false, ts::kAddSumsq>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin,
-                                                    nullptr, 0, out);
-  return ts::mul_launch<32, false, ts::kAddSumsq>(ctx, rows, A, lda, M, k, alpha, Cin, ldcin,
-                                                  nullptr, 0, out);
+  return mul_dispatch<ts::kAddSumsq>(ctx, rows, k, A, lda, M, false, alpha, Cin, ldcin, nullptr,
+                                     0, out);
 }
 
 }  // namespace wssr

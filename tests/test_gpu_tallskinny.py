@@ -22,7 +22,7 @@ def _ops(rows, k, seed):
     return A, B, M, C
 
 
-@pytest.mark.parametrize("k", [32, 64])
+@pytest.mark.parametrize("k", [32, 64, 128])
 @pytest.mark.parametrize("rows", ROWS)
 def test_grams(k, rows):
     from paper_2512_05749_b200 import _lib
@@ -41,7 +41,7 @@ def test_grams(k, rows):
     assert ((out - ref).abs().max() / ref.abs().max()).item() < 1e-14
 
 
-@pytest.mark.parametrize("k", [32, 64])
+@pytest.mark.parametrize("k", [32, 64, 128])
 @pytest.mark.parametrize("rows", ROWS)
 @pytest.mark.parametrize("alpha", [1.0, -1.0])
 def test_products(k, rows, alpha):
