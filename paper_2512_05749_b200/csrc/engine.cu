@@ -1201,6 +1201,54 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   }
   const int64_t r_eff = sr.r_eff;
   if (r_eff < 1) throw Fail{WSSR_ERR_RANK_COLLAPSE, "no singular value passed the relative cutoff"};
+
+  // drift telemetry against the previous factors (optimizers.py:366-374)
+  double sd = 0.0, pd = 0.0;
+  const int64_t r_hist = oh.hist_rank;
+  const int64_t r_drift = in->r_prev > 0 ? std::min(std::min(r_hist, in->r_prev), r_eff) : 0;
+  if (r_drift > 0 && out->drift_host && ctx.aux && !dist) {
+    // asynchronous: the drift runs on the auxiliary stream as soon as U and sigma are final,
+    // beside the preconditioner and the state refresh, and while the caller moves on;
+    // {sigma_drift, projector_drift} land in out->drift_host in aux-stream order
+    if (!ctx.aux_event) WSSR_CUDA(cudaEventCreateWithFlags(&ctx.aux_event, cudaEventDisableTiming));
+    WSSR_CUDA(cudaEventRecord(ctx.aux_event, st));
+    WSSR_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.aux_event, 0));
+    // the aux stream gets its own slab buffer (the main stream's is reused by the next step)
+    cudaStream_t main_stream = ctx.stream;
+    std::swap(ctx.splitk, ctx.aux_splitk);
+    std::swap(ctx.splitk_cap, ctx.aux_splitk_cap);
+    ctx.stream = ctx.aux;
+    auto restore = [&] {
+      ctx.stream = main_stream;
+      std::swap(ctx.splitk, ctx.aux_splitk);
+      std::swap(ctx.splitk_cap, ctx.aux_splitk_cap);
+    };
+    try {
+      Buf sprev(r_hist, ctx.aux), out2(2, ctx.aux);
+      PhaseTimer tm(ctx, 5, 0.0, 0.0);  // events on the aux stream
+      row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
+      drift_enqueue(ctx, P, in->u_prev, in->ld_prev, sprev, r_drift, out->u_next, out->ld_u,
+                    out->sigma, out2);
+      d2h(ctx, out->drift_host, out2, 2 * sizeof(double));
+    } catch (...) {
+      restore();
+      throw;
+    }
+    restore();
+    sd = pd = std::numeric_limits<double>::quiet_NaN();
+  } else if (in->r_prev > 0) {
+    Buf sprev(std::max<int64_t>(r_hist, 1), st);
+    if (r_hist > 0) row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
+    const int64_t r1 = std::min(r_hist, in->r_prev);
+    auto d = drift(ctx, P, in->u_prev, in->ld_prev, sprev, r1, out->u_next, out->ld_u, out->sigma,
+                   r_eff);
+    sd = d.first;
+    pd = d.second;
+  }
+  if (out->drift_host && !std::isnan(sd)) {
+    out->drift_host[0] = sd;
+    out->drift_host[1] = pd;
+  }
   const bool binding = sr.k_pos == k && k == in->r_max && r_eff == in->r_max;
   int64_t next_r_max = in->r_max;
   if (binding) {
@@ -1259,52 +1307,6 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   }
   }
   if (dist) allreduce(ctx, out->lbar_next, r_eff);
-  // drift telemetry against the previous factors (optimizers.py:366-374)
-  double sd = 0.0, pd = 0.0;
-  const int64_t r_hist = oh.hist_rank;
-  const int64_t r_drift = in->r_prev > 0 ? std::min(std::min(r_hist, in->r_prev), r_eff) : 0;
-  if (r_drift > 0 && out->drift_host && ctx.aux && !dist) {
-    // asynchronous: the drift runs on the auxiliary stream (after everything above) while the
-    // caller moves on; {sigma_drift, projector_drift} land in out->drift_host in aux-stream order
-    if (!ctx.aux_event) WSSR_CUDA(cudaEventCreateWithFlags(&ctx.aux_event, cudaEventDisableTiming));
-    WSSR_CUDA(cudaEventRecord(ctx.aux_event, st));
-    WSSR_CUDA(cudaStreamWaitEvent(ctx.aux, ctx.aux_event, 0));
-    // the aux stream gets its own slab buffer (the main stream's is reused by the next step)
-    cudaStream_t main_stream = ctx.stream;
-    std::swap(ctx.splitk, ctx.aux_splitk);
-    std::swap(ctx.splitk_cap, ctx.aux_splitk_cap);
-    ctx.stream = ctx.aux;
-    auto restore = [&] {
-      ctx.stream = main_stream;
-      std::swap(ctx.splitk, ctx.aux_splitk);
-      std::swap(ctx.splitk_cap, ctx.aux_splitk_cap);
-    };
-    try {
-      Buf sprev(r_hist, ctx.aux), out2(2, ctx.aux);
-      PhaseTimer tm(ctx, 5, 0.0, 0.0);  // events on the aux stream
-      row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
-      drift_enqueue(ctx, P, in->u_prev, in->ld_prev, sprev, r_drift, out->u_next, out->ld_u,
-                    out->sigma, out2);
-      d2h(ctx, out->drift_host, out2, 2 * sizeof(double));
-    } catch (...) {
-      restore();
-      throw;
-    }
-    restore();
-    sd = pd = std::numeric_limits<double>::quiet_NaN();
-  } else if (in->r_prev > 0) {
-    Buf sprev(std::max<int64_t>(r_hist, 1), st);
-    if (r_hist > 0) row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
-    const int64_t r1 = std::min(r_hist, in->r_prev);
-    auto d = drift(ctx, P, in->u_prev, in->ld_prev, sprev, r1, out->u_next, out->ld_u, out->sigma,
-                   r_eff);
-    sd = d.first;
-    pd = d.second;
-  }
-  if (out->drift_host && !std::isnan(sd)) {
-    out->drift_host[0] = sd;
-    out->drift_host[1] = pd;
-  }
 
   // No final wait: every host output is known by now (the rank cut synchronised); the
   // preconditioner / state-refresh kernels finish in stream order while the caller builds the
