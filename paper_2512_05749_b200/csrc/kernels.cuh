@@ -1041,9 +1041,9 @@ __global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict
   pdl_wait();
   constexpr int LD = 65;
   __shared__ double A[64 * LD];
-  __shared__ double v[64], p[64], dg[64], od[64], e2[64];
-  __shared__ double s_beta, s_kc, s_lo, s_hi, s_scale;
-  __shared__ int s_skip, s_best;
+  __shared__ double p[64], dg[64], od[64], e2[64];
+  __shared__ double s_lo, s_hi, s_scale;
+  __shared__ int s_best;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int row = tid >> 4, qq = tid & 15;  // 64 rows x 16 column lanes
   if (prof && tid == 0) prof[1] = clock64();
@@ -1052,42 +1052,45 @@ __global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict
     A[r * LD + c] = 0.5 * (Ain[r * k + c] + Ain[c * k + r]);
   }
   __syncthreads();
+  // Two barriers per reflector: every warp forms (v, beta) itself from the column (v stays in
+  // registers, lane l holding v[l] and v[l + 32]; bitwise the same in every warp), the matvec
+  // takes v by shuffle, and every warp reduces K = beta v^T p / 2 itself after the p barrier.
   for (int j = 0; j + 2 < k; ++j) {
     const int n = k - j - 1;
-    if (warp == 0) {
-      const int i0 = lane, i1 = lane + 32;
-      const double x0v = i0 < n ? A[(j + 1 + i0) * LD + j] : 0.0;
-      const double x1v = i1 < n ? A[(j + 1 + i1) * LD + j] : 0.0;
-      const double xnorm2 = warp_sum(fma(x0v, x0v, x1v * x1v));
-      const double x0 = __shfl_sync(0xffffffffu, x0v, 0);
-      const double xn = sqrt(xnorm2);
-      const double alpha = x0 >= 0.0 ? -xn : xn;
-      const double vtv = 2.0 * xn * (xn + fabs(x0));
-      if (i0 < n) v[i0] = x0v - (i0 == 0 ? alpha : 0.0);
-      if (i1 < n) v[i1] = x1v;
-      if (lane == 0) {
-        dg[j] = A[j * LD + j];
-        od[j] = (vtv > 0.0) ? alpha : x0;
-        s_skip = !(vtv > 0.0);
-        s_beta = (vtv > 0.0) ? 2.0 * fast_rcp(vtv) : 0.0;
-      }
+    const int i0 = lane, i1 = lane + 32;
+    const double x0v = i0 < n ? A[(j + 1 + i0) * LD + j] : 0.0;
+    const double x1v = i1 < n ? A[(j + 1 + i1) * LD + j] : 0.0;
+    const double xnorm2 = warp_sum(fma(x0v, x0v, x1v * x1v));
+    const double x0 = __shfl_sync(0xffffffffu, x0v, 0);
+    const double xn = sqrt(xnorm2);
+    const double alpha = x0 >= 0.0 ? -xn : xn;
+    const double vtv = 2.0 * xn * (xn + fabs(x0));
+    if (tid == 0) {
+      dg[j] = A[j * LD + j];
+      od[j] = (vtv > 0.0) ? alpha : x0;
     }
-    __syncthreads();
-    if (s_skip) {  // column already reduced (uniform); barrier before s_skip is rewritten
+    if (!(vtv > 0.0)) {  // column already reduced (uniform in every warp)
       __syncthreads();
       continue;
     }
-    const double beta = s_beta;
-    // p = beta A' v: row `row`, columns qq + 4 i
+    const double v0 = x0v - (i0 == 0 ? alpha : 0.0), v1 = x1v;  // v[lane], v[lane + 32]
+    const double beta = 2.0 * fast_rcp(vtv);
+    // v at the columns qq + 16 i of this thread: lanes qq / qq + 16, slots 0 / 1
+    double vc[4];
+    vc[0] = __shfl_sync(0xffffffffu, v0, qq);
+    vc[1] = __shfl_sync(0xffffffffu, v0, qq + 16);
+    vc[2] = __shfl_sync(0xffffffffu, v1, qq);
+    vc[3] = __shfl_sync(0xffffffffu, v1, qq + 16);
+    // p = beta A' v: row `row`, columns qq + 16 i
+    double* ar = A + (j + 1 + row) * LD + (j + 1);
     double q = 0.0;
     if (row < n) {
-      const double* ar = A + (j + 1 + row) * LD + (j + 1);
       double qa = 0.0, qb = 0.0;
 #pragma unroll
-      for (int i = 0; i < 4; i += 2) {  // fixed trip count: every load issued up front
+      for (int i = 0; i < 4; i += 2) {
         const int c0 = qq + 16 * i, c1 = c0 + 16;
-        if (c0 < n) qa = fma(ar[c0], v[c0], qa);
-        if (c1 < n) qb = fma(ar[c1], v[c1], qb);
+        if (c0 < n) qa = fma(ar[c0], vc[i], qa);
+        if (c1 < n) qb = fma(ar[c1], vc[i + 1], qb);
       }
       q = qa + qb;
     }
@@ -1095,25 +1098,19 @@ __global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict
     for (int o = 1; o < 16; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     if (qq == 0 && row < n) p[row] = beta * q;
     __syncthreads();
-    if (warp == 0) {
-      const int i0 = lane, i1 = lane + 32;
-      const double t = fma(i0 < n ? v[i0] : 0.0, i0 < n ? p[i0] : 0.0,
-                           (i1 < n ? v[i1] : 0.0) * (i1 < n ? p[i1] : 0.0));
-      const double vp = warp_sum(t);
-      if (lane == 0) s_kc = 0.5 * beta * vp;
-    }
-    __syncthreads();
-    // A' -= v w^T + w v^T,  w = p - Kc v
+    const double p0 = i0 < n ? p[i0] : 0.0, p1 = i1 < n ? p[i1] : 0.0;
+    const double kc = 0.5 * beta * warp_sum(fma(v0, p0, v1 * p1));
+    // A' -= v w^T + w v^T,  w = p - Kc v; v_row by shuffle (rows 2w, 2w+1 of warp w sit on the
+    // same side of 32, so the slot choice is warp-uniform)
+    const double vr = __shfl_sync(0xffffffffu, row < 32 ? v0 : v1, row & 31);
     if (row < n) {
-      const double kc = s_kc;
-      const double vr = v[row], wr = p[row] - kc * vr;
-      double* ar = A + (j + 1 + row) * LD + (j + 1);
+      const double wr = p[row] - kc * vr;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int c = qq + 16 * i;
         if (c < n) {
-          const double vc = v[c], wc = p[c] - kc * vc;
-          ar[c] -= vr * wc + wr * vc;
+          const double wc = p[c] - kc * vc[i];
+          ar[c] -= vr * wc + wr * vc[i];
         }
       }
     }
