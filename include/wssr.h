@@ -45,7 +45,8 @@ enum {
   WSSR_ERR_DEGENERATE_BATCH = 6,  /* errors.DegenerateBatch (estimators.py:61-62, 84-85)     */
   WSSR_ERR_CUDA = 7,              /* CUDA runtime failure                                     */
   WSSR_ERR_NCCL = 8,              /* collective failure                                       */
-  WSSR_ERR_UNSUPPORTED = 9        /* configuration not implemented on the device path         */
+  WSSR_ERR_UNSUPPORTED = 9,       /* configuration not implemented on the device path         */
+  WSSR_ERR_NODE_PROXIMITY = 10    /* errors.NodeProximity   (wavefunction.py:317-318)        */
 };
 
 /* ssi / step flags */
@@ -291,6 +292,29 @@ int wssr_set_aux_stream(wssr_ctx* ctx, void* cuda_stream);
 int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const double* a,
                           const double* b, const double* m, const double* cin, double alpha,
                           double* out);
+
+/* --- producer of O: AceWavefunction.grad_theta_batch (wavefunction.py:307-321) on the device.
+ * Every pointer is device memory.  Orbitals follow the reference's canonical basis order; axis is
+ * the Cartesian component of a p orbital (x 0, y 1, z 2; -1 for s), gate 0 up / 1 down /
+ * 2 either; tails are n_features x max_tail orbital indices padded with -1 (the pooled factors of
+ * each feature, build_tuple_index); coef is theta as (n_electrons x n_features). */
+typedef struct wssr_ace_spec {
+  int64_t n_electrons, n_orbitals, n_features, n_nuclei, max_tail;
+  const double* nuclei;      /* [n_nuclei x 3] */
+  const int32_t* spins;      /* [n_electrons]: 0 up, 1 down */
+  const int32_t* orb_center; /* [n_orbitals] */
+  const int32_t* orb_n;
+  const int32_t* orb_axis;
+  const int32_t* orb_gate;
+  const double* orb_zeta;
+  const int32_t* heads;      /* [n_features] */
+  const int32_t* tails;      /* [n_features x max_tail] */
+  const double* coef;        /* [n_electrons x n_features] */
+} wssr_ace_spec;
+/* out [W x ld_out]: row w = d log|psi| / d theta at positions[w] ([W x N x 3]); n_electrons <= 64.
+ * Returns WSSR_ERR_NODE_PROXIMITY when a walker's determinant vanishes or underflows. */
+int wssr_grad_theta_f64(wssr_ctx* ctx, const wssr_ace_spec* spec, const double* positions,
+                        int64_t n_walkers, double* out, int64_t ld_out);
 
 /* --- diagnostics: C(MxN) = alpha * op(A) B (+C); layout 0: A stored [K][M], 1: A stored [M][K] */
 int wssr_gemm_f64(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64_t k, const double* a,

@@ -45,6 +45,15 @@ class AssembleOut(ctypes.Structure):
     ]
 
 
+class AceSpec(ctypes.Structure):
+    _fields_ = [
+        ("n_electrons", _i64), ("n_orbitals", _i64), ("n_features", _i64), ("n_nuclei", _i64),
+        ("max_tail", _i64), ("nuclei", _vp), ("spins", _vp), ("orb_center", _vp), ("orb_n", _vp),
+        ("orb_axis", _vp), ("orb_gate", _vp), ("orb_zeta", _vp), ("heads", _vp), ("tails", _vp),
+        ("coef", _vp),
+    ]
+
+
 class SsiOut(ctypes.Structure):
     _fields_ = [
         ("u", _vp), ("ld_u", _i64), ("sigma", _vp), ("v", _vp), ("ld_v", _i64),
@@ -89,6 +98,7 @@ SIGNATURES = {
     "wssr_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_aux_stream": (ctypes.c_int, [_vp, _vp]),
+    "wssr_grad_theta_f64": (ctypes.c_int, [_vp, ctypes.POINTER(AceSpec), _vp, _i64, _vp, _i64]),
     "wssr_debug_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp,
                                              _dbl, _vp]),
     "wssr_phase_stats": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_dbl),
@@ -138,6 +148,7 @@ _STATUS = {
     7: errors.DeviceError,
     8: errors.DeviceError,
     9: errors.Unsupported,
+    10: errors.NodeProximity,
 }
 
 _lib = None

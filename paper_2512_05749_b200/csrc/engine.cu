@@ -19,6 +19,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "tallskinny.h"
+#include "producer.h"
 
 struct wssr_ctx {
   wssr::Context c;
@@ -1591,6 +1592,28 @@ int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const 
       default: throw Fail{WSSR_ERR_VALUE, "tall-skinny: unknown op"};
     }
     sync(c);
+  });
+}
+
+int wssr_grad_theta_f64(wssr_ctx* ctx, const wssr_ace_spec* spec, const double* positions,
+                        int64_t n_walkers, double* out, int64_t ld_out) {
+  return guarded(ctx, [&] {
+    Context& c = ctx->c;
+    if (!spec || n_walkers < 0 || (n_walkers > 0 && (!positions || !out)))
+      throw Fail{WSSR_ERR_VALUE, "bad arguments"};
+    const wssr_ace_spec& s = *spec;
+    if (s.n_electrons < 1 || s.n_electrons > 64 || s.n_orbitals < 1 || s.n_features < 1 ||
+        s.max_tail < 0 || ld_out < s.n_electrons * s.n_features)
+      throw Fail{WSSR_ERR_VALUE, "bad ansatz dimensions (n_electrons must be 1..64)"};
+    if (grad_theta_smem(s) > 200 * 1024)
+      throw Fail{WSSR_ERR_UNSUPPORTED, "orbital table too large for one CTA"};
+    Buf flag(1, c.stream);
+    WSSR_CUDA(cudaMemsetAsync(flag, 0, sizeof(double), c.stream));
+    WSSR_CUDA(grad_theta(c, s, positions, n_walkers, out, ld_out, flag.i32()));
+    int* hf = reinterpret_cast<int*>(c.hbuf + 6);
+    d2h(c, hf, flag, sizeof(int));
+    sync(c);
+    if (*hf) throw Fail{WSSR_ERR_NODE_PROXIMITY, "parameter gradient requested on top of a node"};
   });
 }
 
