@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(1024) maxeig64_kernel(const double* __restrict
   __shared__ double p[64], dg[64], od[64], e2[64];
   __shared__ double s_lo, s_hi, s_scale;
   __shared__ int s_best;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int row = tid >> 4, qq = tid & 15;  // 64 rows x 16 column lanes
   if (prof && tid == 0) prof[1] = clock64();
   for (int e = tid; e < k * k; e += 1024) {
