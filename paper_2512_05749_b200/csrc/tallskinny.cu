@@ -1,4 +1,4 @@
-// Tall-skinny FP64 kernels for the P x k blocks of the SSI loop (k = 32 or 64, rows = P up to
+// Tall-skinny FP64 kernels for the P x k blocks of the SSI loop (k = 32, 64 or 128, rows = P up to
 // 10^6): the Grams and triangular products of CholeskyQR2 (qr_orthonormalize, linalg.py:29-61),
 // the Rayleigh quotient q^T w and the residual ||w - q (q^T w)||_F (svdengine.py:137-139), and the
 // drift block u2 - u1 (u1^T u2) (svdengine.py:217-221).
@@ -15,7 +15,10 @@
 //     per 8 rows);
 //   * the residual ||W - A M||_F^2 is reduced in registers and never written;
 //   * per-CTA partials are summed in a fixed order (bitwise repeatable, like every reduction in
-//     this library).
+//     this library);
+//   * occupancy over work per thread: the k x k products run 8-row blocks per warp at two CTAs
+//     per SM, the cross-Grams 16 warps per CTA (measured faster than fewer, fatter warps; the
+//     symmetric Gram is the exception - one load feeding 36 DMMAs wins there).
 #include <cuda_runtime.h>
 
 #include <algorithm>

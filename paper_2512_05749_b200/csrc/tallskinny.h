@@ -1,4 +1,4 @@
-// Tall-skinny FP64 kernels for the P x k blocks (k = 32 or 64); see tallskinny.cu.
+// Tall-skinny FP64 kernels for the P x k blocks (k = 32, 64 or 128); see tallskinny.cu.
 #pragma once
 #include <cuda_runtime.h>
 
