@@ -293,7 +293,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmS, const Params p) {
-  pdl_wait();
   constexpr bool F32 = sizeof(TA) == 4;
   constexpr int A_BYTES = BM * BK * (int)sizeof(TA);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -346,6 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: barrier init and TMEM allocation above overlap the previous
+  // kernel's tail; nothing before this point reads memory it writes
+  pdl_wait();
 
   const int64_t units = (int64_t)p.mtiles * p.nblk * p.nch;
   // unit -> (64-column block fastest, then row tile, then K chunk): the column blocks of one row
@@ -688,7 +690,6 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr) {
 template <bool RM>
 __global__ void __launch_bounds__(kPreThreads, 1)
     ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA, const Params p) {
-  pdl_wait();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* bring = smem + (size_t)PA_DIG * PSTAGES;
@@ -726,6 +727,9 @@ __global__ void __launch_bounds__(kPreThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: barrier init and TMEM allocation above overlap the previous
+  // kernel's tail; nothing before this point reads memory it writes
+  pdl_wait();
 
   const int64_t units = (int64_t)p.mtiles * p.nblk * p.nch;
   // unit -> (64-column block fastest, then row tile, then K chunk): the column blocks of one row
