@@ -781,7 +781,12 @@ __global__ void sort_sigma_kernel(const double* __restrict__ Rv, int k, double r
                                   int* __restrict__ ints_out) {
   pdl_wait();
   extern __shared__ double sd[];
-  for (int i = threadIdx.x; i < k; i += blockDim.x) sd[i] = Rv[i * k + i];
+  // NaN keys (a failed factorisation upstream, the with-fallback pass) sort last: the order is a
+  // permutation whatever the values, so the column gathers below never index out of range
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double v = Rv[i * k + i];
+    sd[i] = isnan(v) ? -INFINITY : v;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     const double si = sd[i];
@@ -791,7 +796,7 @@ __global__ void sort_sigma_kernel(const double* __restrict__ Rv, int k, double r
       rank += (sj > si) || (sj == si && j < i);
     }
     order_out[rank] = i;
-    sigma_out[rank] = si;
+    sigma_out[rank] = Rv[i * k + i];
   }
   __syncthreads();
   if (threadIdx.x == 0) {

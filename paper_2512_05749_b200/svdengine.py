@@ -190,7 +190,7 @@ def randomized_svd(ohat, rank, oversample=10, rng_seed=0):
 
 
 def ssi_svd(ohat, rank, max_iters=3, u_init=None, residual_tol=DEFAULT_RESIDUAL_EXIT,
-            *, report_final_residual=True):
+            *, report_final_residual=True, _careful=False):
     """Dominant singular triplets by warm-startable block subspace iteration
     (svdengine.py:88-158).
 
@@ -219,6 +219,8 @@ def ssi_svd(ohat, rank, max_iters=3, u_init=None, residual_tol=DEFAULT_RESIDUAL_
     o = _ohat_struct(s)
     out = _lib.SsiOut(u=u.data_ptr(), ld_u=rank, sigma=sig.data_ptr(), v=v.data_ptr(), ld_v=rank)
     flags = _lib.WSSR_FLAG_FINAL_RESIDUAL if report_final_residual else 0
+    if _careful:  # testing: every QR host-checked, the Gram-Schmidt patch path where it applies
+        flags |= _lib.WSSR_FLAG_CAREFUL
     _lib.context().call("wssr_ssi_svd_f64", ctypes.byref(o), int(rank), int(max_iters),
                         _lib.ptr(block), _arrays.ld(block), float(residual_tol), flags,
                         ctypes.byref(out))
