@@ -57,3 +57,22 @@ def test_node_raises_node_proximity():
     pos[1, 1] = pos[1, 0]  # two same-spin electrons on top of each other: det M = 0
     with pytest.raises(NodeProximity):
         grad_theta_batch(spec, pos)
+
+
+@pytest.mark.parametrize("tag,walkers", [("be2", 300), ("o2", 150)])
+def test_grad_theta_matches_oracle_many_walkers(tag, walkers):
+    """More walkers than the golden file holds (one CTA each, several waves of the grid), checked
+    against the oracle restatement pinned in tests/test_oracle_wavefunction.py."""
+    from oracle import wavefunction_oracle as wfo
+    from paper_2512_05749_b200.wavefunction import grad_theta_batch
+
+    g = load_golden("ace_grad.npz")
+    rng = np.random.default_rng(walkers)
+    nuc = g[f"{tag}_nuclei"]
+    n = g[f"{tag}_spins"].shape[0]
+    pos = nuc[rng.integers(0, nuc.shape[0], size=(walkers, n))] + rng.standard_normal((walkers, n, 3))
+    ref = wfo.grad_theta(g[f"{tag}_nuclei"], g[f"{tag}_spins"], g[f"{tag}_orb"], g[f"{tag}_zeta"],
+                         g[f"{tag}_heads"], g[f"{tag}_tails"], g[f"{tag}_theta"], pos)
+    out = grad_theta_batch(_spec(g, tag), pos).cpu().numpy()
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err < 1e-11, err
