@@ -1,0 +1,93 @@
+"""Host-side logic that needs no GPU: WssrState construction and validation (the reference's
+TestWssrState, test_optimizers.py:254-270), the WSSR snapshot round trip of a state
+(runner.py:145-157, 203-216), the ctypes table against include/wssr.h, and the status-code to
+exception mapping (the reference's error classes).  CPU-only."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+
+def test_initial_state_shape():
+    from paper_2512_05749_b200.optimizers import WssrState
+
+    st = WssrState.initial(7, rank_init=4)
+    assert tuple(st.obar.shape) == (7, 0) and tuple(st.lbar.shape) == (0,)
+    assert tuple(st.u_prev.shape) == (7, 0)
+    assert st.r_max == 4 and st.step == 0
+
+
+@pytest.mark.parametrize("kw", [dict(delta=1.0), dict(delta=-0.1), dict(r_reg=0.0),
+                                dict(r_reg=1.0), dict(sigma_floor=0.0), dict(rank_init=0),
+                                dict(eps_grow=-1.0)])
+def test_initial_state_validation(kw):
+    from paper_2512_05749_b200.optimizers import WssrState
+
+    with pytest.raises(ValueError):
+        WssrState.initial(3, **kw)
+
+
+def test_state_shape_validation():
+    from paper_2512_05749_b200.optimizers import WssrState
+
+    z = np.zeros
+    with pytest.raises(ValueError):
+        WssrState(obar=z((5, 2)), lbar=z(3), u_prev=z((5, 2)), r_max=2)
+    with pytest.raises(ValueError):
+        WssrState(obar=z(5), lbar=z(2), u_prev=z((5, 2)), r_max=2)
+
+
+def test_state_snapshot_round_trip(tmp_path):
+    from paper_2512_05749_b200 import checkpoint
+    from paper_2512_05749_b200.optimizers import WssrState
+
+    rng = np.random.default_rng(3)
+    f64 = dict(dtype=torch.float64)
+    st = WssrState(obar=torch.tensor(rng.standard_normal((9, 3)), **f64),
+                   lbar=torch.tensor(rng.standard_normal(3), **f64),
+                   u_prev=torch.tensor(np.linalg.qr(rng.standard_normal((9, 3)))[0], **f64),
+                   r_max=5, delta=0.9, sigma_floor=2e-3, sigma_floor_relative=True, r_reg=1e-7,
+                   eps_grow=0.2, step=11)
+    scalars, arrays = checkpoint.wssr_state_snapshot(st)
+    assert set(arrays) == {"wssr_obar", "wssr_lbar", "wssr_u_prev"}
+    path = tmp_path / "s.wssr"
+    checkpoint.write_checkpoint(path, {"wssr": scalars}, arrays, [])
+    s2, a2, _ = checkpoint.read_checkpoint(path)
+    back = checkpoint.wssr_state_restore(s2["wssr"], a2, device=torch.device("cpu"))
+    for name in ("delta", "sigma_floor", "sigma_floor_relative", "r_reg", "eps_grow", "r_max",
+                 "step"):
+        assert getattr(back, name) == getattr(st, name)
+    for name in ("obar", "lbar", "u_prev"):
+        assert torch.equal(getattr(back, name), getattr(st, name))
+
+
+def test_ctypes_table_matches_header():
+    """Every entry point the Python side binds is declared in include/wssr.h with the same
+    number of parameters."""
+    from paper_2512_05749_b200 import _lib
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "include", "wssr.h")) as fh:
+        text = re.sub(r"/\*.*?\*/", "", fh.read(), flags=re.S)
+    decls = {}
+    for m in re.finditer(r"\b(wssr_\w+)\s*\(([^;{]*?)\)\s*;", text):
+        args = m.group(2).strip()
+        decls[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    for name, sig in _lib.SIGNATURES.items():
+        assert name in decls, name
+        argtypes = sig[1] if isinstance(sig, tuple) else sig
+        assert len(argtypes) == decls[name], name
+
+
+def test_status_codes_map_to_reference_errors():
+    from paper_2512_05749_b200 import _lib, errors
+
+    want = {1: ValueError, 2: errors.RankTooLarge, 3: errors.DegenerateInput,
+            4: errors.ZeroMatrix, 5: errors.RankCollapse, 6: errors.DegenerateBatch,
+            10: errors.NodeProximity}
+    for code, exc in want.items():
+        assert issubclass(_lib._STATUS[code], exc), code
+
