@@ -37,6 +37,20 @@ class AceSpec:
         for t, (_, tail) in enumerate(feature_index):
             tails[t, :len(tail)] = tail
 
+        # the producer indexes its tables with these values on the device: check them here
+        n_orb, n_nuc = len(orbs), int(np.asarray(nuclei, dtype=np.float64).reshape(-1, 3).shape[0])
+        heads = np.asarray([h for h, _ in feature_index], dtype=np.int64)
+        if heads.size and (heads.min() < 0 or heads.max() >= n_orb):
+            raise ValueError("feature heads must index the orbital list")
+        if tails.size and (tails.min() < -1 or tails.max() >= n_orb):
+            raise ValueError("feature tails must index the orbital list")
+        if any(not 0 <= o.center < n_nuc for o in orbs):
+            raise ValueError("orbital centres must index the nuclei")
+        if any(o.n < 0 or (o.ell == 1 and o.m not in _M_TO_AXIS) for o in orbs):
+            raise ValueError("unsupported orbital (n < 0 or p-type m outside -1..1)")
+        if any(o.spin not in _GATES for o in orbs):
+            raise ValueError("orbital spin gate must be 'up', 'down' or 'either'")
+
         def i32(a):
             return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
 
@@ -69,7 +83,7 @@ class AceSpec:
                    wf.feature_index, wf.theta, device)
 
     def set_theta(self, theta):
-        t = _arrays.to_tensor(theta).to(self.device).reshape(self.n_electrons, self.n_features)
+        t = _arrays.to_tensor(theta, dev=self.device).reshape(self.n_electrons, self.n_features)
         self._coef = t.contiguous()
         if hasattr(self, "_spec"):
             self._spec.coef = self._coef.data_ptr()

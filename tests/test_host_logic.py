@@ -91,3 +91,24 @@ def test_status_codes_map_to_reference_errors():
     for code, exc in want.items():
         assert issubclass(_lib._STATUS[code], exc), code
 
+
+
+def test_ace_spec_rejects_out_of_range_tables():
+    """The producer indexes its tables on the device; AceSpec checks them on the host."""
+    from collections import namedtuple
+
+    from paper_2512_05749_b200.wavefunction import AceSpec
+
+    Orb = namedtuple("Orb", "center n ell m spin zeta")
+    orbs = [Orb(0, 0, 0, 0, "either", 1.0), Orb(0, 1, 1, 1, "up", 0.5)]
+    nuc = np.zeros((1, 3))
+    theta = np.zeros(2 * 2)
+    cpu = torch.device("cpu")
+    AceSpec(nuc, [0, 1], orbs, [(0, ()), (1, (0,))], theta, device=cpu)
+    with pytest.raises(ValueError):
+        AceSpec(nuc, [0, 1], orbs, [(0, ()), (2, (0,))], theta, device=cpu)
+    with pytest.raises(ValueError):
+        AceSpec(nuc, [0, 1], orbs, [(0, ()), (1, (5,))], theta, device=cpu)
+    with pytest.raises(ValueError):
+        AceSpec(nuc, [0, 1], [Orb(1, 0, 0, 0, "up", 1.0)] + orbs[1:], [(0, ()), (1, ())],
+                theta, device=cpu)
