@@ -414,9 +414,10 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": e2e_steps / (float(t.item()) / 1e3), "unit": "steps/s",
-               "h2d_bytes_per_step": rows * P * esize + rows * 8,  # O and E; theta once
-               "h2d_bytes_once": P * 8,
-               "d2h_bytes_per_step": P * 8, "steps": e2e_steps,
+               # whole job (all ranks): O and E rows every step; theta once per rank
+               "h2d_bytes_per_step": N * P * esize + N * 8,
+               "h2d_bytes_once": world * P * 8,
+               "d2h_bytes_per_step": world * P * 8, "steps": e2e_steps,
                "pipelined_upload": pipelined, "upload_streams": nsplit,
                "path": "estimators.assemble + optimizers.wssr_step on batches uploaded from pinned "
                        "host memory every step (the next batch's upload overlapping the current "
