@@ -1006,6 +1006,10 @@ __global__ void __launch_bounds__(256)
   if (best > 0.0) atomicMax(out + p, (unsigned long long)__double_as_longlong(best));
 }
 
+// Columns below 2^-968 keep the scale 2^1022 (the largest finite power of two): their digits then
+// resolve 2^-1022 absolutely, the FP64 normal range, instead of the factor overflowing.
+constexpr int kMinScaleExp = -968;
+
 // mu_inv[p] = {mu_p, 2^(54 - e_p)} with max_p < 2^e_p; padding columns {0, 0}.
 __global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
                               const double* __restrict__ mu, int64_t cols, int64_t cols_pad,
@@ -1018,7 +1022,7 @@ __global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
       m = mu ? mu[p] : 0.0;
       int e = 0;
       frexp(__longlong_as_double((long long)cmax[p]), &e);  // max < 2^e (0 -> e = 0)
-      inv = ldexp(1.0, 54 - e);
+      inv = ldexp(1.0, 54 - max(e, kMinScaleExp));
     }
     mu_inv[2 * tab_slot(p)] = m;
     mu_inv[2 * tab_slot(p) + 1] = inv;
@@ -1040,7 +1044,7 @@ __global__ void mu_inv_minmax_kernel(const double* __restrict__ cmin,
       const double big = fmax(fabs(cmax[p] - m), fabs(cmin[p] - m));
       int e = 0;
       frexp(isfinite(big) ? big : 0.0, &e);
-      inv = ldexp(1.0, 54 - e);
+      inv = ldexp(1.0, 54 - max(e, kMinScaleExp));
     }
     mu_inv[2 * tab_slot(p)] = m;
     mu_inv[2 * tab_slot(p) + 1] = inv;
@@ -1125,6 +1129,7 @@ __global__ void __launch_bounds__(256)
   if (jj < N) {
     int e = 0;
     frexp(__longlong_as_double((long long)cmax[jj]), &e);
+    e = max(e, kMinScaleExp);
     inv = ldexp(1.0, 54 - e);
     if (blockIdx.x == 0 && kg == 0) colfac[jj] = ldexp(1.0, e - 54 - extra_exp);
   } else if (blockIdx.x == 0 && kg == 0) {

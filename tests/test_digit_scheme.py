@@ -1,0 +1,68 @@
+"""The int8 digit scheme of the O-passes (csrc/ozaki.cu), restated in numpy: the arithmetic the
+kernels rely on, checked on the CPU.
+
+* digitising: X = rint((x - mu) 2^(54 - e)) with |x - mu| < 2^e, biased by 0x80 in each of the
+  low 7 bytes (ozaki.cu to_biased / kBias); plane a holds byte 6 - a XOR 0x80, a signed digit
+  (pack_digits8).  The 7 signed digits reconstruct X exactly, and X is (x - mu) to 2^-54 of the
+  column scale;
+* products: level s = a + b collects the digit pairs of one significance; the kernels keep
+  s <= 7 (34 pairs, NL = 8 TMEM levels) and combine the int32 level sums in FP64.  The dropped
+  pairs weigh at most 2^-64 of the top level, so a dot product of length K is exact to
+  ~K 2^-50 of |a| |b| scales - below the FP64 rounding of the same dot product.
+CPU-only."""
+
+import numpy as np
+
+ND, NL = 7, 8
+BIAS = np.uint64(0x0080808080808080)
+
+
+def digits(x, mu, e):
+    e = max(e, -968)  # ozaki.cu kMinScaleExp: the scale factor stays finite
+    X = np.rint((x - mu) * np.ldexp(1.0, 54 - e)).astype(np.int64)
+    y = X.astype(np.uint64) + BIAS
+    planes = [(((y >> np.uint64(8 * (6 - a))) & np.uint64(0xFF)) ^ np.uint64(0x80))
+              .astype(np.uint8).view(np.int8) for a in range(ND)]
+    return X, np.stack(planes)
+
+
+def test_digits_reconstruct_exactly():
+    rng = np.random.default_rng(0)
+    for scale in (1e-300, 1e-8, 1.0, 3e7, 1e300):
+        x = rng.standard_normal(4096) * scale
+        mu = x.mean()
+        e = int(np.frexp(np.abs(x - mu).max())[1])
+        X, planes = digits(x, mu, e)
+        assert planes.min() >= -128 and planes[0].min() >= -64 and planes[0].max() <= 64
+        rec = sum(planes[a].astype(object) * (256 ** (6 - a)) for a in range(ND))
+        assert all(int(r) == int(v) for r, v in zip(rec, X))
+        ec = max(e, -968)
+        err = np.abs(np.ldexp(X.astype(np.float64), ec - 54) - (x - mu)).max()
+        assert err <= np.ldexp(1.0, ec - 55)
+
+
+def test_truncated_pair_product_is_fp64_grade():
+    rng = np.random.default_rng(1)
+    K = 4096
+    a = rng.standard_normal(K) * np.exp(rng.uniform(-4, 4, K))
+    b = rng.standard_normal(K)
+    ea = int(np.frexp(np.abs(a).max())[1])
+    eb = int(np.frexp(np.abs(b).max())[1])
+    XA, pa = digits(a, 0.0, ea)
+    XB, pb = digits(b, 0.0, eb)
+    levels = np.zeros(NL, dtype=np.int64)   # int32 per K-chunk on the device; exact here
+    pairs = 0
+    for i in range(ND):
+        for j in range(ND):
+            if i + j < NL:
+                levels[i + j] += int(np.dot(pa[i].astype(np.int64), pb[j].astype(np.int64)))
+                pairs += 1
+    assert pairs == 34
+    got = sum(np.ldexp(float(levels[s]), 8 * (12 - s) + ea + eb - 108) for s in range(NL))
+    exact = sum(int(u) * int(v) for u, v in zip(XA, XB))             # the digitised operands
+    exact_f = np.ldexp(float(exact), ea + eb - 108)
+    bound = K * 128 * 128 * 2.0 ** (8 * 4 + ea + eb - 108) * 6       # dropped levels s >= 8
+    assert abs(got - exact_f) <= bound + 4 * np.finfo(float).eps * abs(exact_f)
+    ref = float(np.dot(a.astype(np.longdouble), b.astype(np.longdouble)))
+    scale = np.abs(a) @ np.abs(b)
+    assert abs(got - ref) <= 2.0 ** -48 * scale

@@ -30,7 +30,8 @@ def digit_path(request):
     ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
 
 
-def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift=True):
+def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift=True,
+         tiny_cols=0):
     from paper_2512_05749_b200 import _lib
 
     ctx = _lib.context()
@@ -51,6 +52,8 @@ def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift
         else:
             A[:, :K] *= colscale[None, :]
     A = A + 3.0  # a mean to centre away
+    if tiny_cols:  # columns near the bottom of the FP64 range (digit scale clamped at 2^1022)
+        A[:, :tiny_cols] *= 1e-300
     if f32:
         A = A.float()
     shift = (A[:, :params].double().mean(0)).contiguous() if with_shift else None
@@ -84,6 +87,7 @@ def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift
     res = {}
     for name, C in out.items():
         Cn = C.cpu().numpy()
+        assert np.all(np.isfinite(Cn)), name
         d = Cn[:, :N].astype(np.longdouble) - ref
         res[name] = (float(np.sqrt((d * d).sum() / (ref * ref).sum())),
                      float(np.max(np.abs(d) / absref)))
@@ -116,6 +120,13 @@ def test_ozaki_wide_column_scales(layout):
     r = _run(layout, 600, 64, 2000, scale_cols=True)
     assert r["ozaki"][0] < 2e-15, r
     assert r["ozaki"][1] < 1e-13, r
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_ozaki_columns_near_underflow(layout):
+    """Parameter columns of magnitude 1e-300 (below 2^-968) keep a finite digit scale."""
+    r = _run(layout, 300, 64, 1000, tiny_cols=5)
+    assert r["ozaki"][0] < 2e-15, r
 
 
 def test_ozaki_no_shift_and_padding():
