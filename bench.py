@@ -178,9 +178,6 @@ def workload_config(cfg, args):
         "drift": cfg["drift"], "ssi_max_iters": 3, "ssi_residual_tol": 1e-10,
         "report_final_residual": not args.fast_report,
         "parallelism": f"rows x{args.gpus}",
-        "o_pass_arithmetic": "FP64 products as exact int8 digit products on tcgen05 kind::i8 "
-                             "(7 digits per operand, 34 digit pairs, FP64 combine; "
-                             "csrc/ozaki.cu)",
         "l2": "inputs larger than L2 (O = %.2f GB vs 126 MB); no flush" % (
             cfg["N"] * cfg["P"] * (4 if cfg["dtype"] == "f32" else 8) / 1e9),
     }
@@ -441,6 +438,9 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f32 storage, f64 arithmetic" if f32 else "f64",
             "data": "synthetic (seeded device generator, SURVEY.md 8(d) shapes/distributions)",
             "config": workload_config(cfg, args),
+            "o_pass_arithmetic": "FP64 products as exact int8 digit products on tcgen05 kind::i8 "
+                                 "(7 digits per operand, 34 digit pairs, FP64 combine; "
+                                 "csrc/ozaki.cu)",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
             "wall_s_timed_region": wall,
