@@ -30,7 +30,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, n_samples=96):
     import torch
     import torch.distributed as dist
 
@@ -46,7 +46,7 @@ def _worker(rank, world, port, out_q):
         dist.all_reduce(t)
         return t.numpy().copy()
 
-    cfg = synthetic.config("c0", N=96, P=256, k=8, L=16, delta=0.0, lam=1e-3)
+    cfg = synthetic.config("c0", N=n_samples, P=256, k=8, L=16, delta=0.0, lam=1e-3)
     wl = synthetic.HostWorkload.from_config(cfg, 5)
     st = orc.baseline_state(cfg["P"], cfg["k"], wl.v0_raw(), 0.0, cfg["lam"])
     row0, rows = row_shard(cfg["N"], rank, world)
@@ -72,19 +72,29 @@ def _worker(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
-def test_sharded_step_matches_unsharded_oracle_world2():
+def _run_world(world, n_samples):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n_samples))
+             for r in range(world)]
     for p in procs:
         p.start()
     outs = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank in (0, 1):
+    for rank in range(world):
         for upd, sig, grad, same_ints, lbar in outs[rank]:
             assert upd < 1e-10 and sig < 1e-12 and grad < 1e-12 and same_ints and lbar < 1e-9
+
+
+def test_sharded_step_matches_unsharded_oracle_world2():
+    _run_world(2, 96)
+
+
+def test_sharded_step_ragged_shards_world3():
+    """97 samples over 3 ranks: shards of 33, 32 and 32 rows."""
+    _run_world(3, 97)
