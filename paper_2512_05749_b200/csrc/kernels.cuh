@@ -429,9 +429,13 @@ __device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, 
   constexpr int LD = 65;
   double* X = buf;
   double* Y = buf + 64 * LD;
-  // number of corrections / Neumann terms so that em^(n) < 1e-18
-  const double lg = log10(fmax(em, 1e-300));
-  const int terms = em == 0.0 ? 0 : (int)ceil(-18.0 / lg);  // em < 1e-5 -> at most 4
+  // With e = k em >= ||E||_2: X0 = U(E) is off by O(e^2) and each correction gains a factor e,
+  // so n corrections leave e^(n+2); the Neumann sum to (-X)^J leaves e^(J+1).  Both are taken
+  // below 1e-20 (FP64 resolves 1e-16 of the unit diagonal): em = 1e-12 (a typical second
+  // CholeskyQR2 pass) needs no correction and one Horner product.
+  const double lg = log10(fmax(em * (double)k, 1e-300));
+  const int corr = em == 0.0 ? 0 : max(0, (int)ceil(-20.0 / lg) - 2);
+  const int horner = em == 0.0 ? 0 : max(1, (int)ceil(-20.0 / lg) - 1);
   double e[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -442,7 +446,7 @@ __device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, 
       X[i * LD + c] = i < c ? e[a][b] : (i == c ? 0.5 * e[a][b] : 0.0);
     }
   __syncthreads();
-  for (int it = 0; it < terms; ++it) {  // X <- U(E - X^T X)
+  for (int it = 0; it < corr; ++it) {  // X <- U(E - X^T X)
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -470,7 +474,7 @@ __device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, 
       }
     __syncthreads();
   }
-  // Y = sum_j (-X)^j by Horner: Y <- I - X Y, terms + 1 times
+  // Y = sum_{j <= horner} (-X)^j by Horner: Y <- I - X Y, `horner` times
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -479,7 +483,7 @@ __device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, 
       Y[i * LD + c] = (i == c) ? 1.0 : 0.0;
     }
   __syncthreads();
-  for (int it = 0; it <= terms; ++it) {
+  for (int it = 0; it < horner; ++it) {
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
