@@ -480,10 +480,11 @@ __device__ __forceinline__ void chol_series(const double (&w)[4][4], double em, 
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int i = ty + 16 * a, c = tx + 16 * b;
-      Y[i * LD + c] = (i == c) ? 1.0 : 0.0;
+      // the first Horner step from Y = I is Y = I - X (X I is exact): no product
+      Y[i * LD + c] = (i == c ? 1.0 : 0.0) - (horner > 0 ? X[i * LD + c] : 0.0);
     }
   __syncthreads();
-  for (int it = 0; it < horner; ++it) {
+  for (int it = 1; it < horner; ++it) {
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
