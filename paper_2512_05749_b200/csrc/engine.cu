@@ -13,6 +13,11 @@
 #include <limits>
 #include <memory>
 #include <utility>
+#include <chrono>
+#include <map>
+#include <tuple>
+#include <vector>
+#include <cstdlib>
 
 #include "engine.h"
 #include "ozaki.h"
@@ -64,12 +69,113 @@ double* Context::splitk_buffer(size_t n) {
 namespace {
 
 // Stream-ordered scratch allocation from the device's default memory pool.
+// profiling only (WSSR_HOST_PROF=1): host seconds spent in allocation / synchronisation calls
+struct HostProf {
+  bool on = std::getenv("WSSR_HOST_PROF") != nullptr;
+  double alloc_s = 0, sync_s = 0, free_s = 0;
+  int64_t allocs = 0, syncs = 0;
+  static double now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  }
+};
+HostProf g_hprof;
+
+// Step scratch: blocks released by a Buf are kept per (device, stream, size) and handed to the
+// next Buf of that size on the same stream.  Same-stream reuse is exactly the ordering
+// cudaFreeAsync / cudaMallocAsync give, without a pool call per buffer: at c2 (137 GB of O
+// resident) a cudaMallocAsync of a 1 GB P x k block blocked the host for up to 130 ms while the
+// pool searched for space.  On allocation failure the cached blocks are returned to the pool
+// and the allocation is retried.
+struct ScratchCache {
+  std::mutex mu;
+  struct Key {
+    int dev;
+    cudaStream_t st;
+    size_t bytes;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, st, bytes) < std::tie(o.dev, o.st, o.bytes);
+    }
+  };
+  std::map<Key, std::vector<void*>> free_blocks;
+  std::map<void*, size_t> sizes;
+  size_t cached_bytes = 0;
+  void* take(size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.find(Key{dev, st, bytes});
+      if (it != free_blocks.end() && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        cached_bytes -= bytes;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      trim(dev);
+      e = cudaMallocAsync(&p, bytes, st);
+      if (e != cudaSuccess) throw Fail{WSSR_ERR_CUDA, cudaGetErrorString(e)};
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    sizes[p] = bytes;
+    return p;
+  }
+  void give(void* p, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      const size_t bytes = sizes[p];
+      if (cached_bytes + bytes <= kCap) {
+        free_blocks[Key{dev, st, bytes}].push_back(p);
+        cached_bytes += bytes;
+        return;
+      }
+      sizes.erase(p);
+    }
+    cudaFreeAsync(p, st);
+  }
+  // return this device's cached blocks to the pool (after a device synchronisation, so streams
+  // that no longer exist do not matter)
+  void trim(int dev) {
+    std::vector<void*> out;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto it = free_blocks.begin(); it != free_blocks.end();) {
+        if (it->first.dev != dev) {
+          ++it;
+          continue;
+        }
+        for (void* p : it->second) {
+          out.push_back(p);
+          sizes.erase(p);
+          cached_bytes -= it->first.bytes;
+        }
+        it = free_blocks.erase(it);
+      }
+    }
+    if (out.empty()) return;
+    cudaDeviceSynchronize();
+    for (void* p : out) cudaFree(p);
+  }
+  static constexpr size_t kCap = (size_t)16 << 30;  // bytes kept cached over all devices
+};
+ScratchCache g_scratch;
+
 struct Buf {
   double* p = nullptr;
   cudaStream_t st = nullptr;
   Buf() = default;
   Buf(size_t n, cudaStream_t s) : st(s) {
-    if (n) WSSR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(double), s));
+    if (!n) return;
+    const double t0 = g_hprof.on ? HostProf::now() : 0.0;
+    p = static_cast<double*>(g_scratch.take(n * sizeof(double), s));
+    if (g_hprof.on) g_hprof.alloc_s += HostProf::now() - t0, ++g_hprof.allocs;
   }
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
@@ -85,7 +191,10 @@ struct Buf {
   }
   ~Buf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (!p) return;
+    const double t0 = g_hprof.on ? HostProf::now() : 0.0;
+    g_scratch.give(p, st);
+    if (g_hprof.on) g_hprof.free_s += HostProf::now() - t0;
     p = nullptr;
   }
   operator double*() const { return p; }
@@ -107,7 +216,9 @@ void post_launch(Context& ctx) {
 
 void collect_timing(Context& ctx);
 void sync(Context& ctx) {
+  const double t0 = g_hprof.on ? HostProf::now() : 0.0;
   WSSR_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (g_hprof.on) g_hprof.sync_s += HostProf::now() - t0, ++g_hprof.syncs;
   if (!ctx.pending.empty()) collect_timing(ctx);
 }
 
@@ -1141,7 +1252,7 @@ void materialize_ohat(Context& ctx, const wssr_ohat_f64& oh, double delta, doubl
 }
 
 // ---- wssr_step (optimizers.py:292-391), ssi branch -------------------------------------------
-void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
+void step_impl(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   const wssr_ohat_f64& oh = *in->ohat;
   cudaStream_t st = ctx.stream;
   const int64_t P = oh.n_params, k = in->requested;
@@ -1333,6 +1444,18 @@ void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   out->residual = sr.residual;
   out->sigma_drift = sd;
   out->projector_drift = pd;
+}
+
+void step(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
+  if (!g_hprof.on) return step_impl(ctx, in, out);
+  g_hprof = HostProf();
+  const double t0 = HostProf::now();
+  step_impl(ctx, in, out);
+  std::fprintf(stderr,
+               "[wssr host] step %.2f ms: alloc %.2f ms (%lld), free %.2f ms, sync waits %.2f ms "
+               "(%lld)\n",
+               1e3 * (HostProf::now() - t0), 1e3 * g_hprof.alloc_s, (long long)g_hprof.allocs,
+               1e3 * g_hprof.free_s, 1e3 * g_hprof.sync_s, (long long)g_hprof.syncs);
 }
 
 // ---- NCCL (dlopen'd so the library has no link-time NCCL dependency) ------------------------
@@ -1545,6 +1668,7 @@ void wssr_ctx_destroy(wssr_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFreeHost(ctx->c.hbuf);
   }
+  g_scratch.trim(ctx->c.device);
   if (ctx->c.aux_event) cudaEventDestroy(ctx->c.aux_event);
   if (ctx->c.aux_splitk) cudaFree(ctx->c.aux_splitk);
   if (ctx->c.splitk) cudaFree(ctx->c.splitk);
