@@ -108,6 +108,13 @@ int64_t wssr_kernel_launches(const wssr_ctx* ctx);
  *   4 = as 3 with on-the-fly digitising only (tests). */
 int wssr_set_gemm_path(wssr_ctx* ctx, int path);
 
+/* Precision guard of the int8 O-passes (on by default).  The digits keep every element to 2^-54
+ * of its parameter column's scale; when a nonzero sample row keeps fewer than 42 bits of its own
+ * magnitude (heavy-tailed rows: a few samples dominate the column maxima) the step's SSI is
+ * re-run with the O-passes on FP64 DMMA.  wssr_precision_fallbacks counts those re-runs. */
+int wssr_set_precision_guard(wssr_ctx* ctx, int enabled);
+int64_t wssr_precision_fallbacks(const wssr_ctx* ctx);
+
 /* bench instrumentation: per-phase CUDA-event timing of the O-passes.
  * phase 0 = v = Ohat^T q (svdengine.py:133), 1 = u = Ohat v (svdengine.py:134),
  * 2 = assemble's column-statistics pass (estimators.py:91,93).  Enabling resets the totals. */

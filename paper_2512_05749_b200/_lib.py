@@ -95,6 +95,8 @@ SIGNATURES = {
     "wssr_set_stream": (ctypes.c_int, [_vp, _vp]),
     "wssr_kernel_launches": (_i64, [_vp]),
     "wssr_set_gemm_path": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_set_precision_guard": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_precision_fallbacks": (_i64, [_vp]),
     "wssr_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_aux_stream": (ctypes.c_int, [_vp, _vp]),
@@ -241,6 +243,12 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(self.lib.wssr_kernel_launches(self.handle))
+
+    def set_precision_guard(self, enabled: bool) -> None:
+        self.lib.wssr_set_precision_guard(self.handle, int(bool(enabled)))
+
+    def precision_fallbacks(self) -> int:
+        return int(self.lib.wssr_precision_fallbacks(self.handle))
 
     def set_timing(self, enabled: bool) -> None:
         self.lib.wssr_set_timing(self.handle, int(bool(enabled)))

@@ -585,6 +585,10 @@ struct Ohat {
     int64_t rows = 0;  // planes cover samples [0, rows); the rest is digitised on the fly
   };
   mutable std::shared_ptr<Planes> oz_planes;
+  // precision guard (ozaki.cu row_guard_kernel): status word the verdict goes to (status[2] of
+  // the step's device status, see with_fallback), and whether this operand was checked already
+  mutable int* status = nullptr;
+  mutable bool guard_done = false;
   int64_t cols() const { return r + n; }
 };
 
@@ -684,12 +688,28 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
         n_pl = o.oz_planes->rows;
       }
     }
+    // precision guard on the first pass over this operand: the digitising v pass collects the
+    // row headroom as it goes; any other first pass reads the block once for it
+    std::unique_ptr<Buf> guard_rows;
+    unsigned long long* rowor = nullptr;
+    if (o.status && !o.guard_done && ctx.oz_guard) {
+      o.guard_done = true;
+      guard_rows = std::make_unique<Buf>((size_t)o.n, ctx.stream);
+      rowor = reinterpret_cast<unsigned long long*>(guard_rows->p);
+      WSSR_CUDA(cudaMemsetAsync(rowor, 0, sizeof(double) * o.n, ctx.stream));
+      if (layout != Layout::RM || planes) {
+        WSSR_CUDA(ozaki_row_headroom(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, rowor, ctx.stream));
+        WSSR_CUDA(ozaki_row_guard(ctx, rowor, o.n, o.status + 2, ctx.stream));
+        rowor = nullptr;
+      }
+    }
     if (n_pl == 0 || n_pl >= o.n) {
       // profiling (WSSR_FINE_PHASES): 14 = the step's digitising first pass, 15 = the other
       // row-major (v) passes
       const int fp = (ctx.fine_phases && layout == Layout::RM) ? (store ? 14 : 15) : -1;
       PhaseTimer tm(ctx, fp, 0.0, 0.0);
-      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store));
+      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowor));
+      if (rowor) WSSR_CUDA(ozaki_row_guard(ctx, rowor, o.n, o.status + 2, ctx.stream));
       return;
     }
     // planes for samples [0, n_pl), on-the-fly digits for the rest
@@ -708,8 +728,10 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       a2.B = B + n_pl * ldb;
       a2.accumulate = 1;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store));
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a2, o.f32, tab, ctx.stream, nullptr, nullptr));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowor));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a2, o.f32, tab, ctx.stream, nullptr, nullptr,
+                         rowor ? rowor + n_pl : nullptr));
+    if (rowor) WSSR_CUDA(ozaki_row_guard(ctx, rowor, o.n, o.status + 2, ctx.stream));
     return;
   }
   if (o.f32) {
@@ -822,6 +844,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   const int64_t P = o.P, cols = o.cols();
   const bool dist = ctx.world() > 1;
   cudaStream_t st = ctx.stream;
+  o.status = status;  // the O-passes' precision guard reports into status[2]
   Buf qbuf((size_t)P * k, st), ua((size_t)P * k, st), ub((size_t)P * k, st);
   double* q = qbuf;
   Buf va((size_t)std::max<int64_t>(cols, 1) * k, st), vb((size_t)std::max<int64_t>(cols, 1) * k, st);
@@ -939,30 +962,64 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
 }
 
 // Runs the SSI optimistically (no per-QR host checks); if any CholeskyQR2 flagged a block it
-// could not resolve, re-runs in careful mode, which reproduces the reference's QR branches.
+// could not resolve, re-runs in careful mode, which reproduces the reference's QR branches.  If
+// the int8 O-passes' precision guard fired (status[2]: a sample row far below its columns' digit
+// scales, ozaki.cu row_guard_kernel), the SSI is re-run with the O-passes on FP64 DMMA.
+// Device status words: [0] CholeskyQR2 could not resolve a block, [1] zero matrix, [2] guard.
+__global__ void flag_to_double_kernel(const int* f, double* d) {
+  pdl_wait();
+  if (threadIdx.x == 0) d[0] = f[0] ? 1.0 : 0.0;
+}
+__global__ void double_to_flag_kernel(const double* d, int* f) {
+  pdl_wait();
+  if (threadIdx.x == 0) f[0] = d[0] > 0.0 ? 1 : 0;
+}
+// OR of a device int flag over the ranks (row-sharded runs take the same fallback branch)
+void allreduce_flag(Context& ctx, int* flag) {
+  if (ctx.world() <= 1) return;
+  Buf d(1, ctx.stream);
+  launch_pdl(flag_to_double_kernel, 1, 32, 0, ctx.stream, (const int*)flag, d.p);
+  post_launch(ctx);
+  allreduce(ctx, d, 1);
+  launch_pdl(double_to_flag_kernel, 1, 32, 0, ctx.stream, (const double*)d.p, flag);
+  post_launch(ctx);
+}
+
 template <class F>
 auto with_fallback(Context& ctx, int64_t flags, F&& body) -> decltype(body(false, (int*)nullptr)) {
-  if (!(flags & WSSR_FLAG_CAREFUL)) {
-    Buf status(1, ctx.stream);
-    WSSR_CUDA(cudaMemsetAsync(status, 0, sizeof(double), ctx.stream));
-    int* hs = reinterpret_cast<int*>(ctx.hbuf + 4);
+  struct OzakiRestore {
+    Context& c;
+    bool saved;
+    ~OzakiRestore() { c.ozaki = saved; }
+  } restore{ctx, ctx.ozaki};
+  bool careful = (flags & WSSR_FLAG_CAREFUL) != 0;
+  int* hs = reinterpret_cast<int*>(ctx.hbuf + 4);
+  while (true) {
+    Buf status(2, ctx.stream);
+    WSSR_CUDA(cudaMemsetAsync(status, 0, 2 * sizeof(double), ctx.stream));
+    if (careful && !ctx.ozaki) return body(true, status.i32());
     try {
-      auto r = body(false, status.i32());
-      d2h(ctx, hs, status, 2 * sizeof(int));
+      auto r = body(careful, status.i32());
+      if (ctx.ozaki) allreduce_flag(ctx, status.i32() + 2);
+      d2h(ctx, hs, status, 3 * sizeof(int));
       sync(ctx);
-      if (hs[0] == 0) return r;
+      if (hs[2] == 0 && (careful || hs[0] == 0)) return r;
     } catch (const Fail& f) {
       // a host-side verdict (no positive singular values, ...) reached on the values of a block
       // the optimistic pass could not factorise is not the reference's verdict: re-run carefully
       if (f.code == WSSR_ERR_CUDA || f.code == WSSR_ERR_NCCL) throw;
-      d2h(ctx, hs, status, 2 * sizeof(int));
+      d2h(ctx, hs, status, 3 * sizeof(int));
       sync(ctx);
-      if (hs[0] == 0) throw;
+      if (hs[2] == 0 && (careful || hs[0] == 0)) throw;
     }
+    if (hs[2] != 0) {
+      if (std::getenv("WSSR_VERBOSE"))
+        std::fprintf(stderr, "[wssr] precision guard: heavy-tailed sample rows, O-passes on DMMA\n");
+      ctx.ozaki = false;
+      ++ctx.precision_fallbacks;
+    }
+    if (hs[0] != 0) careful = true;
   }
-  Buf status(1, ctx.stream);
-  WSSR_CUDA(cudaMemsetAsync(status, 0, sizeof(double), ctx.stream));
-  return body(true, status.i32());
 }
 
 // ---- largest eigenvalue of a small symmetric matrix ---------------------------------------
@@ -1687,6 +1744,16 @@ int wssr_set_stream(wssr_ctx* ctx, void* stream) {
 }
 
 int64_t wssr_kernel_launches(const wssr_ctx* ctx) { return ctx ? ctx->c.kernel_launches : 0; }
+
+int wssr_set_precision_guard(wssr_ctx* ctx, int enabled) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  ctx->c.oz_guard = enabled != 0;
+  return WSSR_OK;
+}
+
+int64_t wssr_precision_fallbacks(const wssr_ctx* ctx) {
+  return ctx ? ctx->c.precision_fallbacks : 0;
+}
 
 int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
   if (!ctx || path < 0 || path > 4) return WSSR_ERR_VALUE;

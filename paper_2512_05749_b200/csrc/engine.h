@@ -37,6 +37,8 @@ struct Context {
   bool disable_tma = false;  // force the cp.async GEMM path (tests / A-B comparisons)
   bool ozaki = true;         // O-passes on the int8 tensor cores (exact digit products)
   double oz_min_elems = 4194304.0;  // smallest sample block (elements) sent to that path
+  bool oz_guard = true;      // precision guard of the int8 path (ozaki.cu row_guard_kernel)
+  int64_t precision_fallbacks = 0;  // SSI re-runs on DMMA after the guard fired
   bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
   bool tallskinny = true;    // k = 32/64 Grams and products of P x k blocks: tallskinny.cu
   double* hbuf = nullptr;          // pinned host staging for the step's small readbacks (4096)

@@ -138,3 +138,42 @@ class DeviceWorkload:
         e_all = -1.0 + 0.1 * torch.randn(self.N, generator=ge, device=self.device,
                                          dtype=torch.float64)
         return self.O, e_all[self.row0:self.row0 + self.rows].contiguous()
+
+
+class HeavyRowWorkload(HostWorkload):
+    """The BASELINE generator with heavy-tailed sample rows (precision tests of the int8 O-pass
+    digits, which scale per parameter column):
+
+      * ``kind="pair"``: two rows get +mag z and -mag z for one shared N(0,1) P-vector z (a
+        near-node walker pair: the column means do not move, the column maxima do);
+      * ``kind="tscale"``: every row is multiplied by |t_df| with df = mag (Student-t row scales);
+      * ``kind="telem"``: every element is multiplied by an independent |t_df| draw.
+
+    The heavy part is drawn once (seeded) and kept fixed while the O_t drift as in
+    ``HostWorkload``."""
+
+    def __init__(self, N, P, k, L, alpha, drift, data_seed, v0_seed, kind, mag):
+        super().__init__(N, P, k, L, alpha, drift, data_seed, v0_seed)
+        hr = np.random.default_rng(data_seed + 7777)
+        self.kind, self.mag = kind, mag
+        if kind == "pair":
+            z = hr.standard_normal(P)
+            self.rows = (3 % N, (N // 2 + 5) % N)
+            self.add = np.zeros((N, P))
+            self.add[self.rows[0]] += mag * z
+            self.add[self.rows[1]] -= mag * z
+            self.mul = None
+        elif kind == "tscale":
+            self.add = None
+            self.mul = np.abs(hr.standard_t(mag, size=N))[:, None]
+        elif kind == "telem":
+            self.add = None
+            self.mul = np.abs(hr.standard_t(mag, size=(N, P)))
+        else:
+            raise ValueError(kind)
+
+    def next(self):
+        o, e = super().next()
+        if self.add is not None:
+            return o + self.add, e
+        return o * self.mul, e

@@ -6,10 +6,12 @@ box); the resulting .npz files are committed.
 
 Fixtures (inputs are re-generated from seeds by paper_2512_05749_b200.synthetic; each fixture
 stores input checksums so generator drift is caught):
-  c0_T5.npz      BASELINE config 0 (N=1024, P=4096, k=32, lambda=1e-3), 5 warm-started steps
+  c0_T20.npz     BASELINE config 0 (N=1024, P=4096, k=32, lambda=1e-3), T=20 warm-started steps
   hist_T4.npz    small config with history averaging (delta=0.9), 4 steps
   growth_T4.npz  small config with rank growth (eps_grow=0.5) and widened warm starts
   kat.npz        known-answer vectors: QR patch, SSI closed forms, assemble closed form
+  heavy_*.npz    heavy-tailed sample rows (pairs at 1e4/1e6/1e8, Student-t row scales df 1.5 and
+                 1.0, Student-t elements df 1.5) with the reference's own reordering floor
 """
 
 import os
@@ -72,6 +74,49 @@ def run(cfg, index, T, path, eps_grow=0.0, r_reg=1e-6, k_init=None, save_v_every
     print("wrote", path, os.path.getsize(path), "bytes")
 
 
+def heavy(kind, mag, path, T=2, N=1024, P=4096, k=8):
+    """Heavy-tailed sample rows (synthetic.HeavyRowWorkload), run by the reference twice: on the
+    batch as generated and with the samples permuted.  The permuted run only reorders the
+    reference's own FP64 sums; its distance to the first run is the conditioning floor of the
+    outputs on this input, stored beside them (floor_update / floor_sigma / floor_angle)."""
+    cfg = synthetic.config("c0", N=N, P=P, k=k, L=24, delta=0.0, lam=1e-3)
+    out = {"T": T, "N": N, "P": P, "k": k, "kind": kind, "mag": mag, "lam": cfg["lam"]}
+    perm = np.random.default_rng(99).permutation(N)
+    runs = []
+    for permuted in (False, True):
+        wl = synthetic.HeavyRowWorkload(N, P, k, cfg["L"], cfg["alpha"], cfg["drift"], 300, 400,
+                                        kind, mag)
+        v0, _ = qr_orthonormalize(wl.v0_raw())
+        state = WssrState(obar=np.zeros((P, 0)), lbar=np.zeros(0), u_prev=v0, r_max=k,
+                          delta=0.0, sigma_floor=cfg["lam"], eps_grow=0.0, step=1)
+        res = []
+        for t in range(T):
+            o, e = wl.next()
+            if not permuted:
+                out[f"in_sum_{t}"] = np.array([o.sum(), (o * o).sum(), e.sum()])
+            else:
+                o, e = o[perm], e[perm]
+            theta1, state, diag = wssr_step(np.zeros(P), assemble(batch(o, e)), 1.0, state)
+            res.append((-theta1, np.linalg.norm(state.obar, axis=0), state.u_prev,
+                        np.array([diag.effective_rank, diag.ssi.iterations_used])))
+        runs.append(res)
+    for t in range(T):
+        (u1, s1, v1, i1), (u2, s2, v2, i2) = runs[0][t], runs[1][t]
+        out[f"update_{t}"] = u1
+        out[f"sigma_{t}"] = s1
+        out[f"ints_{t}"] = i1
+        if t == T - 1:
+            out[f"V_{t}"] = v1
+        r = min(v1.shape[1], v2.shape[1])
+        out[f"floor_{t}"] = np.array([
+            np.linalg.norm(u2 - u1) / np.linalg.norm(u1),
+            np.linalg.norm(s2[:r] - s1[:r]) / np.linalg.norm(s1[:r]),
+            np.linalg.norm(v2[:, :r] - v1[:, :r] @ (v1[:, :r].T @ v2[:, :r]), 2),
+            float(np.array_equal(i1, i2))])
+    np.savez_compressed(path, **out)
+    print("wrote", path, os.path.getsize(path), "bytes", [out[f"floor_{t}"] for t in range(T)])
+
+
 def kat(path):
     out = {}
     # QR patch (test_linalg.py:45-51 shape): duplicated column -> r[1,1] == 0
@@ -109,12 +154,22 @@ def kat(path):
     print("wrote", path, os.path.getsize(path), "bytes")
 
 
+def main(which):
+    if "base" in which:
+        c0 = synthetic.config("c0")
+        run(c0, 0, 20, os.path.join(HERE, "c0_T20.npz"))
+        small = synthetic.config("c0", N=96, P=300, k=12, L=20, delta=0.9, lam=1e-3)
+        run(small, 7, 4, os.path.join(HERE, "hist_T4.npz"), save_v_every=True)
+        grow = synthetic.config("c0", N=64, P=160, k=6, L=12, delta=0.5, lam=1e-2)
+        run(grow, 8, 4, os.path.join(HERE, "growth_T4.npz"), eps_grow=0.5, k_init=4,
+            save_v_every=True)
+        kat(os.path.join(HERE, "kat.npz"))
+    if "heavy" in which:
+        for kind, mag in (("pair", 1e4), ("pair", 1e6), ("pair", 1e8), ("tscale", 1.5),
+                          ("tscale", 1.0), ("telem", 1.5)):
+            heavy(kind, mag, os.path.join(HERE, f"heavy_{kind}_{mag:g}.npz"))
+
+
 if __name__ == "__main__":
-    c0 = synthetic.config("c0")
-    run(c0, 0, 5, os.path.join(HERE, "c0_T5.npz"))
-    small = synthetic.config("c0", N=96, P=300, k=12, L=20, delta=0.9, lam=1e-3)
-    run(small, 7, 4, os.path.join(HERE, "hist_T4.npz"), save_v_every=True)
-    grow = synthetic.config("c0", N=64, P=160, k=6, L=12, delta=0.5, lam=1e-2)
-    run(grow, 8, 4, os.path.join(HERE, "growth_T4.npz"), eps_grow=0.5, k_init=4,
-        save_v_every=True)
-    kat(os.path.join(HERE, "kat.npz"))
+    # python tests/golden/make_golden.py [base] [heavy]   (default: all)
+    main(sys.argv[1:] or ["base", "heavy"])

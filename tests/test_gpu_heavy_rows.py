@@ -1,0 +1,95 @@
+"""Heavy-tailed sample rows against fixtures written by the reference itself
+(tests/golden/make_golden.py heavy(): +/- outlier pairs at 1e4/1e6/1e8, Student-t row scales
+with df 1.5 and 1.0, Student-t elements with df 1.5).
+
+The int8 O-pass digits keep each element to 2^-54 of its parameter column's scale, so a row far
+below its columns' scales loses bits relative to itself.  On these inputs the outputs are also
+ill-conditioned for FP64 itself: the reference run on the same samples in another order (which
+only reorders its FP64 sums) moves the update by up to 7e-9 (1e8 pairs).  Each fixture stores
+that floor; the tolerances are the north_star ones (update 1e-10 relative L2, singular values
+1e-9, subspace sine 1e-8) or 4x the reference's own floor where that is larger.
+
+Every GEMM path is checked: auto (0), FP64 DMMA (2), int8 with planes (3) and on the fly (4),
+the int8 paths with the precision guard off (raw digits) and on (rows below 2^-12 of their
+columns' scales send the SSI to DMMA: then bitwise equal to path 2)."""
+
+import numpy as np
+import pytest
+
+from conftest import rel, subspace_sine
+from _runs import HEAVY, heavy_device_run
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(ctx, g, path, guard):
+    ctx.lib.wssr_set_gemm_path(ctx.handle, path)
+    ctx.set_precision_guard(guard)
+    try:
+        before = ctx.precision_fallbacks()
+        runs = heavy_device_run(g)
+        return runs, ctx.precision_fallbacks() - before
+    finally:
+        ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
+        ctx.set_precision_guard(True)
+
+
+def _check(runs, g, label):
+    for t, r in enumerate(runs):
+        fl = g[f"floor_{t}"]
+        assert [r["r_eff"], r["iterations"]] == list(g[f"ints_{t}"]), (label, t)
+        eu = rel(r["update"], g[f"update_{t}"])
+        es = rel(r["sigma"], g[f"sigma_{t}"])
+        assert eu <= max(1e-10, 4 * fl[0]), (label, t, eu, fl[0])
+        assert es <= max(1e-9, 4 * fl[1]), (label, t, es, fl[1])
+        if f"V_{t}" in g:
+            ea = subspace_sine(r["V"], g[f"V_{t}"])
+            assert ea <= max(1e-8, 4 * fl[2]), (label, t, ea, fl[2])
+
+
+@pytest.mark.parametrize("name", HEAVY)
+def test_heavy_rows_every_path(golden, name):
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    g = golden(name)
+    dmma, fb = _run(ctx, g, 2, True)
+    assert fb == 0
+    _check(dmma, g, "dmma")
+    for path in (3, 4):
+        raw, fb = _run(ctx, g, path, False)
+        assert fb == 0
+        _check(raw, g, f"int8 path {path}, guard off")
+        guarded, fb = _run(ctx, g, path, True)
+        _check(guarded, g, f"int8 path {path}, guard on")
+        if fb:  # the guard sent the SSI to DMMA: same kernels, same bits as path 2
+            for a, b in zip(guarded, dmma):
+                np.testing.assert_array_equal(a["update"], b["update"])
+                np.testing.assert_array_equal(a["V"], b["V"])
+    auto, _ = _run(ctx, g, 0, True)
+    _check(auto, g, "auto")
+
+
+@pytest.mark.parametrize("name", ["heavy_pair_1e+06.npz", "heavy_pair_1e+08.npz"])
+def test_guard_fires_on_outlier_pairs(golden, name):
+    """1e6/1e8 pairs leave the other rows > 12 bits below their columns' digit scales."""
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    _, fb = _run(ctx, golden(name), 3, True)
+    assert fb == int(golden(name)["T"])  # once per step
+
+
+def test_guard_quiet_on_gaussian_samples(golden):
+    from _runs import device_run
+
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    ctx.lib.wssr_set_gemm_path(ctx.handle, 3)
+    try:
+        before = ctx.precision_fallbacks()
+        device_run("hist_T4.npz", golden("hist_T4.npz"))
+        assert ctx.precision_fallbacks() == before
+    finally:
+        ctx.lib.wssr_set_gemm_path(ctx.handle, 0)

@@ -46,9 +46,9 @@ def test_closed_loop_matches_reference_fixture(golden, name):
 
 
 def test_closed_loop_matches_oracle_c0(golden):
-    g = golden("c0_T5.npz")
-    dev = device_run("c0_T5.npz", g)
-    ora = oracle_run("c0_T5.npz", g)
+    g = golden("c0_T20.npz")
+    dev = device_run("c0_T20.npz", g)
+    ora = oracle_run("c0_T20.npz", g)
     for t, (d, o) in enumerate(zip(dev, ora)):
         assert d["r_eff"] == o["r_eff"] and d["iterations"] == o["iterations"]
         assert rel(d["update"], o["update"]) < UPDATE_TOL

@@ -57,9 +57,9 @@ def test_sharded_matches_single_rank(golden):
 
 
 def test_sharded_fp32_samples(golden):
-    g = golden("c0_T5.npz")
-    single = device_run("c0_T5.npz", g, dtype=np.float32)
-    sharded = _sharded("c0_T5.npz", g, 2, dtype=np.float32)
+    g = golden("c0_T20.npz")
+    single = device_run("c0_T20.npz", g, dtype=np.float32)
+    sharded = _sharded("c0_T20.npz", g, 2, dtype=np.float32)
     for a, b in zip(single, sharded[0]):
         assert a["r_eff"] == b["r_eff"] and a["iterations"] == b["iterations"]
         assert rel(b["update"], a["update"]) < 1e-10
