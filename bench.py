@@ -1,27 +1,31 @@
 """WSSR-step benchmark (BASELINE.json metric: WSSR steps/sec at N x P x k, FP64, and % of the
-roofline: the O-passes run FP64-exact on the int8 tensor cores and are HBM-bound).
+roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
 
-One JSON line on rank 0.  Workload at N=1: BASELINE configs[1] ("c1": N=4096 samples,
-P=131072 params, k=64, float64, lambda=1e-4, seeded synthetic data of SURVEY.md 8(d), generated
-on the device).  A "step" is estimators.assemble + optimizers.wssr_step (svd_backend="ssi",
-ssi_max_iters=3, ssi_residual_tol=1e-10) on one drifted batch; the drift O_t = O_{t-1} +
-1e-3 G_t is applied between steps outside the timed intervals.  Inputs (4.3 GB)
-are larger than L2 (126 MB), so no L2 flush is needed.  Multi-GPU: rows of O are sharded over
-ranks (torchrun, NCCL); the total work is fixed ("strong" scaling) and the time is the max over
-ranks.
+One JSON line on rank 0.  Workload at N=1: BASELINE configs[2] ("c2": N=16384 samples,
+P=1048576 params, k=128, float64, 137.4 GB of O, lambda=1e-4; the largest configuration that fits
+one B200 and the one BASELINE quotes at 1/2/4/8 GPUs), seeded synthetic data of SURVEY.md 8(d)
+generated on the device.  A "step" is estimators.assemble + optimizers.wssr_step
+(svd_backend="ssi", ssi_max_iters=3, ssi_residual_tol=1e-10) on one drifted batch; the drift
+O_t = O_{t-1} + 1e-3 G_t is applied between steps outside the timed intervals.
+Inputs (137 GB) are far larger than L2 (126 MB), so no L2 flush is needed.  c1 (configs[1]) runs
+after c2 as a nested secondary record (``secondary.c1``), with an e2e through host numpy arrays
+(the reference runner's calling convention) beside the pinned pipeline.  Multi-GPU: rows of O are
+sharded over ranks (torchrun, NCCL); the total work is fixed ("strong" scaling) and the time is
+the max over ranks.
 
 --impl reference times the reference algorithm's CPU implementation (the numpy/LAPACK port in
-oracle/, the reference package itself does not travel to the GPU box) on this host's cores.
+oracle/; the reference package itself does not travel to the GPU box) on this host's cores, on
+bounded samples of the same workload (see cpu_sample_rate).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -32,16 +36,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
 METRIC = "WSSR steps/sec at NxPxk (FP64)"
+DMMA_PEAK_FALLBACK = 37.07  # TF/s, DMMA.8x8x4 probe (round 1, profiles/); live probe preferred
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--secondary", default="c1",
+                    help="config of the nested secondary record ('' to skip)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -104,40 +111,105 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------------------------------------
-def cpu_baseline_run(cfg, index, steps, budget_s=None):
-    """The reference algorithm on the host (oracle port, numpy/LAPACK on all host cores)."""
+# ---- the reference algorithm on the host (oracle port) ------------------------------------
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def host_info():
+    import numpy as np
+
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = [x for x in threadpool_info() if x.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')}"
+    except Exception:
+        pass
+    ram = None
+    try:
+        ram = round(os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30, 1)
+    except Exception:
+        pass
+    return {"cpu_model": model, "numpy": np.__version__, "blas": blas, "host_ram_gib": ram}
+
+
+def _warm_blas():
     import numpy as np
 
     from oracle import wssr_oracle as orc
     from paper_2512_05749_b200 import synthetic
 
-    # LAPACK/BLAS initialisation outside the timed region (first call costs ~1 s)
     small = synthetic.HostWorkload.from_config(synthetic.config("c0", N=64, P=256, k=8, L=8), 0)
     o, e = small.next()
     b = orc.assemble(o, e)
     st = orc.baseline_state(256, 8, small.v0_raw(), 0.0, 1e-3)
     orc.wssr_step(np.zeros(256), b["o_matrix"], b["l_vector"], 1.0, st)
 
-    wl = synthetic.HostWorkload.from_config(cfg, index)
-    st = orc.baseline_state(cfg["P"], cfg["k"], wl.v0_raw(), cfg["delta"], cfg["lam"])
-    times = []
-    for t in range(steps):
-        o, e = wl.next()
-        t0 = time.perf_counter()
-        b = orc.assemble(o, e)
-        _, st, info = orc.wssr_step(np.zeros(cfg["P"]), b["o_matrix"], b["l_vector"], 1.0, st)
-        times.append(time.perf_counter() - t0)
-        if budget_s is not None and sum(times) + times[-1] > budget_s:
-            break
-    return times
+
+def _oracle_step_time(cfg, index, rows):
+    """Seconds of one assemble + wssr_step of the CPU oracle on the first `rows` samples of the
+    config's seeded host workload (all P parameters, rank k)."""
+    import numpy as np
+
+    from oracle import wssr_oracle as orc
+    from paper_2512_05749_b200 import synthetic
+
+    sub = dict(cfg, N=rows)
+    wl = synthetic.HostWorkload.from_config(sub, index)
+    st = orc.baseline_state(cfg["P"], min(cfg["k"], rows), wl.v0_raw()[:, :min(cfg["k"], rows)],
+                            cfg["delta"], cfg["lam"])
+    o, e = wl.next()
+    t0 = time.perf_counter()
+    b = orc.assemble(o, e)
+    orc.wssr_step(np.zeros(cfg["P"]), b["o_matrix"], b["l_vector"], 1.0, st)
+    return time.perf_counter() - t0
 
 
-def host_cores():
+def cpu_sample_rate(cfg, index, threads=None):
+    """The reference algorithm (oracle port, numpy/OpenBLAS) on this host, as steps/s of the FULL
+    config.  Configs whose step fits a bounded CPU sample (c0, c1) run whole steps.  Larger ones
+    (c2: the reference needs ~4|O| = 550 GB of RAM and hours per step) run two bounded samples -
+    the first N1 and N2 samples with all P parameters and rank k - and the step time is
+    extrapolated linearly in the sample count, t(N) = t(N1) + (N - N1) (t(N2) - t(N1)) / (N2 - N1)
+    (the O-passes scale with N; the P x k QR / preconditioner work does not, and the fit keeps it
+    as the intercept).  Returns (steps/s, sample description, seconds spent)."""
+    from contextlib import nullcontext
+
     try:
-        return len(os.sched_getaffinity(0))
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(limits=threads) if threads else nullcontext()
     except Exception:
-        return os.cpu_count() or 1
+        lim = nullcontext()
+    with lim:
+        t_start = time.perf_counter()
+        N = cfg["N"]
+        if N * cfg["P"] <= 4096 * 131072:
+            t = _oracle_step_time(cfg, index, N)
+            return 1.0 / t, f"1 full {cfg['name']} step", time.perf_counter() - t_start
+        n1, n2 = 128, 256
+        t1 = _oracle_step_time(cfg, index, n1)
+        t2 = _oracle_step_time(cfg, index, n2)
+        slope = max(t2 - t1, 0.0) / (n2 - n1)
+        tN = t1 + (N - n1) * slope
+        desc = (f"{cfg['name']} step extrapolated from bounded samples: the first {n1} and {n2} "
+                f"samples (all P={cfg['P']} params, k={cfg['k']}) took {t1:.2f} s and {t2:.2f} s; "
+                f"t(N={N}) = t({n1}) + (N-{n1}) * slope = {tN:.1f} s")
+        return 1.0 / tN, desc, time.perf_counter() - t_start
 
 
 def run_reference(args, rank):
@@ -147,29 +219,40 @@ def run_reference(args, rank):
 
     cfg = synthetic.config(args.config)
     idx = int(args.config[1:]) if args.config[1:].isdigit() else 1
-    times = cpu_baseline_run(cfg, idx, max(1, args.steps), budget_s=150.0)
-    total = sum(times)
-    value = len(times) / total
+    _warm_blas()
+    for _ in range(max(0, args.warmup)):
+        cpu_sample_rate(cfg, idx)
+        break  # one warm-up sample is enough for the BLAS thread pool and page faults
+    rates, desc, spent = [], "", 0.0
+    for _ in range(max(1, args.steps)):
+        r, desc, dt = cpu_sample_rate(cfg, idx)
+        rates.append(r)
+        spent += dt
+        if spent > 150.0:
+            break
+    one, desc1, _ = cpu_sample_rate(cfg, idx, threads=1)
+    value = statistics.median(rates)
     cores = host_cores()
-    sample = (f"{len(times)} full {args.config} step(s) (N={cfg['N']}, P={cfg['P']}, k={cfg['k']}), "
-              f"host numpy/OpenBLAS, first steps of the seeded synthetic workload; timed steps "
-              f"capped by a 150 s budget")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s",
-        "n_gpus": args.gpus, "steps": len(times), "requested_steps": args.steps,
-        "warmup": 1, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "n_gpus": args.gpus, "steps": len(rates), "requested_steps": args.steps,
+        "warmup": 1, "ms_per_step": 1e3 / value, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generator, SURVEY.md 8(d))",
         "config": workload_config(cfg, args),
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "statistic": f"median of {len(rates)} samples (150 s budget)",
+                         "sample": desc, "single_thread": {"value": one, "sample": desc1},
+                         **host_info()},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "rates": rates,
     }
     print(json.dumps(line), flush=True)
 
 
 def workload_config(cfg, args):
+    esize = 4 if cfg["dtype"] == "f32" else 8
     return {
         "workload": f"{cfg['name']}: BASELINE configs[{cfg['name'][1:]}] N={cfg['N']} samples, "
                     f"P={cfg['P']} params, k={cfg['k']}, {cfg['dtype']}",
@@ -179,36 +262,61 @@ def workload_config(cfg, args):
         "report_final_residual": not args.fast_report,
         "parallelism": f"rows x{args.gpus}",
         "l2": "inputs larger than L2 (O = %.2f GB vs 126 MB); no flush" % (
-            cfg["N"] * cfg["P"] * (4 if cfg["dtype"] == "f32" else 8) / 1e9),
+            cfg["N"] * cfg["P"] * esize / 1e9),
     }
 
 
-# ------------------------------------------------------------------------------------------
-def run_ours(args, rank, world, local_rank):
+def _peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f).get("hbm_gbs"), "MEASURED_PEAKS.json hbm_gbs (driver-measured)"
+    except Exception:
+        return 6449.4, "fallback: B200_PROFILING.md copy bandwidth"
+
+
+def _ncu_traffic(name):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu --set full capture of
+    this round (profiles/ncu_summary_r02.json, keyed by config), or None."""
+    try:
+        with open(NCU_SUMMARY) as f:
+            d = json.load(f).get(name, {})
+        if d.get("opass_dram_bytes_per_launch"):
+            return d["opass_dram_bytes_per_launch"], f"{os.path.relpath(NCU_SUMMARY, ROOT)}:{name}"
+    except Exception:
+        pass
+    return None, None
+
+
+# ---- our arm ------------------------------------------------------------------------------
+def measure(cfg_name, args, rank, world, local_rank, e2e_numpy=False, cpu=True):
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2512_05749_b200 import _lib, distributed, estimators, linalg, optimizers, synthetic
 
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg = synthetic.config(args.config)
+    cfg = synthetic.config(cfg_name)
     N, P, k = cfg["N"], cfg["P"], cfg["k"]
     row0, rows = distributed.row_shard(N, rank, world)
     ctx = _lib.context(local_rank)
-    if world > 1:
+    if world > 1 and not getattr(ctx, "_nccl_attached", False):
         distributed.attach_nccl(ctx)
+        ctx._nccl_attached = True
     f32 = cfg["dtype"] == "f32"
     esize = 4 if f32 else 8
     wl = synthetic.DeviceWorkload(N, P, k, cfg["L"], cfg["alpha"], cfg["drift"], seed=101,
                                   row0=row0, rows=rows, device=dev,
                                   dtype=torch.float32 if f32 else torch.float64)
     v0 = linalg.qr_orthonormalize(wl.v0_raw())[0]
-    state = optimizers.WssrState(obar=torch.zeros(0, P, dtype=torch.float64, device=dev).t(),
-                                 lbar=torch.zeros(0, dtype=torch.float64, device=dev),
-                                 u_prev=v0, r_max=k, delta=cfg["delta"], sigma_floor=cfg["lam"],
-                                 eps_grow=0.0, step=1)
+
+    def fresh_state():
+        return optimizers.WssrState(obar=torch.zeros(0, P, dtype=torch.float64, device=dev).t(),
+                                    lbar=torch.zeros(0, dtype=torch.float64, device=dev),
+                                    u_prev=v0, r_max=k, delta=cfg["delta"],
+                                    sigma_floor=cfg["lam"], eps_grow=0.0, step=1)
+
+    state = fresh_state()
     theta = torch.zeros(P, dtype=torch.float64, device=dev)
     final_res = not args.fast_report
     configs_tuple = (None,) * rows
@@ -225,15 +333,15 @@ def run_ours(args, rank, world, local_rank):
         O, E = wl.next()
         theta, state, diag = step(O, E, state, theta)
     torch.cuda.synchronize()
-    peak = ctx.dmma_peak_tflops()
+    peak = ctx.dmma_peak_tflops() or DMMA_PEAK_FALLBACK
 
     stream = torch.cuda.current_stream(dev)
     aux = ctx.aux_stream()
     clocks = ClockSampler(local_rank)
     ctx.set_timing(True)
     launches0 = ctx.kernel_launches()
-    iters = []
-    intervals = []
+    fallbacks0 = ctx.precision_fallbacks()
+    iters, intervals = [], []
     clocks.start()
     barrier()
     torch.cuda.synchronize()
@@ -269,12 +377,14 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = step_ms / args.steps
     value = args.steps / (step_ms / 1e3)
 
-    # ---- roofline (dominant kernels: the two O-pass GEMMs) ----------------------------------
-    # The O-passes run on the int8 tensor cores (exact digit products, csrc/ozaki.cu): each pass
-    # streams the sample block once, so the bound is HBM - algorithmic bytes per pass = N*P*esize
-    # over the measured pass duration (CUDA events around every pass, including
-    # its thin-operand digitising and split-K reduction).  The FP64-equivalent flop rate is
-    # reported beside it against the measured DMMA peak (the FP64 tensor path it replaces).
+    # ---- roofline -----------------------------------------------------------------------------
+    # Dominant kernels: the O-passes v = Ohat^T q and u = Ohat v (ozaki_gemm_kernel, digitising
+    # the sample block on the fly, and ozaki_pre_kernel, streaming pre-digitised planes; tcgen05
+    # kind::i8 exact digit products).  Each pass streams the sample block once: algorithmic bytes
+    # per pass = N*P*esize; achieved = those bytes / the CUDA-event average pass
+    # duration over the timed region (events on the launching stream around every pass,
+    # including its thin-operand digits and split-K reduction).
+    hbm_peak, peak_src = _peaks()
     g_ms = phases[0]["ms"] + phases[1]["ms"]
     g_fl = phases[0]["flops"] + phases[1]["flops"]
     g_by = phases[0]["bytes"] + phases[1]["bytes"]
@@ -282,35 +392,30 @@ def run_ours(args, rank, world, local_rank):
     fp64_equiv = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     achieved = g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0
     m_avg = sum(iters) / len(iters)
+    passes = 2 * (m_avg + 1) if final_res else 2 * m_avg
     flops_alg = 2 * m_avg * 2.0 * N * P * k
     bytes_alg = (1 + 2 * m_avg) * N * P * float(esize)
-    traffic = None
-    if os.path.exists(NCU_SUMMARY):
-        try:
-            with open(NCU_SUMMARY) as f:
-                traffic = json.load(f).get("opass_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    hbm_peak = None
-    try:
-        with open(PEAKS_FILE) as f:
-            hbm_peak = json.load(f).get("hbm_gbs")
-    except Exception:
-        hbm_peak = 6449.4
+    t_hbm = bytes_alg / (hbm_peak * 1e9 * world)
+    t_fp64 = flops_alg / (peak * 1e12 * world)
+    traffic, traffic_src = _ncu_traffic(cfg_name)
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
         "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
-        "kernel": "ozaki_gemm_kernel (O-passes v=Ohat^T q and u=Ohat v on tcgen05 kind::i8)",
+        "traffic_source": traffic_src or "no ncu --set full capture committed for this config",
+        "kernel": "O-passes v=Ohat^T q / u=Ohat v: oz::ozaki_gemm_kernel (digits on the fly) + "
+                  "oz::ozaki_pre_kernel (pre-digitised planes), tcgen05.mma kind::i8",
         "launches": g_n, "avg_launch_ms": g_ms / g_n if g_n else None,
         "bytes_per_launch": g_by / g_n if g_n else None,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
+        "peak_source": peak_src,
         "fp64_equivalent": {"tflops": fp64_equiv, "dmma_peak_tflops": peak,
                             "ratio_to_dmma_peak": fp64_equiv / peak if peak else None,
                             "peak_source": "measured live: DMMA.8x8x4 probe"},
         "per_phase": {
             name: {"ms_avg": ph["ms"] / ph["launches"] if ph["launches"] else None,
-                   "tflops": ph["flops"] / (ph["ms"] * 1e-3) / 1e12 if ph["ms"] else None,
                    "gbs": ph["bytes"] / (ph["ms"] * 1e-3) / 1e9 if ph["ms"] else None,
+                   "frac_hbm": (ph["bytes"] / (ph["ms"] * 1e-3) / 1e9 / hbm_peak)
+                   if ph["ms"] else None,
+                   "fp64_equiv_tflops": ph["flops"] / (ph["ms"] * 1e-3) / 1e12 if ph["ms"] else None,
                    "launches": ph["launches"]}
             for name, ph in zip(["v=OhatT_q", "u=Ohat_v", "assemble_colstats"], phases)},
         "step_budget_ms": dict(
@@ -320,131 +425,226 @@ def run_ours(args, rank, world, local_rank):
             other=ms_per_step - sum(ph["ms"] for ph in phases[:8]) / args.steps),
         "step": {
             "flops_alg": flops_alg, "bytes_alg": bytes_alg, "ssi_iterations": m_avg,
-            "t_roof_ms": bytes_alg / (hbm_peak * 1e9 * world) * 1e3,
-            "frac": bytes_alg / (hbm_peak * 1e9 * world) / (ms_per_step * 1e-3),
-            "hbm_peak_gbs": hbm_peak,
-            "note": "HBM roof of 1 + 2m sample-block reads per step; the faithful default also "
-                    "runs the look-ahead pass pair that fills SsiReport.subspace_residual",
+            "o_passes_run": passes,
+            "t_roof_hbm_ms": t_hbm * 1e3, "frac_hbm": t_hbm / (ms_per_step * 1e-3),
+            "t_roof_fp64_tensor_ms": t_fp64 * 1e3,
+            "frac_north_star": max(t_hbm, t_fp64) / (ms_per_step * 1e-3),
+            "hbm_peak_gbs": hbm_peak, "fp64_tensor_peak_tflops": peak,
+            "note": "north_star's roof is the slower of HBM (1 + 2m sample-block reads) and FP64 "
+                    "flops at the FP64 tensor (DMMA) peak; the O-passes run as exact int8 digit "
+                    "products instead, so frac_north_star can exceed 1 and frac_hbm is the "
+                    "honest denominator.  The faithful default also runs the look-ahead pass "
+                    "pair that fills SsiReport.subspace_residual (2 passes beyond 2m)",
         },
     }
+    rec = {"value": value, "ms_per_step": ms_per_step, "roofline": roofline,
+           "gpu_launches": launches, "clocks": clk, "wall_s_timed_region": wall,
+           "ssi_iterations": iters, "dmma_peak_tflops": peak,
+           "precision_fallbacks": ctx.precision_fallbacks() - fallbacks0,
+           "config": workload_config(cfg, args)}
 
     # ---- end to end through the public API with host buffers ------------------------------
-    # Every step uploads its batch (O, E, theta) from pinned host memory and reads theta' back,
-    # all inside the timed region.  When two device copies of O fit, the upload of batch t+1
-    # runs on a copy stream while step t computes (double buffering, as a serving loop would);
-    # otherwise upload and step alternate.
-    e2e = None
     if not args.no_e2e:
-        e2e_steps = max(2, min(args.steps, 6))
-        o_bytes = rows * P * esize
-        free_b, _ = torch.cuda.mem_get_info(dev)
-        pipelined = free_b > 2 * o_bytes + (8 << 30)
-        nbuf = 2 if pipelined else 1
-        O_h = [torch.empty(rows, P, dtype=wl.O.dtype, pin_memory=True) for _ in range(nbuf)]
-        E_h = [torch.empty(rows, dtype=torch.float64, pin_memory=True) for _ in range(nbuf)]
-        for i in range(nbuf):
-            O, E = wl.next()
-            O_h[i].copy_(O)
-            E_h[i].copy_(E)
-        theta_h = torch.zeros(P, dtype=torch.float64, pin_memory=True)
-        out_h = torch.empty(P, dtype=torch.float64, pin_memory=True)
+        rec["e2e"] = _e2e_pinned(wl, step, fresh_state, theta, rows, P, N, esize, world, dev,
+                                 stream, aux, barrier, dist)
+        if e2e_numpy:
+            rec["e2e_numpy"] = _e2e_numpy(wl, fresh_state, rows, P, N, esize, world, dev, stream,
+                                          aux, barrier, dist, final_res)
+    del wl
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    if cpu and rank == 0 and world == 1 and not args.no_cpu_baseline:
+        idx = int(cfg_name[1:]) if cfg_name[1:].isdigit() else 1
+        _warm_blas()
+        v, desc, _ = cpu_sample_rate(cfg, idx)
+        rec["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": host_cores(),
+                               "kind": "port", "sample": desc + " (oracle/wssr_oracle.py on "
+                               "numpy/OpenBLAS, all host threads)", **host_info()}
+    return rec
+
+
+def _e2e_pinned(wl, step, fresh_state, theta, rows, P, N, esize, world, dev, stream, aux,
+                barrier, dist):
+    """Every step uploads its batch (O, E) from pinned host memory and reads theta' back, all
+    inside the timed region.  When two device copies of O fit, the upload of batch t+1 runs on
+    copy streams while step t computes (double buffering, as a serving loop would); otherwise
+    (c2: one 137 GB copy fills the GPU) upload and step alternate, into the workload's own
+    device buffer.  The host batch lives in 2 GiB pinned row blocks (power-of-two sizes for the
+    pinned allocator)."""
+    import torch
+
+    o_bytes = rows * P * esize
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    pipelined = free_b > 2 * o_bytes + (8 << 30)
+    nbuf = 2 if pipelined else 1
+    blk = max(1, min(rows, (2 << 30) // (P * esize)))
+    bounds = list(range(0, rows, blk)) + [rows]
+    O_h, E_h = [], []
+    for i in range(nbuf):
+        O, E = wl.next()
+        O_h.append([torch.empty(bounds[j + 1] - bounds[j], P, dtype=O.dtype, pin_memory=True)
+                    for j in range(len(bounds) - 1)])
+        for j, hb in enumerate(O_h[i]):
+            hb.copy_(O[bounds[j]:bounds[j + 1]])
+        E_h.append(E.to("cpu").pin_memory())
+    theta_h = torch.zeros(P, dtype=torch.float64, pin_memory=True)
+    out_h = torch.empty(P, dtype=torch.float64, pin_memory=True)
+    if pipelined:
         O_d = [torch.empty(rows, P, dtype=wl.O.dtype, device=dev) for _ in range(nbuf)]
-        E_d = [torch.empty(rows, dtype=torch.float64, device=dev) for _ in range(nbuf)]
-        copy_stream = torch.cuda.Stream(dev) if pipelined else stream
-        # the batch is uploaded in row chunks on several copy streams (several copy engines
-        # in flight over PCIe); WSSR_E2E_SPLIT overrides the count
-        nsplit = max(1, int(os.environ.get("WSSR_E2E_SPLIT", "2"))) if pipelined else 1
-        copy_streams = [copy_stream] + [torch.cuda.Stream(dev) for _ in range(nsplit - 1)]
-        ready = [torch.cuda.Event() for _ in range(nbuf)]
-        freed = [torch.cuda.Event() for _ in range(nbuf)]
-        chunk_done = [torch.cuda.Event() for _ in range(nsplit)]
-        del O, E
-        torch.cuda.synchronize()
-        barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
+    else:
+        O_d = [wl.O]  # the single device copy is overwritten by every upload
+    E_d = [torch.empty(rows, dtype=torch.float64, device=dev) for _ in range(nbuf)]
+    copy_streams = [torch.cuda.Stream(dev) for _ in range(2)] if pipelined else [stream]
+    ready = [torch.cuda.Event() for _ in range(nbuf)]
+    freed = [torch.cuda.Event() for _ in range(nbuf)]
+    done2 = torch.cuda.Event()
+    torch.cuda.synchronize()
+    barrier()
 
-        def upload(t):
+    def upload(t):
+        i = t % nbuf
+        for c, cs in enumerate(copy_streams):
+            with torch.cuda.stream(cs):
+                if pipelined:
+                    cs.wait_event(freed[i])
+                for j in range(c, len(bounds) - 1, len(copy_streams)):
+                    O_d[i][bounds[j]:bounds[j + 1]].copy_(O_h[i][j], non_blocking=True)
+                if c == 0:
+                    E_d[i].copy_(E_h[i], non_blocking=True)
+        if len(copy_streams) > 1:
+            done2.record(copy_streams[1])
+            copy_streams[0].wait_event(done2)
+        ready[i].record(copy_streams[0])
+
+    def run(nsteps, st):
+        for i in range(nbuf):
+            freed[i].record(stream)
+        upload(0)
+        th_d = theta_h.to(dev, non_blocking=True)
+        for t in range(nsteps):
             i = t % nbuf
-            bounds = [rows * c // nsplit for c in range(nsplit + 1)]
-            for c, cs in enumerate(copy_streams):
-                with torch.cuda.stream(cs):
-                    if pipelined:
-                        cs.wait_event(freed[i])
-                    O_d[i][bounds[c]:bounds[c + 1]].copy_(O_h[i][bounds[c]:bounds[c + 1]],
-                                                           non_blocking=True)
-                    if c == 0:
-                        E_d[i].copy_(E_h[i], non_blocking=True)
-                    if c > 0:
-                        chunk_done[c].record(cs)
-            for c in range(1, nsplit):
-                copy_stream.wait_event(chunk_done[c])
-            ready[i].record(copy_stream)
+            stream.wait_event(ready[i])
+            if pipelined and t + 1 < nsteps:
+                upload(t + 1)
+            th_d, st, _ = step(O_d[i], E_d[i], st, th_d)
+            freed[i].record(stream)
+            out_h.copy_(th_d, non_blocking=True)
+            if not pipelined and t + 1 < nsteps:
+                upload(t + 1)
+        stream.wait_stream(aux)
+        return st
 
-        def run_e2e(nsteps, st):
-            for i in range(nbuf):
-                freed[i].record(stream)
-            upload(0)
-            th_d = theta_h.to(dev, non_blocking=True)
-            for t in range(nsteps):
-                i = t % nbuf
-                stream.wait_event(ready[i])
-                if pipelined and t + 1 < nsteps:
-                    upload(t + 1)
-                th_d, st, _ = step(O_d[i], E_d[i], st, th_d)
-                freed[i].record(stream)
-                out_h.copy_(th_d, non_blocking=True)
-                if not pipelined and t + 1 < nsteps:
-                    upload(t + 1)
-            stream.wait_stream(aux)
-            return st
+    st = run(2, fresh_state())  # untimed warm-up: first touches of pinned pages, copy engines
+    torch.cuda.synchronize()
+    barrier()
+    nsteps = 3 if not pipelined else 6
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    st = run(nsteps, st)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    res = {"value": nsteps / (float(t.item()) / 1e3), "unit": "steps/s",
+           # whole job (all ranks): O and E rows every step; theta once per rank
+           "h2d_bytes_per_step": N * P * esize + N * 8, "h2d_bytes_once": world * P * 8,
+           "d2h_bytes_per_step": world * P * 8, "steps": nsteps,
+           "pipelined_upload": pipelined,
+           "path": "estimators.assemble + optimizers.wssr_step on batches uploaded from pinned "
+                   "host memory every step" + (" (the next batch's upload overlapping the "
+                                               "current step)" if pipelined else
+                                               " (upload and step alternate: one device copy "
+                                               "of O fits)") + "; theta' read back every step"}
+    del O_h, E_h, O_d, E_d
+    return res
 
-        state = run_e2e(2, state)  # untimed warm-up: first touches of the pinned pages, copy engines
-        torch.cuda.synchronize()
-        barrier()
-        a.record(stream)
-        state = run_e2e(e2e_steps, state)
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = a.elapsed_time(b)
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": e2e_steps / (float(t.item()) / 1e3), "unit": "steps/s",
-               # whole job (all ranks): O and E rows every step; theta once per rank
-               "h2d_bytes_per_step": N * P * esize + N * 8,
-               "h2d_bytes_once": world * P * 8,
-               "d2h_bytes_per_step": world * P * 8, "steps": e2e_steps,
-               "pipelined_upload": pipelined, "upload_streams": nsplit,
-               "path": "estimators.assemble + optimizers.wssr_step on batches uploaded from pinned "
-                       "host memory every step (the next batch's upload overlapping the current "
-                       "step when two device copies fit); theta' read back to the host every "
-                       "step"}
-        del O_d, E_d
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        idx = int(args.config[1:]) if args.config[1:].isdigit() else 1
-        times = cpu_baseline_run(cfg, idx, 1)
-        cpu = {"value": 1.0 / times[0], "unit": "steps/s", "cores": host_cores(), "kind": "port",
-               "sample": f"1 full {args.config} step (assemble + wssr_step) of the seeded host "
-                         f"workload, oracle/wssr_oracle.py on numpy/OpenBLAS"}
+def _e2e_numpy(wl, fresh_state, rows, P, N, esize, world, dev, stream, aux, barrier, dist,
+               final_res):
+    """The reference runner's calling convention (runner.py:284-314): numpy batches in,
+    numpy theta out (optimizers.wssr_step with numpy theta returns numpy, runner_compat), every
+    copy synchronous through pageable host memory."""
+    import numpy as np
+    import torch
 
+    from paper_2512_05749_b200 import estimators, optimizers
+
+    batches = []
+    for _ in range(2):
+        O, E = wl.next()
+        batches.append((O.cpu().numpy(), E.cpu().numpy()))
+    torch.cuda.synchronize()
+    theta = np.zeros(P)
+    cfgs = (None,) * rows
+
+    def run(nsteps, st, theta):
+        for t in range(nsteps):
+            o, e = batches[t % 2]
+            bundle = estimators.assemble(estimators.SampleBatch(cfgs, e, o))
+            theta, st, _ = optimizers.wssr_step(theta, bundle, 1.0, st,
+                                                report_final_residual=final_res)
+            assert isinstance(theta, np.ndarray)
+        stream.wait_stream(aux)
+        return st, theta
+
+    st, theta = run(2, fresh_state(), theta)
+    torch.cuda.synchronize()
+    barrier()
+    nsteps = 4
+    t0 = time.perf_counter()
+    st, theta = run(nsteps, st, theta)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del batches
+    return {"value": nsteps / float(t.item()), "unit": "steps/s",
+            "h2d_bytes_per_step": N * P * esize + N * 8 + world * P * 8,
+            "d2h_bytes_per_step": world * P * 8, "steps": nsteps,
+            "timer": "host wall clock around the steps (synchronous API: numpy in, numpy out)",
+            "path": "estimators.assemble(SampleBatch of numpy arrays) + optimizers.wssr_step(numpy "
+                    "theta) -> numpy theta', the reference runner's convention"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    rec = measure(args.config, args, rank, world, local_rank)
+    secondary = {}
+    if args.secondary and args.secondary != args.config:
+        sec_args = argparse.Namespace(**vars(args))
+        sec_args.steps = max(args.steps, 20)
+        secondary[args.secondary] = measure(args.secondary, sec_args, rank, world, local_rank,
+                                            e2e_numpy=world == 1, cpu=True)
     if rank == 0:
+        f32 = rec["config"]["workload"].endswith("f32")
         line = {
-            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "metric": METRIC, "value": rec["value"], "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 storage, f64 arithmetic" if f32 else "f64",
             "data": "synthetic (seeded device generator, SURVEY.md 8(d) shapes/distributions)",
-            "config": workload_config(cfg, args),
+            "config": rec["config"],
             "o_pass_arithmetic": "FP64 products as exact int8 digit products on tcgen05 kind::i8 "
                                  "(7 digits per operand, 34 digit pairs, FP64 combine; "
                                  "csrc/ozaki.cu)",
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk,
-            "wall_s_timed_region": wall,
-            "ssi_iterations": iters,
+            "roofline": rec["roofline"], "cpu_baseline": rec.get("cpu_baseline"),
+            "e2e": rec.get("e2e"), "gpu_launches": rec["gpu_launches"], "clocks": rec["clocks"],
+            "wall_s_timed_region": rec["wall_s_timed_region"],
+            "ssi_iterations": rec["ssi_iterations"],
+            "precision_fallbacks": rec["precision_fallbacks"],
+            "secondary": {name: {k: r.get(k) for k in (
+                "value", "ms_per_step", "config", "e2e", "e2e_numpy", "cpu_baseline",
+                "gpu_launches", "clocks", "precision_fallbacks")} | {
+                "roofline": {k: r["roofline"][k] for k in ("achieved", "frac", "per_phase",
+                                                           "step_budget_ms", "step")}}
+                for name, r in secondary.items()},
         }
         print(json.dumps(line), flush=True)
 

@@ -109,9 +109,10 @@ int64_t wssr_kernel_launches(const wssr_ctx* ctx);
 int wssr_set_gemm_path(wssr_ctx* ctx, int path);
 
 /* Precision guard of the int8 O-passes (on by default).  The digits keep every element to 2^-54
- * of its parameter column's scale; when a nonzero sample row keeps fewer than 42 bits of its own
- * magnitude (heavy-tailed rows: a few samples dominate the column maxima) the step's SSI is
- * re-run with the O-passes on FP64 DMMA.  wssr_precision_fallbacks counts those re-runs. */
+ * of its parameter column's scale; when fewer than 1/64 of a sample row's nonzero elements keep
+ * 42 bits of their own magnitude (heavy-tailed rows: a few samples dominate the column maxima)
+ * the step's SSI is re-run with the O-passes on FP64 DMMA.  wssr_precision_fallbacks counts
+ * those re-runs. */
 int wssr_set_precision_guard(wssr_ctx* ctx, int enabled);
 int64_t wssr_precision_fallbacks(const wssr_ctx* ctx);
 

@@ -1,13 +1,39 @@
 """Host-array <-> device-tensor plumbing for the drop-in API.
 
 Inputs may be numpy arrays, Python sequences or torch tensors (any device); the device path
-works on float64 CUDA tensors.  Outputs are float64 CUDA tensors.
+works on float64 CUDA tensors.  Array outputs are float64 CUDA tensors of the ``DeviceArray``
+subclass, which numpy reads (``np.asarray`` copies to the host), so reference-side code that hands
+them to numpy (the runner's snapshot, checkpoint.write_checkpoint) keeps working.
 """
 
 from __future__ import annotations
 
 import numpy as np
 import torch
+
+
+class DeviceArray(torch.Tensor):
+    """A (CUDA) tensor numpy can read: ``np.asarray(x)`` returns a host copy.  Everything else is
+    torch.Tensor."""
+
+    def __array__(self, dtype=None, copy=None):
+        a = torch.Tensor.detach(self).cpu().numpy()
+        return a if dtype is None else a.astype(dtype, copy=False)
+
+    def __deepcopy__(self, memo):
+        return device_array(torch.Tensor.clone(self.as_subclass(torch.Tensor)))
+
+
+def device_array(t):
+    """View a tensor as a DeviceArray (no copy)."""
+    if t is None or not isinstance(t, torch.Tensor) or isinstance(t, DeviceArray):
+        return t
+    return t.as_subclass(DeviceArray)
+
+
+def is_host_array(x) -> bool:
+    """numpy arrays and Python sequences: the reference's calling convention (host in, host out)."""
+    return not isinstance(x, torch.Tensor)
 
 
 def device() -> torch.device:

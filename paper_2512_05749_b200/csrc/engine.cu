@@ -691,16 +691,16 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
     // precision guard on the first pass over this operand: the digitising v pass collects the
     // row headroom as it goes; any other first pass reads the block once for it
     std::unique_ptr<Buf> guard_rows;
-    unsigned long long* rowor = nullptr;
+    unsigned long long* rowcnt = nullptr;
     if (o.status && !o.guard_done && ctx.oz_guard) {
       o.guard_done = true;
       guard_rows = std::make_unique<Buf>((size_t)o.n, ctx.stream);
-      rowor = reinterpret_cast<unsigned long long*>(guard_rows->p);
-      WSSR_CUDA(cudaMemsetAsync(rowor, 0, sizeof(double) * o.n, ctx.stream));
+      rowcnt = reinterpret_cast<unsigned long long*>(guard_rows->p);
+      WSSR_CUDA(cudaMemsetAsync(rowcnt, 0, sizeof(double) * o.n, ctx.stream));
       if (layout != Layout::RM || planes) {
-        WSSR_CUDA(ozaki_row_headroom(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, rowor, ctx.stream));
-        WSSR_CUDA(ozaki_row_guard(ctx, rowor, o.n, o.status + 2, ctx.stream));
-        rowor = nullptr;
+        WSSR_CUDA(ozaki_row_headroom(ctx, o.samp, o.f32, o.lds, o.n, o.P, tab, rowcnt, ctx.stream));
+        WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
+        rowcnt = nullptr;
       }
     }
     if (n_pl == 0 || n_pl >= o.n) {
@@ -708,8 +708,8 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       // row-major (v) passes
       const int fp = (ctx.fine_phases && layout == Layout::RM) ? (store ? 14 : 15) : -1;
       PhaseTimer tm(ctx, fp, 0.0, 0.0);
-      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowor));
-      if (rowor) WSSR_CUDA(ozaki_row_guard(ctx, rowor, o.n, o.status + 2, ctx.stream));
+      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowcnt));
+      if (rowcnt) WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
       return;
     }
     // planes for samples [0, n_pl), on-the-fly digits for the rest
@@ -728,10 +728,10 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       a2.B = B + n_pl * ldb;
       a2.accumulate = 1;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowor));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowcnt));
     WSSR_CUDA(ozaki_gemm(ctx, layout, a2, o.f32, tab, ctx.stream, nullptr, nullptr,
-                         rowor ? rowor + n_pl : nullptr));
-    if (rowor) WSSR_CUDA(ozaki_row_guard(ctx, rowor, o.n, o.status + 2, ctx.stream));
+                         rowcnt ? rowcnt + n_pl : nullptr));
+    if (rowcnt) WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
     return;
   }
   if (o.f32) {

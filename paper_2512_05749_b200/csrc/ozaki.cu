@@ -261,11 +261,14 @@ __host__ __device__ __forceinline__ int64_t tab_slot(int64_t p) {
 __device__ __forceinline__ uint64_t to_biased(double x) {
   return (uint64_t)__double2ll_rn(x) + kBias;
 }
-// |X| (ones' complement for negative X: same bit length except at powers of two) of a biased
-// integer, for the precision guard
-__device__ __forceinline__ uint64_t abs_digits(uint64_t y) {
+// Precision guard counts of one biased digit integer y = X + kBias, packed for one 64-bit sum:
+// low word +1 when X != 0, high word +1 when |X| >= 2^(54 - kGuardBits) (the element keeps at
+// least 54 - kGuardBits bits of its own magnitude).
+constexpr int kGuardBits = 12;
+__device__ __forceinline__ uint64_t guard_count(uint64_t y) {
   const int64_t x = (int64_t)(y - kBias);
-  return (uint64_t)(x ^ (x >> 63));
+  const uint64_t a = (uint64_t)(x ^ (x >> 63));  // |X| (ones' complement: |X| - 1 for X < 0)
+  return (uint64_t)(x != 0) | ((uint64_t)((a >> (54 - kGuardBits)) != 0) << 32);
 }
 
 // profiling only (debug 9): per-K-block timestamps of CTA 0, see tools/ozaki_timeline.py
@@ -290,8 +293,8 @@ struct Params {
   int64_t prows, pblocks;
   const int8_t* bd;        // blocked, pre-swizzled thin digits [nblk * kblocks][448][32]
   int8_t* store;           // on-the-fly v pass: also write the digit planes (layout as `planes`)
-  unsigned long long* rowor;  // on-the-fly v pass: per sample row, OR of |X| over the row (the
-                              // precision guard's row headroom; see row_guard_kernel)
+  unsigned long long* rowcnt;  // on-the-fly v pass: per sample row, packed digit-integer counts
+                               // of the precision guard (see row_guard_kernel)
   int debug;               // profiling only, low bits: 1 = skip digitising, 2 = skip MMAs,
                            // 3 = both, 4 = skip the sample-block loads too; +8 = trace CTA 0
 };
@@ -570,12 +573,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint2*>(dst + a * BM * BK) = make_uint2(w[a][0], w[a][1]);
     };
     uint32_t g = 0, t = 0;
-    const bool guard = RM && p.rowor != nullptr;
+    const bool guard = RM && p.rowcnt != nullptr;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
       int64_t m0, kb0, kb1;
       int nb, kc;
       decode(u, m0, nb, kc, kb0, kb1);
-      uint64_t orA = 0, orB = 0;  // precision guard: OR of |X| over this unit's K range
+      uint64_t cntA = 0, cntB = 0;  // precision guard counts over this unit's K range
       double muA = 0.0, invA = 0.0, muB = 0.0, invB = 0.0;
       if (!RM) {
         if (m0 + rowA < p.M) {
@@ -607,8 +610,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (guard) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            orA |= abs_digits(yA[i]);
-            orB |= abs_digits(yB[i]);
+            cntA += guard_count(yA[i]);
+            cntB += guard_count(yB[i]);
           }
         }
         __syncwarp();
@@ -627,14 +630,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) g_oz_trace[7][g] = clock64();
       }
       if (guard) {
-        // the 4 K-quarter lanes of a row, then one atomic per row (OR: order-independent)
-        orA |= __shfl_xor_sync(0xffffffffu, orA, 8);
-        orA |= __shfl_xor_sync(0xffffffffu, orA, 16);
-        orB |= __shfl_xor_sync(0xffffffffu, orB, 8);
-        orB |= __shfl_xor_sync(0xffffffffu, orB, 16);
+        // the 4 K-quarter lanes of a row, then one atomic per row (integer sums: exact and
+        // order-independent)
+        cntA += __shfl_xor_sync(0xffffffffu, cntA, 8);
+        cntA += __shfl_xor_sync(0xffffffffu, cntA, 16);
+        cntB += __shfl_xor_sync(0xffffffffu, cntB, 8);
+        cntB += __shfl_xor_sync(0xffffffffu, cntB, 16);
         if (q == 0) {
-          if (orA && m0 + rowA < p.M) atomicOr(p.rowor + m0 + rowA, (unsigned long long)orA);
-          if (orB && m0 + rowB < p.M) atomicOr(p.rowor + m0 + rowB, (unsigned long long)orB);
+          if (cntA && m0 + rowA < p.M) atomicAdd(p.rowcnt + m0 + rowA, (unsigned long long)cntA);
+          if (cntB && m0 + rowB < p.M) atomicAdd(p.rowcnt + m0 + rowB, (unsigned long long)cntB);
         }
       }
       // ---- epilogue: D_s (s = 0..7) -> FP64 ----
@@ -1010,41 +1014,43 @@ __global__ void __launch_bounds__(256)
 
 // ---- precision guard ------------------------------------------------------------------------
 // The digits represent every element to 2^-54 of its parameter column's scale.  A sample row whose
-// elements all sit far below their columns' scales (heavy-tailed rows: a few samples dominate the
+// elements sit far below their columns' scales (heavy-tailed rows: a few samples dominate the
 // column maxima) keeps fewer bits, so its v = Ohat^T q entries lose precision relative to
-// themselves (normwise they stay FP64-grade).  rowor[n] = OR over p of |X_np|; a row whose largest
-// digit integer is below 2^(54 - kGuardBits) sets *flag, and the engine re-runs the step's SSI on
-// the FP64 DMMA path (engine.cu with_fallback).  All-zero rows carry no information and are exempt.
-constexpr int kGuardBits = 12;
-
-__global__ void row_guard_kernel(const unsigned long long* __restrict__ rowor, int64_t rows,
+// themselves (normwise they stay FP64-grade).  rowcnt[n] packs, over the row's parameters, the
+// number of nonzero digit integers (low word) and of those within kGuardBits bits of full scale
+// (high word).  A row with fewer than 1/64 of its nonzero elements within kGuardBits bits of
+// their columns' scales sets *flag, and the engine re-runs the step's SSI on the FP64 DMMA path
+// (engine.cu with_fallback).  Gaussian samples keep > 99.9% of their elements within 12 bits;
+// all-zero rows carry no information and are exempt.
+__global__ void row_guard_kernel(const unsigned long long* __restrict__ rowcnt, int64_t rows,
                                  int* __restrict__ flag) {
   pdl_wait();
   bool bad = false;
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < rows;
        n += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long v = rowor[n];
-    bad |= v != 0 && (64 - __clzll(v)) < 54 - kGuardBits;
+    const unsigned long long v = rowcnt[n];
+    const uint64_t nonzero = v & 0xffffffffull, big = v >> 32;
+    bad |= nonzero != 0 && 64 * big < nonzero;
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
-// rowor from the sample block itself (one read of O): used when the step's first O-pass is not a
-// digitising v pass.  One CTA per row chunk of 8 rows, threads over parameters.
+// rowcnt from the sample block itself (one read of O): used when the step's first O-pass is not
+// a digitising v pass.  CTAs over rows, threads over parameters.
 template <typename TA>
 __global__ void __launch_bounds__(256)
     row_headroom_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
-                        const double* __restrict__ mu_inv, unsigned long long* __restrict__ rowor) {
+                        const double* __restrict__ mu_inv, unsigned long long* __restrict__ rowcnt) {
   pdl_wait();
   for (int64_t n = blockIdx.x; n < rows; n += gridDim.x) {
     uint64_t acc = 0;
     for (int64_t pp = threadIdx.x; pp < cols; pp += blockDim.x) {
       const double m = mu_inv[2 * tab_slot(pp)], inv = mu_inv[2 * tab_slot(pp) + 1];
-      acc |= abs_digits(to_biased(((double)A[n * lda + pp] - m) * inv));
+      acc += guard_count(to_biased(((double)A[n * lda + pp] - m) * inv));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicOr(rowor + n, (unsigned long long)acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(rowcnt + n, (unsigned long long)acc);
   }
 }
 
@@ -1363,30 +1369,30 @@ cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, i
 }
 
 cudaError_t ozaki_row_headroom(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
-                               int64_t cols, const double* mu_inv, unsigned long long* rowor,
+                               int64_t cols, const double* mu_inv, unsigned long long* rowcnt,
                                cudaStream_t st) {
   const int grid = (int)std::min<int64_t>(std::max<int64_t>(rows, 1), 8 * ctx.num_sms);
   if (f32)
     launch_pdl(oz::row_headroom_kernel<float>, grid, 256, 0, st, static_cast<const float*>(A), lda,
-               rows, cols, mu_inv, rowor);
+               rows, cols, mu_inv, rowcnt);
   else
     launch_pdl(oz::row_headroom_kernel<double>, grid, 256, 0, st, static_cast<const double*>(A),
-               lda, rows, cols, mu_inv, rowor);
+               lda, rows, cols, mu_inv, rowcnt);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
 }
 
-cudaError_t ozaki_row_guard(Context& ctx, const unsigned long long* rowor, int64_t rows, int* flag,
-                            cudaStream_t st) {
+cudaError_t ozaki_row_guard(Context& ctx, const unsigned long long* rowcnt, int64_t rows,
+                            int* flag, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((rows + 255) / 256, ctx.num_sms);
-  launch_pdl(oz::row_guard_kernel, std::max(grid, 1), 256, 0, st, rowor, rows, flag);
+  launch_pdl(oz::row_guard_kernel, std::max(grid, 1), 256, 0, st, rowcnt, rows, flag);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
 }
 
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
                        cudaStream_t st, const int8_t* planes, int8_t* store,
-                       unsigned long long* rowor) {
+                       unsigned long long* rowcnt) {
   using namespace oz;
   const bool RMm = L == Layout::RM;
   const int64_t M = a.M, N = a.N, K = a.K;
@@ -1462,7 +1468,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   p.bd = Bd;
   p.planes = planes;
   p.store = (!planes && RMm) ? store : nullptr;
-  p.rowor = (!planes && RMm) ? rowor : nullptr;
+  p.rowcnt = (!planes && RMm) ? rowcnt : nullptr;
   if (planes || p.store) {
     p.prows = ozaki_plane_rows(RMm ? M : K);
     p.pblocks = ozaki_plane_pitch(RMm ? K : M) / 32;

@@ -30,19 +30,19 @@ bool ozaki_supported(Layout L, const GemmArgs& a, bool f32);
 // planes: the step's pre-digitised sample block (ozaki_digitize) or nullptr (digitise on the
 // fly); store: with planes == nullptr and the row-major (v) layout, also write the digit planes
 // the on-the-fly pass produces (same layout as ozaki_digitize), so later passes can stream them.
-// rowor (on-the-fly v pass only): per sample row, OR of |X| over the row's digit integers
-// (precision guard, see ozaki_row_guard)
+// rowcnt (on-the-fly v pass only): per sample row, the precision guard's packed digit-integer
+// counts (see ozaki_row_guard)
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
                        cudaStream_t st, const int8_t* planes = nullptr, int8_t* store = nullptr,
-                       unsigned long long* rowor = nullptr);
+                       unsigned long long* rowcnt = nullptr);
 
-// Precision guard: rowor from the sample block directly (one read; for a first O-pass that is not
-// the digitising v pass), and the verdict: *flag |= 1 when a nonzero sample row keeps fewer than
-// 54 - 12 bits of its own magnitude under the per-column digit scales.
+// Precision guard: the row counts from the sample block directly (one read; for a first O-pass
+// that is not the digitising v pass), and the verdict: *flag |= 1 when fewer than 1/64 of a
+// sample row's nonzero elements lie within 12 bits of their columns' digit scales.
 cudaError_t ozaki_row_headroom(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
-                               int64_t cols, const double* mu_inv, unsigned long long* rowor,
+                               int64_t cols, const double* mu_inv, unsigned long long* rowcnt,
                                cudaStream_t st);
-cudaError_t ozaki_row_guard(Context& ctx, const unsigned long long* rowor, int64_t rows, int* flag,
+cudaError_t ozaki_row_guard(Context& ctx, const unsigned long long* rowcnt, int64_t rows, int* flag,
                             cudaStream_t st);
 
 // Digit planes [7][rows][ozaki_plane_pitch(cols)] int8 of the centred, scaled sample block

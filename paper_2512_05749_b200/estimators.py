@@ -40,29 +40,23 @@ class SampleBatch:
         return len(self.configs)
 
 
+@dataclass(frozen=True, eq=False, repr=False)
 class EstimatorBundle:
-    """Everything one optimizer step consumes (estimators.py:34-50).
+    """Everything one optimizer step consumes (estimators.py:34-50): a frozen dataclass with the
+    reference's fields (``dataclasses.fields/replace/asdict`` work).
 
     Constructed either by ``assemble`` (then it holds the raw sample-major derivative block,
-    its column means ``mu`` and ``scale`` = 1/sqrt(N), and ``o_matrix`` is the lazy view
-    ((derivs - mu) * scale).T) or directly with an explicit (n_params, batch) ``o_matrix`` as in
+    its column means and scale 1/sqrt(N); ``o_matrix`` is the lazy view ((derivs - mu) *
+    scale).T, materialised on first access, and ``loss``/``raw_loss`` of a single-rank assemble
+    resolve when first read) or directly with an explicit (n_params, batch) ``o_matrix`` as in
     the reference's test helpers (test_optimizers.py:27-34).
     """
 
-    __slots__ = ("_loss", "_raw_loss", "l_vector", "gradient", "_samples", "_mu", "_scale",
-                 "_fro2_val", "_gradient_exact", "_o_cache", "_n_global", "_scale_table",
-                 "_deferred")
-
-    def __init__(self, loss, raw_loss, o_matrix, l_vector, gradient):
-        o = _arrays.to_tensor(o_matrix)
-        if o.dim() == 1:
-            o = o[:, None]
-        samples = o.t()
-        if not (samples.stride(1) == 1 and samples.stride(0) >= samples.shape[1]):
-            samples = samples.contiguous()
-        self._init(float(loss), float(raw_loss), samples, None, 1.0, -1.0,
-                   _arrays.to_tensor(l_vector), _arrays.to_tensor(gradient), False,
-                   samples.shape[0])
+    loss: float                # mean clipped energy
+    raw_loss: float            # mean energy before clipping
+    o_matrix: object           # (n_params, batch), centered, 1/sqrt(batch)
+    l_vector: object           # (batch,), clipped residuals, 1/sqrt(batch)
+    gradient: object           # (n_params,) = 2 * O @ L
 
     @classmethod
     def _assembled(cls, loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, n_global,
@@ -71,7 +65,8 @@ class EstimatorBundle:
         the scalars of an assemble that returned without waiting for the device; they resolve on
         first access (the optimizer step takes fro2 from the device copy and never waits)."""
         self = cls.__new__(cls)
-        self._init(loss, raw_loss, samples, mu, scale, fro2, l_vector, gradient, True, n_global)
+        self._init(loss, raw_loss, samples, mu, scale, fro2, _arrays.device_array(l_vector),
+                   _arrays.device_array(gradient), True, n_global)
         object.__setattr__(self, "_scale_table", scale_table)
         object.__setattr__(self, "_deferred", deferred)
         return self
@@ -81,8 +76,8 @@ class EstimatorBundle:
         set_ = object.__setattr__
         set_(self, "_loss", loss)
         set_(self, "_raw_loss", raw_loss)
-        set_(self, "l_vector", l_vector)
-        set_(self, "gradient", gradient)
+        set_(self, "_l_vector", l_vector)
+        set_(self, "_gradient", gradient)
         set_(self, "_samples", samples)
         set_(self, "_mu", mu)
         set_(self, "_scale", scale)
@@ -92,9 +87,6 @@ class EstimatorBundle:
         set_(self, "_o_cache", None)
         set_(self, "_n_global", n_global)
         set_(self, "_scale_table", None)
-
-    def __setattr__(self, name, value):
-        raise AttributeError("EstimatorBundle is immutable")
 
     def _resolve(self):
         d = self._deferred
@@ -107,18 +99,6 @@ class EstimatorBundle:
             set_(self, "_raw_loss", float(vals[1]))
             set_(self, "_fro2_val", float(vals[4]))
             set_(self, "_deferred", None)
-
-    @property
-    def loss(self) -> float:
-        """mean of the clipped local energies (estimators.py:92)"""
-        self._resolve()
-        return self._loss
-
-    @property
-    def raw_loss(self) -> float:
-        """mean of the raw local energies (estimators.py:89)"""
-        self._resolve()
-        return self._raw_loss
 
     @property
     def _fro2(self) -> float:
@@ -136,17 +116,11 @@ class EstimatorBundle:
                 return -1.0, d[2]
         return self._fro2_val, None
 
-    @property
-    def o_matrix(self) -> torch.Tensor:
-        """(n_params, batch) centred and scaled matrix (materialised on first access)."""
-        if self._o_cache is None:
-            x = self._samples.to(torch.float64)
-            if self._mu is None and self._scale == 1.0:
-                o = x.t()
-            else:
-                o = ((x - self._mu[None, :]) * self._scale).t()
-            object.__setattr__(self, "_o_cache", o)
-        return self._o_cache
+    def __repr__(self):
+        # the lazy o_matrix stays unmaterialised (at BASELINE sizes it is the whole batch)
+        return (f"EstimatorBundle(loss={self.loss!r}, raw_loss={self.raw_loss!r}, "
+                f"o_matrix=<({self.n_params}, {self.batch_size}) lazy>, "
+                f"l_vector=<({self.batch_size},)>, gradient=<({self.n_params},)>)")
 
     @property
     def n_params(self):
@@ -155,6 +129,59 @@ class EstimatorBundle:
     @property
     def batch_size(self):
         return int(self._samples.shape[0])
+
+
+def _bundle_init(self, loss, raw_loss, o_matrix, l_vector, gradient):
+    """EstimatorBundle(loss, raw_loss, o_matrix, l_vector, gradient) (the reference constructor)"""
+    o = _arrays.to_tensor(o_matrix)
+    if o.dim() == 1:
+        o = o[:, None]
+    samples = o.t()
+    if not (samples.stride(1) == 1 and samples.stride(0) >= samples.shape[1]):
+        samples = samples.contiguous()
+    self._init(float(loss), float(raw_loss), samples, None, 1.0, -1.0,
+               _arrays.device_array(_arrays.to_tensor(l_vector)),
+               _arrays.device_array(_arrays.to_tensor(gradient)), False, samples.shape[0])
+
+
+def _get_loss(self):
+    """mean of the clipped local energies (estimators.py:92)"""
+    self._resolve()
+    return self._loss
+
+
+def _get_raw_loss(self):
+    """mean of the raw local energies (estimators.py:89)"""
+    self._resolve()
+    return self._raw_loss
+
+
+def _get_o_matrix(self):
+    """(n_params, batch) centred and scaled matrix (materialised on first access)"""
+    if self._o_cache is None:
+        x = self._samples.to(torch.float64)
+        if self._mu is None and self._scale == 1.0:
+            o = x.t()
+        else:
+            o = ((x - self._mu[None, :]) * self._scale).t()
+        object.__setattr__(self, "_o_cache", _arrays.device_array(o))
+    return self._o_cache
+
+
+def _readonly(name):
+    def _set(self, value):
+        raise AttributeError(f"EstimatorBundle.{name} is read-only")
+    return _set
+
+
+# the dataclass fields are served lazily (deferred scalars, lazy o_matrix); the generated
+# __init__ is replaced by the reference constructor above, so fields/replace/asdict all work
+EstimatorBundle.__init__ = _bundle_init
+EstimatorBundle.loss = property(_get_loss, _readonly("loss"))
+EstimatorBundle.raw_loss = property(_get_raw_loss, _readonly("raw_loss"))
+EstimatorBundle.o_matrix = property(_get_o_matrix, _readonly("o_matrix"))
+EstimatorBundle.l_vector = property(lambda self: self._l_vector, _readonly("l_vector"))
+EstimatorBundle.gradient = property(lambda self: self._gradient, _readonly("gradient"))
 
 
 def clip_local_energies(energies, n_std=5.0):

@@ -74,4 +74,4 @@ def qr_orthonormalize(a):
     r = torch.empty(n, n, dtype=torch.float64, device=a.device)
     _lib.context().call("wssr_qr_f64", m, n, _lib.ptr(a), _arrays.ld(a), _lib.ptr(q), n,
                         _lib.ptr(r), 0)
-    return q, r
+    return _arrays.device_array(q), _arrays.device_array(r)

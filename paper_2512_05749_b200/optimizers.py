@@ -1,7 +1,9 @@
 """Warm-started low-rank preconditioned update on the device: drop-in for the WSSR part of
 vmcsr.optimizers (optimizers.py:188-401).
 
-``wssr_step`` keeps the reference signature and returns (theta', state', WssrDiagnostics); the
+``wssr_step`` keeps the reference signature and returns (theta', state', WssrDiagnostics) - theta'
+as numpy when theta came in as a host array (the reference runner's convention), else as a CUDA
+tensor; the
 whole step after the host-side warm-start preparation is ONE call into libwssr
 (wssr_step_f64): SSI factorisation, rank cut/growth, gbar, the fused preconditioner apply,
 drift telemetry and the state refresh.  State arrays are float64 CUDA tensors; ``obar`` is kept
@@ -86,23 +88,21 @@ class WssrState:
                    sigma_floor_relative=sigma_floor_relative, r_reg=r_reg, eps_grow=eps_grow)
 
 
+@dataclass(frozen=True)
 class WssrDiagnostics:
-    """Per-step telemetry mirrored into the trace file (optimizers.py:250-258).
+    """Per-step telemetry mirrored into the trace file (optimizers.py:250-258): a frozen
+    dataclass with the reference's fields.
 
-    Same fields as the reference's frozen dataclass.  The two drift values of a single-rank
-    step are computed on a side stream after the step's own work; they resolve (waiting for
-    that stream) on first access, so a caller that never reads them never waits.
+    The two drift values of a single-rank step are computed on a side stream after the step's
+    own work; they resolve (waiting for that stream) on first access, so a caller that never
+    reads them never waits.
     """
 
-    __slots__ = ("ssi", "effective_rank", "r_max", "_drift", "_pending")
-
-    def __init__(self, ssi, effective_rank, r_max, sigma_drift, projector_drift):
-        set_ = object.__setattr__
-        set_(self, "ssi", ssi)
-        set_(self, "effective_rank", effective_rank)
-        set_(self, "r_max", r_max)
-        set_(self, "_drift", (float(sigma_drift), float(projector_drift)))
-        set_(self, "_pending", None)
+    ssi: SsiReport
+    effective_rank: int
+    r_max: int
+    sigma_drift: float
+    projector_drift: float
 
     @classmethod
     def _deferred(cls, ssi, effective_rank, r_max, event, host):
@@ -111,35 +111,29 @@ class WssrDiagnostics:
         return self
 
     def _resolve(self):
-        if self._pending is not None:
-            event, host = self._pending
+        pending = self.__dict__.get("_pending")
+        if pending is not None:
+            event, host = pending
             event.synchronize()
-            object.__setattr__(self, "_drift", tuple(float(x) for x in host.tolist()))
-            object.__setattr__(self, "_pending", None)
-        return self._drift
+            sd, pd = (float(x) for x in host.tolist())
+            self.__dict__["_sigma_drift"] = sd
+            self.__dict__["_projector_drift"] = pd
+            self.__dict__["_pending"] = None
+        return self.__dict__["_sigma_drift"], self.__dict__["_projector_drift"]
 
-    @property
-    def sigma_drift(self) -> float:
-        return self._resolve()[0]
 
-    @property
-    def projector_drift(self) -> float:
-        return self._resolve()[1]
+def _drift_setter(name):
+    def _set(self, value):
+        if "_" + name in self.__dict__:
+            raise AttributeError(f"WssrDiagnostics.{name} is read-only")
+        self.__dict__["_" + name] = float(value)  # the dataclass __init__ (object.__setattr__)
+    return _set
 
-    def __setattr__(self, name, value):
-        raise AttributeError("WssrDiagnostics is immutable")
 
-    def __eq__(self, other):
-        if not isinstance(other, WssrDiagnostics):
-            return NotImplemented
-        return (self.ssi, self.effective_rank, self.r_max, self.sigma_drift,
-                self.projector_drift) == (other.ssi, other.effective_rank, other.r_max,
-                                          other.sigma_drift, other.projector_drift)
-
-    def __repr__(self):
-        return (f"WssrDiagnostics(ssi={self.ssi!r}, effective_rank={self.effective_rank!r}, "
-                f"r_max={self.r_max!r}, sigma_drift={self.sigma_drift!r}, "
-                f"projector_drift={self.projector_drift!r})")
+WssrDiagnostics.sigma_drift = property(lambda self: self._resolve()[0],
+                                       _drift_setter("sigma_drift"))
+WssrDiagnostics.projector_drift = property(lambda self: self._resolve()[1],
+                                           _drift_setter("projector_drift"))
 
 
 def _per_step_seed(rng_seed, step):
@@ -176,6 +170,7 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         raise ValueError(f"svd_backend must be one of {SVD_BACKENDS}, got {svd_backend!r}")
     dense = state.step == 0 or svd_backend in ("exact", "randomized")
     ctx = _lib.context()
+    host_theta = _arrays.is_host_array(theta)
     theta = _arrays.to_tensor(theta).reshape(-1).contiguous()
     samples = bundle._samples
     m = bundle.n_params
@@ -292,9 +287,9 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
                 t.record_stream(aux)
     state_next = replace(
         state,
-        obar=obar_t[:r_eff].t(),
-        lbar=lbar_next[:r_eff],
-        u_prev=u_next[:, :r_eff],
+        obar=_arrays.device_array(obar_t[:r_eff].t()),
+        lbar=_arrays.device_array(lbar_next[:r_eff]),
+        u_prev=_arrays.device_array(u_next[:, :r_eff]),
         r_max=int(sout.next_r_max),
         step=state.step + 1,
     )
@@ -306,6 +301,10 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
         diag = WssrDiagnostics(ssi=report, effective_rank=r_eff, r_max=int(state.r_max),
                                sigma_drift=float(sout.sigma_drift),
                                projector_drift=float(sout.projector_drift))
+    if host_theta:
+        # the reference runner's convention (runner.py:299, 314): numpy theta in, numpy theta'
+        # out (one P-double copy); the state stays on the device (numpy-readable DeviceArrays)
+        theta_next = theta_next.cpu().numpy()
     if return_update:
         return theta_next, state_next, diag, update
     return theta_next, state_next, diag

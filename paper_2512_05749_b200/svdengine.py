@@ -31,6 +31,8 @@ class TruncatedSvd:
     v: object      # (r, n)
 
     def __post_init__(self):
+        for name in ("u", "sigma", "v"):  # numpy-readable device arrays (_arrays.DeviceArray)
+            object.__setattr__(self, name, _arrays.device_array(getattr(self, name)))
         r = self.sigma.shape[0]
         if self.u.dim() != 2 if isinstance(self.u, torch.Tensor) else np.ndim(self.u) != 2:
             raise ValueError("malformed factor shapes")

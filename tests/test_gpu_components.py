@@ -298,4 +298,5 @@ def test_wssr_validation_and_unsupported():
     # dense first step beyond the hand-written dense-SVD limit (512): cuSOLVER on the device
     big = _raw_bundle(np.ones((600, 700)) + np.eye(600, 700), np.ones(700) / 700.0)
     th, st1, _ = wssr_step(np.zeros(600), big, 0.1, WssrState.initial(600, rank_init=2))
-    assert bool(torch.isfinite(th).all()) and st1.step == 1 and st1.u_prev.shape[1] >= 1
+    assert isinstance(th, np.ndarray) and np.isfinite(th).all()
+    assert st1.step == 1 and st1.u_prev.shape[1] >= 1

@@ -72,7 +72,8 @@ def test_heavy_rows_every_path(golden, name):
 
 @pytest.mark.parametrize("name", ["heavy_pair_1e+06.npz", "heavy_pair_1e+08.npz"])
 def test_guard_fires_on_outlier_pairs(golden, name):
-    """1e6/1e8 pairs leave the other rows > 12 bits below their columns' digit scales."""
+    """1e6/1e8 pairs leave > 63/64 of the other rows' elements > 12 bits below their columns' digit
+    scales."""
     from paper_2512_05749_b200 import _lib
 
     ctx = _lib.context()

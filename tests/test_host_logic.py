@@ -112,3 +112,43 @@ def test_ace_spec_rejects_out_of_range_tables():
     with pytest.raises(ValueError):
         AceSpec(nuc, [0, 1], [Orb(1, 0, 0, 0, "up", 1.0)] + orbs[1:], [(0, ()), (1, ())],
                 theta, device=cpu)
+
+
+def test_bundle_and_diagnostics_are_reference_dataclasses():
+    """estimators.py:34-50 / optimizers.py:250-258: frozen dataclasses with the reference
+    fields; the bundle's deferred scalars and lazy o_matrix behave as fields (CPU tensors)."""
+    import dataclasses
+
+    import torch
+
+    from paper_2512_05749_b200.estimators import EstimatorBundle
+    from paper_2512_05749_b200.optimizers import WssrDiagnostics
+    from paper_2512_05749_b200.svdengine import SsiReport
+
+    s = torch.tensor([[1.0, 2.0, 3.0], [3.0, 2.0, 1.0]], dtype=torch.float64)
+    mu = s.mean(0)
+    b = EstimatorBundle._assembled(1.0, 2.0, s, mu, 2 ** -0.5, 4.0, torch.zeros(2),
+                                   torch.zeros(3), 2)
+    assert [f.name for f in dataclasses.fields(b)] == ["loss", "raw_loss", "o_matrix",
+                                                       "l_vector", "gradient"]
+    np.testing.assert_allclose(np.asarray(b.o_matrix),
+                               ((s - mu) * 2 ** -0.5).t().numpy())
+    assert sorted(dataclasses.asdict(b)) == ["gradient", "l_vector", "loss", "o_matrix",
+                                             "raw_loss"]
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        b.raw_loss = 0.0
+    assert "lazy" in repr(b)
+    d = WssrDiagnostics(SsiReport(3, 1e-6, True), 4, 5, 0.25, 0.5)
+    assert dataclasses.replace(d, effective_rank=2).effective_rank == 2
+    assert dataclasses.asdict(d)["projector_drift"] == 0.5
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        d.sigma_drift = 1.0
+
+    class _Done:
+        def synchronize(self):
+            pass
+
+    lazy = WssrDiagnostics._deferred(SsiReport(3, 1e-6, True), 4, 5, _Done(),
+                                     torch.tensor([0.125, 0.75], dtype=torch.float64))
+    assert (lazy.sigma_drift, lazy.projector_drift) == (0.125, 0.75)
+    assert lazy == WssrDiagnostics(SsiReport(3, 1e-6, True), 4, 5, 0.125, 0.75)
