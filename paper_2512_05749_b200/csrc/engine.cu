@@ -412,23 +412,14 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
   if (k <= 64) {
     // dynamic shared memory enables the near-identity series path (second CholeskyQR2 pass)
     const int series_smem = (int)(2 * 64 * 65 * sizeof(double));  // series path / blocked sweep
-    static bool attr = false;
-    if (!attr) {
-      WSSR_CUDA(cudaFuncSetAttribute(chol_inv_reg64_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(2 * 64 * 65 * sizeof(double))));
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    WSSR_CUDA(smem_attr_once(attr, chol_inv_reg64_kernel, series_smem));
     launch_pdl(chol_inv_reg64_kernel, 1, 256, series_smem, ctx.stream, G, k, R, Rinv, status,
                                                                  kCholPivotRel,
                                                                  ctx.chol_series ? 1 : 0, nullptr);
   } else if (smem <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      WSSR_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    WSSR_CUDA(smem_attr_once(attr, chol_inv_smem_kernel, 200 * 1024));
     launch_pdl(chol_inv_smem_kernel, 1, 256, smem, ctx.stream, G, k, R, Rinv, status, kCholPivotRel);
   } else {
     Buf W(chol_scratch_doubles(k), ctx.stream);
@@ -1030,12 +1021,8 @@ void maxeig(Context& ctx, const double* A, int k, double* out_dev) {
   }
   const size_t smem = sizeof(double) * ((size_t)k * (k + 1) + 4 * (size_t)k);
   if (smem <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      WSSR_CUDA(cudaFuncSetAttribute(maxeig_smem_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    WSSR_CUDA(smem_attr_once(attr, maxeig_smem_kernel, 200 * 1024));
     launch_pdl(maxeig_smem_kernel, 1, 256, smem, ctx.stream, A, k, out_dev);
   } else {
     Buf W((size_t)k * (k + 1) + 4 * (size_t)k, ctx.stream);

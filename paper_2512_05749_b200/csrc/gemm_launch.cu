@@ -61,13 +61,9 @@ template <Layout L, int BM, int BN, int BK, int WMW, int WNW, int ST, int VA, in
 cudaError_t launch_one(const GemmArgs& a, int splits, cudaStream_t st) {
   using Cfg = GemmCfg<L, BM, BN, BK, WMW, WNW, ST>;
   auto kern = gemm_dmma_kernel<L, BM, BN, BK, WMW, WNW, ST, VA, VB>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_set{0};  // per instantiation, one bit per device
+  cudaError_t e = smem_attr_once(attr_set, kern, (int)Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)((a.N + BN - 1) / BN), (unsigned)splits);
   launch_pdl(kern, grid, Cfg::kThreads, Cfg::kSmemBytes, st, a);
   ++g_launches;
@@ -117,13 +113,9 @@ struct TmaTile {
   }
   static cudaError_t launch(const GemmArgs& a, int splits, bool, bool, cudaStream_t st) {
     auto kern = gemm_tma_kernel<L, BM, BN, BK, WMW, WNW, ST, TA, PERSIST>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)Cfg::kSmemBytes);
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};
+    cudaError_t e = smem_attr_once(attr_set, kern, (int)Cfg::kSmemBytes);
+    if (e != cudaSuccess) return e;
     CUtensorMap tA, tB, tS;
     std::memset(&tS, 0, sizeof(tS));
     bool ok;

@@ -560,7 +560,10 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int i = ty + 16 * a, c = tx + 16 * b;
-        em = fmax(em, fabs(w[a][b] - (i == c ? 1.0 : 0.0)));
+        // NaN/Inf entries force em = +inf (fmax would drop a NaN): such a Gram takes the
+        // blocked sweep, whose pivot test reports it
+        const double d = fabs(w[a][b] - (i == c ? 1.0 : 0.0));
+        em = d <= 1.79769313486231570e308 ? fmax(em, d) : __longlong_as_double(0x7ff0000000000000ll);
       }
     __shared__ double red_em[8];
     em = warp_max(em);

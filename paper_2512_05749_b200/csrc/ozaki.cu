@@ -1262,27 +1262,18 @@ bool make_map_cm(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer
 template <bool RM, typename TA>
 cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tS,
                    const Params& p, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<RM, TA>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t e = smem_attr_once(attr, ozaki_gemm_kernel<RM, TA>, (int)kSmem);
+  if (e != cudaSuccess) return e;
   launch_pdl(ozaki_gemm_kernel<RM, TA>, grid, kThreads, kSmem, st, tA, tB, tS, p);
   return cudaGetLastError();
 }
 
 template <bool RM>
 cudaError_t launch_pre(const CUtensorMap& tA, const Params& p, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ozaki_pre_kernel<RM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kPreSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t e = smem_attr_once(attr, ozaki_pre_kernel<RM>, (int)kPreSmem);
+  if (e != cudaSuccess) return e;
   launch_pdl(ozaki_pre_kernel<RM>, grid, kPreThreads, kPreSmem, st, tA, p);
   return cudaGetLastError();
 }

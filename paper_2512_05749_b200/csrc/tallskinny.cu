@@ -518,13 +518,9 @@ cudaError_t mul_launch(Context& ctx, int64_t rows, const double* A, int64_t lda,
     if (!partial) return cudaErrorMemoryAllocation;
   }
   constexpr int smem = KC * KC * 8;  // R^-1 / M in fragment order
-  static bool attr = false;  // one per instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(mul_kernel<KC, TRI, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};  // one per instantiation, one bit per device
+  cudaError_t e = smem_attr_once(attr, mul_kernel<KC, TRI, MODE>, smem);
+  if (e != cudaSuccess) return e;
   launch_pdl(mul_kernel<KC, TRI, MODE>, grid, kThreads, smem, ctx.stream, A, lda, M, ldm, alpha,
              Cin, ldcin, Y, ldy, rows, partial);
   ctx.kernel_launches += 1;

@@ -44,6 +44,18 @@ def test_cholesky_flags_deficient_and_zero():
     assert st == (1, 1)
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_cholesky_near_identity_nonfinite_is_flagged(bad):
+    # a near-identity Gram (the series path's domain) with one non-finite off-diagonal pair must
+    # not come back as a finite-looking factor with status 0 (fmax dropped NaN)
+    k = 64
+    g = np.eye(k) + 1e-14 * np.random.default_rng(5).standard_normal((k, k))
+    g = 0.5 * (g + g.T)
+    g[3, 40] = g[40, 3] = bad
+    r, rinv, st = _small(0, g)
+    assert st[0] != 0 or not (np.isfinite(r).all() and np.isfinite(rinv).all())
+
+
 @pytest.mark.parametrize("k", [1, 2, 3, 17, 64, 128, 255])
 def test_maxeig(k):
     rng = np.random.default_rng(100 + k)

@@ -46,9 +46,10 @@ if __name__ == "__main__":
         print(f"{one(layout, N, P, k, bool(f32)):.3f}")
         sys.exit(0)
     N, P = 16384, 131072
-    for f32 in (0, 1):
+    quick = len(sys.argv) > 1 and sys.argv[1] == "--quick"  # FP64, k = 128 only
+    for f32 in ((0,) if quick else (0, 1)):
         for layout in (1, 0):
-            for k in (64, 128):
+            for k in ((128,) if quick else (64, 128)):
                 row = []
                 for mode in (0, 1, 2, 3, 4):
                     env = dict(os.environ, WSSR_OZ_DEBUG=str(mode))
