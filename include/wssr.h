@@ -80,8 +80,9 @@ typedef struct wssr_ohat_f64 {
   int64_t samples_f32; /* 1: `samples` points to float32 data (FP32 variant, BASELINE configs[3]);
                           the library widens it to FP64 in registers. Requires ld % 4 == 0,
                           16-byte alignment, mu and samples_fro2 (i.e. an assembled bundle). */
-  const double* samples_scale_table; /* optional [2 * roundup(n_params, 32)]: the per-parameter
-                          {mu_p, 2^(54 - e_p)} table of the int8 tensor-core O-passes, as written
+  const double* samples_scale_table; /* optional [4 * roundup(n_params, 32)]: the per-parameter
+                          {cw_p, 2^(54 - e_p), mu_p, 0} table of the int8 tensor-core O-passes
+                          (cw_p: integer centring word, csrc/ozaki.cu biased_digits), as written
                           by assemble (wssr_assemble_out.scale_table); NULL: computed on demand
                           with one extra read of the sample block. */
   const double* samples_fro2_dev; /* optional: when samples_fro2 < 0, the device value of the
@@ -154,7 +155,7 @@ typedef struct wssr_assemble_out {
   double loss, raw_loss, e_mean, e_std;
   double fro2;      /* ||o_matrix||_F^2                                                      */
   int64_t n_global;
-  double* scale_table; /* optional [2 * roundup(P, 32)]: per-parameter scales of the int8
+  double* scale_table; /* optional [4 * roundup(P, 32)]: per-parameter scales of the int8
                           tensor-core O-passes, from the same column pass (this rank's rows) */
   /* optional deferred host outputs (single rank): when `deferred` (pinned host memory, 5
      doubles) is non-NULL the call returns without waiting for the device; {loss, raw_loss,

@@ -266,8 +266,9 @@ class Context:
 
 
 def scale_table_len(n_params: int) -> int:
-    """Doubles in the per-parameter scale table of the int8 tensor-core O-passes."""
-    return 2 * ((int(n_params) + 31) // 32 * 32)
+    """Doubles in the per-parameter scale table of the int8 tensor-core O-passes (4 per slot,
+    one slot per parameter rounded up to 32; see csrc/ozaki.cu biased_digits)."""
+    return 4 * ((int(n_params) + 31) // 32 * 32)
 
 
 _contexts: dict = {}

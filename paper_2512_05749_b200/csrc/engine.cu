@@ -650,7 +650,7 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
     const double* tab = o.scale_tab;
     if (!tab) {
       if (!o.oz_scale) {
-        o.oz_scale = std::make_shared<Buf>(2 * ozaki_scale_len(o.P), ctx.stream);
+        o.oz_scale = std::make_shared<Buf>(ozaki_table_doubles(o.P), ctx.stream);
         WSSR_CUDA(ozaki_scales(ctx, o.samp, o.f32, o.lds, o.n, o.P, o.mu, *o.oz_scale, ctx.stream));
       }
       tab = *o.oz_scale;
@@ -1193,7 +1193,7 @@ void assemble(Context& ctx, const T* derivs, int64_t n, int64_t p, int64_t ld,
     if (n > 0) {
       WSSR_CUDA(ozaki_scales_minmax(ctx, cmin, cmax, out->mu, p, out->scale_table, st));
     } else {
-      WSSR_CUDA(cudaMemsetAsync(out->scale_table, 0, sizeof(double) * 2 * ozaki_scale_len(p), st));
+      WSSR_CUDA(ozaki_table_clear(ctx, out->scale_table, p, st));  // padding slots only
     }
   }
   // gradient = 2 * o_matrix @ l_vector = 2 * gsum / N   (estimators.py:93)
@@ -2081,7 +2081,7 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
     if (!ozaki_supported(L, g, a_f32 != 0)) throw Fail{WSSR_ERR_UNSUPPORTED, "operands not TMA-aligned"};
     // parameters run along K (RM) or M (CM); samples along the other
     const int64_t params = L == Layout::RM ? k : m, samples = L == Layout::RM ? m : k;
-    Buf scale((size_t)2 * ozaki_scale_len(params), cx.stream);
+    Buf scale((size_t)ozaki_table_doubles(params), cx.stream);
     WSSR_CUDA(ozaki_scales(cx, a, a_f32 != 0, lda, samples, params, shift, scale, cx.stream));
     Buf planes;
     if (cx.oz_pre == 0) {

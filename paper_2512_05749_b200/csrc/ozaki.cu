@@ -7,8 +7,9 @@
 //
 //   * every element of the centred sample block  x = O - mu  is scaled by a power of two per
 //     parameter column p (2^(54-e_p), e_p = exponent bound of max_n |O_np - mu_p|) and rounded to
-//     an integer |X| < 2^54, split into 7 signed base-256 digits  X = sum_i d_i 256^i,
-//     d_i in [-128, 127] (bytes of X + 0x0080808080808080, each XOR 0x80);
+//     an integer |X| <= 2^54 + 1 (integer centring rint(O s) - rint(mu s), or rint((O - mu) s)
+//     when O - mu is exact; see biased_digits), split into 7 signed base-256 digits
+//     X = sum_i d_i 256^i, d_i in [-128, 127] (bytes of X + 0x0080808080808080, each XOR 0x80);
 //   * the thin operand (q or v, P x k / N x k) is split the same way per output column;
 //   * digit products are exact int8 x int8 -> int32 tensor-core MMAs; the 34 digit pairs (a, b)
 //     with a + b <= 7 (most-significant-first) are kept - the dropped ones sum below 2^-59 of
@@ -73,7 +74,8 @@ constexpr uint64_t kBias = 0x0080808080808080ull;
 constexpr int A_RAW = BM * BK * 8;            // 32 KB (FP64 tile; FP32 uses half)
 constexpr int A_DIG = ND * BM * BK;           // 28 KB
 constexpr int B_DIG = BROWS * BK;             // 14 KB
-constexpr int MI_BYTES = 2 * BK * 8;          // mu / scale slice (row-major mode only)
+constexpr int TABW = 4;                       // doubles per scale-table slot (see tab_slot)
+constexpr int MI_BYTES = TABW * BK * 8;       // scale-table slice (row-major mode only)
 constexpr int RSTAGE = A_RAW;                 // raw tile, 1 KB aligned
 constexpr int DSTAGE = A_DIG;                 // 28 KB, 1 KB aligned
 constexpr int BSTAGE = B_DIG;                 // 14 KB, 1 KB aligned
@@ -261,6 +263,57 @@ __host__ __device__ __forceinline__ int64_t tab_slot(int64_t p) {
 __device__ __forceinline__ uint64_t to_biased(double x) {
   return (uint64_t)__double2ll_rn(x) + kBias;
 }
+
+// ---- digit integers ---------------------------------------------------------------------------
+// X_np, the integer the 7 digits of element (n, p) represent, with s_p = 2^(54 - e_p):
+//   |mu_p| <  2^(e_p + 1):  X = rint(O_np s_p) - rint(mu_p s_p)   (integer centring: |O s| < 2^56,
+//                                                                  both conversions exact)
+//   |mu_p| >= 2^(e_p + 1):  X = rint((O_np - mu_p) s_p)          (O - mu is exact by Sterbenz:
+//                                                                  every O_np lies within 2^e_p
+//                                                                  of mu_p, i.e. within a factor 2)
+// Either way X is (O - mu) s to within one unit and |X| <= 2^54 + 1.  The scaling by s is an
+// integer add to the exponent field, then one conversion (F2I): no FP64 arithmetic on the common
+// path (FP64 SIMT shares the SM datapath with the int8 MMAs and stalls beside them; ncu of the
+// earlier DADD/DMUL converters: "math" stalls on the DADDs dominated the converter warps).
+// Scale-table slot p (tab_slot order, TABW doubles): {cw_p, s_p, mu_p, f} with
+// cw_p = kBias - rint(mu_p s_p) as a 64-bit pattern, or kCwExact for the Sterbenz form, and f
+// (a 64-bit pattern) nonzero in every slot of a 32-parameter block that holds a Sterbenz-form
+// column: the converters branch on it once per K-block.  Padding slots: {kBias, 0, 0, f}.
+constexpr uint64_t kCwExact = 0x8000000000000000ull;
+
+// rint(v s) for s = 2^d, given as its high word hs = (d + 1023) << 20 (0 for padding columns):
+// an integer add to the exponent field, then one conversion.  Branch-free; zero, subnormal,
+// underflowing (|v s| < 2^-1022: rint 0) and non-finite inputs give 0.  The callers guarantee
+// |v s| < 2^57, so the shifted exponent cannot overflow.
+__device__ __forceinline__ long long rint_pow2(double v, uint32_t hs) {
+  const uint32_t hi = (uint32_t)__double2hiint(v);
+  const uint32_t ef = hi & 0x7ff00000u;
+  const bool ok = ef - 0x00100000u < 0x7fe00000u && ef + hs > 0x3ff00000u;
+  const long long r =
+      __double2ll_rn(__hiloint2double((int)(hi + hs - 0x3ff00000u), __double2loint(v)));
+  return ok ? r : 0;
+}
+__device__ __forceinline__ long long rint_pow2(float v, uint32_t hs) {
+  const uint32_t b = (uint32_t)__float_as_int(v);
+  const uint32_t ef = b & 0x7f800000u;
+  const int d = (int)(hs >> 20) - 1023;
+  const bool ok = ef - 0x00800000u < 0x7f000000u && (int)(ef >> 23) + d > 0;
+  const long long r = __float2ll_rn(__int_as_float((int)(b + ((uint32_t)d << 23))));
+  return ok ? r : 0;
+}
+__device__ __forceinline__ uint32_t hi_word(double s) { return (uint32_t)__double2hiint(s); }
+// biased digit integer Y = X + kBias of sample value v: integer-form column {cw, s} ...
+template <typename T>
+__device__ __forceinline__ uint64_t biased_int(T v, uint64_t cw, uint32_t hs) {
+  return (uint64_t)rint_pow2(v, hs) + cw;
+}
+// ... or a column of either form {cw, s, mu}
+template <typename T>
+__device__ __forceinline__ uint64_t biased_digits(T v, uint64_t cw, double s, double mu) {
+  if (cw != kCwExact) return biased_int(v, cw, hi_word(s));
+  return (uint64_t)rint_pow2((double)v - mu, hi_word(s)) + kBias;
+}
+__device__ __forceinline__ uint64_t as_u64(double x) { return (uint64_t)__double_as_longlong(x); }
 // Precision guard counts of one biased digit integer y = X + kBias, packed for one 64-bit sum:
 // low word +1 when X != 0, high word +1 when |X| >= 2^(54 - kGuardBits) (the element keeps at
 // least 54 - kGuardBits bits of its own magnitude).
@@ -395,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (RM) {
             tma_load_2d(a_raw(s), &tmA, k0, (int)m0, &rfull[s]);
             if (!F32) tma_load_2d(a_raw(s) + 16384, &tmA, k0 + 16, (int)m0, &rfull[s]);
-            tma_load_1d((void*)s_mi(s), &tmS, 2 * k0, &rfull[s]);
+            tma_load_1d((void*)s_mi(s), &tmS, TABW * k0, &rfull[s]);
           } else {
             tma_load_2d(a_raw(s), &tmA, (int)m0, k0, &rfull[s]);
           }
@@ -524,10 +577,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;                // TMEM lane quadrant of this warp (epilogue)
     const int ecol = 16 * (cw >> 2);          // epilogue column group
     const int erow = quad * 32 + lane;
-    auto convert8 = [&](int s, int row, double mu_r, double inv_r, uint64_t (&y)[8]) {
+    auto convert8 = [&](int s, int row, uint64_t cw_r, double inv_r, double mu_r, bool exact,
+                        uint64_t (&y)[8]) {
       if (RM) {
-        // (mu, 2^(54-e)) of K index 8 q + i sits in table slot 4 i + q
-        const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + q;
+        // the table slot of K index 8 q + i is 4 i + q: {cw, s} at double2 8 i + 2 q, mu next;
+        // `exact`: this K-block has Sterbenz-form columns (uniform over the CTA)
+        const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + 2 * q;
         if (F32) {
           const unsigned char* base = a_raw(s) + row * 128;
 #pragma unroll
@@ -537,32 +592,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float fv[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const double2 m = mi[4 * (4 * c + e)];
-              y[4 * c + e] = to_biased(((double)fv[e] - m.x) * m.y);
+              const double2 m = mi[8 * (4 * c + e)];
+              y[4 * c + e] = exact ? biased_digits(fv[e], as_u64(m.x), m.y, mi[8 * (4 * c + e) + 1].x)
+                                   : biased_int(fv[e], as_u64(m.x), hi_word(m.y));
             }
           }
         } else {
           const unsigned char* base = a_raw(s) + (q >> 1) * 16384 + row * 128;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int mode = p.debug & 7;  // profiling: 5 = loads only, 6 = arithmetic only
-            const double2 v = mode == 6 ? make_double2(row * 1e-3, c * 1e-3)
-                                        : *reinterpret_cast<const double2*>(
-                                              base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
-            const double2 m0v = mi[4 * (2 * c)], m1v = mi[4 * (2 * c + 1)];
-            if (mode == 5) {
-              y[2 * c] = __double_as_longlong(v.x) ^ __double_as_longlong(m0v.y);
-              y[2 * c + 1] = __double_as_longlong(v.y) ^ __double_as_longlong(m1v.y);
-              continue;
+            const double2 v =
+                *reinterpret_cast<const double2*>(base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
+            const double2 m0v = mi[8 * (2 * c)], m1v = mi[8 * (2 * c + 1)];
+            if (exact) {
+              y[2 * c] = biased_digits(v.x, as_u64(m0v.x), m0v.y, mi[8 * (2 * c) + 1].x);
+              y[2 * c + 1] = biased_digits(v.y, as_u64(m1v.x), m1v.y, mi[8 * (2 * c + 1) + 1].x);
+            } else {
+              y[2 * c] = biased_int(v.x, as_u64(m0v.x), hi_word(m0v.y));
+              y[2 * c + 1] = biased_int(v.y, as_u64(m1v.x), hi_word(m1v.y));
             }
-            y[2 * c] = to_biased((v.x - m0v.x) * m0v.y);
-            y[2 * c + 1] = to_biased((v.y - m1v.x) * m1v.y);
           }
         }
       } else {
         const TA* base = reinterpret_cast<const TA*>(a_raw(s)) + (8 * q) * BM + row;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = to_biased(((double)base[i * BM] - mu_r) * inv_r);
+        for (int i = 0; i < 8; ++i)
+          y[i] = exact ? biased_digits(base[i * BM], cw_r, inv_r, mu_r)
+                       : biased_int(base[i * BM], cw_r, hi_word(inv_r));
       }
     };
     auto store8 = [&](int d, int row, const uint32_t (&w)[ND][2]) {
@@ -580,16 +636,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode(u, m0, nb, kc, kb0, kb1);
       uint64_t cntA = 0, cntB = 0;  // precision guard counts over this unit's K range
       double muA = 0.0, invA = 0.0, muB = 0.0, invB = 0.0;
+      uint64_t cwA = kBias, cwB = kBias;
       if (!RM) {
         if (m0 + rowA < p.M) {
-          muA = p.mu_inv[2 * tab_slot(m0 + rowA)];
-          invA = p.mu_inv[2 * tab_slot(m0 + rowA) + 1];
+          const double* t = p.mu_inv + TABW * tab_slot(m0 + rowA);
+          cwA = as_u64(t[0]);
+          invA = t[1];
+          muA = t[2];
         }
         if (m0 + rowB < p.M) {
-          muB = p.mu_inv[2 * tab_slot(m0 + rowB)];
-          invB = p.mu_inv[2 * tab_slot(m0 + rowB) + 1];
+          const double* t = p.mu_inv + TABW * tab_slot(m0 + rowB);
+          cwB = as_u64(t[0]);
+          invB = t[1];
+          muB = t[2];
         }
       }
+      // CM: a row's column form is fixed over the unit; one vote makes the branch warp-uniform
+      const bool exactCM = !RM && __any_sync(0xffffffffu, cwA == kCwExact || cwB == kCwExact);
       for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
         if ((int)(g & 1) != cg) continue;
         const int s = g % RSTAGES, d = g % DSTAGES;
@@ -604,21 +667,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&conv[d]);
           continue;
         }
-        uint64_t yA[8], yB[8];
-        convert8(s, rowA, muA, invA, yA);
-        convert8(s, rowB, muB, invB, yB);
-        if (guard) {
+        // one row at a time (digits packed before the next row converts: fewer live registers)
+        uint32_t wA[ND][2], wB[ND][2];
+        {
+          uint64_t y[8];
+          const bool exact =
+              RM ? __double_as_longlong(s_mi(s)[3]) != 0 : exactCM;  // uniform per K-block
+          convert8(s, rowA, cwA, invA, muA, exact, y);
+          if (guard) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            cntA += guard_count(yA[i]);
-            cntB += guard_count(yB[i]);
+            for (int i = 0; i < 8; ++i) cntA += guard_count(y[i]);
           }
+          pack_digits8(y, wA);
+        }
+        {
+          uint64_t y[8];
+          const bool exact = RM ? __double_as_longlong(s_mi(s)[3]) != 0 : exactCM;
+          convert8(s, rowB, cwB, invB, muB, exact, y);
+          if (guard) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cntB += guard_count(y[i]);
+          }
+          pack_digits8(y, wB);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[s]);  // raw tile consumed (values are in registers)
-        uint32_t wA[ND][2], wB[ND][2];
-        pack_digits8(yA, wA);
-        pack_digits8(yB, wB);
         if (tr) g_oz_trace[5][g] = clock64();
         mbar_wait(&dempty[d], ((g / DSTAGES) & 1) ^ 1);  // MMA done with this digit slot
         if (tr) g_oz_trace[6][g] = clock64();
@@ -646,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int64_t gm = m0 + erow;
       double rowfac = 1.0;
-      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[2 * tab_slot(gm) + 1];
+      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[TABW * tab_slot(gm) + 1];
       double acc[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = 0.0;
@@ -907,7 +980,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
       tc_fence_after();
       const int64_t gm = m0 + erow;
       double rowfac = 1.0;
-      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[2 * tab_slot(gm) + 1];
+      if (!RM && gm < p.M) rowfac = 1.0 / p.mu_inv[TABW * tab_slot(gm) + 1];
       double out[NB];
 #pragma unroll
       for (int jc = 0; jc < NB / 16; ++jc) {
@@ -982,12 +1055,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t pp = p0 + i;
-      double x = 0.0;
+      y[i] = kBias;
       if (pp < cols) {
-        const double m = mu_inv[2 * tab_slot(pp)], inv = mu_inv[2 * tab_slot(pp) + 1];
-        x = ((double)A[n * lda + pp] - m) * inv;
+        const double* t = mu_inv + TABW * tab_slot(pp);
+        y[i] = biased_digits(A[n * lda + pp], as_u64(t[0]), t[1], t[2]);
       }
-      y[i] = to_biased(x);
     }
     const uint32_t l0 = (uint32_t)y[0], l1 = (uint32_t)y[1], l2 = (uint32_t)y[2], l3 = (uint32_t)y[3];
     const uint32_t h0 = (uint32_t)(y[0] >> 32), h1 = (uint32_t)(y[1] >> 32);
@@ -1045,8 +1117,8 @@ __global__ void __launch_bounds__(256)
   for (int64_t n = blockIdx.x; n < rows; n += gridDim.x) {
     uint64_t acc = 0;
     for (int64_t pp = threadIdx.x; pp < cols; pp += blockDim.x) {
-      const double m = mu_inv[2 * tab_slot(pp)], inv = mu_inv[2 * tab_slot(pp) + 1];
-      acc += guard_count(to_biased(((double)A[n * lda + pp] - m) * inv));
+      const double* t = mu_inv + TABW * tab_slot(pp);
+      acc += guard_count(biased_digits(A[n * lda + pp], as_u64(t[0]), t[1], t[2]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1084,7 +1156,23 @@ __global__ void __launch_bounds__(256)
 // resolve 2^-1022 absolutely, the FP64 normal range, instead of the factor overflowing.
 constexpr int kMinScaleExp = -968;
 
-// mu_inv[p] = {mu_p, 2^(54 - e_p)} with max_p < 2^e_p; padding columns {0, 0}.
+// centring word of a slot (see biased_digits)
+__device__ __forceinline__ uint64_t centre_word(double m, double s, int e) {
+  if (fabs(m) < ldexp(1.0, e + 1)) return kBias - (uint64_t)__double2ll_rn(m * s);
+  return kCwExact;
+}
+// Called by every lane of a warp for 32 consecutive parameters (one slot block): the block's
+// Sterbenz flag is a warp vote.
+__device__ __forceinline__ void write_slot(double* tab, int64_t p, uint64_t cw, double s, double m) {
+  const bool blk = __any_sync(0xffffffffu, cw == kCwExact);
+  double* t = tab + TABW * tab_slot(p);
+  t[0] = __longlong_as_double((long long)cw);
+  t[1] = s;
+  t[2] = m;
+  t[3] = __longlong_as_double(blk ? 1ll : 0ll);
+}
+
+// mu_inv[p] = {cw_p, 2^(54 - e_p), mu_p, 0} with max_p < 2^e_p; padding columns {kBias, 0, 0, 0}.
 __global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
                               const double* __restrict__ mu, int64_t cols, int64_t cols_pad,
                               double* __restrict__ mu_inv) {
@@ -1092,14 +1180,16 @@ __global__ void mu_inv_kernel(const unsigned long long* __restrict__ cmax,
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cols_pad;
        p += (int64_t)gridDim.x * blockDim.x) {
     double m = 0.0, inv = 0.0;
+    uint64_t cw = kBias;
     if (p < cols) {
       m = mu ? mu[p] : 0.0;
       int e = 0;
       frexp(__longlong_as_double((long long)cmax[p]), &e);  // max < 2^e (0 -> e = 0)
-      inv = ldexp(1.0, 54 - max(e, kMinScaleExp));
+      e = max(e, kMinScaleExp);
+      inv = ldexp(1.0, 54 - e);
+      cw = centre_word(m, inv, e);
     }
-    mu_inv[2 * tab_slot(p)] = m;
-    mu_inv[2 * tab_slot(p) + 1] = inv;
+    write_slot(mu_inv, p, cw, inv, m);
   }
 }
 
@@ -1113,15 +1203,17 @@ __global__ void mu_inv_minmax_kernel(const double* __restrict__ cmin,
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < cols_pad;
        p += (int64_t)gridDim.x * blockDim.x) {
     double m = 0.0, inv = 0.0;
+    uint64_t cw = kBias;
     if (p < cols) {
       m = mu ? mu[p] : 0.0;
       const double big = fmax(fabs(cmax[p] - m), fabs(cmin[p] - m));
       int e = 0;
       frexp(isfinite(big) ? big : 0.0, &e);
-      inv = ldexp(1.0, 54 - max(e, kMinScaleExp));
+      e = max(e, kMinScaleExp);
+      inv = ldexp(1.0, 54 - e);
+      cw = centre_word(m, inv, e);
     }
-    mu_inv[2 * tab_slot(p)] = m;
-    mu_inv[2 * tab_slot(p) + 1] = inv;
+    write_slot(mu_inv, p, cw, inv, m);
   }
 }
 
@@ -1132,7 +1224,7 @@ __device__ __forceinline__ double thin_value(const double* B, int64_t ldb, int64
   const double b = B[k * ldb + j];
   if (!mu_inv) return b;
   // 2^54 / inv exactly, from the exponent field of the power of two inv (no division)
-  const long long ebits = __double_as_longlong(mu_inv[2 * tab_slot(k) + 1]) >> 52;
+  const long long ebits = __double_as_longlong(mu_inv[TABW * tab_slot(k) + 1]) >> 52;
   return b * __longlong_as_double((long long)(2046 + 54 - ebits) << 52);
 }
 
@@ -1161,7 +1253,7 @@ __global__ void __launch_bounds__(256)
         if (k < K) {
           v[i] = __ldg(B + k * ldb + jj);
           if (mu_inv) {
-            const double inv = __ldg(mu_inv + 2 * tab_slot(k) + 1);
+            const double inv = __ldg(mu_inv + TABW * tab_slot(k) + 1);
             // 2^54 / inv from the exponent field (0 for padding columns: inv == 0)
             mul[i] = inv == 0.0 ? 0.0
                                 : __longlong_as_double(
@@ -1214,7 +1306,7 @@ __global__ void __launch_bounds__(256)
   for (int i = 0; i < 4; ++i) {
     const int64_t k = k0 + i;
     double x = 0.0;
-    if (jj < N && k < K && !(mu_inv && mu_inv[2 * tab_slot(k) + 1] == 0.0))
+    if (jj < N && k < K && !(mu_inv && mu_inv[TABW * tab_slot(k) + 1] == 0.0))
       x = thin_value(B, ldb, k, jj, mu_inv) * inv;
     y[i] = to_biased(x);
   }
@@ -1301,6 +1393,15 @@ cudaError_t ozaki_trace(long long* host, size_t n) {
 }
 
 int64_t ozaki_scale_len(int64_t cols) { return ((cols + oz::BK - 1) / oz::BK) * oz::BK; }
+int64_t ozaki_table_doubles(int64_t cols) { return oz::TABW * ozaki_scale_len(cols); }
+
+cudaError_t ozaki_table_clear(Context& ctx, double* mu_inv, int64_t cols, cudaStream_t st) {
+  const int64_t cpad = ozaki_scale_len(cols);
+  launch_pdl(oz::mu_inv_kernel, (int)std::max<int64_t>(1, std::min<int64_t>((cpad + 255) / 256, 4 * ctx.num_sms)), 256, 0, st,
+             (const unsigned long long*)nullptr, (const double*)nullptr, (int64_t)0, cpad, mu_inv);
+  ctx.kernel_launches += 1;
+  return cudaGetLastError();
+}
 
 cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
                          int64_t cols, const double* mu, double* mu_inv, cudaStream_t st) {
@@ -1488,7 +1589,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     ctx.gemm_launches += 1;
   } else if (RMm) {
     ok = make_map_2d(&tA, a.A, K, M, a.lda, BM, es) &&
-         make_map_1d(&tS, mu_inv, 2 * kpad, 2 * BK);
+         make_map_1d(&tS, mu_inv, TABW * kpad, TABW * BK);
   } else {
     ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
   }

@@ -8,14 +8,20 @@
 
 namespace wssr {
 
-// Length (in {mu, scale} pairs) of the per-parameter scale table for `cols` parameters.
+// Slots of the per-parameter scale table for `cols` parameters (cols rounded up to 32).
 int64_t ozaki_scale_len(int64_t cols);
+// Doubles of that table (4 per slot).
+int64_t ozaki_table_doubles(int64_t cols);
 
-// Per-parameter table {mu_p, 2^(54 - e_p)} (stored in a block-transposed slot order, see
-// tab_slot in ozaki.cu), e_p the exponent bound of
-// max_n |O_np - mu_p| over the (rows x cols, ld lda) sample block; pads to ozaki_scale_len.
+// Per-parameter table, slot {cw_p, 2^(54 - e_p), mu_p, 0} (stored in a block-transposed slot
+// order, see tab_slot in ozaki.cu; cw_p the integer centring word, see biased_digits), e_p the
+// exponent bound of max_n |O_np - mu_p| over the (rows x cols, ld lda) sample block; pads to
+// ozaki_scale_len slots.
 cudaError_t ozaki_scales(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
                          int64_t cols, const double* mu, double* mu_inv, cudaStream_t st);
+
+// A table of padding slots only (a rank without samples).
+cudaError_t ozaki_table_clear(Context& ctx, double* mu_inv, int64_t cols, cudaStream_t st);
 
 // The same table from per-column extrema of the sample block (fused into assemble's pass).
 cudaError_t ozaki_scales_minmax(Context& ctx, const double* cmin, const double* cmax,

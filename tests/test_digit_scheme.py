@@ -1,10 +1,11 @@
 """The int8 digit scheme of the O-passes (csrc/ozaki.cu), restated in numpy: the arithmetic the
 kernels rely on, checked on the CPU.
 
-* digitising: X = rint((x - mu) 2^(54 - e)) with |x - mu| < 2^e, biased by 0x80 in each of the
-  low 7 bytes (ozaki.cu to_biased / kBias); plane a holds byte 6 - a XOR 0x80, a signed digit
-  (pack_digits8).  The 7 signed digits reconstruct X exactly, and X is (x - mu) to 2^-54 of the
-  column scale;
+* digitising (ozaki.cu biased_digits), s = 2^(54 - e) with |x - mu| < 2^e:
+  X = rint(x s) - rint(mu s) when |mu| < 2^(e + 1) (integer centring), else
+  X = rint((x - mu) s) (x - mu exact by Sterbenz), biased by 0x80 in each of the low 7 bytes
+  (kBias); plane a holds byte 6 - a XOR 0x80, a signed digit (pack_digits8).  The 7 signed digits
+  reconstruct X exactly, and X is (x - mu) to one unit of 2^-54 of the column scale;
 * products: level s = a + b collects the digit pairs of one significance; the kernels keep
   s <= 7 (34 pairs, NL = 8 TMEM levels) and combine the int32 level sums in FP64.  The dropped
   pairs weigh at most 2^-64 of the top level, so a dot product of length K is exact to
@@ -17,9 +18,19 @@ ND, NL = 7, 8
 BIAS = np.uint64(0x0080808080808080)
 
 
-def digits(x, mu, e):
+def digit_ints(x, mu, e):
+    """X of ozaki.cu biased_digits (np.rint is round-half-even, like the device conversion)."""
     e = max(e, -968)  # ozaki.cu kMinScaleExp: the scale factor stays finite
-    X = np.rint((x - mu) * np.ldexp(1.0, 54 - e)).astype(np.int64)
+    s = np.ldexp(1.0, 54 - e)
+    if abs(mu) < np.ldexp(1.0, e + 1):
+        return np.rint(x * s).astype(np.int64) - np.int64(np.rint(mu * s))
+    d = x - mu  # exact (Sterbenz): every x lies within 2^e of mu, and |mu| >= 2^(e+1)
+    assert np.all(d + mu == x)
+    return np.rint(d * s).astype(np.int64)
+
+
+def digits(x, mu, e):
+    X = digit_ints(x, mu, e)
     y = X.astype(np.uint64) + BIAS
     planes = [(((y >> np.uint64(8 * (6 - a))) & np.uint64(0xFF)) ^ np.uint64(0x80))
               .astype(np.uint8).view(np.int8) for a in range(ND)]
@@ -38,7 +49,26 @@ def test_digits_reconstruct_exactly():
         assert all(int(r) == int(v) for r, v in zip(rec, X))
         ec = max(e, -968)
         err = np.abs(np.ldexp(X.astype(np.float64), ec - 54) - (x - mu)).max()
-        assert err <= np.ldexp(1.0, ec - 55)
+        # one unit against the exact x - mu (two half-unit roundings), plus the half-ulp rounding
+        # of the reference fl(x - mu) itself (one unit in the top binade)
+        assert err <= np.ldexp(1.0, ec - 53) * (1 + 1e-12)
+
+
+def test_both_centring_forms_stay_in_digit_range():
+    """A column whose mean dwarfs its spread takes the exact-difference form; one whose mean is
+    below 2^(e+1) the integer form.  Both keep |X| <= 2^54 + 1 and one unit of accuracy."""
+    rng = np.random.default_rng(7)
+    for mu_scale in (0.0, 0.7, 1.9, 2.1, 1e3, 1e12):
+        x = 1.0 + 0.5 * rng.standard_normal(2048)
+        x = x - x.mean() + mu_scale
+        mu = x.mean()
+        e = int(np.frexp(np.abs(x - mu).max())[1])
+        X, planes = digits(x, mu, e)
+        assert np.abs(X).max() <= 2 ** 54 + 1
+        rec = sum(planes[a].astype(object) * (256 ** (6 - a)) for a in range(ND))
+        assert all(int(r) == int(v) for r, v in zip(rec, X))
+        err = np.abs(np.ldexp(X.astype(np.float64), e - 54) - (x - mu)).max()
+        assert err <= np.ldexp(1.0, e - 53) * (1 + 1e-12)
 
 
 def test_truncated_pair_product_is_fp64_grade():

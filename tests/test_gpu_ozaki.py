@@ -31,7 +31,7 @@ def digit_path(request):
 
 
 def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift=True,
-         tiny_cols=0):
+         tiny_cols=0, offset=0.0, offset_every=1):
     from paper_2512_05749_b200 import _lib
 
     ctx = _lib.context()
@@ -52,6 +52,11 @@ def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift
         else:
             A[:, :K] *= colscale[None, :]
     A = A + 3.0  # a mean to centre away
+    if offset:  # means far above the spread: those columns take the exact-difference form
+        if layout == 0:
+            A[:, :M:offset_every] += offset
+        else:
+            A[:, :K:offset_every] += offset
     if tiny_cols:  # columns near the bottom of the FP64 range (digit scale clamped at 2^1022)
         A[:, :tiny_cols] *= 1e-300
     if f32:
@@ -106,6 +111,19 @@ def test_ozaki_accuracy_vs_dmma(layout, M, N, K):
     assert oz[0] < 2e-15, r
     assert oz[1] < 1e-14, r
     assert oz[0] <= 4 * dm[0] + 1e-16, r
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("offset,every", [(1e3, 1), (1e9, 1), (1e6, 3), (20.0, 37)])
+@pytest.mark.parametrize("f32", [False, True])
+def test_ozaki_large_column_means(layout, offset, every, f32):
+    """Columns whose mean dwarfs their spread are digitised as rint((O - mu) s) (O - mu exact by
+    Sterbenz), the others by integer centring rint(O s) - rint(mu s) (ozaki.cu biased_digits);
+    K-blocks mixing both forms take the per-block branch.  Same accuracy either way."""
+    if f32 and offset > 1e6:
+        pytest.skip("float32 samples keep 24 bits: the offset would swallow the data")
+    r = _run(layout, 384, 64, 3000, f32=f32, offset=offset, offset_every=every)
+    assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
 
 
 @pytest.mark.parametrize("layout", [0, 1])
