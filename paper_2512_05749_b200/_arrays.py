@@ -52,7 +52,10 @@ def to_tensor(x, dtype=torch.float64, dev=None) -> torch.Tensor:
         if x.dtype != dtype or x.device != dev:
             x = x.to(device=dev, dtype=dtype)
         return x
-    return torch.as_tensor(np.asarray(x, dtype=np.float64), dtype=dtype).to(dev)
+    a = np.asarray(x, dtype=np.float64)
+    if any(st < 0 for st in a.strides):  # reversed views (a[::-1]): torch rejects them
+        a = np.ascontiguousarray(a)
+    return torch.as_tensor(a, dtype=dtype).to(dev)
 
 
 def to_tensor_f64_or_f32(x, dev=None) -> torch.Tensor:
