@@ -254,8 +254,10 @@ typedef struct wssr_step_out {
 } wssr_step_out;
 int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
 
-/* --- linalg.exact_svd (linalg.py:108-121) for min(m, n) <= 512: u [m x q], sigma [q] sorted
- * descending, vt [q x n], q = min(m, n).  Larger problems return WSSR_ERR_UNSUPPORTED. */
+/* --- linalg.exact_svd (linalg.py:108-121; numpy's dgesdd there): u [m x q], sigma [q] sorted
+ * descending, vt [q x n], q = min(m, n).  min(m, n) <= 512: QR pre-reduction + single-CTA
+ * one-sided Jacobi; larger: blocked one-sided Jacobi on the min(m, n) vectors of a (csrc/jacobi.cuh,
+ * DMMA Grams and updates, any rank). */
 int wssr_exact_svd_f64(wssr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
                        double* u, int64_t ldu, double* sigma, double* vt, int64_t ldvt);
 /* Ohat of optimizers.py:323 written out parameter-major: out [P x (hist_rank + n_samples)]. */
@@ -288,6 +290,12 @@ int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
  * (CholeskyQR2, Rayleigh quotient and residual, drift) on the tall-skinny kernels
  * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
+
+/* engine option: dense SVD mode, 0 (default) = single-CTA Jacobi up to min(m, n) = 512 and the
+ * blocked Jacobi above; 1 = the blocked Jacobi at every size (tests). */
+int wssr_set_dense_svd_mode(wssr_ctx* ctx, int mode);
+/* outer sweeps of the last blocked dense SVD (diagnostics) */
+int wssr_dense_svd_sweeps(const wssr_ctx* ctx);
 
 /* auxiliary CUDA stream for the asynchronous drift telemetry of wssr_step_f64 (NULL: none).  The
  * caller keeps the step's inputs/outputs alive until that stream passes the step (e.g. torch's

@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "tallskinny.h"
 #include "producer.h"
+#include "jacobi.cuh"
 
 struct wssr_ctx {
   wssr::Context c;
@@ -1246,12 +1247,96 @@ void transpose(Context& ctx, const double* in, int64_t ldi, int64_t rows, int64_
   post_launch(ctx);
 }
 
+// Dense SVD for min(m, n) > kDenseSvdMax: blocked one-sided Jacobi (jacobi.cuh) directly on the
+// min(m, n) vectors of A (no QR pre-reduction: the step-0 Ohat is exactly rank-deficient - its
+// sample columns sum to zero - which CholeskyQR cannot factor; one-sided Jacobi needs no full
+// rank and keeps high relative accuracy).
+void dense_svd_blocked(Context& ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                       double* U, int64_t ldu, double* S, double* VT, int64_t ldvt) {
+  cudaStream_t st = ctx.stream;
+  const bool by_cols = m >= n;  // vectors: the columns of A (X = A^T) or its rows (X = A)
+  const int64_t nv = by_cols ? n : m, L = by_cols ? m : n;
+  int nb = (int)((nv + 15) / 16);
+  nb += nb & 1;
+  const int64_t nvp = 16 * (int64_t)nb, ldx = L + (L & 1);  // even ld: 16-byte aligned rows
+  Buf X((size_t)(nvp * ldx), st), Wm((size_t)(nvp * nvp), st), sig((size_t)(2 * nv + 2), st);
+  WSSR_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * nvp * ldx, st));
+  if (by_cols)
+    transpose(ctx, A, lda, m, n, nullptr, 1.0, X, ldx);  // X (n x m) = A^T
+  else
+    copy2d(ctx, A, lda, m, n, 1.0, X, ldx);
+  launch_pdl(bj::identity_kernel, blocks_for(nvp * nvp, 256, 16 * ctx.num_sms), 256, 0, st,
+             Wm.p, nvp);
+  post_launch(ctx);
+  static std::atomic<uint64_t> attr{0};
+  WSSR_CUDA(smem_attr_once(attr, bj::round_kernel, (int)bj::kSmem));
+  // rounding of a length-L Gram entry grows like sqrt(L) eps (LAPACK dgesvj uses sqrt(m) eps)
+  const double tol = std::max(1e-15, 4.0 * std::numeric_limits<double>::epsilon() *
+                                          std::sqrt((double)L));
+  int* rotated = reinterpret_cast<int*>(sig.p + 2 * nv);
+  int* h_rot = reinterpret_cast<int*>(ctx.hbuf + 4000);
+  auto sweep = [&](double t) {
+    WSSR_CUDA(cudaMemsetAsync(rotated, 0, sizeof(int), st));
+    for (int round = 0; round < nb - 1; ++round) {
+      launch_pdl(bj::round_kernel, nb / 2, bj::kThreads, bj::kSmem, st, X.p, ldx, L, Wm.p, nvp,
+                 nb, round, t, rotated);
+      post_launch(ctx);
+    }
+  };
+  int sweeps = 0;
+  for (; sweeps < 60; ++sweeps) {
+    sweep(tol);
+    d2h(ctx, h_rot, rotated, sizeof(int));
+    sync(ctx);
+    if (*h_rot == 0) break;
+  }
+  if (sweeps >= 60) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "dense SVD: Jacobi did not converge"};
+  // polish: two sweeps that rotate every pair measurably off orthogonal (tol = eps) take the
+  // remaining cosines from the convergence threshold down to the noise of the Gram itself
+  for (int i = 0; i < 2; ++i) sweep(std::numeric_limits<double>::epsilon());
+  sweeps += 2;
+  double* norms = sig.p;
+  double* sorted = sig.p + nv;
+  Buf order((size_t)(nv + 1) / 2 + 1, st);
+  int* ord = order.i32();
+  launch_pdl(bj::row_norms_kernel, blocks_for(nv * 32, 256, 16 * ctx.num_sms), 256, 0, st, X.p,
+             ldx, L, (int)nv, norms);
+  post_launch(ctx);
+  launch_pdl(bj::rank_kernel, blocks_for(nv, 128, 16 * ctx.num_sms), 128, 0, st, norms, (int)nv,
+             ord, sorted);
+  post_launch(ctx);
+  WSSR_CUDA(cudaMemcpyAsync(S, sorted, sizeof(double) * nv, cudaMemcpyDeviceToDevice, st));
+  const int q = (int)nv;
+  if (by_cols) {
+    // A W^T = X_final^T = U Sigma: U[:, j] = X[order_j]^T / sigma_j, V^T[j] = W[order_j]
+    dim3 grid((unsigned)((m + 31) / 32), (unsigned)((q + 31) / 32));
+    launch_pdl(bj::gather_transpose_kernel, grid, dim3(32, 8), 0, st, X.p, ldx, m, ord, sorted,
+               q, 1, U, ldu);
+    post_launch(ctx);
+    launch_pdl(bj::gather_rows_kernel, blocks_for((int64_t)q * n, 256, 16 * ctx.num_sms), 256, 0,
+               st, Wm.p, nvp, n, ord, sorted, q, 0, VT, ldvt);
+    post_launch(ctx);
+  } else {
+    // A = W^T X_final: U[:, j] = W[order_j]^T, V^T[j] = X[order_j] / sigma_j
+    dim3 grid((unsigned)((m + 31) / 32), (unsigned)((q + 31) / 32));
+    launch_pdl(bj::gather_transpose_kernel, grid, dim3(32, 8), 0, st, Wm.p, nvp, m, ord, sorted,
+               q, 0, U, ldu);
+    post_launch(ctx);
+    launch_pdl(bj::gather_rows_kernel, blocks_for((int64_t)q * n, 256, 16 * ctx.num_sms), 256, 0,
+               st, X.p, ldx, n, ord, sorted, q, 1, VT, ldvt);
+    post_launch(ctx);
+  }
+  ctx.dense_svd_sweeps = sweeps + 1;
+}
+
 void dense_svd(Context& ctx, int64_t m, int64_t n, const double* A, int64_t lda, double* U,
                int64_t ldu, double* S, double* VT, int64_t ldvt) {
   cudaStream_t st = ctx.stream;
   const int64_t q = std::min(m, n), rows = std::max(m, n);
-  if (q > kDenseSvdMax)
-    throw Fail{WSSR_ERR_UNSUPPORTED, "dense SVD on the device is limited to min(m, n) <= 512"};
+  if (q > kDenseSvdMax || ctx.force_blocked_svd) {
+    dense_svd_blocked(ctx, m, n, A, lda, U, ldu, S, VT, ldvt);
+    return;
+  }
   Buf T;
   const double* Tp = A;
   int64_t ldt = lda;
@@ -1750,6 +1835,14 @@ int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
   ctx->c.oz_pre = path == 4 ? 1 : 0;
   return WSSR_OK;
 }
+
+int wssr_set_dense_svd_mode(wssr_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 1) return WSSR_ERR_VALUE;
+  ctx->c.force_blocked_svd = mode == 1;
+  return WSSR_OK;
+}
+
+int wssr_dense_svd_sweeps(const wssr_ctx* ctx) { return ctx ? ctx->c.dense_svd_sweeps : -1; }
 
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled) {
   if (!ctx) return WSSR_ERR_VALUE;

@@ -41,6 +41,8 @@ struct Context {
   int64_t precision_fallbacks = 0;  // SSI re-runs on DMMA after the guard fired
   bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
   bool tallskinny = true;    // k = 32/64 Grams and products of P x k blocks: tallskinny.cu
+  bool force_blocked_svd = false;  // dense SVD: blocked Jacobi at every size (tests)
+  int dense_svd_sweeps = 0;        // outer sweeps of the last blocked dense SVD
   double* hbuf = nullptr;          // pinned host staging for the step's small readbacks (4096)
   cudaStream_t aux = nullptr;      // optional: asynchronous drift telemetry (wssr_set_aux_stream)
   cudaEvent_t aux_event = nullptr;

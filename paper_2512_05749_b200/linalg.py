@@ -29,11 +29,11 @@ def _as_matrix(a):
 def exact_svd(a):
     """Economy SVD a = u @ diag(sigma) @ vt with sigma nonincreasing (linalg.py:108-121).
 
-    On the device for min(m, n) <= 512 (QR pre-reduction + one-sided Jacobi in libwssr);
-    singular vectors carry an arbitrary joint sign, as LAPACK's do.  Larger problems - only the
-    dense first step / 'exact' backend at BASELINE sizes reaches them (optimizers.py:327-330) -
-    use cuSOLVER's SVD through torch.linalg on the device: a library call off the hot path (the
-    warm-started step never takes it).
+    On the device, in libwssr: min(m, n) <= 512 by a QR pre-reduction + single-CTA one-sided
+    Jacobi; larger problems (the dense first step / 'exact' backend at BASELINE sizes,
+    optimizers.py:327-330) by the blocked one-sided Jacobi of csrc/jacobi.cuh, which needs no
+    full rank (the step-0 Ohat is rank-deficient by construction).  Singular vectors carry an
+    arbitrary joint sign, as LAPACK's do.
     """
     a = _as_matrix(a)
     if not bool(torch.isfinite(a).all()):
@@ -48,9 +48,6 @@ def exact_svd(a):
         u[:q, :q] = torch.eye(q, dtype=torch.float64, device=dev)
         vt[:q, :q] = torch.eye(q, dtype=torch.float64, device=dev)
         return u, sig, vt
-    if q > 512:
-        uu, ss, vv = torch.linalg.svd(a, full_matrices=False)
-        return uu.contiguous(), ss.contiguous(), vv.contiguous()
     a = _arrays.rows_view(a)
     _lib.context().call("wssr_exact_svd_f64", m, n, _lib.ptr(a), _arrays.ld(a), _lib.ptr(u), q,
                         _lib.ptr(sig), _lib.ptr(vt), n)

@@ -134,7 +134,7 @@ def _positive_prefix(sigma, limit):
 def exact_truncated_svd(ohat, rank):
     """Dense SVD truncated to the leading triplets, exact zeros dropped (svdengine.py:75-85).
 
-    Device path: libwssr's QR + Jacobi for min(m, n) <= 512, cuSOLVER above (linalg.exact_svd).
+    Device path: libwssr's one-sided Jacobi SVD (single-CTA up to min(m, n) = 512, blocked above).
     """
     from .linalg import exact_svd
 
