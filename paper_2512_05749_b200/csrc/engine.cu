@@ -606,18 +606,24 @@ bool ensure_planes(Context& ctx, size_t bytes) {
 }
 
 // Samples whose digit planes the step keeps (a multiple of 128, or all of them): every sample
-// when the planes fit next to the step's workspace (16 P x k blocks + 2 GiB), else as many as
-// HBM allows (c2/c3: the 7-byte planes of 16384 x 2^20 samples are 120 GB), 0 below 1024.
+// when the planes fit next to the step's workspace, else as many as HBM allows (c2/c3: the
+// 7-byte planes of 16384 x 2^20 samples are 120 GB), 0 below 1024.  The first step plans with a
+// cold margin (2 GiB + 16 P x k blocks: its scratch is not allocated yet); a partial plan is
+// revisited once at the next step, when the step's scratch sits in the context's pool and
+// cudaMemGetInfo already counts it, with a warm margin of 2 GiB + 2 P x k blocks.
 int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
   const size_t full = ozaki_planes_bytes(o.n, o.P);
   const char* cap_env0 = std::getenv("WSSR_OZ_PLANE_ROWS");
+  const bool same = ctx.plan_n == o.n && ctx.plan_p == o.P && ctx.plan_k == k;
+  const bool warm = ctx.steps_done > 0;
   // no memory query when the decision is already known: cudaMemGetInfo can stall the host for
   // milliseconds (it contends with NVML clients), and the stream drains meanwhile
   if (!cap_env0) {
     if (full <= ctx.oz_planes_cap) return o.n;
-    if (ctx.plan_n == o.n && ctx.plan_p == o.P && ctx.plan_k == k) return ctx.plan_rows;
+    if (same && !(ctx.plan_provisional && warm)) return ctx.plan_rows;
   }
-  const size_t margin = ((size_t)2 << 30) + (size_t)16 * o.P * std::max<int64_t>(k, 1) * 8;
+  const size_t blocks = warm && same ? 2 : 16;
+  const size_t margin = ((size_t)2 << 30) + blocks * o.P * std::max<int64_t>(k, 1) * 8;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
@@ -629,8 +635,11 @@ int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
   const char* cap_env = std::getenv("WSSR_OZ_PLANE_ROWS");
   const int64_t cap = cap_env ? std::max<int64_t>(0, std::atoll(cap_env)) / 128 * 128 : -1;
   if (full <= avail && (cap < 0 || cap >= o.n)) return ensure_planes(ctx, full) ? o.n : 0;
+  const int64_t prev = same ? ctx.plan_rows : 0;
   ctx.plan_n = o.n, ctx.plan_p = o.P, ctx.plan_k = k, ctx.plan_rows = 0;
+  ctx.plan_provisional = !(warm && same);
   int64_t rows = (int64_t)(avail / ozaki_planes_bytes(128, o.P)) * 128;
+  rows = std::max(rows, prev);  // never shrink an existing plan
   if (cap >= 0) rows = std::min(rows, cap);
   else if (rows < 1024) return 0;
   if (rows <= 0) return 0;
@@ -2113,6 +2122,7 @@ int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out) {
     if (!in || !out || !in->ohat) throw Fail{WSSR_ERR_VALUE, "null argument"};
     if (in->max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
     step(ctx->c, in, out);
+    ++ctx->c.steps_done;
   });
 }
 
