@@ -291,6 +291,12 @@ int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
  * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
 
+/* engine option: sample digits of the int8 O-passes for float32 samples (BASELINE configs[3]):
+ * 5 (default) = the 5 most significant of the 7 digits (each element to 2^-38 of its column's
+ * scale, exact for float32 values within 14 binades of the column maximum; 20 digit pairs and 5
+ * planes in HBM), 7 = the FP64-grade scheme of float64 samples (34 pairs, 7 planes). */
+int wssr_set_fp32_digits(wssr_ctx* ctx, int digits);
+
 /* engine option: dense SVD mode, 0 (default) = single-CTA Jacobi up to min(m, n) = 512 and the
  * blocked Jacobi above; 1 = the blocked Jacobi at every size (tests). */
 int wssr_set_dense_svd_mode(wssr_ctx* ctx, int mode);

@@ -611,10 +611,16 @@ bool ensure_planes(Context& ctx, size_t bytes) {
 // cold margin (2 GiB + 16 P x k blocks: its scratch is not allocated yet); a partial plan is
 // revisited once at the next step, when the step's scratch sits in the context's pool and
 // cudaMemGetInfo already counts it, with a warm margin of 2 GiB + 2 P x k blocks.
+int sample_digits(const Context& ctx, const Ohat& o) {
+  return (o.f32 && ctx.f32_digits == 5) ? 5 : 7;
+}
+
 int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
-  const size_t full = ozaki_planes_bytes(o.n, o.P);
+  const int nds = sample_digits(ctx, o);
+  const size_t full = ozaki_planes_bytes(o.n, o.P, nds);
   const char* cap_env0 = std::getenv("WSSR_OZ_PLANE_ROWS");
-  const bool same = ctx.plan_n == o.n && ctx.plan_p == o.P && ctx.plan_k == k;
+  const bool same = ctx.plan_n == o.n && ctx.plan_p == o.P && ctx.plan_k == k &&
+                    ctx.plan_nds == nds;
   const bool warm = ctx.steps_done > 0;
   // no memory query when the decision is already known: cudaMemGetInfo can stall the host for
   // milliseconds (it contends with NVML clients), and the stream drains meanwhile
@@ -634,20 +640,27 @@ int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
   // testing only: cap the planes at WSSR_OZ_PLANE_ROWS samples (exercises the split passes)
   const char* cap_env = std::getenv("WSSR_OZ_PLANE_ROWS");
   const int64_t cap = cap_env ? std::max<int64_t>(0, std::atoll(cap_env)) / 128 * 128 : -1;
-  if (full <= avail && (cap < 0 || cap >= o.n)) return ensure_planes(ctx, full) ? o.n : 0;
+  if (full <= avail && (cap < 0 || cap >= o.n)) {
+    const bool ok = ensure_planes(ctx, full);
+    if (std::getenv("WSSR_VERBOSE"))
+      std::fprintf(stderr, "[wssr] digit planes (%d digits) for all %lld samples (%s; free %.1f GB)\n",
+                   nds, (long long)o.n, ok ? "ok" : "alloc failed", free_b / 1e9);
+    return ok ? o.n : 0;
+  }
   const int64_t prev = same ? ctx.plan_rows : 0;
-  ctx.plan_n = o.n, ctx.plan_p = o.P, ctx.plan_k = k, ctx.plan_rows = 0;
+  ctx.plan_n = o.n, ctx.plan_p = o.P, ctx.plan_k = k, ctx.plan_rows = 0, ctx.plan_nds = nds;
   ctx.plan_provisional = !(warm && same);
-  int64_t rows = (int64_t)(avail / ozaki_planes_bytes(128, o.P)) * 128;
+  int64_t rows = (int64_t)(avail / ozaki_planes_bytes(128, o.P, nds)) * 128;
   rows = std::max(rows, prev);  // never shrink an existing plan
   if (cap >= 0) rows = std::min(rows, cap);
   else if (rows < 1024) return 0;
   if (rows <= 0) return 0;
-  const bool ok = ensure_planes(ctx, ozaki_planes_bytes(rows, o.P));
+  const bool ok = ensure_planes(ctx, ozaki_planes_bytes(rows, o.P, nds));
   if (!cap_env) ctx.plan_rows = ok ? rows : 0;
   if (std::getenv("WSSR_VERBOSE"))
-    std::fprintf(stderr, "[wssr] digit planes for %lld of %lld samples (%s; free %.1f GB)\n",
-                 (long long)rows, (long long)o.n, ok ? "ok" : "alloc failed", free_b / 1e9);
+    std::fprintf(stderr, "[wssr] digit planes (%d digits) for %lld of %lld samples (%s; free %.1f GB, "
+                 "avail %.1f GB)\n", nds, (long long)rows, (long long)o.n, ok ? "ok" : "alloc failed",
+                 free_b / 1e9, avail / 1e9);
   return ok ? rows : 0;
 }
 
@@ -667,6 +680,7 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
     }
     const int8_t* planes = nullptr;
     int8_t* store = nullptr;
+    const int nds = sample_digits(ctx, o);
     int64_t n_pl = 0;  // samples covered by planes (or by the store of this first pass)
     if (ctx.oz_pre == 0) {
       if (!o.oz_planes) {
@@ -678,7 +692,7 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
             store = ctx.oz_planes;
           } else {
             WSSR_CUDA(ozaki_digitize(ctx, o.samp, o.f32, o.lds, n_pl, o.P, tab, ctx.oz_planes,
-                                     ctx.stream));
+                                     ctx.stream, nds));
             planes = ctx.oz_planes;
           }
           o.oz_planes->ptr = ctx.oz_planes;
@@ -709,7 +723,7 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       // row-major (v) passes
       const int fp = (ctx.fine_phases && layout == Layout::RM) ? (store ? 14 : 15) : -1;
       PhaseTimer tm(ctx, fp, 0.0, 0.0);
-      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowcnt));
+      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowcnt, nds));
       if (rowcnt) WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
       return;
     }
@@ -729,9 +743,9 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       a2.B = B + n_pl * ldb;
       a2.accumulate = 1;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowcnt));
+    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowcnt, nds));
     WSSR_CUDA(ozaki_gemm(ctx, layout, a2, o.f32, tab, ctx.stream, nullptr, nullptr,
-                         rowcnt ? rowcnt + n_pl : nullptr));
+                         rowcnt ? rowcnt + n_pl : nullptr, nds));
     if (rowcnt) WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
     return;
   }
@@ -1845,6 +1859,12 @@ int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
   return WSSR_OK;
 }
 
+int wssr_set_fp32_digits(wssr_ctx* ctx, int digits) {
+  if (!ctx || (digits != 5 && digits != 7)) return WSSR_ERR_VALUE;
+  ctx->c.f32_digits = digits;
+  return WSSR_OK;
+}
+
 int wssr_set_dense_svd_mode(wssr_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 1) return WSSR_ERR_VALUE;
   ctx->c.force_blocked_svd = mode == 1;
@@ -2187,13 +2207,14 @@ int wssr_debug_ozaki_gemm(wssr_ctx* ctx, int layout, int64_t m, int64_t n, int64
     Buf scale((size_t)ozaki_table_doubles(params), cx.stream);
     WSSR_CUDA(ozaki_scales(cx, a, a_f32 != 0, lda, samples, params, shift, scale, cx.stream));
     Buf planes;
+    const int nds = (a_f32 && cx.f32_digits == 5) ? 5 : 7;
     if (cx.oz_pre == 0) {
-      planes = Buf((ozaki_planes_bytes(samples, params) + 7) / 8, cx.stream);
+      planes = Buf((ozaki_planes_bytes(samples, params, nds) + 7) / 8, cx.stream);
       WSSR_CUDA(ozaki_digitize(cx, a, a_f32 != 0, lda, samples, params, scale,
-                               reinterpret_cast<int8_t*>(planes.p), cx.stream));
+                               reinterpret_cast<int8_t*>(planes.p), cx.stream, nds));
     }
     WSSR_CUDA(ozaki_gemm(cx, L, g, a_f32 != 0, scale, cx.stream,
-                         reinterpret_cast<const int8_t*>(planes.p)));
+                         reinterpret_cast<const int8_t*>(planes.p), nullptr, nullptr, nds));
     sync(cx);
   });
 }

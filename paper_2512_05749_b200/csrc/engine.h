@@ -52,7 +52,9 @@ struct Context {
   int8_t* oz_planes = nullptr;  // the step's pre-digitised sample block (reused across steps)
   size_t oz_planes_cap = 0;     // bytes
   int64_t plan_n = -1, plan_p = -1, plan_k = -1, plan_rows = 0;  // last partial-planes decision
+  int plan_nds = 7;
   bool plan_provisional = false;  // that decision used the cold (first-step) memory margin
+  int f32_digits = 5;             // sample digits of the int8 O-passes for float32 samples (5|7)
   int64_t steps_done = 0;         // completed wssr_step calls (the scratch pool is warm after one)
   double* oz_ws = nullptr;   // Ozaki thin-operand digits + factors
   size_t oz_ws_cap = 0;      // doubles

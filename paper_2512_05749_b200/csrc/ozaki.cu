@@ -324,6 +324,54 @@ __device__ __forceinline__ uint64_t guard_count(uint64_t y) {
   return (uint64_t)(x != 0) | ((uint64_t)((a >> (54 - kGuardBits)) != 0) << 32);
 }
 
+// ---- digit pairs of one K-block -------------------------------------------------------------
+// Sample digit a (most significant first) against the thin digits b, into the int32 level
+// accumulators D_s, s = a + b < nl (TMEM columns 64 s ...), thin digits concatenated along N (up
+// to 256 per MMA).  nds = 7, nl = 8: the FP64 scheme (34 pairs, dropped levels below 2^-59 of the
+// product of the column scales).  nds = 5, nl = 6 for float32 samples: the top 5 of the same 7
+// digit planes (X to 2^-38 of its column's scale - every float32 element within 14 binades of
+// its column's maximum exactly) and levels to 2^-48: 20 pairs, 5 planes in HBM.  Digit 1 goes
+// first and digit 0's range is split at column 64, so on a unit's first K-block (first = 0)
+// every TMEM column is first written by an MMA with accumulate = 0.
+// levels kept for NDS sample digits: 8 (FP64 scheme) or NDS + 1
+template <int NDS>
+__host__ __device__ constexpr int levels() { return NDS == ND ? NL : NDS + 1; }
+
+// One MMA per <= 256 thin-digit rows: sample digit a against thin digits b0 .. b0 + nb - 1,
+// written to the levels a + b0 ... (all compile-time: descriptors and TMEM columns fold into
+// immediates, so the issuing thread does no address arithmetic between MMAs).
+template <int A, int B0, int NB, typename ADesc, typename BDesc>
+__device__ __forceinline__ void issue_range(uint32_t tmem, ADesc adesc, BDesc bdesc,
+                                            uint32_t amajor, uint32_t acc) {
+  constexpr int left = 64 * NB, n0 = left > 256 ? 256 : left;
+  if constexpr (left > 0) {
+    mma_i8(tmem + 64 * (A + B0), adesc(A), bdesc(64 * B0), idesc_i8(n0) | amajor, acc);
+    if constexpr (left > 256)
+      issue_range<A, B0 + 4, NB - 4>(tmem, adesc, bdesc, amajor, acc);
+  }
+}
+template <int A, int NDS, typename ADesc, typename BDesc>
+__device__ __forceinline__ void issue_rest(uint32_t tmem, ADesc adesc, BDesc bdesc,
+                                           uint32_t amajor) {
+  if constexpr (A < NDS) {
+    constexpr int L = levels<NDS>(), nb = (L - A) < ND ? (L - A) : ND;
+    issue_range<A, 0, nb>(tmem, adesc, bdesc, amajor, 1u);
+    issue_rest<A + 1, NDS>(tmem, adesc, bdesc, amajor);
+  }
+}
+template <int NDS, typename ADesc, typename BDesc>
+__device__ __forceinline__ void issue_pairs(uint32_t tmem, ADesc adesc, BDesc bdesc,
+                                            uint32_t amajor, uint32_t first) {
+  constexpr int L = levels<NDS>();
+  constexpr int nb1 = (L - 1) < ND ? (L - 1) : ND, nb0 = (L < ND ? L : ND) - 1;
+  issue_range<1, 0, nb1>(tmem, adesc, bdesc, amajor, first);
+  issue_range<0, 0, 1>(tmem, adesc, bdesc, amajor, first);
+  issue_range<0, 1, nb0>(tmem, adesc, bdesc, amajor, 1u);
+  issue_rest<2, NDS>(tmem, adesc, bdesc, amajor);
+}
+// thin-digit rows of a K-block that the pairs read (64 per thin digit b < min(7, nl))
+__host__ __device__ constexpr int thin_rows(int nl) { return NB * (nl < ND ? nl : ND); }
+
 // profiling only (debug 9): per-K-block timestamps of CTA 0, see tools/ozaki_timeline.py
 constexpr int kTraceBlocks = 96;
 __device__ long long g_oz_trace[8][kTraceBlocks];
@@ -348,11 +396,13 @@ struct Params {
   int8_t* store;           // on-the-fly v pass: also write the digit planes (layout as `planes`)
   unsigned long long* rowcnt;  // on-the-fly v pass: per sample row, packed digit-integer counts
                                // of the precision guard (see row_guard_kernel)
+  int nds, nl;             // sample digits used (7; 5 for float32 samples) and levels kept
+                           // (8; 6), see issue_pairs
   int debug;               // profiling only, low bits: 1 = skip digitising, 2 = skip MMAs,
                            // 3 = both, 4 = skip the sample-block loads too; +8 = trace CTA 0
 };
 
-template <bool RM, typename TA>
+template <bool RM, typename TA, int NDS>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
@@ -466,8 +516,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
           const int b = g % BSTAGES;
           mbar_sleep_wait(&bempty[b], ((g / BSTAGES) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bfull[b], B_DIG);
-          bulk_load(b_dig(b), p.bd + (nb * p.kblocks + kb) * (int64_t)B_DIG, B_DIG, &bfull[b]);
+          constexpr uint32_t bbytes = thin_rows(levels<NDS>()) * BK;
+          mbar_arrive_expect_tx(&bfull[b], bbytes);
+          bulk_load(b_dig(b), p.bd + (nb * p.kblocks + kb) * (int64_t)B_DIG, bbytes, &bfull[b]);
         }
       }
     }
@@ -513,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // this stage's slot is released below)
           const int64_t pstride = p.pblocks * p.prows * 32;
 #pragma unroll
-          for (int a = 0; a < ND; ++a)
+          for (int a = 0; a < NDS; ++a)
             asm volatile(
                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 4096;\n" ::"l"(
                     p.store + a * pstride + (kb * p.prows + m0) * 32),
@@ -524,33 +575,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           if ((p.debug & 7) != 2 && (p.debug & 7) != 3) {
             const uint32_t abase = smem_u32(a_dig(d)), bbase = smem_u32(b_dig(bs));
-            // 11 MMAs: digit a of the sample block against the thin digits b <= min(6, 7 - a),
-            // written to the level blocks D_(a+b) (TMEM columns 64 (a+b) ...).  Digit 1 goes
-            // first and digit 0's range is split at column 64, so on a unit's first K-block
-            // every TMEM column is first written by an MMA with accumulate = 0.
             const uint32_t first = kb == kb0 ? 0u : 1u;
-            const uint64_t ad1 = smem_desc_sw32(abase + 1 * BM * BK);
-            const uint64_t ad0 = smem_desc_sw32(abase);
-            mma_i8(tmem + 64, ad1, smem_desc_sw32(bbase), idesc_i8(256), first);
-            mma_i8(tmem + 320, ad1, smem_desc_sw32(bbase + 256 * BK), idesc_i8(192), first);
-            mma_i8(tmem + 0, ad0, smem_desc_sw32(bbase), idesc_i8(64), first);
-            mma_i8(tmem + 64, ad0, smem_desc_sw32(bbase + 64 * BK), idesc_i8(256), 1u);
-            mma_i8(tmem + 320, ad0, smem_desc_sw32(bbase + 320 * BK), idesc_i8(128), 1u);
-#pragma unroll
-            for (int a = 2; a < ND; ++a) {
-              const uint64_t adesc = smem_desc_sw32(abase + a * BM * BK);
-              int col = NB * a, brow = 0, left = NB * (NL - a);
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                if (left > 0) {
-                  const int n = left > 256 ? 256 : left;
-                  mma_i8(tmem + col, adesc, smem_desc_sw32(bbase + brow * BK), idesc_i8(n), 1u);
-                  col += n;
-                  brow += n;
-                  left -= n;
-                }
-              }
-            }
+            issue_pairs<NDS>(
+                tmem, [&](int a) { return smem_desc_sw32(abase + a * BM * BK); },
+                [&](int row) { return smem_desc_sw32(bbase + row * BK); }, 0u, first);
           }
           // commits track this thread's MMAs; the tensor pipe executes in issue order, so the
           // other warp's earlier K-blocks are complete as well
@@ -724,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = 0.0;
 #pragma unroll
-      for (int sd = 0; sd < NL; ++sd) {
+      for (int sd = 0; sd < levels<NDS>(); ++sd) {
         uint32_t r[16];
         tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + NB * sd + ecol, r);
         tmem_ld_wait();
@@ -792,7 +820,7 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t addr) {
          (2ull << 61);
 }
 
-template <bool RM>
+template <bool RM, int NDS>
 __global__ void __launch_bounds__(kPreThreads, 1)
     ozaki_pre_kernel(const __grid_constant__ CUtensorMap tmA, const Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -868,7 +896,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
               mbar_arrive(&afull[s]);
               continue;
             }
-            mbar_arrive_expect_tx(&afull[s], PA_DIG);
+            mbar_arrive_expect_tx(&afull[s], NDS * BM * PBK);
             // 128-byte rows over the pre-swizzled planes, no TMA swizzle
             if (RM)  // [7][128 n][32 p]: one 4 KB run per plane
               tma_load_4d(a_dig(s), &tmA, 0, (int)(m0 / 4), (int)kb, 0, &afull[s]);
@@ -882,8 +910,9 @@ __global__ void __launch_bounds__(kPreThreads, 1)
               mbar_arrive(&bfull[b]);
               continue;
             }
-            mbar_arrive_expect_tx(&bfull[b], PB_DIG);
-            bulk_load(b_dig(b), p.bd + (nb * p.kblocks + kb) * (int64_t)PB_DIG, PB_DIG, &bfull[b]);
+            constexpr uint32_t bbytes = thin_rows(levels<NDS>()) * PBK;
+            mbar_arrive_expect_tx(&bfull[b], bbytes);
+            bulk_load(b_dig(b), p.bd + (nb * p.kblocks + kb) * (int64_t)PB_DIG, bbytes, &bfull[b]);
           }
         }
       }
@@ -921,6 +950,23 @@ __global__ void __launch_bounds__(kPreThreads, 1)
         if (tr) g_oz_trace[3][g] = clock64();
         tc_fence_after();
         if (lane == 0 && (p.debug & 7) == 7) {  // profiling: no MMAs
+          mma_commit(&aempty[s]);
+          mma_commit(&bempty[bs]);
+          if (kb + 1 == kb1) mma_commit(tfull);
+        } else if (lane == 0) {
+          // two MMA-K steps per stage: K-major operands advance 32 bytes inside the 64-byte
+          // swizzled rows; the MN-major sample digits advance 32 rows (4 KB)
+#pragma unroll
+          for (int kk = 0; kk < PBK / 32; ++kk) {
+            const uint32_t abase = smem_u32(a_dig(s));
+            const uint32_t bbase = smem_u32(b_dig(bs)) + 32u * kk;
+            const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
+            auto bdesc = [&](int row) {
+              return PBK == 64 ? smem_desc_sw64(bbase + row * PBK) : smem_desc_sw32(bbase + row * PBK);
+            };
+            issue_pairs<NDS>(tmem, [&](int a) { return adesc_of(abase + a * BM * PBK); }, bdesc,
+                             amajor, first);
+          }
           mma_commit(&aempty[s]);
           mma_commit(&bempty[bs]);
           if (kb + 1 == kb1) mma_commit(tfull);
@@ -988,7 +1034,7 @@ __global__ void __launch_bounds__(kPreThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.0;
 #pragma unroll
-        for (int sd = 0; sd < NL; ++sd) {
+        for (int sd = 0; sd < levels<NDS>(); ++sd) {
           uint32_t r[16];
           tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + NB * sd + 16 * jc, r);
           tmem_ld_wait();
@@ -1040,7 +1086,7 @@ template <typename TA>
 __global__ void __launch_bounds__(256)
     digitize_kernel(const TA* __restrict__ A, int64_t lda, int64_t rows, int64_t prows,
                     int64_t cols, int64_t ppad, const double* __restrict__ mu_inv,
-                    int8_t* __restrict__ planes) {
+                    int8_t* __restrict__ planes, int nds) {
   pdl_wait();
   const int64_t pblocks = ppad / 32;
   const int64_t plane = prows * ppad;
@@ -1080,7 +1126,8 @@ __global__ void __launch_bounds__(256)
     w[0] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
     int8_t* dst = planes + (pb * prows + n) * 32 + ((4 * q8) ^ (((n >> 2) & 1) << 4));
 #pragma unroll
-    for (int a = 0; a < ND; ++a) *reinterpret_cast<uint32_t*>(dst + a * plane) = w[a];
+    for (int a = 0; a < ND; ++a)
+      if (a < nds) *reinterpret_cast<uint32_t*>(dst + a * plane) = w[a];
   }
 }
 
@@ -1351,34 +1398,45 @@ bool make_map_cm(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <bool RM, typename TA, int NDS>
+cudaError_t launch_nds(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tS,
+                       const Params& p, int grid, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t e = smem_attr_once(attr, ozaki_gemm_kernel<RM, TA, NDS>, (int)kSmem);
+  if (e != cudaSuccess) return e;
+  launch_pdl(ozaki_gemm_kernel<RM, TA, NDS>, grid, kThreads, kSmem, st, tA, tB, tS, p);
+  return cudaGetLastError();
+}
 template <bool RM, typename TA>
 cudaError_t launch(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tS,
                    const Params& p, int grid, cudaStream_t st) {
-  static std::atomic<uint64_t> attr{0};
-  cudaError_t e = smem_attr_once(attr, ozaki_gemm_kernel<RM, TA>, (int)kSmem);
-  if (e != cudaSuccess) return e;
-  launch_pdl(ozaki_gemm_kernel<RM, TA>, grid, kThreads, kSmem, st, tA, tB, tS, p);
-  return cudaGetLastError();
+  if (sizeof(TA) == 4 && p.nds == 5) return launch_nds<RM, TA, 5>(tA, tB, tS, p, grid, st);
+  return launch_nds<RM, TA, ND>(tA, tB, tS, p, grid, st);
 }
 
+template <bool RM, int NDS>
+cudaError_t launch_pre_nds(const CUtensorMap& tA, const Params& p, int grid, cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t e = smem_attr_once(attr, ozaki_pre_kernel<RM, NDS>, (int)kPreSmem);
+  if (e != cudaSuccess) return e;
+  launch_pdl(ozaki_pre_kernel<RM, NDS>, grid, kPreThreads, kPreSmem, st, tA, p);
+  return cudaGetLastError();
+}
 template <bool RM>
 cudaError_t launch_pre(const CUtensorMap& tA, const Params& p, int grid, cudaStream_t st) {
-  static std::atomic<uint64_t> attr{0};
-  cudaError_t e = smem_attr_once(attr, ozaki_pre_kernel<RM>, (int)kPreSmem);
-  if (e != cudaSuccess) return e;
-  launch_pdl(ozaki_pre_kernel<RM>, grid, kPreThreads, kPreSmem, st, tA, p);
-  return cudaGetLastError();
+  return p.nds == 5 ? launch_pre_nds<RM, 5>(tA, p, grid, st)
+                    : launch_pre_nds<RM, ND>(tA, p, grid, st);
 }
 
 // 4-D map over the blocked, pre-swizzled digit planes viewed as 128-byte rows:
 // {128 B (4 sample rows), prows / 4, ppad / 32 parameter blocks, 7 planes}, no TMA swizzle
 bool make_map_planes(CUtensorMap* map, const int8_t* planes, int64_t prows, int64_t pblocks,
-                     bool rm) {
+                     bool rm, int nds) {
   auto fn = tma_encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[4] = {128, (cuuint64_t)(prows / 4), (cuuint64_t)pblocks, (cuuint64_t)ND};
+  cuuint64_t dims[4] = {128, (cuuint64_t)(prows / 4), (cuuint64_t)pblocks, (cuuint64_t)nds};
   cuuint64_t strides[3] = {128, (cuuint64_t)(32 * prows), (cuuint64_t)(32 * prows * pblocks)};
-  cuuint32_t box[4] = {128, rm ? 32u : 8u, rm ? 1u : 4u, (cuuint32_t)ND};
+  cuuint32_t box[4] = {128, rm ? 32u : 8u, rm ? 1u : 4u, (cuuint32_t)nds};
   cuuint32_t es[4] = {1u, 1u, 1u, 1u};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1441,21 +1499,22 @@ bool ozaki_supported(Layout L, const GemmArgs& a, bool f32) {
 
 int64_t ozaki_plane_pitch(int64_t cols) { return ((cols + 127) / 128) * 128; }
 int64_t ozaki_plane_rows(int64_t rows) { return ((rows + 127) / 128) * 128; }
-size_t ozaki_planes_bytes(int64_t rows, int64_t cols) {
-  return (size_t)oz::ND * ozaki_plane_rows(rows) * ozaki_plane_pitch(cols);
+size_t ozaki_planes_bytes(int64_t rows, int64_t cols, int nds) {
+  return (size_t)nds * ozaki_plane_rows(rows) * ozaki_plane_pitch(cols);
 }
 
 cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,
-                           int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st) {
+                           int64_t cols, const double* mu_inv, int8_t* planes, cudaStream_t st,
+                           int nds) {
   const int64_t ppad = ozaki_plane_pitch(cols), prows = ozaki_plane_rows(rows);
   const int64_t work = rows * (ppad / 4);  // threads: one per 4 parameters of a row
   const int grid = (int)std::min<int64_t>((work + 255) / 256, 16 * ctx.num_sms);
   if (f32)
     launch_pdl(oz::digitize_kernel<float>, grid, 256, 0, st, static_cast<const float*>(A), lda, rows,
-                                                     prows, cols, ppad, mu_inv, planes);
+                                                     prows, cols, ppad, mu_inv, planes, nds);
   else
     launch_pdl(oz::digitize_kernel<double>, grid, 256, 0, st, static_cast<const double*>(A), lda, rows,
-                                                      prows, cols, ppad, mu_inv, planes);
+                                                      prows, cols, ppad, mu_inv, planes, nds);
   ctx.kernel_launches += 1;
   return cudaGetLastError();
 }
@@ -1484,7 +1543,8 @@ cudaError_t ozaki_row_guard(Context& ctx, const unsigned long long* rowcnt, int6
 
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
                        cudaStream_t st, const int8_t* planes, int8_t* store,
-                       unsigned long long* rowcnt) {
+                       unsigned long long* rowcnt, int nds) {
+  if (nds != 5 && nds != oz::ND) return cudaErrorInvalidValue;
   using namespace oz;
   const bool RMm = L == Layout::RM;
   const int64_t M = a.M, N = a.N, K = a.K;
@@ -1558,6 +1618,9 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   p.accumulate = a.accumulate;
   p.slab = nullptr;
   p.bd = Bd;
+  if (nds == 5 && !f32) nds = oz::ND;  // the 5-digit scheme is for float32 samples only
+  p.nds = nds;
+  p.nl = nds == oz::ND ? oz::NL : nds + 1;
   p.planes = planes;
   p.store = (!planes && RMm) ? store : nullptr;
   p.rowcnt = (!planes && RMm) ? rowcnt : nullptr;
@@ -1581,7 +1644,7 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   const int es = f32 ? 4 : 8;
   bool ok;
   if (planes) {
-    if (!make_map_planes(&tA, planes, p.prows, p.pblocks, RMm)) return cudaErrorInvalidValue;
+    if (!make_map_planes(&tA, planes, p.prows, p.pblocks, RMm, nds)) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nblk * nch;
     const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
     e = RMm ? launch_pre<true>(tA, p, grid, st) : launch_pre<false>(tA, p, grid, st);

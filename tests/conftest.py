@@ -37,3 +37,24 @@ def subspace_sine(a, b):
     qa = np.linalg.qr(np.asarray(a))[0]
     qb = np.linalg.qr(np.asarray(b))[0]
     return float(np.linalg.norm(qb - qa @ (qa.T @ qb), ord=2))
+
+
+# Step-level tolerances on float32 samples against an FP64 evaluation of the same float32 inputs,
+# for the default 5-digit int8 scheme (each element to 2^-38 of its column's scale,
+# csrc/ozaki.cu issue_pairs) and the 7-digit one (wssr_set_fp32_digits(ctx, 7)); north_star's
+# own FP32 bar is 1e-4 on the update.
+# (measured: 5 digits reach update ~7e-12, sigma ~6e-14, sine ~2e-11 at k = 128 and c3, so the
+# FP64 bars hold for both schemes.)
+F32_DIGIT_TOL = {5: dict(update=1e-10, sigma=1e-9, sine=1e-8),
+                 7: dict(update=1e-10, sigma=1e-9, sine=1e-8)}
+
+
+@pytest.fixture(params=[5, 7], ids=["f32digits5", "f32digits7"])
+def fp32_digits(request):
+    """Runs a float32-sample test with the 5-digit (default) and the 7-digit int8 scheme."""
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    ctx.lib.wssr_set_fp32_digits(ctx.handle, request.param)
+    yield request.param
+    ctx.lib.wssr_set_fp32_digits(ctx.handle, 5)

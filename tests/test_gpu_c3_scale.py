@@ -7,12 +7,14 @@ identity update = U (c / sigma^2) + (g - U c) / lambda."""
 
 import pytest
 
+from conftest import F32_DIGIT_TOL
+
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
 
 
-def test_c3_step_int8_vs_dmma():
+def test_c3_step_int8_vs_dmma(fp32_digits):
     from paper_2512_05749_b200 import _lib, estimators, linalg, optimizers, synthetic
 
     if torch.cuda.get_device_properties(0).total_memory < 150e9:
@@ -45,8 +47,9 @@ def test_c3_step_int8_vs_dmma():
     assert d8.ssi.iterations_used == d2.ssi.iterations_used
     e_upd = (torch.linalg.vector_norm(u8 - u2) / torch.linalg.vector_norm(u2)).item()
     e_sig = (torch.linalg.vector_norm(s8 - s2) / torch.linalg.vector_norm(s2)).item()
-    print(f"c3 int8 vs DMMA: update {e_upd:.2e}, sigma {e_sig:.2e}")
-    assert e_upd < 1e-10 and e_sig < 1e-9
+    print(f"c3 int8 ({fp32_digits} digits) vs DMMA: update {e_upd:.2e}, sigma {e_sig:.2e}")
+    tol = F32_DIGIT_TOL[fp32_digits]
+    assert e_upd < tol["update"] and e_sig < tol["sigma"]
     # size-independent properties of the production step
     r = U8.shape[1]
     gram = U8.t() @ U8

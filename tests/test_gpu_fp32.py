@@ -5,7 +5,7 @@ widened to FP64 in registers, so the step equals the FP64 oracle run on the FP32
 import numpy as np
 import pytest
 
-from conftest import rel, subspace_sine
+from conftest import F32_DIGIT_TOL, rel, subspace_sine
 
 pytestmark = pytest.mark.gpu
 
@@ -39,7 +39,7 @@ def test_fp32_operand_gemm(layout, M, N, K):
     assert err < 1e-13
 
 
-def test_fp32_steps_match_fp64_oracle():
+def test_fp32_steps_match_fp64_oracle(fp32_digits):
     import torch
 
     from oracle import wssr_oracle as orc
@@ -66,8 +66,9 @@ def test_fp32_steps_match_fp64_oracle():
         _, st, diag, upd = optimizers.wssr_step(np.zeros(P), bundle, 1.0, st, return_update=True)
         upd = upd.cpu().numpy()
         assert diag.effective_rank == info32["r_eff"]
-        assert rel(upd, info32["update"]) < 1e-10                  # same inputs, FP64 arithmetic
+        tol = F32_DIGIT_TOL[fp32_digits]
+        assert rel(upd, info32["update"]) < tol["update"]          # same inputs, FP64 oracle
         assert rel(upd, info64["update"]) < 1e-4                   # BASELINE FP32 tolerance
         sig = torch.linalg.vector_norm(st.obar, dim=0).cpu().numpy()
-        assert rel(sig, info32["sigma"]) < 1e-9
-        assert subspace_sine(st.u_prev.cpu().numpy(), ost32.u_prev) < 1e-8
+        assert rel(sig, info32["sigma"]) < tol["sigma"]
+        assert subspace_sine(st.u_prev.cpu().numpy(), ost32.u_prev) < tol["sine"]

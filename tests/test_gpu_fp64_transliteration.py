@@ -110,7 +110,7 @@ def test_transliteration_pinned_to_oracle_c1():
     assert subspace_sine(tst.u_prev.cpu().numpy(), ost.u_prev) < 1e-10
 
 
-def _closed_loop(cfg, steps, seed, dtype=torch.float64, tag=""):
+def _closed_loop(cfg, steps, seed, dtype=torch.float64, tag="", tol=None):
     import fp64_transliteration as t64
     from paper_2512_05749_b200 import linalg, synthetic
 
@@ -134,8 +134,9 @@ def _closed_loop(cfg, steps, seed, dtype=torch.float64, tag=""):
         e_sig = _t_rel(sig, tinfo["sigma"])
         e_sin = _t_sine(tst.u_prev, st.u_prev)
         worst = [max(worst[0], e_upd), max(worst[1], e_sig), max(worst[2], e_sin)]
-        assert e_upd < UPD_TOL and e_sig < SIG_TOL and e_sin < SINE_TOL, (tag, t, e_upd, e_sig,
-                                                                          e_sin)
+        tu, ts, tn = (UPD_TOL, SIG_TOL, SINE_TOL) if tol is None else (
+            tol["update"], tol["sigma"], tol["sine"])
+        assert e_upd < tu and e_sig < ts and e_sin < tn, (tag, t, e_upd, e_sig, e_sin)
         np.testing.assert_allclose(diag.ssi.subspace_residual, tinfo["residual"], rtol=1e-6)
         np.testing.assert_allclose(diag.projector_drift, tinfo["projector_drift"], rtol=1e-6,
                                    atol=1e-12)
@@ -176,12 +177,15 @@ def test_c2_full_size_three_steps_vs_transliteration(release_memory, monkeypatch
     _closed_loop(synthetic.config("c2"), 3, seed=202, tag="c2")
 
 
-def test_c3_full_size_three_steps_vs_transliteration(release_memory, monkeypatch):
+def test_c3_full_size_three_steps_vs_transliteration(release_memory, monkeypatch, fp32_digits):
+    from conftest import F32_DIGIT_TOL
     from paper_2512_05749_b200 import synthetic
 
     _need_big_gpu()
-    monkeypatch.setenv("WSSR_OZ_PLANE_ROWS", "8192")
-    _closed_loop(synthetic.config("c3"), 3, seed=303, dtype=torch.float32, tag="c3")
+    if fp32_digits == 7:  # the 7-byte planes of all samples do not fit beside O and the test's
+        monkeypatch.setenv("WSSR_OZ_PLANE_ROWS", "8192")  # own temporaries: half of them
+    _closed_loop(synthetic.config("c3"), 3, seed=303, dtype=torch.float32,
+                 tag=f"c3 ({fp32_digits} digits)", tol=F32_DIGIT_TOL[fp32_digits])
 
 
 def test_c4_semantics_slice_T10_vs_transliteration(release_memory):

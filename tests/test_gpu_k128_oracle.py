@@ -6,18 +6,21 @@ tall-skinny kernels and the O-passes the int8 tensor-core path), with history av
 import numpy as np
 import pytest
 
-from conftest import rel, subspace_sine
+from conftest import F32_DIGIT_TOL, rel, subspace_sine
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("f32", [False, True])
-def test_k128_two_steps_match_oracle(f32):
+def test_k128_two_steps_match_oracle(f32, fp32_digits):
     import torch
 
     from oracle import wssr_oracle as orc
     from paper_2512_05749_b200 import _lib, estimators, optimizers, synthetic
 
+    if not f32 and fp32_digits == 5:
+        pytest.skip("the float32 digit mode does not apply to float64 samples")
+    tol = F32_DIGIT_TOL[fp32_digits] if f32 else F32_DIGIT_TOL[7]
     cfg = synthetic.config("c2", N=1024, P=65536, k=128, L=192, delta=0.5, lam=1e-4)
     P, N, k = cfg["P"], cfg["N"], cfg["k"]
     wl = synthetic.HostWorkload.from_config(cfg, 12)
@@ -43,10 +46,13 @@ def test_k128_two_steps_match_oracle(f32):
                 return_update=True)
             assert diag.effective_rank == info["r_eff"]
             assert diag.ssi.iterations_used == info["iterations"]
-            assert rel(upd.cpu().numpy(), info["update"]) < 1e-10, t
+            e_upd = rel(upd.cpu().numpy(), info["update"])
             sig = torch.linalg.vector_norm(st.obar, dim=0).cpu().numpy()
-            assert rel(sig, info["sigma"]) < 1e-9, t
-            assert subspace_sine(st.u_prev.cpu().numpy(), ost.u_prev) < 1e-8, t
+            e_sig = rel(sig, info["sigma"])
+            e_sin = subspace_sine(st.u_prev.cpu().numpy(), ost.u_prev)
+            print(f"k128 f32={f32} digits={fp32_digits} step {t}: update {e_upd:.2e} "
+                  f"sigma {e_sig:.2e} sine {e_sin:.2e}")
+            assert e_upd < tol["update"] and e_sig < tol["sigma"] and e_sin < tol["sine"], t
             np.testing.assert_allclose(diag.projector_drift, info["projector_drift"], rtol=1e-6,
                                        atol=1e-13)
     finally:

@@ -116,20 +116,31 @@ def test_ozaki_accuracy_vs_dmma(layout, M, N, K):
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("offset,every", [(1e3, 1), (1e9, 1), (1e6, 3), (20.0, 37)])
 @pytest.mark.parametrize("f32", [False, True])
-def test_ozaki_large_column_means(layout, offset, every, f32):
+def test_ozaki_large_column_means(layout, offset, every, f32, fp32_digits):
     """Columns whose mean dwarfs their spread are digitised as rint((O - mu) s) (O - mu exact by
     Sterbenz), the others by integer centring rint(O s) - rint(mu s) (ozaki.cu biased_digits);
     K-blocks mixing both forms take the per-block branch.  Same accuracy either way."""
     if f32 and offset > 1e6:
         pytest.skip("float32 samples keep 24 bits: the offset would swallow the data")
+    if not f32 and fp32_digits == 5:
+        pytest.skip("the float32 digit mode does not apply to float64 samples")
     r = _run(layout, 384, 64, 3000, f32=f32, offset=offset, offset_every=every)
-    assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
+    if f32 and fp32_digits == 5:
+        assert r["ozaki"][0] < 1e-11 and r["ozaki"][1] < 1e-11, r
+    else:
+        assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
 
 
 @pytest.mark.parametrize("layout", [0, 1])
-def test_ozaki_fp32_samples(layout):
+def test_ozaki_fp32_samples(layout, fp32_digits):
+    """Float32 samples: 7 digits are FP64-grade; the default 5 (the top 5 of the same digits,
+    20 pairs) represent each element to 2^-38 of its column's scale, so products are accurate to
+    ~2^-39 of |X| |B| entrywise."""
     r = _run(layout, 700, 64, 3000, f32=True, pad=1)
-    assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
+    if fp32_digits == 7:
+        assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
+    else:
+        assert r["ozaki"][0] < 1e-11 and r["ozaki"][1] < 1e-11, r
 
 
 @pytest.mark.parametrize("layout", [0, 1])
