@@ -291,6 +291,11 @@ int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
  * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
 
+/* engine option (row-sharded runs): 1 (default) works the P x k tail of the SSI in P-slices, one
+ * per rank (reduce-scatter of u and w, slice CholeskyQR2 with allreduced k x k Grams, all-gather
+ * of q); 0 keeps it replicated on every rank (allreduce of u). */
+int wssr_set_tail_shard(wssr_ctx* ctx, int enabled);
+
 /* engine option: sample digits of the int8 O-passes for float32 samples (BASELINE configs[3]):
  * 5 (default) = the 5 most significant of the 7 digits (each element to 2^-38 of its column's
  * scale, exact for float32 values within 14 binades of the column maximum; 20 digit pairs and 5

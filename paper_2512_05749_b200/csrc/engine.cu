@@ -775,9 +775,11 @@ void apply_OT(Context& ctx, const Ohat& o, const double* q, int64_t ldq, int64_t
   }
 }
 
-// u (P x k, ldu) = Ohat v   (svdengine.py:134), summed over ranks
+// u (P x k, ldu) = Ohat v   (svdengine.py:134), summed over ranks: all of it (allreduce), or
+// with slice > 0 only this rank's slice of `slice` rows (reduce-scatter; u then has world * slice
+// rows of storage)
 void apply_O(Context& ctx, const Ohat& o, const double* v, int64_t ldv, int64_t k, double* u,
-             int64_t ldu) {
+             int64_t ldu, int64_t slice = 0) {
   if (o.n > 0) {
     PhaseTimer tm(ctx, 1, 2.0 * o.n * o.P * k, (o.f32 ? 4.0 : 8.0) * o.n * o.P);
     gemm_samples(ctx, Layout::CM, o, o.P, k, o.n, v + o.r * ldv, ldv, u, ldu, o.ss);
@@ -788,8 +790,39 @@ void apply_O(Context& ctx, const Ohat& o, const double* v, int64_t ldv, int64_t 
     gemm_cm(ctx, o.P, k, o.r, o.hist, o.ldh, nullptr, v, ldv, u, ldu, o.sh, true);
   if (ctx.world() > 1) {
     if (ldu != k) throw Fail{WSSR_ERR_VALUE, "sharded apply_O needs a dense output"};
-    allreduce(ctx, u, (size_t)(o.P * k));
+    if (slice > 0) {
+      if (ctx.comm->reduce_scatter_sum(u, (size_t)(slice * k), ctx.stream) != cudaSuccess)
+        throw Fail{WSSR_ERR_NCCL, "reduce-scatter failed"};
+    } else {
+      allreduce(ctx, u, (size_t)(o.P * k));
+    }
   }
+}
+
+// Tail sharding of a row-sharded run: the P x k blocks of the SSI (q, u, w) are worked on in
+// P-slices, one per rank - u and w arrive by reduce-scatter instead of allreduce, the
+// CholeskyQR2 of each block runs on the slice (k x k Grams allreduced) and q is all-gathered
+// for the next O-pass - so the P x k work of a step divides by the number of ranks and the u
+// exchange costs what the allreduce did.  Slices are S = ceil(P / world) rows; storage is padded
+// to world * S rows (the pad rows of the last slice are never read).  The careful (reference
+// Gram-Schmidt) re-run stays replicated.
+struct PSlice {
+  bool on = false;
+  int64_t S = 0, p0 = 0, rows = 0, padded = 0;
+};
+PSlice p_slice(const Context& ctx, int64_t P, bool careful) {
+  PSlice sl;
+  sl.rows = sl.padded = sl.S = P;
+  const int G = ctx.world();
+  if (G <= 1 || !ctx.tail_shard || careful) return sl;
+  const int64_t S = (P + G - 1) / G;
+  if (S * (G - 1) >= P) return sl;  // the last rank would have no rows
+  sl.on = true;
+  sl.S = S;
+  sl.p0 = (int64_t)ctx.comm->rank * S;
+  sl.rows = std::min(S, P - sl.p0);
+  sl.padded = S * G;
+  return sl;
 }
 
 // ||Ohat||_F^2 (svdengine.py:118,129): history block plus the sample block (known from
@@ -860,8 +893,18 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   const bool dist = ctx.world() > 1;
   cudaStream_t st = ctx.stream;
   o.status = status;  // the O-passes' precision guard reports into status[2]
-  Buf qbuf((size_t)P * k, st), ua((size_t)P * k, st), ub((size_t)P * k, st);
+  const PSlice sl = p_slice(ctx, P, careful);
+  Buf qbuf((size_t)sl.padded * k, st), ua((size_t)sl.padded * k, st),
+      ub((size_t)sl.padded * k, st);
   double* q = qbuf;
+  const int64_t r0 = sl.on ? sl.p0 : 0, nr = sl.on ? sl.rows : P;  // rows this rank works on
+  // q = QR(in) on this rank's slice (k x k Grams allreduced), then all-gathered; or replicated
+  auto qr_block = [&](const double* in, int64_t ldin, double* out) {
+    qr(ctx, nr, k, in + r0 * ldin, ldin, out + r0 * k, k, nullptr, status, careful, sl.on);
+    if (sl.on && ctx.comm->all_gather(out, (size_t)(sl.S * k), st) != cudaSuccess)
+      throw Fail{WSSR_ERR_NCCL, "all-gather failed"};
+  };
+  const int64_t scatter = sl.on ? sl.S : 0;
   Buf va((size_t)std::max<int64_t>(cols, 1) * k, st), vb((size_t)std::max<int64_t>(cols, 1) * k, st);
   Buf quot((size_t)k * k, st), scal(4, st);
   double* u = ua;
@@ -869,17 +912,17 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   double* v = va;
   double* v2 = vb;
 
-  qr(ctx, P, k, u_init, ld_init, q, k, nullptr, status, careful, false);  // svdengine.py:130
+  qr_block(u_init, ld_init, q);  // svdengine.py:130
   apply_OT(ctx, o, q, k, k, v, k);
-  apply_O(ctx, o, v, k, k, u, k);
+  apply_O(ctx, o, v, k, k, u, k, scatter);
   SsiResult res;
   int64_t it = 0;
   bool deferred_residual = false;
   while (true) {  // svdengine.py:132-142
     // the last iteration's q is the returned U when the order comes out sorted
     // (svdengine.py:151): write it there directly
-    if (it + 1 == max_iters && ldU == k && U_out) q = U_out;
-    qr(ctx, P, k, u, k, q, k, nullptr, status, careful, false);
+    if (it + 1 == max_iters && ldU == k && U_out && !sl.on) q = U_out;
+    qr_block(u, k, q);
     ++it;
     if (it >= max_iters && !final_res) {
       res.residual = std::numeric_limits<double>::quiet_NaN();  // look-ahead skipped
@@ -887,18 +930,22 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
     }
     // look-ahead pass: w = Ohat Ohat^T q is also the next iteration's u (svdengine.py:137)
     apply_OT(ctx, o, q, k, k, v2, k);
-    apply_O(ctx, o, v2, k, k, w, k);
+    apply_O(ctx, o, v2, k, k, w, k, scatter);
     {
       PhaseTimer tm(ctx, 4, 0.0, 0.0);
-      cross(ctx, P, k, q, k, w, k, quot);  // quotient = q^T w
-      if (ctx.tallskinny && ts_mul_supported(k, q, k, w, k)) {
+      const double* qs = q + r0 * k;
+      const double* ws = w + r0 * k;
+      cross(ctx, nr, k, qs, k, ws, k, quot);  // quotient = q^T w
+      if (sl.on) allreduce(ctx, quot, (size_t)(k * k));
+      if (ctx.tallskinny && ts_mul_supported(k, qs, k, ws, k)) {
         // ||w - q quotient||_F^2 straight from registers (nothing written)
-        WSSR_CUDA(ts_mul_add_sumsq(ctx, P, k, q, k, quot, -1.0, w, k, scal));
+        WSSR_CUDA(ts_mul_add_sumsq(ctx, nr, k, qs, k, quot, -1.0, ws, k, scal));
       } else {
-        Buf tmp((size_t)P * k, st);
-        gemm_rm_add(ctx, P, k, k, q, k, quot, k, w, k, tmp, k, -1.0);  // w - q quotient
-        sumsq_matrix(ctx, tmp, P, k, k, scal);
+        Buf tmp((size_t)nr * k, st);
+        gemm_rm_add(ctx, nr, k, k, qs, k, quot, k, ws, k, tmp, k, -1.0);  // w - q quotient
+        sumsq_matrix(ctx, tmp, nr, k, k, scal);
       }
+      if (sl.on) allreduce(ctx, scal, 1);
       launch_pdl(small_norms_kernel, 1, 256, 0, st, nullptr, nullptr, 0, quot, (int)k, scal + 1);
       post_launch(ctx);
     }
@@ -960,6 +1007,18 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
   for (int64_t j = 0; j < kp && identity; ++j) identity = hord[j] == j;
   if (identity) {
     if (q != U_out) copy2d(ctx, q, k, P, k, 1.0, U_out, ldU);
+  } else if (sl.on) {
+    // this rank's slice of u, permuted, QR'd on the slices and all-gathered
+    Buf uperm((size_t)sl.padded * kp, st), ufull((size_t)sl.padded * kp, st);
+    launch_pdl(gather_cols_kernel, blocks_for(nr * kp, 256, 16 * ctx.num_sms), 256, 0, st,
+               (const double*)(u + r0 * k), k, nr, res.order.i64(), (int)kp,
+               uperm.p + r0 * kp, kp);
+    post_launch(ctx);
+    qr(ctx, nr, kp, uperm.p + r0 * kp, kp, ufull.p + r0 * kp, kp, nullptr, status, careful,
+       true);
+    if (ctx.comm->all_gather(ufull, (size_t)(sl.S * kp), st) != cudaSuccess)
+      throw Fail{WSSR_ERR_NCCL, "all-gather failed"};
+    copy2d(ctx, ufull, kp, P, kp, 1.0, U_out, ldU);
   } else {
     Buf uperm((size_t)P * kp, st);
     launch_pdl(gather_cols_kernel, blocks_for(P * kp, 256, 16 * ctx.num_sms), 256, 0, st, 
@@ -1619,6 +1678,8 @@ struct NcclUniqueId {
 typedef int (*nccl_get_id_fn)(NcclUniqueId*);
 typedef int (*nccl_init_rank_fn)(void**, int, NcclUniqueId, int);
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_reduce_scatter_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_all_gather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
 typedef int (*nccl_destroy_fn)(void*);
 
 struct NcclLib {
@@ -1626,6 +1687,8 @@ struct NcclLib {
   nccl_get_id_fn get_id = nullptr;
   nccl_init_rank_fn init_rank = nullptr;
   nccl_allreduce_fn allreduce = nullptr;
+  nccl_reduce_scatter_fn reduce_scatter = nullptr;
+  nccl_all_gather_fn all_gather = nullptr;
   nccl_destroy_fn destroy = nullptr;
   bool load() {
     if (h) return true;
@@ -1638,8 +1701,10 @@ struct NcclLib {
     get_id = (nccl_get_id_fn)dlsym(h, "ncclGetUniqueId");
     init_rank = (nccl_init_rank_fn)dlsym(h, "ncclCommInitRank");
     allreduce = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+    reduce_scatter = (nccl_reduce_scatter_fn)dlsym(h, "ncclReduceScatter");
+    all_gather = (nccl_all_gather_fn)dlsym(h, "ncclAllGather");
     destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
-    return get_id && init_rank && allreduce && destroy;
+    return get_id && init_rank && allreduce && reduce_scatter && all_gather && destroy;
   }
 };
 NcclLib g_nccl;
@@ -1649,6 +1714,16 @@ struct NcclComm : Comm {
   cudaError_t allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
     // ncclFloat64 = 8, ncclSum = 0
     int r = g_nccl.allreduce(buf, buf, n, 8, 0, comm, st);
+    return r == 0 ? cudaSuccess : cudaErrorUnknown;
+  }
+  // in place: recvbuff = sendbuff + rank * count (nccl.h "in-place operations")
+  cudaError_t reduce_scatter_sum(double* buf, size_t count, cudaStream_t st) override {
+    int r = g_nccl.reduce_scatter(buf, buf + (size_t)rank * count, count, 8, 0, comm, st);
+    return r == 0 ? cudaSuccess : cudaErrorUnknown;
+  }
+  // in place: sendbuff = recvbuff + rank * count
+  cudaError_t all_gather(double* buf, size_t count, cudaStream_t st) override {
+    int r = g_nccl.all_gather(buf + (size_t)rank * count, buf, count, 8, comm, st);
     return r == 0 ? cudaSuccess : cudaErrorUnknown;
   }
   ~NcclComm() override {
@@ -1734,6 +1809,26 @@ struct EmuComm : Comm {
     }
     if (!g->barrier()) return cudaErrorUnknown;
     e = cudaMemcpyAsync(buf, g->scratch, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (!g->barrier()) return cudaErrorUnknown;
+    return e;
+  }
+  // every rank copies the other ranks' slices straight from their buffers (same device)
+  cudaError_t all_gather(double* buf, size_t count, cudaStream_t st) override {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      g->abort();
+      return e;
+    }
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->bufs[rank] = buf;
+    }
+    if (!g->barrier()) return cudaErrorUnknown;
+    for (int r = 0; r < world && e == cudaSuccess; ++r)
+      if (r != rank)
+        e = cudaMemcpyAsync(buf + (size_t)r * count, g->bufs[r] + (size_t)r * count,
+                            count * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (!g->barrier()) return cudaErrorUnknown;
     return e;
@@ -1856,6 +1951,12 @@ int wssr_set_gemm_path(wssr_ctx* ctx, int path) {
   ctx->c.ozaki = path == 0 || path >= 3;
   ctx->c.oz_min_elems = path >= 3 ? 0.0 : 4194304.0;
   ctx->c.oz_pre = path == 4 ? 1 : 0;
+  return WSSR_OK;
+}
+
+int wssr_set_tail_shard(wssr_ctx* ctx, int enabled) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  ctx->c.tail_shard = enabled != 0;
   return WSSR_OK;
 }
 

@@ -21,6 +21,13 @@ struct Comm {
   int rank = 0, world = 1;
   virtual ~Comm() = default;
   virtual cudaError_t allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
+  // In place over buf[world * count]: afterwards this rank's slice [rank * count, +count) holds
+  // the sum over ranks (the other slices are unspecified).
+  virtual cudaError_t reduce_scatter_sum(double* buf, size_t count, cudaStream_t st) {
+    return allreduce_sum(buf, (size_t)world * count, st);
+  }
+  // In place over buf[world * count]: every rank's slice is copied to all ranks.
+  virtual cudaError_t all_gather(double* buf, size_t count, cudaStream_t st) = 0;
 };
 
 struct Context {
@@ -42,6 +49,7 @@ struct Context {
   bool chol_series = true;   // near-identity Grams: series Cholesky (kernels.cuh chol_series)
   bool tallskinny = true;    // k = 32/64 Grams and products of P x k blocks: tallskinny.cu
   bool force_blocked_svd = false;  // dense SVD: blocked Jacobi at every size (tests)
+  bool tail_shard = true;          // row-sharded runs: the P x k tail of the SSI on P-slices
   int dense_svd_sweeps = 0;        // outer sweeps of the last blocked dense SVD
   double* hbuf = nullptr;          // pinned host staging for the step's small readbacks (4096)
   cudaStream_t aux = nullptr;      // optional: asynchronous drift telemetry (wssr_set_aux_stream)

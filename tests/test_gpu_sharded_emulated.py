@@ -167,3 +167,93 @@ def test_sharded_int8_o_passes(golden, path):
             assert a["r_eff"] == b["r_eff"] and a["iterations"] == b["iterations"]
             assert rel(b["update"], a["update"]) < 1e-11
             assert rel(b["sigma"], a["sigma"]) < 1e-11
+
+
+def _with_tail_shard(shard, fn):
+    """Run fn on an emulated rank with the engine's tail sharding switched on or off."""
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    ctx.lib.wssr_set_tail_shard(ctx.handle, int(shard))
+    try:
+        return fn()
+    finally:
+        ctx.lib.wssr_set_tail_shard(ctx.handle, 1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["c0_T20.npz", "hist_T4.npz"])
+def test_tail_shard_matches_replicated_tail(golden, name, world):
+    """The P-sliced SSI tail (reduce-scatter of u/w, slice CholeskyQR2, all-gather of q) against
+    the replicated tail (allreduce of u, every rank factorising all of P) on the same shards:
+    only the summation order of the k x k Grams differs.  Replicated outputs stay identical across
+    ranks."""
+    from paper_2512_05749_b200.distributed import EmulatedGroup, row_shard
+    from _runs import fixture_config
+
+    g = golden(name)
+    n = fixture_config(name, g)[0]["N"]
+    res = {}
+    for shard in (1, 0):
+        with EmulatedGroup(world) as grp:
+            res[shard] = grp.run(lambda r, w, s=shard: _with_tail_shard(
+                s, lambda: device_run(name, g, rows=row_shard(n, r, w))))
+    for r in range(world):
+        for a, b in zip(res[0][r], res[1][r]):
+            assert a["r_eff"] == b["r_eff"] and a["iterations"] == b["iterations"]
+            assert rel(b["update"], a["update"]) < 1e-11
+            assert rel(b["sigma"], a["sigma"]) < 1e-11
+            assert subspace_sine(b["V"], a["V"]) < 1e-9
+    for t in range(len(res[1][0])):
+        for r in range(1, world):
+            assert np.array_equal(res[1][r][t]["update"], res[1][0][t]["update"])
+            assert np.array_equal(res[1][r][t]["V"], res[1][0][t]["V"])
+
+
+def test_tail_shard_k128_uneven_slices():
+    """k = 128 (the c2/c3 rank, tall-skinny kernels) on 3 uneven P-slices (P = 65536 = 3 x 21846
+    - 2) with int8 O-passes, against the single-rank run."""
+    import torch
+
+    from paper_2512_05749_b200 import _lib, estimators, linalg, optimizers, synthetic
+    from paper_2512_05749_b200.distributed import EmulatedGroup, row_shard
+
+    cfg = synthetic.config("c2", N=1536, P=65536, k=128, L=192, delta=0.5, lam=1e-4)
+    N, P, k = cfg["N"], cfg["P"], cfg["k"]
+
+    def run(rows):
+        ctx = _lib.context()
+        ctx.lib.wssr_set_gemm_path(ctx.handle, 3)
+        try:
+            wl = synthetic.HostWorkload.from_config(cfg, 21)
+            v0 = linalg.qr_orthonormalize(wl.v0_raw())[0]
+            dev = torch.device("cuda")
+            st = optimizers.WssrState(obar=torch.zeros(0, P, dtype=torch.float64, device=dev).t(),
+                                      lbar=torch.zeros(0, dtype=torch.float64, device=dev),
+                                      u_prev=v0, r_max=k, delta=cfg["delta"],
+                                      sigma_floor=cfg["lam"], eps_grow=0.0, step=1)
+            out = []
+            for _ in range(2):
+                o, e = wl.next()
+                if rows is not None:
+                    o, e = o[rows[0]:rows[0] + rows[1]], e[rows[0]:rows[0] + rows[1]]
+                b = estimators.assemble(estimators.SampleBatch((None,) * o.shape[0], e, o))
+                _, st, diag, upd = optimizers.wssr_step(
+                    torch.zeros(P, dtype=torch.float64, device=dev), b, 1.0, st,
+                    return_update=True)
+                out.append(dict(update=upd.cpu().numpy(), V=st.u_prev.cpu().numpy(),
+                                sigma=optimizers.sigma_of(st).cpu().numpy(),
+                                it=diag.ssi.iterations_used, r_eff=diag.effective_rank))
+            return out
+        finally:
+            ctx.lib.wssr_set_gemm_path(ctx.handle, 0)
+
+    single = run(None)
+    with EmulatedGroup(3) as grp:
+        per_rank = grp.run(lambda r, w: run(row_shard(N, r, w)))
+    for runs in per_rank:
+        for a, b in zip(single, runs):
+            assert a["it"] == b["it"] and a["r_eff"] == b["r_eff"]
+            assert rel(b["update"], a["update"]) < 1e-10
+            assert rel(b["sigma"], a["sigma"]) < 1e-10
+            assert subspace_sine(b["V"], a["V"]) < 1e-8
