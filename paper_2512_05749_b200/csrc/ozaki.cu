@@ -649,6 +649,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                        : biased_int(base[i * BM], cw_r, hi_word(inv_r));
       }
     };
+    // row-major fast path (no Sterbenz-form column in the K-block): the table entries of this
+    // thread's 8 K values are read once and serve both of its rows
+    auto load_tab = [&](int s, uint64_t (&cw)[8], uint32_t (&hs)[8]) {
+      const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + 2 * q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double2 m = mi[8 * j];
+        cw[j] = as_u64(m.x);
+        hs[j] = hi_word(m.y);
+      }
+    };
+    auto convert8_tab = [&](int s, int row, const uint64_t (&cw)[8], const uint32_t (&hs)[8],
+                            uint64_t (&y)[8]) {
+      if (F32) {
+        const unsigned char* base = a_raw(s) + row * 128;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float4 f =
+              *reinterpret_cast<const float4*>(base + (((2 * q + c) ^ (row & 7)) << 4));
+          const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) y[4 * c + e] = biased_int(fv[e], cw[4 * c + e], hs[4 * c + e]);
+        }
+      } else {
+        const unsigned char* base = a_raw(s) + (q >> 1) * 16384 + row * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double2 v =
+              *reinterpret_cast<const double2*>(base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
+          y[2 * c] = biased_int(v.x, cw[2 * c], hs[2 * c]);
+          y[2 * c + 1] = biased_int(v.y, cw[2 * c + 1], hs[2 * c + 1]);
+        }
+      }
+    };
     auto store8 = [&](int d, int row, const uint32_t (&w)[ND][2]) {
       unsigned char* dst =
           a_dig(d) + row * BK + ((((q >> 1) ^ ((row >> 2) & 1))) << 4) + ((q & 1) << 3);
@@ -697,26 +731,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // one row at a time (digits packed before the next row converts: fewer live registers)
         uint32_t wA[ND][2], wB[ND][2];
-        {
-          uint64_t y[8];
-          const bool exact =
-              RM ? __double_as_longlong(s_mi(s)[3]) != 0 : exactCM;  // uniform per K-block
-          convert8(s, rowA, cwA, invA, muA, exact, y);
-          if (guard) {
+        const bool exact =
+            RM ? __double_as_longlong(s_mi(s)[3]) != 0 : exactCM;  // uniform per K-block
+        if (RM && !exact) {
+          uint64_t tcw[8];
+          uint32_t ths[8];
+          load_tab(s, tcw, ths);
+          {
+            uint64_t y[8];
+            convert8_tab(s, rowA, tcw, ths, y);
+            if (guard) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) cntA += guard_count(y[i]);
+              for (int i = 0; i < 8; ++i) cntA += guard_count(y[i]);
+            }
+            pack_digits8(y, wA);
           }
-          pack_digits8(y, wA);
-        }
-        {
-          uint64_t y[8];
-          const bool exact = RM ? __double_as_longlong(s_mi(s)[3]) != 0 : exactCM;
-          convert8(s, rowB, cwB, invB, muB, exact, y);
-          if (guard) {
+          {
+            uint64_t y[8];
+            convert8_tab(s, rowB, tcw, ths, y);
+            if (guard) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) cntB += guard_count(y[i]);
+              for (int i = 0; i < 8; ++i) cntB += guard_count(y[i]);
+            }
+            pack_digits8(y, wB);
           }
-          pack_digits8(y, wB);
+        } else {
+          {
+            uint64_t y[8];
+            convert8(s, rowA, cwA, invA, muA, exact, y);
+            if (guard) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) cntA += guard_count(y[i]);
+            }
+            pack_digits8(y, wA);
+          }
+          {
+            uint64_t y[8];
+            convert8(s, rowB, cwB, invB, muB, exact, y);
+            if (guard) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) cntB += guard_count(y[i]);
+            }
+            pack_digits8(y, wB);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[s]);  // raw tile consumed (values are in registers)
