@@ -291,6 +291,10 @@ int wssr_debug_ozaki_trace(wssr_ctx* ctx, long long* out, int64_t n);
  * (csrc/tallskinny.cu); 0 on the generic tile GEMMs. */
 int wssr_set_tallskinny(wssr_ctx* ctx, int enabled);
 
+/* returns the context's cached device memory (digit planes, scratch blocks, the stream-ordered
+ * pool's reserve) to the driver; everything regrows on demand.  Synchronises the device. */
+int wssr_release_memory(wssr_ctx* ctx);
+
 /* engine option (row-sharded runs): 1 (default) works the P x k tail of the SSI in P-slices, one
  * per rank (reduce-scatter of u and w, slice CholeskyQR2 with allreduced k x k Grams, all-gather
  * of q); 0 keeps it replicated on every rank (allreduce of u). */

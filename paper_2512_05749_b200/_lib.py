@@ -102,6 +102,7 @@ SIGNATURES = {
     "wssr_set_dense_svd_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_fp32_digits": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_tail_shard": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_release_memory": (ctypes.c_int, [_vp]),
     "wssr_dense_svd_sweeps": (ctypes.c_int, [_vp]),
     "wssr_set_aux_stream": (ctypes.c_int, [_vp, _vp]),
     "wssr_grad_theta_f64": (ctypes.c_int, [_vp, ctypes.POINTER(AceSpec), _vp, _i64, _vp, _i64]),

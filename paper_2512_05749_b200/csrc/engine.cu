@@ -1927,6 +1927,26 @@ void wssr_ctx_destroy(wssr_ctx* ctx) {
 
 const char* wssr_last_error(const wssr_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : ""; }
 
+int wssr_release_memory(wssr_ctx* ctx) {
+  if (!ctx) return WSSR_ERR_VALUE;
+  Context& c = ctx->c;
+  cudaSetDevice(c.device);
+  cudaDeviceSynchronize();
+  if (c.oz_planes) cudaFree(c.oz_planes);
+  c.oz_planes = nullptr;
+  c.oz_planes_cap = 0;
+  c.plan_n = c.plan_p = c.plan_k = -1;
+  c.plan_rows = 0;
+  c.plan_provisional = false;
+  if (c.oz_ws) cudaFree(c.oz_ws);
+  c.oz_ws = nullptr;
+  c.oz_ws_cap = 0;
+  g_scratch.trim(c.device);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  return cudaGetLastError() == cudaSuccess ? WSSR_OK : WSSR_ERR_CUDA;
+}
+
 int wssr_set_stream(wssr_ctx* ctx, void* stream) {
   if (!ctx) return WSSR_ERR_VALUE;
   ctx->c.stream = reinterpret_cast<cudaStream_t>(stream);

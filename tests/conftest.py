@@ -58,3 +58,25 @@ def fp32_digits(request):
     ctx.lib.wssr_set_fp32_digits(ctx.handle, request.param)
     yield request.param
     ctx.lib.wssr_set_fp32_digits(ctx.handle, 5)
+
+
+def release_device_memory():
+    """Return torch's cache and the engine's cached device memory (digit planes, scratch, pool
+    reserve) to the driver: the full-size tests need most of the 180 GB."""
+    import gc
+
+    import torch
+
+    from paper_2512_05749_b200 import _lib
+
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    _lib.context().call("wssr_release_memory")
+
+
+@pytest.fixture
+def big_memory():
+    release_device_memory()
+    yield
+    release_device_memory()

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-def test_c3_step_int8_vs_dmma(fp32_digits):
+def test_c3_step_int8_vs_dmma(fp32_digits, big_memory):
     from paper_2512_05749_b200 import _lib, estimators, linalg, optimizers, synthetic
 
     if torch.cuda.get_device_properties(0).total_memory < 150e9:

@@ -1,4 +1,4 @@
-"""Where the host time of one c1 step goes: Python around the C calls vs the C calls themselves
+"""Where the host time of one step (c1, or the config named on the command line) goes: Python around the C calls vs the C calls themselves
 (each wssr_* call is timed with perf_counter; the step ends with a device sync, so the wall time
 of a step ~ its device time)."""
 import sys
@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2512_05749_b200 import _lib, estimators, optimizers, synthetic  # noqa: E402
 
-cfg = synthetic.config("c1")
+cfg = synthetic.config(sys.argv[1] if len(sys.argv) > 1 else "c1")
 ctx = _lib.context()
 calls = []
 orig = ctx.call
