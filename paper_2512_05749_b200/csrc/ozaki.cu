@@ -683,6 +683,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
+    // column-major fast path: the K rows of the raw tile are 1 KB apart, so the four K-quarter
+    // lane groups of a row would hit the same banks (4-way).  Odd quarters read row B while even
+    // ones read row A (64 bytes apart: the other 16 banks), then the other row: 2-way at most,
+    // i.e. the ideal two wavefronts per 256-byte load.
+    auto convert16_cm = [&](int s, uint64_t cw_a, uint32_t hs_a, uint64_t cw_b, uint32_t hs_b,
+                            uint64_t (&ya)[8], uint64_t (&yb)[8]) {
+      const TA* base = reinterpret_cast<const TA*>(a_raw(s)) + (8 * q) * BM;
+      const bool odd = q & 1;
+      const TA* p0 = base + (odd ? rowB : rowA);
+      const TA* p1 = base + (odd ? rowA : rowB);
+      TA x0[8], x1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x0[i] = p0[i * BM];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x1[i] = p1[i * BM];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ya[i] = biased_int(odd ? x1[i] : x0[i], cw_a, hs_a);
+        yb[i] = biased_int(odd ? x0[i] : x1[i], cw_b, hs_b);
+      }
+    };
     auto store8 = [&](int d, int row, const uint32_t (&w)[ND][2]) {
       unsigned char* dst =
           a_dig(d) + row * BK + ((((q >> 1) ^ ((row >> 2) & 1))) << 4) + ((q & 1) << 3);
@@ -733,7 +754,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t wA[ND][2], wB[ND][2];
         const bool exact =
             RM ? __double_as_longlong(s_mi(s)[3]) != 0 : exactCM;  // uniform per K-block
-        if (RM && !exact) {
+        if (!RM && !exact) {
+          uint64_t ya[8], yb[8];
+          convert16_cm(s, cwA, hi_word(invA), cwB, hi_word(invB), ya, yb);
+          pack_digits8(ya, wA);
+          pack_digits8(yb, wB);
+        } else if (RM && !exact) {
           uint64_t tcw[8];
           uint32_t ths[8];
           load_tab(s, tcw, ths);
