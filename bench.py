@@ -180,36 +180,81 @@ def _oracle_step_time(cfg, index, rows):
     return time.perf_counter() - t0
 
 
-def cpu_sample_rate(cfg, index, threads=None):
+def _oracle_row_time(cfg, index, nb=1024):
+    """Seconds per sample row of the sample-count-dependent work of one oracle step on `nb` rows
+    (all P parameters, rank k): assemble (means, centring, the transposed o_matrix copy, the
+    gradient) plus the 12 O-pass GEMMs of 3 SSI iterations (svdengine.py:133-137:
+    v = ohat^T q, u = ohat v, and the look-ahead pair, per iteration)."""
+    import numpy as np
+
+    from oracle import wssr_oracle as orc
+    from paper_2512_05749_b200 import synthetic
+
+    wl = synthetic.HostWorkload.from_config(dict(cfg, N=nb), index)
+    o, e = wl.next()
+    q = np.linalg.qr(np.random.default_rng(1).standard_normal((cfg["P"], cfg["k"])))[0]
+    t0 = time.perf_counter()
+    b = orc.assemble(o, e)
+    oh = b["o_matrix"]
+    for _ in range(6):
+        v = oh.T @ q
+        q = oh @ v
+        q /= np.linalg.norm(q, axis=0)
+    return (time.perf_counter() - t0) / nb
+
+
+def cpu_sample_rate(cfg, index, threads=None, warm=False, ratio=None):
     """The reference algorithm (oracle port, numpy/OpenBLAS) on this host, as steps/s of the FULL
-    config.  Configs whose step fits a bounded CPU sample (c0, c1) run whole steps.  Larger ones
-    (c2: the reference needs ~4|O| = 550 GB of RAM and hours per step) run two bounded samples -
-    the first N1 and N2 samples with all P parameters and rank k - and the step time is
-    extrapolated linearly in the sample count, t(N) = t(N1) + (N - N1) (t(N2) - t(N1)) / (N2 - N1)
-    (the O-passes scale with N; the P x k QR / preconditioner work does not, and the fit keeps it
-    as the intercept).  Returns (steps/s, sample description, seconds spent)."""
+    config.  Configs whose step fits a bounded CPU sample (c0, c1) run whole steps (warm=True:
+    one discarded step first).  Larger ones (c2: the reference needs ~4|O| = 550 GB of RAM and
+    hours per step) are estimated from bounded samples: one whole step on the first N1 = 128
+    samples (all P parameters and rank k: every P x k QR, the drift SVD, the preconditioner),
+    plus the per-row cost of the sample-count-dependent work (assemble and the 12 O-pass GEMMs)
+    timed on 1024 rows: t(N) = t(N1) + (N - N1) t_row.  ratio (single-thread runs of large
+    configs): the single-thread/all-thread ratio of a P/32 slice of the same sample, times the
+    all-thread estimate passed in.  Returns (steps/s, sample description, seconds spent,
+    t(N) in seconds)."""
     from contextlib import nullcontext
 
     try:
         from threadpoolctl import threadpool_limits
-        lim = threadpool_limits(limits=threads) if threads else nullcontext()
     except Exception:
-        lim = nullcontext()
-    with lim:
-        t_start = time.perf_counter()
-        N = cfg["N"]
-        if N * cfg["P"] <= 4096 * 131072:
+        threadpool_limits = None
+
+    def limit(n):
+        return threadpool_limits(limits=n) if (threadpool_limits and n) else nullcontext()
+
+    t_start = time.perf_counter()
+    N = cfg["N"]
+    if N * cfg["P"] <= 4096 * 131072:
+        with limit(threads):
+            if warm:
+                _oracle_step_time(cfg, index, N)
             t = _oracle_step_time(cfg, index, N)
-            return 1.0 / t, f"1 full {cfg['name']} step", time.perf_counter() - t_start
-        n1, n2 = 128, 256
+        return 1.0 / t, f"1 full {cfg['name']} step", time.perf_counter() - t_start, t
+    n1 = 128
+    if ratio is not None:  # single thread: a P/32 slice at 1 and at all threads
+        sl = dict(cfg, P=cfg["P"] // 32)
+        with limit(None):
+            t_all = _oracle_step_time(sl, index, n1)
+        with limit(threads):
+            t_one = _oracle_step_time(sl, index, n1)
+        tN = ratio * t_one / t_all
+        desc = (f"{cfg['name']} step, single thread, scaled: a P/32 slice of the {n1}-sample "
+                f"step took {t_one:.2f} s on 1 thread and {t_all:.2f} s on all threads; "
+                f"x the all-thread estimate {ratio:.1f} s = {tN:.1f} s")
+        return 1.0 / tN, desc, time.perf_counter() - t_start, tN
+    with limit(threads):
+        if warm:
+            _oracle_step_time(cfg, index, 32)
         t1 = _oracle_step_time(cfg, index, n1)
-        t2 = _oracle_step_time(cfg, index, n2)
-        slope = max(t2 - t1, 0.0) / (n2 - n1)
-        tN = t1 + (N - n1) * slope
-        desc = (f"{cfg['name']} step extrapolated from bounded samples: the first {n1} and {n2} "
-                f"samples (all P={cfg['P']} params, k={cfg['k']}) took {t1:.2f} s and {t2:.2f} s; "
-                f"t(N={N}) = t({n1}) + (N-{n1}) * slope = {tN:.1f} s")
-        return 1.0 / tN, desc, time.perf_counter() - t_start
+        t_row = _oracle_row_time(cfg, index)
+    tN = t1 + (N - n1) * t_row
+    desc = (f"{cfg['name']} step estimated from bounded samples: one whole step on the first "
+            f"{n1} samples (all P={cfg['P']} params, k={cfg['k']}) took {t1:.2f} s; assemble + "
+            f"the 12 O-pass GEMMs cost {1e3 * t_row:.3f} ms per sample row (timed on 1024 rows); "
+            f"t(N={N}) = {t1:.1f} + {N - n1} x {1e3 * t_row:.3f} ms = {tN:.1f} s")
+    return 1.0 / tN, desc, time.perf_counter() - t_start, tN
 
 
 def run_reference(args, rank):
@@ -220,17 +265,15 @@ def run_reference(args, rank):
     cfg = synthetic.config(args.config)
     idx = int(args.config[1:]) if args.config[1:].isdigit() else 1
     _warm_blas()
-    for _ in range(max(0, args.warmup)):
-        cpu_sample_rate(cfg, idx)
-        break  # one warm-up sample is enough for the BLAS thread pool and page faults
-    rates, desc, spent = [], "", 0.0
-    for _ in range(max(1, args.steps)):
-        r, desc, dt = cpu_sample_rate(cfg, idx)
+    rates, times, desc, spent = [], [], "", 0.0
+    for i in range(max(1, args.steps)):
+        r, desc, dt, tN = cpu_sample_rate(cfg, idx, warm=(i == 0 and args.warmup > 0))
         rates.append(r)
+        times.append(tN)
         spent += dt
-        if spent > 150.0:
+        if spent > 120.0:
             break
-    one, desc1, _ = cpu_sample_rate(cfg, idx, threads=1)
+    one, desc1, _, _ = cpu_sample_rate(cfg, idx, threads=1, ratio=statistics.median(times))
     value = statistics.median(rates)
     cores = host_cores()
     line = {
@@ -241,7 +284,7 @@ def run_reference(args, rank):
         "data": "synthetic (seeded numpy generator, SURVEY.md 8(d))",
         "config": workload_config(cfg, args),
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "statistic": f"median of {len(rates)} samples (150 s budget)",
+                         "statistic": f"median of {len(rates)} samples (120 s budget)",
                          "sample": desc, "single_thread": {"value": one, "sample": desc1},
                          **host_info()},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
@@ -445,6 +488,10 @@ def measure(cfg_name, args, rank, world, local_rank, e2e_numpy=False, cpu=True):
 
     # ---- end to end through the public API with host buffers ------------------------------
     if not args.no_e2e:
+        # the e2e loop holds its own host-side staging and per-step tensors: let the engine
+        # re-plan its digit planes from scratch against that footprint
+        torch.cuda.synchronize()
+        ctx.call("wssr_release_memory")
         rec["e2e"] = _e2e_pinned(wl, step, fresh_state, theta, rows, P, N, esize, world, dev,
                                  stream, aux, barrier, dist)
         if e2e_numpy:
@@ -457,7 +504,7 @@ def measure(cfg_name, args, rank, world, local_rank, e2e_numpy=False, cpu=True):
     if cpu and rank == 0 and world == 1 and not args.no_cpu_baseline:
         idx = int(cfg_name[1:]) if cfg_name[1:].isdigit() else 1
         _warm_blas()
-        v, desc, _ = cpu_sample_rate(cfg, idx)
+        v, desc, _, _ = cpu_sample_rate(cfg, idx, warm=True)
         rec["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": host_cores(),
                                "kind": "port", "sample": desc + " (oracle/wssr_oracle.py on "
                                "numpy/OpenBLAS, all host threads)", **host_info()}

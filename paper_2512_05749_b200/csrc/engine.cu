@@ -610,7 +610,8 @@ bool ensure_planes(Context& ctx, size_t bytes) {
 // 7-byte planes of 16384 x 2^20 samples are 120 GB), 0 below 1024.  The first step plans with a
 // cold margin (2 GiB + 16 P x k blocks: its scratch is not allocated yet); a partial plan is
 // revisited once at the next step, when the step's scratch sits in the context's pool and
-// cudaMemGetInfo already counts it, with a warm margin of 2 GiB + 2 P x k blocks.
+// cudaMemGetInfo already counts it, with a warm margin of 2 GiB + 6 P x k blocks (room for the
+// caller's own per-step tensors).
 int sample_digits(const Context& ctx, const Ohat& o) {
   return (o.f32 && ctx.f32_digits == 5) ? 5 : 7;
 }
@@ -628,7 +629,7 @@ int64_t plan_plane_rows(Context& ctx, const Ohat& o, int64_t k) {
     if (full <= ctx.oz_planes_cap) return o.n;
     if (same && !(ctx.plan_provisional && warm)) return ctx.plan_rows;
   }
-  const size_t blocks = warm && same ? 2 : 16;
+  const size_t blocks = warm && same ? 6 : 16;
   const size_t margin = ((size_t)2 << 30) + blocks * o.P * std::max<int64_t>(k, 1) * 8;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
