@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-producer", action="store_true",
+                    help="skip the device-producer record (secondary c1 only)")
     ap.add_argument("--fast-report", action="store_true",
                     help="skip the telemetry-only final look-ahead (SsiReport.subspace_residual)")
     return ap.parse_args()
@@ -658,6 +660,99 @@ def _e2e_numpy(wl, fresh_state, rows, P, N, esize, world, dev, stream, aux, barr
                     "theta) -> numpy theta', the reference runner's convention"}
 
 
+def measure_producer(cfg_name, args):
+    """(f)2, the device producer of O: AceWavefunction.grad_theta_batch (csrc/producer.cu) on a
+    seeded synthetic ansatz with the config's P (n_electrons x n_features) and N walkers
+    (paper_2512_05749_b200/synthetic_ansatz.py).  Reports the producer's own throughput and an
+    end-to-end VMC-style step where the host uploads only walker positions and local energies:
+    positions -> O on the device -> assemble -> wssr_step -> theta' read back (and fed to the
+    ansatz), all inside the timed region."""
+    import numpy as np
+    import torch
+
+    from paper_2512_05749_b200 import (_lib, estimators, linalg, optimizers, synthetic,
+                                       synthetic_ansatz, wavefunction)
+
+    cfg = synthetic.config(cfg_name)
+    N, P, k = cfg["N"], cfg["P"], cfg["k"]
+    n_el = 16
+    kw, walkers = synthetic_ansatz.ansatz(n_electrons=n_el, n_features=P // n_el, seed=5)
+    spec = wavefunction.AceSpec(**kw)
+    dev = torch.device("cuda")
+    stream = torch.cuda.current_stream()
+    ctx = _lib.context()
+    x = torch.as_tensor(walkers(N, 0), device=dev)
+    for _ in range(3):
+        wavefunction.grad_theta_batch(spec, x)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    a.record(stream)
+    for _ in range(reps):
+        O = wavefunction.grad_theta_batch(spec, x)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    out_bytes = N * P * 8
+    peak = _peaks()[0]
+    producer = {"ms_per_batch": ms, "walkers_per_s": N / (ms * 1e-3),
+                "o_written_gbs": out_bytes / (ms * 1e-3) / 1e9,
+                "frac_hbm": out_bytes / (ms * 1e-3) / 1e9 / peak,
+                "shape": f"{N} walkers x {n_el} electrons x {P // n_el} features (P = {P}), "
+                         f"{len(kw['orbitals'])} orbitals, 2-orbital tails",
+                "note": "algorithmic bytes = the O block written once (N x P x 8); the feature "
+                        "block is staged in the output rows and transformed in place, so DRAM "
+                        "traffic is a few times that"}
+
+    # end to end: positions (and energies) from pinned host memory every step
+    v0 = linalg.qr_orthonormalize(torch.randn(P, k, dtype=torch.float64, device=dev,
+                                              generator=torch.Generator(device=dev).manual_seed(9)))[0]
+
+    def fresh():
+        return optimizers.WssrState(obar=torch.zeros(0, P, dtype=torch.float64, device=dev).t(),
+                                    lbar=torch.zeros(0, dtype=torch.float64, device=dev),
+                                    u_prev=v0, r_max=k, delta=cfg["delta"],
+                                    sigma_floor=cfg["lam"], eps_grow=0.0, step=1)
+
+    pos_h = [torch.as_tensor(walkers(N, t + 1)).pin_memory() for t in range(2)]
+    e_h = [torch.as_tensor(-1.0 + 0.1 * np.random.default_rng(t).standard_normal(N)).pin_memory()
+           for t in range(2)]
+    theta_h = torch.as_tensor(kw["theta"]).pin_memory()
+    out_h = torch.empty(P, dtype=torch.float64, pin_memory=True)
+    cfgs = (None,) * N
+    fallbacks0 = ctx.precision_fallbacks()
+
+    def run(nsteps, st):
+        th = theta_h.to(dev, non_blocking=True)
+        for t in range(nsteps):
+            xp = pos_h[t % 2].to(dev, non_blocking=True)
+            e = e_h[t % 2].to(dev, non_blocking=True)
+            spec.set_theta(th)
+            o = wavefunction.grad_theta_batch(spec, xp)
+            bundle = estimators.assemble(estimators.SampleBatch(cfgs, e, o))
+            th, st, _ = optimizers.wssr_step(th, bundle, 1e-3, st)
+            out_h.copy_(th, non_blocking=True)
+        torch.cuda.synchronize()
+        return st
+
+    st = run(2, fresh())
+    nsteps = 10
+    a.record(stream)
+    st = run(nsteps, st)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / nsteps
+    return {"producer": producer,
+            "e2e": {"value": 1e3 / e2e_ms, "unit": "steps/s",
+                    "h2d_bytes_per_step": N * n_el * 3 * 8 + N * 8,
+                    "d2h_bytes_per_step": P * 8, "steps": nsteps,
+                    "precision_fallbacks": ctx.precision_fallbacks() - fallbacks0,
+                    "path": "walker positions + local energies uploaded from pinned host memory "
+                            "-> wavefunction.grad_theta_batch (O on the device) -> "
+                            "estimators.assemble -> optimizers.wssr_step (eta 1e-3) -> theta' "
+                            "read back and set on the ansatz, every step"}}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -669,6 +764,9 @@ def run_ours(args, rank, world, local_rank):
         sec_args.steps = max(args.steps, 20)
         secondary[args.secondary] = measure(args.secondary, sec_args, rank, world, local_rank,
                                             e2e_numpy=world == 1, cpu=True)
+    producer = None
+    if args.secondary == "c1" and world == 1 and not args.no_producer:
+        producer = measure_producer("c1", args)
     if rank == 0:
         f32 = rec["config"]["workload"].endswith("f32")
         line = {
@@ -678,9 +776,12 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f32 storage, f64 arithmetic" if f32 else "f64",
             "data": "synthetic (seeded device generator, SURVEY.md 8(d) shapes/distributions)",
             "config": rec["config"],
-            "o_pass_arithmetic": "FP64 products as exact int8 digit products on tcgen05 kind::i8 "
-                                 "(7 digits per operand, 34 digit pairs, FP64 combine; "
-                                 "csrc/ozaki.cu)",
+            "o_pass_arithmetic": (
+                "float32 samples: the 5 most significant of the 7 int8 digits (each element to "
+                "2^-38 of its column's scale), 20 digit pairs on tcgen05 kind::i8, FP64 combine "
+                "(csrc/ozaki.cu)" if f32 else
+                "FP64 products as exact int8 digit products on tcgen05 kind::i8 (7 digits per "
+                "operand, 34 digit pairs, FP64 combine; csrc/ozaki.cu)"),
             "roofline": rec["roofline"], "cpu_baseline": rec.get("cpu_baseline"),
             "e2e": rec.get("e2e"), "gpu_launches": rec["gpu_launches"], "clocks": rec["clocks"],
             "wall_s_timed_region": rec["wall_s_timed_region"],
@@ -693,6 +794,8 @@ def run_ours(args, rank, world, local_rank):
                                                            "step_budget_ms", "step")}}
                 for name, r in secondary.items()},
         }
+        if producer is not None:
+            line["secondary"]["c1_producer"] = producer
         print(json.dumps(line), flush=True)
 
 

@@ -2036,7 +2036,7 @@ int wssr_grad_theta_f64(wssr_ctx* ctx, const wssr_ace_spec* spec, const double* 
     if (s.n_electrons < 1 || s.n_electrons > 64 || s.n_orbitals < 1 || s.n_features < 1 ||
         s.max_tail < 0 || ld_out < s.n_electrons * s.n_features)
       throw Fail{WSSR_ERR_VALUE, "bad ansatz dimensions (n_electrons must be 1..64)"};
-    if (grad_theta_smem(s) > 200 * 1024)
+    if (grad_theta_smem(s, grad_theta_tile(s)) > 200 * 1024)
       throw Fail{WSSR_ERR_UNSUPPORTED, "orbital table too large for one CTA"};
     Buf flag(1, c.stream);
     WSSR_CUDA(cudaMemsetAsync(flag, 0, sizeof(double), c.stream));

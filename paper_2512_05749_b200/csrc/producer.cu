@@ -24,11 +24,14 @@ namespace wssr {
 namespace prod {
 
 constexpr int kThreads = 256;
+constexpr int kTile = 128;  // feature columns per tile of the F C^T contraction (at most)
+constexpr int kMaxPairs = 16;  // (i, k) pairs of M per thread: n_electrons <= 64
 constexpr double kLogAbsUnderflow = -700.0;  // system.py:16
 
 __global__ void __launch_bounds__(kThreads)
     grad_theta_kernel(const wssr_ace_spec s, const double* __restrict__ pos, int64_t W,
-                      double* __restrict__ out, int64_t ldo, int* __restrict__ node_flag) {
+                      double* __restrict__ out, int64_t ldo, int* __restrict__ node_flag,
+                      int tile) {
   pdl_wait();
   const int64_t w = blockIdx.x;
   if (w >= W) return;
@@ -38,6 +41,8 @@ __global__ void __launch_bounds__(kThreads)
   double* phi = sm;                      // N x NO
   double* pooled = phi + N * NO;         // N x NO
   double* Mx = pooled + N * NO;          // N x (2N): [M | I] -> [I | M^-1]
+  double* Fs = Mx + 2 * N * N;           // N x (tile + 1): a tile of F (padded rows)
+  double* Cs = Fs + N * (tile + 1);      // N x (tile + 1): the same tile of C
   __shared__ double s_logabs;
   __shared__ int s_sing;
   const int tid = threadIdx.x;
@@ -69,32 +74,54 @@ __global__ void __launch_bounds__(kThreads)
     pooled[e] = tot - phi[i * NO + o];
   }
   __syncthreads();
-  // features into the output row: F[i][t] at ow[i T + t]
-  for (int64_t e = tid; e < (int64_t)N * T; e += kThreads) {
-    const int i = (int)(e / T), t = (int)(e % T);
-    double f = phi[i * NO + s.heads[t]];
-    for (int q = 0; q < MT; ++q) {
-      const int p = s.tails[(int64_t)t * MT + q];
-      if (p < 0) break;
-      f *= pooled[i * NO + p];
+  // Features into the output row (F[i][t] at ow[i T + t]) and M = F C^T, tile by tile: each
+  // tile of F is computed into shared memory (and written out once for the O pass below), the
+  // matching tile of C (L2-resident: every walker reads it) is staged beside it, and every
+  // thread accumulates its (i, k) entries of M from the two tiles (rows padded: conflict-free).
+  const int npairs = N * N;
+  double acc[kMaxPairs];
+#pragma unroll
+  for (int j = 0; j < kMaxPairs; ++j) acc[j] = 0.0;
+  for (int t0 = 0; t0 < T; t0 += tile) {
+    for (int e = tid; e < N * tile; e += kThreads) {
+      const int i = e / tile, tt = e % tile, t = t0 + tt;
+      double f = 0.0, c = 0.0;
+      if (t < T) {
+        f = phi[i * NO + s.heads[t]];
+        for (int q = 0; q < MT; ++q) {
+          const int p = s.tails[(int64_t)t * MT + q];
+          if (p < 0) break;
+          f *= pooled[i * NO + p];
+        }
+        ow[(int64_t)i * T + t] = f;
+        c = s.coef[(int64_t)i * T + t];  // C has the same N x T shape
+      }
+      Fs[i * (tile + 1) + tt] = f;
+      Cs[i * (tile + 1) + tt] = c;
     }
-    ow[e] = f;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kMaxPairs; ++j) {
+      const int pr = tid + j * kThreads;
+      if (pr < npairs) {
+        const double* fr = Fs + (pr / N) * (tile + 1);
+        const double* cr = Cs + (pr % N) * (tile + 1);
+        double a = acc[j];
+        for (int tt = 0; tt < tile; ++tt) a = fma(fr[tt], cr[tt], a);
+        acc[j] = a;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // M = F C^T, augmented with I
-  for (int e = tid; e < N * N; e += kThreads) {
-    const int i = e / N, k = e % N;
-    const double* fr = ow + (int64_t)i * T;
-    const double* cr = s.coef + (int64_t)k * T;
-    double a0 = 0.0, a1 = 0.0;
-    int t = 0;
-    for (; t + 1 < T; t += 2) {
-      a0 = fma(fr[t], cr[t], a0);
-      a1 = fma(fr[t + 1], cr[t + 1], a1);
+  // M augmented with I
+#pragma unroll
+  for (int j = 0; j < kMaxPairs; ++j) {
+    const int pr = tid + j * kThreads;
+    if (pr < npairs) {
+      const int i = pr / N, k = pr % N;
+      Mx[i * 2 * N + k] = acc[j];
+      Mx[i * 2 * N + N + k] = (i == k) ? 1.0 : 0.0;
     }
-    if (t < T) a0 = fma(fr[t], cr[t], a0);
-    Mx[i * 2 * N + k] = a0 + a1;
-    Mx[i * 2 * N + N + k] = (i == k) ? 1.0 : 0.0;
   }
   if (tid == 0) {
     s_logabs = 0.0;
@@ -164,20 +191,29 @@ __global__ void __launch_bounds__(kThreads)
 
 }  // namespace prod
 
-size_t grad_theta_smem(const wssr_ace_spec& s) {
+size_t grad_theta_smem(const wssr_ace_spec& s, int tile) {
   return sizeof(double) *
-         (2 * (size_t)s.n_electrons * s.n_orbitals + 2 * (size_t)s.n_electrons * s.n_electrons);
+         (2 * (size_t)s.n_electrons * s.n_orbitals + 2 * (size_t)s.n_electrons * s.n_electrons +
+          2 * (size_t)s.n_electrons * (tile + 1));
+}
+
+// the widest feature tile (<= 128) whose staging fits beside the per-walker tables
+int grad_theta_tile(const wssr_ace_spec& s) {
+  int tile = prod::kTile;
+  while (tile > 8 && grad_theta_smem(s, tile) > (size_t)200 * 1024) tile /= 2;
+  return tile;
 }
 
 cudaError_t grad_theta(Context& ctx, const wssr_ace_spec& s, const double* positions, int64_t W,
                        double* out, int64_t ldo, int* node_flag) {
   if (W <= 0) return cudaSuccess;
-  const size_t smem = grad_theta_smem(s);
+  const int tile = grad_theta_tile(s);
+  const size_t smem = grad_theta_smem(s, tile);
   cudaError_t e = cudaFuncSetAttribute(prod::grad_theta_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = launch_pdl(prod::grad_theta_kernel, (unsigned)W, prod::kThreads, smem, ctx.stream, s,
-                 positions, W, out, ldo, node_flag);
+                 positions, W, out, ldo, node_flag, tile);
   ctx.kernel_launches += 1;
   return e;
 }
