@@ -877,6 +877,338 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- transposed on-the-fly variant (row-major pass, 65-128 thin columns) --------------------
+// With 128 thin columns (k = 128: c2/c3) the kernel above runs each 128-row tile twice, once per
+// 64-column block, because one block's 8 int32 level accumulators fill the 512 TMEM columns -
+// and so converts every sample twice.  This variant swaps the operand roles: the thin digits are
+// the MMA's A operand (M = 128 thin columns) and the sample digits its B operand (N = 64 samples
+// per digit, digits stacked along N), so D_s holds 128 thin columns x 64 samples per level
+// (8 x 64 TMEM columns again) and every sample is converted once for all 128 columns.  The
+// tensor-core operand traffic per product is unchanged; the conversion traffic through the
+// shared-memory pipe (raw-tile TMA writes and reads, digit stores, scale table) halves.
+constexpr int TBM = 64;                         // sample rows per unit
+constexpr int T_RSTAGES = 4;                    // raw ring
+constexpr int T_DSTAGES = 3;                    // sample-digit ring (converters -> MMA)
+constexpr int T_BSTAGES = 3;                    // thin-digit ring (bulk copies -> MMA)
+constexpr int T_RSTAGE = TBM * BK * 8;          // 16 KB (FP64 tile; FP32 uses half)
+constexpr int T_DSTAGE = ND * TBM * BK;         // 14 KB
+constexpr int T_BSTAGE = ND * 128 * BK;         // 28 KB
+constexpr size_t kTSmem = (size_t)T_RSTAGE * T_RSTAGES + (size_t)T_DSTAGE * T_DSTAGES +
+                          (size_t)T_BSTAGE * T_BSTAGES + (size_t)MI_BYTES * T_RSTAGES + 256 + 1024;
+static_assert(kTSmem <= 232448, "shared memory budget");
+
+// Digit pairs with the roles swapped: A digit x (thin, 7 digits) against B digits y (samples,
+// NB digits), levels x + y < L.  First writers as in issue_pairs: x = 1 covers levels 1..L-1
+// (NB >= L - 1), then x = 0 splits at level 0.
+template <int X, int Y0, int NY, typename ADesc, typename BDesc>
+__device__ __forceinline__ void issue_range_t(uint32_t tmem, ADesc adesc, BDesc bdesc,
+                                              uint32_t acc) {
+  constexpr int left = 64 * NY, n0 = left > 256 ? 256 : left;
+  if constexpr (left > 0) {
+    mma_i8(tmem + 64 * (X + Y0), adesc(X), bdesc(64 * Y0), idesc_i8(n0), acc);
+    if constexpr (left > 256) issue_range_t<X, Y0 + 4, NY - 4>(tmem, adesc, bdesc, acc);
+  }
+}
+template <int X, int NB, int L, typename ADesc, typename BDesc>
+__device__ __forceinline__ void issue_rest_t(uint32_t tmem, ADesc adesc, BDesc bdesc) {
+  if constexpr (X < ND && X < L) {
+    constexpr int ny = (L - X) < NB ? (L - X) : NB;
+    issue_range_t<X, 0, ny>(tmem, adesc, bdesc, 1u);
+    issue_rest_t<X + 1, NB, L>(tmem, adesc, bdesc);
+  }
+}
+template <int NB, typename ADesc, typename BDesc>
+__device__ __forceinline__ void issue_pairs_t(uint32_t tmem, ADesc adesc, BDesc bdesc,
+                                              uint32_t first) {
+  constexpr int L = levels<NB>();
+  static_assert(NB >= L - 1, "x = 1 must cover levels 1..L-1");
+  issue_range_t<1, 0, L - 1>(tmem, adesc, bdesc, first);
+  issue_range_t<0, 0, 1>(tmem, adesc, bdesc, first);
+  issue_range_t<0, 1, (L < NB ? L : NB) - 1>(tmem, adesc, bdesc, 1u);
+  issue_rest_t<2, NB, L>(tmem, adesc, bdesc);
+}
+
+template <typename TA, int NDS>
+__global__ void __launch_bounds__(kThreads, 1)
+    ozaki_gemm_t_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmS, const Params p) {
+  constexpr bool F32 = sizeof(TA) == 4;
+  constexpr int A_BYTES = TBM * BK * (int)sizeof(TA);
+  constexpr int L = levels<NDS>();
+  constexpr int THIN = L < ND ? L : ND;  // thin digits the pairs read
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* dring = smem + (size_t)T_RSTAGE * T_RSTAGES;
+  unsigned char* bring = dring + (size_t)T_DSTAGE * T_DSTAGES;
+  unsigned char* miring = bring + (size_t)T_BSTAGE * T_BSTAGES;
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(miring + (size_t)MI_BYTES * T_RSTAGES);
+  uint64_t* rempty = rfull + T_RSTAGES;
+  uint64_t* bfull = rempty + T_RSTAGES;
+  uint64_t* bempty = bfull + T_BSTAGES;
+  uint64_t* conv = bempty + T_BSTAGES;
+  uint64_t* dempty = conv + T_DSTAGES;
+  uint64_t* tfull = dempty + T_DSTAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto a_raw = [&](int s) { return smem + (size_t)s * T_RSTAGE; };
+  auto s_mi = [&](int s) { return reinterpret_cast<const double*>(miring + (size_t)s * MI_BYTES); };
+  auto s_dig = [&](int d) { return dring + (size_t)d * T_DSTAGE; };
+  auto t_dig = [&](int b) { return bring + (size_t)b * T_BSTAGE; };
+
+  if (tid == 0) {
+    for (int s = 0; s < T_RSTAGES; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], kConvWarps / 2);
+    }
+    for (int d = 0; d < T_DSTAGES; ++d) {
+      mbar_init(&conv[d], kConvWarps / 2);
+      mbar_init(&dempty[d], 1);
+    }
+    for (int b = 0; b < T_BSTAGES; ++b) {
+      mbar_init(&bfull[b], 1);
+      mbar_init(&bempty[b], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kConvWarps);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  const int64_t units = (int64_t)p.mtiles * p.nch;  // mtiles: 64-row tiles here
+  auto decode = [&](int64_t u, int64_t& m0, int& kc, int64_t& kb0, int64_t& kb1) {
+    m0 = (u % p.mtiles) * TBM;
+    kc = (int)(u / p.mtiles);
+    kb0 = p.kblocks * kc / p.nch;
+    kb1 = p.kblocks * (kc + 1) / p.nch;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer: raw ring (64 sample rows x 32 parameters + the scale-table slice) =====
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmS);
+      uint32_t g = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t m0, kb0, kb1;
+        int kc;
+        decode(u, m0, kc, kb0, kb1);
+        for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % T_RSTAGES;
+          mbar_sleep_wait(&rempty[s], ((g / T_RSTAGES) & 1) ^ 1);
+          const int k0 = (int)(kb * BK);
+          mbar_arrive_expect_tx(&rfull[s], A_BYTES + MI_BYTES);
+          tma_load_2d(a_raw(s), &tmA, k0, (int)m0, &rfull[s]);
+          if (!F32) tma_load_2d(a_raw(s) + TBM * 128, &tmA, k0 + 16, (int)m0, &rfull[s]);
+          tma_load_1d((void*)s_mi(s), &tmS, TABW * k0, &rfull[s]);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ===== bulk producer: thin digits of a K-block, [digit][128 columns][32 K] =====
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t m0, kb0, kb1;
+        int kc;
+        decode(u, m0, kc, kb0, kb1);
+        for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+          const int b = g % T_BSTAGES;
+          mbar_sleep_wait(&bempty[b], ((g / T_BSTAGES) & 1) ^ 1);
+          constexpr uint32_t bbytes = THIN * 128 * BK;
+          mbar_arrive_expect_tx(&bfull[b], bbytes);
+          bulk_load(t_dig(b), p.bd + kb * (int64_t)T_BSTAGE, bbytes, &bfull[b]);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 3) {
+    // ===== MMA issuers, alternate K-blocks (see ozaki_gemm_kernel) =====
+    const int me = warp == 1 ? 0 : 1;
+    int64_t total = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      int64_t m0, kb0, kb1;
+      int kc;
+      decode(u, m0, kc, kb0, kb1);
+      total += kb1 - kb0;
+    }
+    uint32_t g = 0, t = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      int64_t m0, kb0, kb1;
+      int kc;
+      decode(u, m0, kc, kb0, kb1);
+      mbar_sleep_wait(tempty, (t & 1) ^ 1);
+      for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        if ((int)(g & 1) != me) continue;
+        const int d = g % T_DSTAGES, bs = g % T_BSTAGES;
+        mbar_sleep_wait(&bfull[bs], (g / T_BSTAGES) & 1);
+        mbar_sleep_wait(&conv[d], (g / T_DSTAGES) & 1);
+        if (g > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + me) : "memory");  // token in
+        tc_fence_after();
+        const bool stored = p.store != nullptr && m0 < p.prows;
+        if (lane == 0 && stored) {
+          // one 2 KB bulk store per plane: the 64-row digit tile is already in the planes'
+          // pre-swizzled layout
+          const int64_t pstride = p.pblocks * p.prows * 32;
+#pragma unroll
+          for (int a = 0; a < NDS; ++a)
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 2048;\n" ::"l"(
+                    p.store + a * pstride + (kb * p.prows + m0) * 32),
+                "r"(smem_u32(s_dig(d) + a * TBM * BK))
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        if (lane == 0) {
+          const uint32_t abase = smem_u32(t_dig(bs)), bbase = smem_u32(s_dig(d));
+          const uint32_t first = kb == kb0 ? 0u : 1u;
+          issue_pairs_t<NDS>(
+              tmem, [&](int x) { return smem_desc_sw32(abase + x * 128 * BK); },
+              [&](int row) { return smem_desc_sw32(bbase + row * BK); }, first);
+          if (stored) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+          mma_commit(&dempty[d]);
+          mma_commit(&bempty[bs]);
+          if (kb + 1 == kb1) mma_commit(tfull);
+        }
+        __syncwarp();
+        if ((int64_t)g + 1 < total) asm volatile("bar.arrive %0, 64;\n" ::"r"(2 - me) : "memory");
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== converters + epilogue =====
+    // Two groups of 8 warps take alternate K-blocks.  Group warp wi owns tile rows 8 wi + r8,
+    // lane = r8 + 8 q: K quarter q (8 consecutive K values), one row per thread.
+    const int cw = warp - 4;
+    const int cg = cw >> 3, wi = cw & 7;
+    const int q = lane >> 3;
+    const int row = 8 * wi + (lane & 7);
+    const int quad = warp & 3;          // TMEM lane quadrant of this warp (epilogue)
+    const int ecol = 16 * (cw >> 2);    // epilogue: 16 sample columns
+    const bool guard = p.rowcnt != nullptr;
+    uint32_t g = 0, t = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
+      int64_t m0, kb0, kb1;
+      int kc;
+      decode(u, m0, kc, kb0, kb1);
+      uint64_t cnt = 0;
+      for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
+        if ((int)(g & 1) != cg) continue;
+        const int s = g % T_RSTAGES, d = g % T_DSTAGES;
+        mbar_wait(&rfull[s], (g / T_RSTAGES) & 1);
+        const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + 2 * q;
+        const bool exact = __double_as_longlong(s_mi(s)[3]) != 0;  // uniform per K-block
+        uint64_t y[8];
+        if (F32) {
+          const unsigned char* base = a_raw(s) + row * 128;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float4 f =
+                *reinterpret_cast<const float4*>(base + (((2 * q + c) ^ (row & 7)) << 4));
+            const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const double2 m = mi[8 * (4 * c + e)];
+              y[4 * c + e] = exact ? biased_digits(fv[e], as_u64(m.x), m.y, mi[8 * (4 * c + e) + 1].x)
+                                   : biased_int(fv[e], as_u64(m.x), hi_word(m.y));
+            }
+          }
+        } else {
+          const unsigned char* base = a_raw(s) + (q >> 1) * (TBM * 128) + row * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double2 v =
+                *reinterpret_cast<const double2*>(base + (((4 * (q & 1) + c) ^ (row & 7)) << 4));
+            const double2 m0v = mi[8 * (2 * c)], m1v = mi[8 * (2 * c + 1)];
+            if (exact) {
+              y[2 * c] = biased_digits(v.x, as_u64(m0v.x), m0v.y, mi[8 * (2 * c) + 1].x);
+              y[2 * c + 1] = biased_digits(v.y, as_u64(m1v.x), m1v.y, mi[8 * (2 * c + 1) + 1].x);
+            } else {
+              y[2 * c] = biased_int(v.x, as_u64(m0v.x), hi_word(m0v.y));
+              y[2 * c + 1] = biased_int(v.y, as_u64(m1v.x), hi_word(m1v.y));
+            }
+          }
+        }
+        if (guard) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cnt += guard_count(y[i]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[s]);  // raw tile consumed
+        uint32_t w[ND][2];
+        pack_digits8(y, w);
+        mbar_wait(&dempty[d], ((g / T_DSTAGES) & 1) ^ 1);
+        unsigned char* dst = s_dig(d) + row * BK + ((((q >> 1) ^ ((row >> 2) & 1))) << 4) +
+                             ((q & 1) << 3);
+#pragma unroll
+        for (int a = 0; a < ND; ++a)
+          *reinterpret_cast<uint2*>(dst + a * TBM * BK) = make_uint2(w[a][0], w[a][1]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[d]);
+      }
+      if (guard) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
+        if (q == 0 && cnt && m0 + row < p.M) atomicAdd(p.rowcnt + m0 + row, (unsigned long long)cnt);
+      }
+      // ---- epilogue: D_s (128 thin columns x 64 samples per level) -> FP64 ----
+      mbar_sleep_wait(tfull, t & 1);
+      tc_fence_after();
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int sd = 0; sd < L; ++sd) {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + NB * sd + ecol, r);
+        tmem_ld_wait();
+        const double wgt = __longlong_as_double((long long)(1023 + 96 - 8 * sd) << 52);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)r[j], wgt, acc[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      const int64_t jcol = quad * 32 + lane;  // thin column = TMEM lane
+      if (jcol < p.N) {
+        const double cf = p.alpha * p.colfac[jcol];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int64_t gm = m0 + ecol + c;
+          if (gm < p.M) {
+            const double v = cf * acc[c];
+            if (p.nch > 1) {
+              p.slab[((int64_t)kc * p.M + gm) * p.N + jcol] = v;
+            } else {
+              double* dst = p.C + gm * p.ldc + jcol;
+              *dst = p.accumulate ? *dst + v : v;
+            }
+          }
+        }
+      }
+    }
+  }
+  if ((warp == 1 || warp == 3) && lane == 0 && p.store)
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem)
+                 : "memory");
+  }
+}
+
 // ---- pre-digitised variant ---------------------------------------------------------------------
 // When the step's digit planes fit in HBM they are written once per step (digitize_kernel, with
 // no tensor-core work running: FP64 SIMT arithmetic shares the SM's math datapath with the
@@ -1413,7 +1745,7 @@ __global__ void __launch_bounds__(256)
     thin_digits_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
                        int64_t kpad, const double* __restrict__ mu_inv,
                        const unsigned long long* __restrict__ cmax, int extra_exp,
-                       int8_t* __restrict__ Bd, double* __restrict__ colfac) {
+                       int8_t* __restrict__ Bd, double* __restrict__ colfac, int tlay) {
   pdl_wait();
   // thread: column jl (of 32) and K group kg (of 8, 4 rows each); block covers 32 K x 32 columns
   const int kg = threadIdx.x & 7, jl = threadIdx.x >> 3;
@@ -1458,6 +1790,14 @@ __global__ void __launch_bounds__(256)
     w[2] = __byte_perm(u0, v0, 0x5410) ^ 0x80808080u;
     w[1] = __byte_perm(u0, v0, 0x7632) ^ 0x80808080u;
     w[0] = __byte_perm(u1, v1, 0x5410) ^ 0x80808080u;
+  }
+  if (tlay) {  // [K-block][digit][128 columns][32]: the A operand of ozaki_gemm_t_kernel
+#pragma unroll
+    for (int a = 0; a < ND; ++a)
+      *reinterpret_cast<uint32_t*>(
+          Bd + (((int64_t)blockIdx.x * ND + a) * 128 + nb * 64 + j) * 32 +
+          ((4 * kg) ^ (((j >> 2) & 1) << 4))) = w[a];
+    return;
   }
 #pragma unroll
   for (int a = 0; a < ND; ++a)
@@ -1505,6 +1845,22 @@ cudaError_t launch_pre_nds(const CUtensorMap& tA, const Params& p, int grid, cud
   launch_pdl(ozaki_pre_kernel<RM, NDS>, grid, kPreThreads, kPreSmem, st, tA, p);
   return cudaGetLastError();
 }
+template <typename TA, int NDS>
+cudaError_t launch_t_nds(const CUtensorMap& tA, const CUtensorMap& tS, const Params& p, int grid,
+                         cudaStream_t st) {
+  static std::atomic<uint64_t> attr{0};
+  cudaError_t e = smem_attr_once(attr, ozaki_gemm_t_kernel<TA, NDS>, (int)kTSmem);
+  if (e != cudaSuccess) return e;
+  launch_pdl(ozaki_gemm_t_kernel<TA, NDS>, grid, kThreads, kTSmem, st, tA, tS, p);
+  return cudaGetLastError();
+}
+template <typename TA>
+cudaError_t launch_t(const CUtensorMap& tA, const CUtensorMap& tS, const Params& p, int grid,
+                     cudaStream_t st) {
+  if (sizeof(TA) == 4 && p.nds == 5) return launch_t_nds<TA, 5>(tA, tS, p, grid, st);
+  return launch_t_nds<TA, ND>(tA, tS, p, grid, st);
+}
+
 template <bool RM>
 cudaError_t launch_pre(const CUtensorMap& tA, const Params& p, int grid, cudaStream_t st) {
   return p.nds == 5 ? launch_pre_nds<RM, 5>(tA, p, grid, st)
@@ -1636,7 +1992,14 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   const int kstep = planes ? PBK : BK;  // K per pipeline stage
   const int64_t kpad = ((K + kstep - 1) / kstep) * kstep;
   const int64_t kblocks = kpad / kstep;
-  const int mtiles = (int)((M + BM - 1) / BM);
+  // the transposed on-the-fly kernel: row-major pass, 65-128 thin columns, digits not yet in
+  // HBM (WSSR_OZ_TKERNEL=0 falls back to one 64-column block per unit)
+  static const bool t_enabled = [] {
+    const char* e = std::getenv("WSSR_OZ_TKERNEL");
+    return !(e && e[0] == '0');
+  }();
+  const bool tkern = t_enabled && RMm && !planes && nblk == 2;
+  const int mtiles = tkern ? (int)((M + TBM - 1) / TBM) : (int)((M + BM - 1) / BM);
   // thin-operand digits + factors (workspace owned by the context)
   const size_t dig_bytes = (size_t)nblk * BROWS * kpad;
   const size_t ws_doubles = (dig_bytes + 7) / 8 + (size_t)nblk * NB + N + 64;
@@ -1658,13 +2021,13 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     launch_pdl(thin_colmax_kernel, dim3((unsigned)((K + 127) / 128), nblk), 256, 0, st, a.B, a.ldb, K, N,
                                                                                bmu, cmax);
     launch_pdl(thin_digits_kernel, dim3((unsigned)(kpad / 32), 2 * nblk), 256, 0, st, 
-        a.B, a.ldb, K, N, kpad, bmu, cmax, RMm ? 54 : 0, Bd, colfac);
+        a.B, a.ldb, K, N, kpad, bmu, cmax, RMm ? 54 : 0, Bd, colfac, tkern ? 1 : 0);
     ctx.kernel_launches += 2;
   }
   // K chunks: int32 bound, then enough units to fill the machine evenly
   int nch = (int)((kpad + KCHUNK - 1) / KCHUNK);
   {
-    const int64_t base = (int64_t)mtiles * nblk;
+    const int64_t base = (int64_t)mtiles * (tkern ? 1 : nblk);
     int best = nch;
     double best_eff = 0.0;
     for (int c = nch; c <= std::max(nch, 64); ++c) {
@@ -1734,12 +2097,19 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     ctx.kernel_launches += 1;
     ctx.gemm_launches += 1;
   } else if (RMm) {
-    ok = make_map_2d(&tA, a.A, K, M, a.lda, BM, es) &&
+    ok = make_map_2d(&tA, a.A, K, M, a.lda, tkern ? TBM : BM, es) &&
          make_map_1d(&tS, mu_inv, TABW * kpad, TABW * BK);
   } else {
     ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
   }
-  if (!planes) {
+  if (!planes && tkern) {
+    if (!ok) return cudaErrorInvalidValue;
+    const int64_t units = (int64_t)mtiles * nch;
+    const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
+    e = f32 ? launch_t<float>(tA, tS, p, grid, st) : launch_t<double>(tA, tS, p, grid, st);
+    ctx.kernel_launches += 1;
+    ctx.gemm_launches += 1;
+  } else if (!planes) {
     std::memset(&tB, 0, sizeof(tB));  // thin digits arrive by plain bulk copies
     if (!ok) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nblk * nch;

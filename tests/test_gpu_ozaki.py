@@ -104,7 +104,8 @@ def _run(layout, M, N, K, f32=False, pad=0, seed=0, scale_cols=False, with_shift
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("M,N,K", [(128, 64, 32), (300, 10, 1000), (1000, 64, 777),
                                    (513, 65, 4097), (200, 130, 20000), (4096, 1, 512),
-                                   (96, 200, 3000)])
+                                   (96, 200, 3000), (2000, 128, 5000), (333, 100, 20000),
+                                   (64, 128, 64)])
 def test_ozaki_accuracy_vs_dmma(layout, M, N, K):
     r = _run(layout, M, N, K)
     oz, dm = r["ozaki"], r["dmma"]
