@@ -260,6 +260,18 @@ int wssr_step_f64(wssr_ctx* ctx, const wssr_step_in* in, wssr_step_out* out);
  * DMMA Grams and updates, any rank). */
 int wssr_exact_svd_f64(wssr_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
                        double* u, int64_t ldu, double* sigma, double* vt, int64_t ldvt);
+/* exact_truncated_svd (svdengine.py:75-85) of the implicit Ohat of optimizers.py:323 (history
+ * scaled by sqrt(delta), samples by sqrt(1 - delta)) without forming it: oversampled block power
+ * iteration on the O-pass kernels until the leading `rank` Ritz triplets have residual
+ * ||Ohat v_i - s_i u_i|| <= tol * s_i (or stagnate at the rounding floor), then Rayleigh-Ritz.
+ * Row-sharded: every rank passes its own samples (history on rank 0), cols_global = r + N over
+ * all ranks and col0 = this rank's first global column; u and sigma come out replicated and
+ * v_local holds this rank's rows of the right vectors (cols x rank).  k_pos = leading positive
+ * singular values kept (svdengine.py:70-72). */
+int wssr_implicit_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, double delta, int64_t rank,
+                          int64_t cols_global, int64_t col0, uint64_t seed, int64_t max_iters,
+                          double tol, double* u, int64_t ldu, double* sigma, double* v_local,
+                          int64_t ldv, int64_t* k_pos, int64_t* iterations, double* residual);
 /* Ohat of optimizers.py:323 written out parameter-major: out [P x (hist_rank + n_samples)]. */
 int wssr_materialize_ohat_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, double delta, double* out,
                               int64_t ldo);

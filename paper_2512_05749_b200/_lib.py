@@ -132,6 +132,10 @@ SIGNATURES = {
     "wssr_step_f64": (ctypes.c_int, [_vp, ctypes.POINTER(StepIn), ctypes.POINTER(StepOut)]),
     "wssr_exact_svd_f64": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64]),
     "wssr_materialize_ohat_f64": (ctypes.c_int, [_vp, ctypes.POINTER(OhatF64), _dbl, _vp, _i64]),
+    "wssr_implicit_svd_f64": (ctypes.c_int, [_vp, ctypes.POINTER(OhatF64), _dbl, _i64, _i64, _i64,
+                                             ctypes.c_uint64, _i64, _dbl, _vp, _i64, _vp, _vp,
+                                             _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                             ctypes.POINTER(_dbl)]),
     "wssr_debug_small_f64": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp,
                                             ctypes.POINTER(ctypes.c_int)]),
     "wssr_debug_gemm_f32a": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp,

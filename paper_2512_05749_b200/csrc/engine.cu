@@ -1463,6 +1463,173 @@ void materialize_ohat(Context& ctx, const wssr_ohat_f64& oh, double delta, doubl
     transpose(ctx, oh.samples, oh.samples_ld, oh.n_samples, P, oh.mu, ss, out + r, ldo);
 }
 
+// ---- exact truncated SVD without forming Ohat (svdengine.py:75-85 -> linalg.py:108-121) --------
+// The dense first step factorises the P x (r + N) Ohat.  Written out it is as large as the sample
+// block itself (137 GB at BASELINE configs[2], on every rank under row sharding), so this path
+// never forms it: a block power iteration with oversampling on the implicit operator (the O-pass
+// kernels of the SSI, rows sharded with the same collectives) run until the leading `rank` Ritz
+// triplets have converged, then Rayleigh-Ritz on the small global block Y = Ohat^T Q:
+//   Q = orth(Z),  Y = Ohat^T Q  (cols x b),  Z = Ohat Y = Ohat Ohat^T Q,
+//   Y = V_y S W_y^T (device dense SVD)  =>  Ohat ~= (Q W_y) S V_y^T,
+// and since Ohat V_y = Z W_y S^-1, the Ritz residual of triplet i is
+//   ||Ohat v_i - s_i u_i|| = ||Z w_i / s_i - s_i Q w_i||   (no extra O-pass).
+// The top singular triplets are unique (up to sign) wherever the reference's are well defined,
+// so the result agrees with LAPACK's to the accuracy the residual certifies.
+__global__ void fill_normal_kernel(double* x, int64_t n, uint64_t seed) {
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    // splitmix64 of (seed, i) -> two uniforms -> Box-Muller
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double u1 = ((double)(z >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    uint64_t y = z * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+    y = (y ^ (y >> 29)) * 0xBF58476D1CE4E5B9ull;
+    y ^= y >> 32;
+    const double u2 = ((double)(y >> 11)) * (1.0 / 9007199254740992.0);
+    x[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+// partial[b][j] = sum over this block's rows of (T_pj / s_j - s_j U_pj)^2, j < k (fixed order)
+__global__ void ritz_residual_kernel(const double* __restrict__ T, const double* __restrict__ U,
+                                     int64_t ld, int64_t rows, int k, const double* __restrict__ S,
+                                     double* __restrict__ partial) {
+  pdl_wait();
+  const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const double s = S[j], inv = s > 0.0 ? 1.0 / s : 0.0;
+    double acc = 0.0;
+    for (int64_t r = r0; r < r1; ++r) {
+      const double d = T[r * ld + j] * inv - s * U[r * ld + j];
+      acc = fma(d, d, acc);
+    }
+    partial[(int64_t)blockIdx.x * k + j] = acc;
+  }
+}
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int nb, int k,
+                                    double* __restrict__ out) {
+  pdl_wait();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += partial[(int64_t)b * k + j];
+    out[j] = acc;
+  }
+}
+
+struct ImplicitSvdResult {
+  int64_t k_pos = 0;
+  int64_t iterations = 0;
+  double residual = 0.0;  // max_i ||Ohat v_i - s_i u_i|| / s_i over the returned triplets
+};
+
+// U (P x rank, ldu), sigma (rank), V_local (this rank's cols x rank, ldv: rows c0 .. c0 + cols of
+// the global right vectors).  cols_global = r + N over all ranks; c0 = this rank's first column.
+ImplicitSvdResult implicit_svd(Context& ctx, const Ohat& o, int64_t rank, int64_t cols_global,
+                               int64_t c0, uint64_t seed, int64_t max_iters, double tol, double* U,
+                               int64_t ldu, double* sigma, double* V, int64_t ldv, int* status,
+                               bool careful) {
+  cudaStream_t st = ctx.stream;
+  const int64_t P = o.P, cols = o.cols(), mn = std::min(P, cols_global);
+  if (rank < 1 || rank > mn)
+    throw Fail{WSSR_ERR_RANK_TOO_LARGE, "rank outside [1, min(m, n)]"};
+  o.status = status;
+  // block width: 2x oversampling (at least 16 extra columns), within the single-CTA dense SVD
+  int64_t b = std::max<int64_t>(2 * rank, rank + 16);
+  if (b > kDenseSvdMax) b = std::max<int64_t>(rank + 16, kDenseSvdMax);
+  b = std::min(b, mn);
+  const bool dist = ctx.world() > 1;
+  Buf Q((size_t)P * b, st), Z((size_t)P * b, st), Yl((size_t)std::max<int64_t>(cols, 1) * b, st),
+      Yg(dist ? (size_t)cols_global * b : 0, st), Vy((size_t)cols_global * b, st), S(b, st),
+      WyT((size_t)b * b, st), Wy((size_t)b * b, st), T((size_t)P * rank, st),
+      Uk((size_t)P * rank, st), res(rank, st);
+  const int nbp = (int)std::min<int64_t>(4 * ctx.num_sms, std::max<int64_t>(1, P / 64));
+  Buf partial((size_t)nbp * rank, st);
+  launch_pdl(fill_normal_kernel, blocks_for(P * b, 256, 16 * ctx.num_sms), 256, 0, st, Z.p,
+             P * b, seed);
+  post_launch(ctx);
+  std::vector<double> hs(b), hres(rank);
+  ImplicitSvdResult out;
+  double best = std::numeric_limits<double>::infinity();
+  int stalls = 0;
+  for (int64_t it = 1; it <= max_iters; ++it) {
+    qr(ctx, P, b, Z, b, Q, b, nullptr, status, careful, false);  // replicated: Z is global
+    apply_OT(ctx, o, Q, b, b, Yl, b);                          // this rank's rows of Y
+    if (it == 1) {  // Y = Ohat^T Q vanishes (Q random) only for Ohat = 0
+      Buf y2(1, st);
+      sumsq_matrix(ctx, Yl, cols, b, b, y2);
+      if (dist) allreduce(ctx, y2, 1);
+      if (!(read_scalar(ctx, y2) > 0.0))
+        throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+    }
+    apply_O(ctx, o, Yl, b, b, Z, b);                           // Z = Ohat Y (summed over ranks)
+    if (dist) {
+      WSSR_CUDA(cudaMemsetAsync(Yg, 0, sizeof(double) * cols_global * b, st));
+      if (cols > 0) copy2d(ctx, Yl, b, cols, b, 1.0, Yg.p + c0 * b, b);
+      allreduce(ctx, Yg, (size_t)(cols_global * b));  // disjoint rows: the sum is exact
+    }
+    dense_svd(ctx, cols_global, b, dist ? Yg.p : Yl.p, b, Vy, b, S, WyT, b);  // Y = V_y S W_y^T
+    transpose(ctx, WyT, b, b, b, nullptr, 1.0, Wy, b);
+    gemm_rm(ctx, P, rank, b, Z, b, nullptr, Wy, b, T, rank, 1.0, false);   // Z w_i
+    gemm_rm(ctx, P, rank, b, Q, b, nullptr, Wy, b, Uk, rank, 1.0, false);  // u_i = Q w_i
+    launch_pdl(ritz_residual_kernel, nbp, 128, 0, st, (const double*)T.p, (const double*)Uk.p,
+               rank, P, (int)rank, (const double*)S.p, partial.p);
+    post_launch(ctx);
+    launch_pdl(sum_partials_kernel, 1, 128, 0, st, (const double*)partial.p, nbp, (int)rank, res.p);
+    post_launch(ctx);
+    d2h(ctx, hs.data(), S, sizeof(double) * b);
+    d2h(ctx, hres.data(), res, sizeof(double) * rank);
+    sync(ctx);
+    if (!(hs[0] > 0.0)) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+    // residual of the triplets that count (exact zeros are dropped, svdengine.py:70-72),
+    // relative to each singular value
+    double worst = 0.0;
+    for (int64_t i = 0; i < rank; ++i)
+      if (hs[i] > 0.0) worst = std::max(worst, std::sqrt(hres[i]) / hs[i]);
+      else if (hs[i] != 0.0 || !(hres[i] >= 0.0)) worst = std::numeric_limits<double>::infinity();
+    out.iterations = it;
+    out.residual = worst;
+    // the block spans the whole space: exact after one pass
+    if (worst <= tol || b == mn) break;
+    // stagnation at the rounding floor: no halving over two iterations
+    if (worst < 0.5 * best) {
+      best = worst;
+      stalls = 0;
+    } else if (++stalls >= 2) {
+      break;
+    }
+  }
+  int64_t kp = 0;
+  while (kp < rank && hs[kp] > 0.0) ++kp;
+  out.k_pos = kp;
+  if (kp == 0) throw Fail{WSSR_ERR_DEGENERATE_INPUT, "cannot factorize an all-zero matrix"};
+  copy2d(ctx, Uk, rank, P, kp, 1.0, U, ldu);
+  copy2d(ctx, S, 1, 1, kp, 1.0, sigma, kp);
+  if (cols > 0) copy2d(ctx, Vy.p + c0 * b, b, cols, kp, 1.0, V, ldv);
+  return out;
+}
+
+Ohat ohat_from(const Context& ctx, const wssr_ohat_f64& oh, double delta) {
+  const bool owner = ctx.world() <= 1 || ctx.comm->rank == 0;  // history block lives on rank 0
+  Ohat o;
+  o.P = oh.n_params;
+  o.hist = oh.hist;
+  o.r = owner ? oh.hist_rank : 0;
+  o.ldh = oh.hist_ld;
+  o.sh = std::sqrt(delta) * oh.hist_scale;
+  o.samp = oh.samples;
+  o.n = oh.n_samples;
+  o.lds = oh.samples_ld;
+  o.mu = oh.mu;
+  o.ss = std::sqrt(1.0 - delta) * oh.samples_scale;
+  o.f32 = oh.samples_f32 != 0;
+  o.scale_tab = oh.samples_scale_table;
+  return o;
+}
+
 // ---- wssr_step (optimizers.py:292-391), ssi branch -------------------------------------------
 void step_impl(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
   const wssr_ohat_f64& oh = *in->ohat;
@@ -2282,6 +2449,28 @@ int wssr_materialize_ohat_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, double d
   return guarded(ctx, [&] {
     if (!ohat || !out) throw Fail{WSSR_ERR_VALUE, "null argument"};
     materialize_ohat(ctx->c, *ohat, delta, out, ldo);
+  });
+}
+
+int wssr_implicit_svd_f64(wssr_ctx* ctx, const wssr_ohat_f64* ohat, double delta, int64_t rank,
+                          int64_t cols_global, int64_t col0, uint64_t seed, int64_t max_iters,
+                          double tol, double* u, int64_t ldu, double* sigma, double* v_local,
+                          int64_t ldv, int64_t* k_pos, int64_t* iterations, double* residual) {
+  return guarded(ctx, [&] {
+    if (!ohat || !u || !sigma || !k_pos) throw Fail{WSSR_ERR_VALUE, "null argument"};
+    if (max_iters < 1) throw Fail{WSSR_ERR_VALUE, "max_iters must be at least 1"};
+    Context& c = ctx->c;
+    const ImplicitSvdResult r = with_fallback(c, 0, [&](bool careful, int* status) {
+      const Ohat o = ohat_from(c, *ohat, delta);  // fresh per attempt (precision guard)
+      if (col0 < 0 || col0 + o.cols() > cols_global)
+        throw Fail{WSSR_ERR_VALUE, "column range outside the global Ohat"};
+      return implicit_svd(c, o, rank, cols_global, col0, seed, max_iters, tol, u, ldu, sigma,
+                          v_local, ldv, status, careful);
+    });
+    sync(c);
+    *k_pos = r.k_pos;
+    if (iterations) *iterations = r.iterations;
+    if (residual) *residual = r.residual;
   });
 }
 

@@ -928,7 +928,7 @@ __device__ __forceinline__ void issue_pairs_t(uint32_t tmem, ADesc adesc, BDesc 
   issue_rest_t<2, NB, L>(tmem, adesc, bdesc);
 }
 
-template <typename TA, int NDS>
+template <bool RM, typename TA, int NDS>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm_t_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmS, const Params p) {
@@ -995,10 +995,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (warp == 0) {
-    // ===== TMA producer: raw ring (64 sample rows x 32 parameters + the scale-table slice) =====
+    // ===== TMA producer: raw ring (RM: 64 sample rows x 32 parameters + the scale-table slice;
+    // CM: 32 sample rows x 64 parameters) =====
     if (lane == 0) {
       prefetch_tmap(&tmA);
-      prefetch_tmap(&tmS);
+      if (RM) prefetch_tmap(&tmS);
       uint32_t g = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t m0, kb0, kb1;
@@ -1008,10 +1009,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % T_RSTAGES;
           mbar_sleep_wait(&rempty[s], ((g / T_RSTAGES) & 1) ^ 1);
           const int k0 = (int)(kb * BK);
-          mbar_arrive_expect_tx(&rfull[s], A_BYTES + MI_BYTES);
-          tma_load_2d(a_raw(s), &tmA, k0, (int)m0, &rfull[s]);
-          if (!F32) tma_load_2d(a_raw(s) + TBM * 128, &tmA, k0 + 16, (int)m0, &rfull[s]);
-          tma_load_1d((void*)s_mi(s), &tmS, TABW * k0, &rfull[s]);
+          if (RM) {
+            mbar_arrive_expect_tx(&rfull[s], A_BYTES + MI_BYTES);
+            tma_load_2d(a_raw(s), &tmA, k0, (int)m0, &rfull[s]);
+            if (!F32) tma_load_2d(a_raw(s) + TBM * 128, &tmA, k0 + 16, (int)m0, &rfull[s]);
+            tma_load_1d((void*)s_mi(s), &tmS, TABW * k0, &rfull[s]);
+          } else {
+            mbar_arrive_expect_tx(&rfull[s], A_BYTES);
+            tma_load_2d(a_raw(s), &tmA, (int)m0, k0, &rfull[s]);
+          }
         }
       }
     }
@@ -1055,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_sleep_wait(&conv[d], (g / T_DSTAGES) & 1);
         if (g > 0) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + me) : "memory");  // token in
         tc_fence_after();
-        const bool stored = p.store != nullptr && m0 < p.prows;
+        const bool stored = RM && p.store != nullptr && m0 < p.prows;
         if (lane == 0 && stored) {
           // one 2 KB bulk store per plane: the 64-row digit tile is already in the planes'
           // pre-swizzled layout
@@ -1086,29 +1092,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===== converters + epilogue =====
-    // Two groups of 8 warps take alternate K-blocks.  Group warp wi owns tile rows 8 wi + r8,
-    // lane = r8 + 8 q: K quarter q (8 consecutive K values), one row per thread.
+    // Two groups of 8 warps take alternate K-blocks; one tile row and one K quarter q (8
+    // consecutive K values) per thread.
+    //   RM: group warp wi owns tile rows 8 wi + r8, lane = r8 + 8 q (the raw rows are 128-byte
+    //       swizzled, so the quarter-warps of one row range read distinct banks).
+    //   CM: the raw tile is [32 samples][64 parameters] unswizzled, K rows 512 bytes apart, so
+    //       the lanes of a warp cover 16 consecutive parameters (128 bytes, all 32 banks) x 2
+    //       quarters: row = 16 (wi & 3) + r16, q = 2 (wi >> 2) + lane / 16.  Loads are then two
+    //       wavefronts per 256 bytes, and the digit stores of 16 rows x 16 bytes (one 16-byte
+    //       half of each row, flipped with bit 2 of the row) hit every bank once per 8 rows.
     const int cw = warp - 4;
     const int cg = cw >> 3, wi = cw & 7;
-    const int q = lane >> 3;
-    const int row = 8 * wi + (lane & 7);
+    const int q = RM ? lane >> 3 : 2 * (wi >> 2) + (lane >> 4);
+    const int row = RM ? 8 * wi + (lane & 7) : 16 * (wi & 3) + (lane & 15);
     const int quad = warp & 3;          // TMEM lane quadrant of this warp (epilogue)
-    const int ecol = 16 * (cw >> 2);    // epilogue: 16 sample columns
-    const bool guard = p.rowcnt != nullptr;
+    const int ecol = 16 * (cw >> 2);    // epilogue: 16 sample (RM) / parameter (CM) columns
+    const bool guard = RM && p.rowcnt != nullptr;
     uint32_t g = 0, t = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++t) {
       int64_t m0, kb0, kb1;
       int kc;
       decode(u, m0, kc, kb0, kb1);
       uint64_t cnt = 0;
+      // CM: this thread's parameter column is fixed over the unit
+      uint64_t cwr = kBias;
+      double invr = 0.0, mur = 0.0;
+      if (!RM && m0 + row < p.M) {
+        const double* tb = p.mu_inv + TABW * tab_slot(m0 + row);
+        cwr = as_u64(tb[0]);
+        invr = tb[1];
+        mur = tb[2];
+      }
+      const bool exactCM = !RM && __any_sync(0xffffffffu, cwr == kCwExact);
       for (int64_t kb = kb0; kb < kb1; ++kb, ++g) {
         if ((int)(g & 1) != cg) continue;
         const int s = g % T_RSTAGES, d = g % T_DSTAGES;
         mbar_wait(&rfull[s], (g / T_RSTAGES) & 1);
         const double2* mi = reinterpret_cast<const double2*>(s_mi(s)) + 2 * q;
-        const bool exact = __double_as_longlong(s_mi(s)[3]) != 0;  // uniform per K-block
         uint64_t y[8];
-        if (F32) {
+        if (!RM) {
+          const TA* base = reinterpret_cast<const TA*>(a_raw(s)) + (8 * q) * TBM + row;
+          TA x[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = base[i * TBM];
+          if (exactCM) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) y[i] = biased_digits(x[i], cwr, invr, mur);
+          } else {
+            const uint32_t hs = hi_word(invr);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) y[i] = biased_int(x[i], cwr, hs);
+          }
+        } else if (F32) {
+          const bool exact = __double_as_longlong(s_mi(s)[3]) != 0;  // uniform per K-block
           const unsigned char* base = a_raw(s) + row * 128;
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
@@ -1123,6 +1159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
+          const bool exact = __double_as_longlong(s_mi(s)[3]) != 0;  // uniform per K-block
           const unsigned char* base = a_raw(s) + (q >> 1) * (TBM * 128) + row * 128;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -1186,7 +1223,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 16; ++c) {
           const int64_t gm = m0 + ecol + c;
           if (gm < p.M) {
-            const double v = cf * acc[c];
+            // CM: output row = parameter column gm, whose digits carry the scale s_gm
+            const double v =
+                RM ? cf * acc[c] : cf * acc[c] / p.mu_inv[TABW * tab_slot(gm) + 1];
             if (p.nch > 1) {
               p.slab[((int64_t)kc * p.M + gm) * p.N + jcol] = v;
             } else {
@@ -1198,7 +1237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if ((warp == 1 || warp == 3) && lane == 0 && p.store)
+  if ((warp == 1 || warp == 3) && lane == 0 && RM && p.store)
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   tc_fence_before();
   __syncthreads();
@@ -1808,12 +1847,12 @@ __global__ void __launch_bounds__(256)
 
 // (K x M) row-major sample block, box = 128 parameters x 32 samples, no swizzle
 bool make_map_cm(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t pitch,
-                 int esize) {
+                 int esize, int box_inner = BM) {
   auto fn = tma_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   cuuint64_t strides[1] = {(cuuint64_t)(pitch * esize)};
-  cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)BK};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)BK};
   cuuint32_t es[2] = {1u, 1u};
   return fn(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
             const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1845,20 +1884,20 @@ cudaError_t launch_pre_nds(const CUtensorMap& tA, const Params& p, int grid, cud
   launch_pdl(ozaki_pre_kernel<RM, NDS>, grid, kPreThreads, kPreSmem, st, tA, p);
   return cudaGetLastError();
 }
-template <typename TA, int NDS>
+template <bool RM, typename TA, int NDS>
 cudaError_t launch_t_nds(const CUtensorMap& tA, const CUtensorMap& tS, const Params& p, int grid,
                          cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
-  cudaError_t e = smem_attr_once(attr, ozaki_gemm_t_kernel<TA, NDS>, (int)kTSmem);
+  cudaError_t e = smem_attr_once(attr, ozaki_gemm_t_kernel<RM, TA, NDS>, (int)kTSmem);
   if (e != cudaSuccess) return e;
-  launch_pdl(ozaki_gemm_t_kernel<TA, NDS>, grid, kThreads, kTSmem, st, tA, tS, p);
+  launch_pdl(ozaki_gemm_t_kernel<RM, TA, NDS>, grid, kThreads, kTSmem, st, tA, tS, p);
   return cudaGetLastError();
 }
-template <typename TA>
+template <bool RM, typename TA>
 cudaError_t launch_t(const CUtensorMap& tA, const CUtensorMap& tS, const Params& p, int grid,
                      cudaStream_t st) {
-  if (sizeof(TA) == 4 && p.nds == 5) return launch_t_nds<TA, 5>(tA, tS, p, grid, st);
-  return launch_t_nds<TA, ND>(tA, tS, p, grid, st);
+  if (sizeof(TA) == 4 && p.nds == 5) return launch_t_nds<RM, TA, 5>(tA, tS, p, grid, st);
+  return launch_t_nds<RM, TA, ND>(tA, tS, p, grid, st);
 }
 
 template <bool RM>
@@ -1992,13 +2031,14 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
   const int kstep = planes ? PBK : BK;  // K per pipeline stage
   const int64_t kpad = ((K + kstep - 1) / kstep) * kstep;
   const int64_t kblocks = kpad / kstep;
-  // the transposed on-the-fly kernel: row-major pass, 65-128 thin columns, digits not yet in
-  // HBM (WSSR_OZ_TKERNEL=0 falls back to one 64-column block per unit)
-  static const bool t_enabled = [] {
+  // the transposed on-the-fly kernel: 65-128 thin columns, digits not yet in HBM
+  // (WSSR_OZ_TKERNEL=0 falls back to one 64-column block per unit for both passes, =1 keeps it
+  // for the row-major pass only)
+  static const int t_mode = [] {
     const char* e = std::getenv("WSSR_OZ_TKERNEL");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 2;
   }();
-  const bool tkern = t_enabled && RMm && !planes && nblk == 2;
+  const bool tkern = !planes && nblk == 2 && (RMm ? t_mode >= 1 : t_mode >= 2);
   const int mtiles = tkern ? (int)((M + TBM - 1) / TBM) : (int)((M + BM - 1) / BM);
   // thin-operand digits + factors (workspace owned by the context)
   const size_t dig_bytes = (size_t)nblk * BROWS * kpad;
@@ -2100,13 +2140,17 @@ cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, cons
     ok = make_map_2d(&tA, a.A, K, M, a.lda, tkern ? TBM : BM, es) &&
          make_map_1d(&tS, mu_inv, TABW * kpad, TABW * BK);
   } else {
-    ok = make_map_cm(&tA, a.A, M, K, a.lda, es);
+    ok = make_map_cm(&tA, a.A, M, K, a.lda, es, tkern ? TBM : BM);
   }
   if (!planes && tkern) {
     if (!ok) return cudaErrorInvalidValue;
     const int64_t units = (int64_t)mtiles * nch;
     const int grid = (int)std::min<int64_t>(units, ctx.num_sms);
-    e = f32 ? launch_t<float>(tA, tS, p, grid, st) : launch_t<double>(tA, tS, p, grid, st);
+    if (RMm)
+      e = f32 ? launch_t<true, float>(tA, tS, p, grid, st) : launch_t<true, double>(tA, tS, p, grid, st);
+    else
+      e = f32 ? launch_t<false, float>(tA, tS, p, grid, st)
+              : launch_t<false, double>(tA, tS, p, grid, st);
     ctx.kernel_launches += 1;
     ctx.gemm_launches += 1;
   } else if (!planes) {

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -156,6 +157,30 @@ def _prepare_warm_start(u_prev, requested, n_rows, seed):
     return q
 
 
+# Dense first step / 'exact' backend without forming Ohat (engine.cu implicit_svd): taken when
+# Ohat would not fit beside the sample block, for float32 samples, and under row sharding (each
+# rank would otherwise hold the whole P x (r + N) matrix).  WSSR_DENSE_STEP=implicit|materialize
+# forces either path.
+IMPLICIT_MAX_ITERS = 100
+IMPLICIT_TOL = 1e-12       # ||Ohat v_i - s_i u_i|| / s_i of every kept triplet (or stagnation)
+_IMPLICIT_SEED = 0x5EED
+# telemetry of the last implicit solve: power iterations and max_i ||Ohat v_i - s_i u_i|| / s_i
+last_implicit_svd: dict = {}
+
+
+def _implicit_dense_step(ctx, samples, m, n_cols):
+    mode = os.environ.get("WSSR_DENSE_STEP", "auto")
+    if mode == "implicit":
+        return True
+    if mode == "materialize":
+        return False
+    if int(getattr(ctx, "world", 1)) > 1 or samples.dtype == torch.float32:
+        return True
+    # Ohat plus the dense SVD's working copies
+    free, _ = torch.cuda.mem_get_info(samples.device)
+    return 3 * 8 * m * n_cols > free
+
+
 def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
               ssi_max_iters=DEFAULT_SSI_MAX_ITERS, ssi_residual_tol=1e-10, rng_seed=0,
               *, report_final_residual=True, return_update=False):
@@ -210,7 +235,38 @@ def wssr_step(theta, bundle, eta, state, svd_backend="ssi",
     lvec = bundle.l_vector.contiguous()
     grad = bundle.gradient if bundle._gradient_exact else None
     ext = None
-    if dense:
+    if dense and svd_backend != "randomized" and _implicit_dense_step(
+            ctx, samples, m, r + n_global):
+        # optimizers.py:327-338 without forming Ohat: exact_truncated_svd of the implicit
+        # operator on the O-pass kernels (svdengine.py:75-85; engine.cu implicit_svd), rows
+        # sharded like the SSI; every rank gets U and sigma, and its own rows of V
+        world = int(getattr(ctx, "world", 1))
+        if world > 1:
+            counts = torch.zeros(world, dtype=torch.float64, device=dev)
+            counts[ctx.rank] = n
+            ctx.call("wssr_allreduce_f64", _lib.ptr(counts), world)
+            counts = [int(c) for c in counts.tolist()]
+            c0 = 0 if ctx.rank == 0 else r + sum(counts[:ctx.rank])
+            n_local = (r if ctx.rank == 0 else 0) + n
+            o_imp = _ohat_struct(samples, bundle._mu, bundle._scale, bundle._fro2,
+                                 hist if ctx.rank == 0 else hist[:0], 1.0, bundle._scale_table)
+            n_cols = r + sum(counts)
+        else:
+            c0, n_local, o_imp, n_cols = 0, r + n, o, r + n
+        fu = torch.empty(m, k, dtype=torch.float64, device=dev)
+        fs = torch.empty(k, dtype=torch.float64, device=dev)
+        fv = torch.empty(max(n_local, 1), k, dtype=torch.float64, device=dev)
+        k_pos, iters, resid = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        ctx.call("wssr_implicit_svd_f64", ctypes.byref(o_imp), float(state.delta), k, n_cols, c0,
+                 ctypes.c_uint64(_IMPLICIT_SEED + int(state.step)), IMPLICIT_MAX_ITERS,
+                 IMPLICIT_TOL, _lib.ptr(fu), k, _lib.ptr(fs), _lib.ptr(fv), k,
+                 ctypes.byref(k_pos), ctypes.byref(iters), ctypes.byref(resid))
+        ext = (fu, fs, fv, int(k_pos.value))
+        # the reference reports iterations_used=0 / residual 0.0 for the dense step
+        # (optimizers.py:328-331); the implicit solve's own certificate is kept here
+        last_implicit_svd.update(iterations=int(iters.value), residual=float(resid.value),
+                                 block=min(max(2 * k, k + 16), m, n_cols))
+    elif dense:
         # optimizers.py:327-338: dense first step / 'exact' backend, or the randomized sketch
         from .svdengine import exact_truncated_svd, randomized_svd
         world = int(getattr(ctx, "world", 1))

@@ -117,7 +117,8 @@ def test_ozaki_accuracy_vs_dmma(layout, M, N, K):
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("offset,every", [(1e3, 1), (1e9, 1), (1e6, 3), (20.0, 37)])
 @pytest.mark.parametrize("f32", [False, True])
-def test_ozaki_large_column_means(layout, offset, every, f32, fp32_digits):
+@pytest.mark.parametrize("N", [64, 128])
+def test_ozaki_large_column_means(layout, offset, every, f32, fp32_digits, N):
     """Columns whose mean dwarfs their spread are digitised as rint((O - mu) s) (O - mu exact by
     Sterbenz), the others by integer centring rint(O s) - rint(mu s) (ozaki.cu biased_digits);
     K-blocks mixing both forms take the per-block branch.  Same accuracy either way."""
@@ -125,7 +126,7 @@ def test_ozaki_large_column_means(layout, offset, every, f32, fp32_digits):
         pytest.skip("float32 samples keep 24 bits: the offset would swallow the data")
     if not f32 and fp32_digits == 5:
         pytest.skip("the float32 digit mode does not apply to float64 samples")
-    r = _run(layout, 384, 64, 3000, f32=f32, offset=offset, offset_every=every)
+    r = _run(layout, 384, N, 3000, f32=f32, offset=offset, offset_every=every)
     if f32 and fp32_digits == 5:
         assert r["ozaki"][0] < 1e-11 and r["ozaki"][1] < 1e-11, r
     else:
@@ -133,11 +134,12 @@ def test_ozaki_large_column_means(layout, offset, every, f32, fp32_digits):
 
 
 @pytest.mark.parametrize("layout", [0, 1])
-def test_ozaki_fp32_samples(layout, fp32_digits):
+@pytest.mark.parametrize("N", [64, 128])
+def test_ozaki_fp32_samples(layout, fp32_digits, N):
     """Float32 samples: 7 digits are FP64-grade; the default 5 (the top 5 of the same digits,
     20 pairs) represent each element to 2^-38 of its column's scale, so products are accurate to
     ~2^-39 of |X| |B| entrywise."""
-    r = _run(layout, 700, 64, 3000, f32=True, pad=1)
+    r = _run(layout, 700, N, 3000, f32=True, pad=1)
     if fp32_digits == 7:
         assert r["ozaki"][0] < 2e-15 and r["ozaki"][0] <= 4 * r["dmma"][0] + 1e-16, r
     else:
@@ -145,9 +147,10 @@ def test_ozaki_fp32_samples(layout, fp32_digits):
 
 
 @pytest.mark.parametrize("layout", [0, 1])
-def test_ozaki_wide_column_scales(layout):
+@pytest.mark.parametrize("N", [64, 128])
+def test_ozaki_wide_column_scales(layout, N):
     """Per-parameter power-of-two scaling keeps columns spanning 12 decades at FP64 accuracy."""
-    r = _run(layout, 600, 64, 2000, scale_cols=True)
+    r = _run(layout, 600, N, 2000, scale_cols=True)
     assert r["ozaki"][0] < 2e-15, r
     assert r["ozaki"][1] < 1e-13, r
 
@@ -169,6 +172,10 @@ def test_ozaki_k_chunks_beyond_int32_bound():
     r = _run(1, 256, 64, 40000)
     assert r["ozaki"][0] < 2e-15, r
     r = _run(0, 300, 64, 40000)
+    assert r["ozaki"][0] < 2e-15, r
+    r = _run(0, 130, 128, 33000)  # the transposed on-the-fly kernel (65-128 thin columns)
+    assert r["ozaki"][0] < 2e-15, r
+    r = _run(1, 70, 128, 33000)
     assert r["ozaki"][0] < 2e-15, r
 
 
