@@ -102,7 +102,12 @@ def test_sharded_dense_first_step():
             assert a["r_eff"] == b["r_eff"]
             assert rel(b["update"], a["update"]) < 1e-10
             assert rel(b["sigma"], a["sigma"]) < 1e-10
-            assert rel(b["lbar"], a["lbar"]) < 1e-8
+            # a dense factorisation fixes each (u_j, v_j) pair only up to a joint sign, and the
+            # materialised and implicit first steps pick it differently: lbar = V^T l carries
+            # that sign, obar lbar does not.  Align on the returned basis before comparing.
+            sgn = np.sign(np.sum(a["V"] * b["V"], axis=0))
+            assert np.all(sgn != 0)
+            assert rel(b["lbar"] * sgn, a["lbar"]) < 1e-8
             assert subspace_sine(b["V"], a["V"]) < 1e-8
 
 
