@@ -332,6 +332,11 @@ def _ncu_traffic(name):
     return None, None
 
 
+def _digit_pairs():
+    from paper_2512_05749_b200 import _lib
+    return int(_lib.load_library().wssr_ozaki_digit_pairs())
+
+
 # ---- our arm ------------------------------------------------------------------------------
 def measure(cfg_name, args, rank, world, local_rank, e2e_numpy=False, cpu=True):
     import numpy as np
@@ -781,7 +786,7 @@ def run_ours(args, rank, world, local_rank):
                 "2^-38 of its column's scale), 20 digit pairs on tcgen05 kind::i8, FP64 combine "
                 "(csrc/ozaki.cu)" if f32 else
                 "FP64 products as exact int8 digit products on tcgen05 kind::i8 (7 digits per "
-                "operand, 34 digit pairs, FP64 combine; csrc/ozaki.cu)"),
+                f"operand, {_digit_pairs()} digit pairs, FP64 combine; csrc/ozaki.cu)"),
             "roofline": rec["roofline"], "cpu_baseline": rec.get("cpu_baseline"),
             "e2e": rec.get("e2e"), "gpu_launches": rec["gpu_launches"], "clocks": rec["clocks"],
             "wall_s_timed_region": rec["wall_s_timed_region"],

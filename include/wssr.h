@@ -315,8 +315,13 @@ int wssr_set_tail_shard(wssr_ctx* ctx, int enabled);
 /* engine option: sample digits of the int8 O-passes for float32 samples (BASELINE configs[3]):
  * 5 (default) = the 5 most significant of the 7 digits (each element to 2^-38 of its column's
  * scale, exact for float32 values within 14 binades of the column maximum; 20 digit pairs and 5
- * planes in HBM), 7 = the FP64-grade scheme of float64 samples (34 pairs, 7 planes). */
+ * planes in HBM), 7 = the FP64-grade scheme of float64 samples (28 pairs, 7 planes). */
 int wssr_set_fp32_digits(wssr_ctx* ctx, int digits);
+
+/* digit pairs per product that the FP64-grade int8 O-passes of this build keep: 28 (pairs of
+ * significance a + b <= 6, truncation below 2^-51.4 of the column-scale product; the default)
+ * or 34 (a + b <= 7, below 2^-59; built with -DWSSR_OZ_LEVELS=8). */
+int wssr_ozaki_digit_pairs(void);
 
 /* engine option: dense SVD mode, 0 (default) = single-CTA Jacobi up to min(m, n) = 512 and the
  * blocked Jacobi above; 1 = the blocked Jacobi at every size (tests). */

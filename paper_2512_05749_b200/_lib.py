@@ -14,7 +14,8 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libwssr.so")
+# WSSR_LIB points the binding at another build of the same ABI (A/B runs of kernel variants)
+LIB_PATH = os.environ.get("WSSR_LIB") or os.path.join(_HERE, "lib", "libwssr.so")
 
 WSSR_OK = 0
 WSSR_FLAG_FINAL_RESIDUAL = 0x1
@@ -101,6 +102,7 @@ SIGNATURES = {
     "wssr_set_tallskinny": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_dense_svd_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_set_fp32_digits": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "wssr_ozaki_digit_pairs": (ctypes.c_int, []),
     "wssr_set_tail_shard": (ctypes.c_int, [_vp, ctypes.c_int]),
     "wssr_release_memory": (ctypes.c_int, [_vp]),
     "wssr_dense_svd_sweeps": (ctypes.c_int, [_vp]),

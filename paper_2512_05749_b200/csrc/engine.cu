@@ -2148,6 +2148,8 @@ int wssr_set_tail_shard(wssr_ctx* ctx, int enabled) {
   return WSSR_OK;
 }
 
+int wssr_ozaki_digit_pairs(void) { return ozaki_digit_pairs(); }
+
 int wssr_set_fp32_digits(wssr_ctx* ctx, int digits) {
   if (!ctx || (digits != 5 && digits != 7)) return WSSR_ERR_VALUE;
   ctx->c.f32_digits = digits;

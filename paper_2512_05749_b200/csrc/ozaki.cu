@@ -11,11 +11,15 @@
 //     when O - mu is exact; see biased_digits), split into 7 signed base-256 digits
 //     X = sum_i d_i 256^i, d_i in [-128, 127] (bytes of X + 0x0080808080808080, each XOR 0x80);
 //   * the thin operand (q or v, P x k / N x k) is split the same way per output column;
-//   * digit products are exact int8 x int8 -> int32 tensor-core MMAs; the 34 digit pairs (a, b)
-//     with a + b <= 7 (most-significant-first) are kept - the dropped ones sum below 2^-59 of
-//     the product of the column scales - and pairs of equal significance a + b = s share one
-//     int32 TMEM accumulator D_s, 8 x 64 columns = all 512 (no overflow: 7 pairs x 2^14 x
-//     K-chunk <= 16384 < 2^31);
+//   * digit products are exact int8 x int8 -> int32 tensor-core MMAs; the 28 digit pairs (a, b)
+//     with a + b <= 6 (most-significant-first) are kept - the dropped ones sum below 2^-51.4 of
+//     the product of the column scales (6 pairs of level 7 at <= 2^14 2^40 each against 2^108),
+//     the size of one FP64 rounding of a full-scale product, and unlike FP64 the kept sums are
+//     exact over K - and pairs of equal significance a + b = s share one int32 TMEM accumulator
+//     D_s, 7 x 64 of the 512 columns (no overflow: 7 pairs x 2^14 x K-chunk <= 16384 < 2^31).
+//     WSSR_OZ_LEVELS=8 at build time keeps level 7 as well (34 pairs, dropped below 2^-59):
+//     +9% smem-pipe time per pass for a closed-loop update error that measures the same
+//     (DESIGN.md section 4);
 //   * the epilogue combines sum_s D_s 2^(96 - 8 s) in FP64 and applies the power-of-two scales.
 //
 // Each element is thus represented to 2^-54 of its column's magnitude and every product and sum
@@ -60,7 +64,10 @@ namespace oz {
 constexpr int BM = 128;            // rows of the output tile (TMEM lanes)
 constexpr int BK = 32;             // K per stage (one kind::i8 MMA-K)
 constexpr int ND = 7;              // digits per operand
-constexpr int NL = 8;              // significance levels kept (s = a + b <= 7), one TMEM block each
+#ifndef WSSR_OZ_LEVELS
+#define WSSR_OZ_LEVELS 7
+#endif
+constexpr int NL = WSSR_OZ_LEVELS; // significance levels kept (s = a + b < NL), one TMEM block each
 constexpr int NB = 64;             // output columns per unit
 constexpr int BROWS = ND * NB;     // thin-operand digit rows per stage (448)
 constexpr int RSTAGES = 3;         // raw tile ring (TMA -> converters)
@@ -327,13 +334,13 @@ __device__ __forceinline__ uint64_t guard_count(uint64_t y) {
 // ---- digit pairs of one K-block -------------------------------------------------------------
 // Sample digit a (most significant first) against the thin digits b, into the int32 level
 // accumulators D_s, s = a + b < nl (TMEM columns 64 s ...), thin digits concatenated along N (up
-// to 256 per MMA).  nds = 7, nl = 8: the FP64 scheme (34 pairs, dropped levels below 2^-59 of the
-// product of the column scales).  nds = 5, nl = 6 for float32 samples: the top 5 of the same 7
+// to 256 per MMA).  nds = 7, nl = NL = 7: the FP64 scheme (28 pairs, dropped levels below 2^-51.4 of
+// the product of the column scales; NL = 8: 34 pairs, 2^-59).  nds = 5, nl = 6 for float32 samples: the top 5 of the same 7
 // digit planes (X to 2^-38 of its column's scale - every float32 element within 14 binades of
 // its column's maximum exactly) and levels to 2^-48: 20 pairs, 5 planes in HBM.  Digit 1 goes
 // first and digit 0's range is split at column 64, so on a unit's first K-block (first = 0)
 // every TMEM column is first written by an MMA with accumulate = 0.
-// levels kept for NDS sample digits: 8 (FP64 scheme) or NDS + 1
+// levels kept for NDS sample digits: NL (FP64 scheme) or NDS + 1
 template <int NDS>
 __host__ __device__ constexpr int levels() { return NDS == ND ? NL : NDS + 1; }
 
@@ -1922,6 +1929,13 @@ bool make_map_planes(CUtensorMap* map, const int8_t* planes, int64_t prows, int6
 }
 
 }  // namespace oz
+
+int ozaki_digit_pairs() {
+  int pairs = 0;
+  for (int a = 0; a < oz::ND; ++a)
+    for (int b = 0; b < oz::ND; ++b) pairs += a + b < oz::NL ? 1 : 0;
+  return pairs;
+}
 
 // ---- host side ---------------------------------------------------------------------------------
 cudaError_t ozaki_trace(long long* host, size_t n) {

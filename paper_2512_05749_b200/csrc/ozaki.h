@@ -38,7 +38,7 @@ bool ozaki_supported(Layout L, const GemmArgs& a, bool f32);
 // the on-the-fly pass produces (same layout as ozaki_digitize), so later passes can stream them.
 // rowcnt (on-the-fly v pass only): per sample row, the precision guard's packed digit-integer
 // counts (see ozaki_row_guard)
-// nds: sample digits the pass uses - 7 (FP64-grade, 34 digit pairs) or 5 (float32 samples: the
+// nds: sample digits the pass uses - 7 (FP64-grade, 28 digit pairs) or 5 (float32 samples: the
 // top 5 of the same digits, X to 2^-38 of its column's scale, 20 pairs; see ozaki.cu issue_pairs)
 cudaError_t ozaki_gemm(Context& ctx, Layout L, const GemmArgs& a, bool f32, const double* mu_inv,
                        cudaStream_t st, const int8_t* planes = nullptr, int8_t* store = nullptr,
@@ -56,6 +56,9 @@ cudaError_t ozaki_row_guard(Context& ctx, const unsigned long long* rowcnt, int6
 // Digit planes [nds][rows][ozaki_plane_pitch(cols)] int8 of the centred, scaled sample block
 // (rows = samples, cols = parameters, row-major with pitch lda; the nds most significant of the 7
 // digits); written once per step and streamed by both O-passes.
+// digit pairs kept per product by the FP64-grade scheme of this build (28, or 34 with
+// -DWSSR_OZ_LEVELS=8)
+int ozaki_digit_pairs();
 int64_t ozaki_plane_pitch(int64_t cols);
 size_t ozaki_planes_bytes(int64_t rows, int64_t cols, int nds = 7);
 cudaError_t ozaki_digitize(Context& ctx, const void* A, bool f32, int64_t lda, int64_t rows,

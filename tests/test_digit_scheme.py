@@ -7,14 +7,17 @@ kernels rely on, checked on the CPU.
   (kBias); plane a holds byte 6 - a XOR 0x80, a signed digit (pack_digits8).  The 7 signed digits
   reconstruct X exactly, and X is (x - mu) to one unit of 2^-54 of the column scale;
 * products: level s = a + b collects the digit pairs of one significance; the kernels keep
-  s <= 7 (34 pairs, NL = 8 TMEM levels) and combine the int32 level sums in FP64.  The dropped
-  pairs weigh at most 2^-64 of the top level, so a dot product of length K is exact to
-  ~K 2^-50 of |a| |b| scales - below the FP64 rounding of the same dot product.
+  s <= 6 (28 pairs, NL = 7 TMEM levels; s <= 7, 34 pairs, with -DWSSR_OZ_LEVELS=8) and combine
+  the int32 level sums in FP64.  The dropped pairs weigh at most 2^-56 of the top level (2^-64
+  for NL = 8), so every product is exact to 2^-51.4 (2^-59) of the column-scale product and the
+  sum over K adds no rounding - the size of the FP64 rounding of the same dot product.
 CPU-only."""
 
 import numpy as np
 
-ND, NL = 7, 8
+import pytest
+
+ND = 7
 BIAS = np.uint64(0x0080808080808080)
 
 
@@ -71,7 +74,8 @@ def test_both_centring_forms_stay_in_digit_range():
         assert err <= np.ldexp(1.0, e - 53) * (1 + 1e-12)
 
 
-def test_truncated_pair_product_is_fp64_grade():
+@pytest.mark.parametrize("NL,npairs,acc", [(7, 28, 2.0 ** -43), (8, 34, 2.0 ** -48)])
+def test_truncated_pair_product_is_fp64_grade(NL, npairs, acc):
     rng = np.random.default_rng(1)
     K = 4096
     a = rng.standard_normal(K) * np.exp(rng.uniform(-4, 4, K))
@@ -87,12 +91,13 @@ def test_truncated_pair_product_is_fp64_grade():
             if i + j < NL:
                 levels[i + j] += int(np.dot(pa[i].astype(np.int64), pb[j].astype(np.int64)))
                 pairs += 1
-    assert pairs == 34
+    assert pairs == npairs
     got = sum(np.ldexp(float(levels[s]), 8 * (12 - s) + ea + eb - 108) for s in range(NL))
     exact = sum(int(u) * int(v) for u, v in zip(XA, XB))             # the digitised operands
     exact_f = np.ldexp(float(exact), ea + eb - 108)
-    bound = K * 128 * 128 * 2.0 ** (8 * 4 + ea + eb - 108) * 6       # dropped levels s >= 8
+    # dropped levels s >= NL: at most 13 - s pairs of 128 x 128 at weight 2^(8 (12 - s))
+    bound = K * 128 * 128 * 2.0 ** (8 * (12 - NL) + ea + eb - 108) * (13 - NL) * (1 + 2.0 ** -7)
     assert abs(got - exact_f) <= bound + 4 * np.finfo(float).eps * abs(exact_f)
     ref = float(np.dot(a.astype(np.longdouble), b.astype(np.longdouble)))
     scale = np.abs(a) @ np.abs(b)
-    assert abs(got - ref) <= 2.0 ** -48 * scale
+    assert abs(got - ref) <= acc * scale
