@@ -665,7 +665,7 @@ def _e2e_numpy(wl, fresh_state, rows, P, N, esize, world, dev, stream, aux, barr
                     "theta) -> numpy theta', the reference runner's convention"}
 
 
-def measure_producer(cfg_name, args):
+def measure_producer(cfg_name, args, reps=20, nsteps=10):
     """(f)2, the device producer of O: AceWavefunction.grad_theta_batch (csrc/producer.cu) on a
     seeded synthetic ansatz with the config's P (n_electrons x n_features) and N walkers
     (paper_2512_05749_b200/synthetic_ansatz.py).  Reports the producer's own throughput and an
@@ -687,14 +687,16 @@ def measure_producer(cfg_name, args):
     stream = torch.cuda.current_stream()
     ctx = _lib.context()
     x = torch.as_tensor(walkers(N, 0), device=dev)
+    # one output block, reused: at c2 it is 137 GB, and a freed block of that size must not be
+    # carved up by the caching allocator between steps
+    O_buf = torch.empty(N, P, dtype=torch.float64, device=dev)
     for _ in range(3):
-        wavefunction.grad_theta_batch(spec, x)
+        wavefunction.grad_theta_batch(spec, x, out=O_buf)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
     a.record(stream)
     for _ in range(reps):
-        O = wavefunction.grad_theta_batch(spec, x)
+        wavefunction.grad_theta_batch(spec, x, out=O_buf)
     b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
@@ -733,15 +735,15 @@ def measure_producer(cfg_name, args):
             xp = pos_h[t % 2].to(dev, non_blocking=True)
             e = e_h[t % 2].to(dev, non_blocking=True)
             spec.set_theta(th)
-            o = wavefunction.grad_theta_batch(spec, xp)
+            o = wavefunction.grad_theta_batch(spec, xp, out=O_buf)
             bundle = estimators.assemble(estimators.SampleBatch(cfgs, e, o))
             th, st, _ = optimizers.wssr_step(th, bundle, 1e-3, st)
             out_h.copy_(th, non_blocking=True)
+            del bundle, o  # the next batch overwrites the block
         torch.cuda.synchronize()
         return st
 
     st = run(2, fresh())
-    nsteps = 10
     a.record(stream)
     st = run(nsteps, st)
     b.record(stream)
@@ -758,12 +760,35 @@ def measure_producer(cfg_name, args):
                             "read back and set on the ansatz, every step"}}
 
 
+def _release_device_memory(local_rank):
+    import gc
+
+    import torch
+
+    from paper_2512_05749_b200 import _lib
+
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    _lib.context(local_rank).call("wssr_release_memory")
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
     torch.cuda.set_device(local_rank)
     rec = measure(args.config, args, rank, world, local_rank)
     secondary = {}
+    producer_main = None
+    if args.config == "c2" and world == 1 and not args.no_producer:
+        # the headline config fed by walker positions instead of a 137 GB upload; a failure here
+        # (e.g. no room for the block) is reported, not fatal
+        try:
+            _release_device_memory(local_rank)
+            producer_main = measure_producer("c2", args, reps=3, nsteps=4)
+        except Exception as exc:  # noqa: BLE001
+            producer_main = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        _release_device_memory(local_rank)
     if args.secondary and args.secondary != args.config:
         sec_args = argparse.Namespace(**vars(args))
         sec_args.steps = max(args.steps, 20)
@@ -801,6 +826,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if producer is not None:
             line["secondary"]["c1_producer"] = producer
+        if producer_main is not None:
+            line["secondary"]["c2_producer"] = producer_main
         print(json.dumps(line), flush=True)
 
 

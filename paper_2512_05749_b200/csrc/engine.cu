@@ -422,6 +422,12 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
     static std::atomic<uint64_t> attr{0};
     WSSR_CUDA(smem_attr_once(attr, chol_inv_smem_kernel, 200 * 1024));
     launch_pdl(chol_inv_smem_kernel, 1, 256, smem, ctx.stream, G, k, R, Rinv, status, kCholPivotRel);
+  } else if (sizeof(double) * chol_packed_doubles(k) <= 200 * 1024) {
+    // k = 128 (BASELINE configs[2], [3]): L and L^-1 share one shared-memory array
+    static std::atomic<uint64_t> attr{0};
+    WSSR_CUDA(smem_attr_once(attr, chol_inv_packed_kernel, 200 * 1024));
+    launch_pdl(chol_inv_packed_kernel, 1, 256, sizeof(double) * chol_packed_doubles(k), ctx.stream,
+               G, k, R, Rinv, status, kCholPivotRel);
   } else {
     Buf W(chol_scratch_doubles(k), ctx.stream);
     launch_pdl(chol_inv_gmem_kernel, 1, 256, 0, ctx.stream, G, k, W, R, Rinv, status, kCholPivotRel);
@@ -1128,15 +1134,28 @@ __global__ void drift_finalize_kernel(const double* __restrict__ in, double* __r
 }
 
 // Enqueue the drift on ctx.stream; out2 (device, 2 doubles) = {sigma_drift, projector_drift}.
+// sliced (row-sharded runs with the P-sliced tail): u1 and u2 are replicated, so each rank works
+// its own P-slice of the two P x r passes and the r x r cross product and Gram are allreduced.
 void drift_enqueue(Context& ctx, int64_t rows, const double* u1, int64_t ld1, const double* s1,
-                   int64_t r, const double* u2, int64_t ld2, const double* s2, double* out2) {
+                   int64_t r, const double* u2, int64_t ld2, const double* s2, double* out2,
+                   bool sliced = false) {
   cudaStream_t st = ctx.stream;
+  if (sliced) {
+    const PSlice sl = p_slice(ctx, rows, false);
+    sliced = sl.on;
+    if (sl.on) {
+      u1 += sl.p0 * ld1;
+      u2 += sl.p0 * ld2;
+      rows = sl.rows;
+    }
+  }
   Buf C((size_t)r * r, st), X((size_t)rows * r, st), GX((size_t)r * r, st), out(3, st);
   launch_pdl(small_norms_kernel, 1, 256, 0, st, s1, s2, (int)r, nullptr, 0, out);
   post_launch(ctx);
   cross(ctx, rows, r, u1, ld1, u2, ld2, C);                  // u1^T u2
+  if (sliced) allreduce(ctx, C, (size_t)(r * r));
   sub_mul_small(ctx, rows, r, u1, ld1, C, u2, ld2, X, r);    // u2 - u1 (u1^T u2)
-  gram(ctx, rows, r, X, r, GX, false);
+  gram(ctx, rows, r, X, r, GX, sliced);
   maxeig(ctx, GX, (int)r, out + 2);
   post_launch(ctx);
   launch_pdl(drift_finalize_kernel, 1, 32, 0, st, (const double*)out, out2);
@@ -1145,13 +1164,13 @@ void drift_enqueue(Context& ctx, int64_t rows, const double* u1, int64_t ld1, co
 
 std::pair<double, double> drift(Context& ctx, int64_t rows, const double* u1, int64_t ld1,
                                 const double* s1, int64_t r1, const double* u2, int64_t ld2,
-                                const double* s2, int64_t r2) {
+                                const double* s2, int64_t r2, bool sliced = false) {
   const int64_t r = std::min(r1, r2);
   if (r == 0) return {0.0, 0.0};
   Buf out2(2, ctx.stream);
   {
     PhaseTimer tm(ctx, 5, 0.0, 0.0);
-    drift_enqueue(ctx, rows, u1, ld1, s1, r, u2, ld2, s2, out2);
+    drift_enqueue(ctx, rows, u1, ld1, s1, r, u2, ld2, s2, out2, sliced);
   }
   double h[2];
   d2h(ctx, h, out2, sizeof(h));
@@ -1741,7 +1760,7 @@ void step_impl(Context& ctx, const wssr_step_in* in, wssr_step_out* out) {
     if (r_hist > 0) row_norms(ctx, oh.hist, r_hist, P, oh.hist_ld, sprev);
     const int64_t r1 = std::min(r_hist, in->r_prev);
     auto d = drift(ctx, P, in->u_prev, in->ld_prev, sprev, r1, out->u_next, out->ld_u, out->sigma,
-                   r_eff);
+                   r_eff, dist);
     sd = d.first;
     pd = d.second;
   }

@@ -324,6 +324,10 @@ __global__ void matrix_sumsq_partials_kernel(const double* __restrict__ x, int64
 // W is k x (k+1) scratch (odd stride).  status[0] = 1-based index of the first pivot that is not
 // safely positive (CholeskyQR2 would lose orthogonality there: the host re-runs the block on the
 // Gram-Schmidt path of linalg.py:64-105); status[1] = zero matrix (linalg.py:53-54).
+// PACKED: X = L^-1 (lower triangular, like L) lives transposed in the unused upper part of W,
+// X[i][c] at W[c][i + 1] (the odd stride k + 1 leaves column k free), so one k x (k + 1) array
+// holds both and k = 128 fits in shared memory (133 KB) instead of falling to global scratch.
+template <bool PACKED>
 __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, double* X,
                               double* dorig, double* __restrict__ R, double* __restrict__ Rinv,
                               int* __restrict__ status, double pivot_rel) {
@@ -332,10 +336,11 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
   const int tid = threadIdx.x, nt = blockDim.x;
   const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 grid (blockDim.x == 256)
   const int ld = k + 1;
+  auto XA = [&](int i, int c) -> double& { return PACKED ? W[c * ld + i + 1] : X[i * ld + c]; };
   for (int r = ty; r < k; r += 16)
     for (int c = tx; c < k; c += 16) {
-      W[r * ld + c] = G[r * k + c];
-      X[r * ld + c] = (r == c) ? 1.0 : 0.0;
+      if (!PACKED || c <= r) W[r * ld + c] = G[r * k + c];
+      if (!PACKED || c <= r) XA(r, c) = (r == c) ? 1.0 : 0.0;
     }
   for (int j = tid; j < k; j += nt) dorig[j] = G[j * k + j];
   __syncthreads();
@@ -380,17 +385,15 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     if (s_fail) break;
     const double inv = s_inv;
     for (int i = j + 1 + tid; i < k; i += nt) W[i * ld + j] *= inv;
-    for (int c = tid; c <= j; c += nt) X[j * ld + c] *= inv;
+    for (int c = tid; c <= j; c += nt) XA(j, c) *= inv;
     if (tid == 0) W[j * ld + j] = s_sq;
     __syncthreads();
     for (int i = j + 1 + ty; i < k; i += 16) {
       const double lij = W[i * ld + j];
       double* wi = W + i * ld;
-      double* xi = X + i * ld;
-      const double* xj = X + j * ld;
       for (int c = tx; c <= i; c += 16) {
         if (c <= j) {
-          xi[c] = fma(-lij, xj[c], xi[c]);
+          XA(i, c) = fma(-lij, XA(j, c), XA(i, c));
         } else {
           const double nv = fma(-lij, W[c * ld + j], wi[c]);
           wi[c] = nv;
@@ -412,7 +415,7 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
         Rinv[e] = 0.0;
       } else {
         R[e] = W[c * ld + r];     // L[c][r]
-        Rinv[e] = X[c * ld + r];  // X[c][r]
+        Rinv[e] = XA(c, r);       // X[c][r]
       }
     }
 }
@@ -748,6 +751,9 @@ __global__ void __launch_bounds__(256) chol_inv_reg64_kernel(const double* __res
 __host__ __device__ inline size_t chol_scratch_doubles(int k) {
   return 2 * (size_t)k * (k + 1) + (size_t)k;
 }
+__host__ __device__ inline size_t chol_packed_doubles(int k) {
+  return (size_t)k * (k + 1) + (size_t)k;
+}
 
 __global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int k, double* R,
                                                             double* Rinv, int* status,
@@ -756,7 +762,16 @@ __global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int
   extern __shared__ __align__(16) double smem[];
   double* W = smem;
   double* X = W + (size_t)k * (k + 1);
-  chol_inv_body(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
+  chol_inv_body<false>(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
+}
+// L and L^-1 packed into one k x (k + 1) shared array (k <= ~160)
+__global__ void __launch_bounds__(256) chol_inv_packed_kernel(const double* G, int k, double* R,
+                                                              double* Rinv, int* status,
+                                                              double pivot_rel) {
+  pdl_wait();
+  extern __shared__ __align__(16) double smem[];
+  double* W = smem;
+  chol_inv_body<true>(G, k, W, nullptr, W + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
 }
 __global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int k, double* ws,
                                                             double* R, double* Rinv, int* status,
@@ -764,7 +779,7 @@ __global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int
   pdl_wait();
   double* W = ws;
   double* X = W + (size_t)k * (k + 1);
-  chol_inv_body(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
+  chol_inv_body<false>(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
 }
 
 // C = A * B for k x k upper-triangular A, B (row-major, ld k).

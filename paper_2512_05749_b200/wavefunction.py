@@ -89,10 +89,12 @@ class AceSpec:
             self._spec.coef = self._coef.data_ptr()
 
 
-def grad_theta_batch(spec, positions):
+def grad_theta_batch(spec, positions, out=None):
     """(W, n_params) float64 CUDA tensor of d log|psi| / d theta (wavefunction.py:307-321).
 
     `spec` is an AceSpec or a reference AceWavefunction (tables built per call then).
+    `out` (not in the reference): a preallocated (W, n_params) float64 CUDA tensor to write
+    into, for runs whose sample block fills the GPU and is reused from step to step.
     Raises NodeProximity when a walker's determinant vanishes or underflows, as the reference.
     """
     if not isinstance(spec, AceSpec):
@@ -101,7 +103,12 @@ def grad_theta_batch(spec, positions):
     if x.dim() != 3 or x.shape[1] != spec.n_electrons or x.shape[2] != 3:
         raise ValueError(f"positions must be (W, {spec.n_electrons}, 3), got {tuple(x.shape)}")
     w = int(x.shape[0])
-    out = torch.empty(w, spec.n_params, dtype=torch.float64, device=spec.device)
+    if out is None:
+        out = torch.empty(w, spec.n_params, dtype=torch.float64, device=spec.device)
+    elif (tuple(out.shape) != (w, spec.n_params) or out.dtype != torch.float64
+          or out.device != x.device or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous ({w}, {spec.n_params}) float64 tensor on "
+                         f"{x.device}")
     _lib.context().call("wssr_grad_theta_f64", ctypes.byref(spec._spec), _lib.ptr(x), w,
                         _lib.ptr(out), spec.n_params)
     return out

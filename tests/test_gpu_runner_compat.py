@@ -150,3 +150,29 @@ def test_dataclass_contract_of_the_step_outputs():
     ref = orc.assemble(o, e)
     np.testing.assert_allclose(np.asarray(b.o_matrix), ref["o_matrix"], atol=1e-15)
     assert isinstance(np.asarray(st1.obar), np.ndarray)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_large_host_arrays_upload_through_the_pinned_pipeline(dtype, monkeypatch):
+    """numpy blocks above 256 MB (the runner's per-step sample block) go up in pinned chunks
+    (_arrays._upload_pipelined): same bytes as the direct copy, for sizes that are not a multiple
+    of the staging buffer, read-only arrays, and back-to-back calls reusing the buffers."""
+    import torch
+
+    from paper_2512_05749_b200 import _arrays
+
+    monkeypatch.setattr(_arrays, "_STAGE_BYTES", 8 << 20)
+    monkeypatch.setattr(_arrays, "_PIPELINE_MIN_BYTES", 16 << 20)
+    monkeypatch.setattr(_arrays, "_stage_local", __import__("threading").local())
+    rng = np.random.default_rng(3)
+    for rows, cols in ((1031, 4099), (2048, 4096)):
+        a = rng.standard_normal((rows, cols)).astype(dtype)
+        a.setflags(write=False)
+        t = _arrays.to_tensor_f64_or_f32(a)
+        b = _arrays.to_tensor_f64_or_f32(a[::-1])  # a second upload right behind the first
+        assert t.dtype == (torch.float64 if dtype == np.float64 else torch.float32)
+        assert t.shape == a.shape and t.is_cuda
+        assert np.array_equal(t.cpu().numpy(), a)
+        assert np.array_equal(b.cpu().numpy(), a[::-1])
+    small = rng.standard_normal((8, 8))
+    assert np.array_equal(_arrays.to_tensor(small).cpu().numpy(), small)

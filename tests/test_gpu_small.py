@@ -21,7 +21,7 @@ def _small(op, a):
     return o1.cpu().numpy(), o2.cpu().numpy(), (st[0], st[1])
 
 
-@pytest.mark.parametrize("k", [1, 2, 7, 32, 64, 100, 128, 200])
+@pytest.mark.parametrize("k", [1, 2, 7, 32, 64, 100, 128, 150, 200])
 def test_cholesky_inverse(k):
     rng = np.random.default_rng(k)
     x = rng.standard_normal((3 * k + 5, k)) * np.exp(rng.uniform(-3, 3, k))

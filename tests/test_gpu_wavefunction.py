@@ -38,6 +38,12 @@ def test_grad_theta_matches_reference(tag):
     ref = g[f"{tag}_grad"]
     err = np.abs(out - ref).max() / np.abs(ref).max()
     assert err < 1e-11, err
+    # a caller-owned output block (reused from step to step at BASELINE configs[2]'s size)
+    buf = torch.full(out.shape, 7.0, dtype=torch.float64, device="cuda")
+    same = grad_theta_batch(spec, g[f"{tag}_positions"], out=buf)
+    assert same.data_ptr() == buf.data_ptr() and np.array_equal(buf.cpu().numpy(), out)
+    with pytest.raises(ValueError):
+        grad_theta_batch(spec, g[f"{tag}_positions"], out=buf[:, :-1])
     # feeds the step directly: a SampleBatch of device O
     from paper_2512_05749_b200 import estimators
 
