@@ -754,6 +754,9 @@ def measure_producer(cfg_name, args, reps=20, nsteps=10):
                     "h2d_bytes_per_step": N * n_el * 3 * 8 + N * 8,
                     "d2h_bytes_per_step": P * 8, "steps": nsteps,
                     "precision_fallbacks": ctx.precision_fallbacks() - fallbacks0,
+                    "precision_fallbacks_note": "steps (warm-up included) whose sample block had "
+                    "rows far below their columns' digit scales (near-node walkers set the column "
+                    "maxima): the precision guard re-ran their SSI with the O-passes on FP64 DMMA",
                     "path": "walker positions + local energies uploaded from pinned host memory "
                             "-> wavefunction.grad_theta_batch (O on the device) -> "
                             "estimators.assemble -> optimizers.wssr_step (eta 1e-3) -> theta' "

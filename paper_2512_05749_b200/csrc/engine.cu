@@ -427,7 +427,7 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
     static std::atomic<uint64_t> attr{0};
     WSSR_CUDA(smem_attr_once(attr, chol_inv_packed_kernel, 200 * 1024));
     launch_pdl(chol_inv_packed_kernel, 1, 256, sizeof(double) * chol_packed_doubles(k), ctx.stream,
-               G, k, R, Rinv, status, kCholPivotRel);
+               G, k, R, Rinv, status, kCholPivotRel, ctx.chol_series ? 1 : 0);
   } else {
     Buf W(chol_scratch_doubles(k), ctx.stream);
     launch_pdl(chol_inv_gmem_kernel, 1, 256, 0, ctx.stream, G, k, W, R, Rinv, status, kCholPivotRel);

@@ -765,12 +765,35 @@ __global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int
   chol_inv_body<false>(G, k, W, X, X + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
 }
 // L and L^-1 packed into one k x (k + 1) shared array (k <= ~160)
+// Near-identity Grams (the second pass of CholeskyQR2, G = I + E with k max|E| <= 1e-9) skip the
+// sweep: with X = U(E) (strict upper part plus half the diagonal), R = I + X satisfies
+// R^T R = I + E + X^T X and R^-1 = I - X + X^2 - ..., so R = I + X and R^-1 = I - X hold to
+// k max|E|^2 <= 1e-18 (the first-order case of chol_series for k <= 64).
+constexpr double kCholFirstOrderMax = 1e-9;
 __global__ void __launch_bounds__(256) chol_inv_packed_kernel(const double* G, int k, double* R,
                                                               double* Rinv, int* status,
-                                                              double pivot_rel) {
+                                                              double pivot_rel, int use_series) {
   pdl_wait();
   extern __shared__ __align__(16) double smem[];
   double* W = smem;
+  if (use_series) {
+    double em = 0.0;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+      const double d = fabs(G[e] - (e / k == e % k ? 1.0 : 0.0));
+      // NaN/Inf entries force em = +inf (fmax would drop a NaN): the sweep's pivot test reports
+      em = d <= 1.79769313486231570e308 ? fmax(em, d) : __longlong_as_double(0x7ff0000000000000ll);
+    }
+    em = block_max(em, W);
+    if (em * k <= kCholFirstOrderMax) {
+      for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int r = e / k, c = e % k;
+        const double x = c > r ? G[e] : 0.5 * (G[e] - 1.0);
+        R[e] = c > r ? x : (c == r ? 1.0 + x : 0.0);
+        Rinv[e] = c > r ? -x : (c == r ? 1.0 - x : 0.0);
+      }
+      return;
+    }
+  }
   chol_inv_body<true>(G, k, W, nullptr, W + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
 }
 __global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int k, double* ws,
