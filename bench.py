@@ -428,8 +428,9 @@ def measure(cfg_name, args, rank, world, local_rank, e2e_numpy=False, cpu=True):
     value = args.steps / (step_ms / 1e3)
 
     # ---- roofline -----------------------------------------------------------------------------
-    # Dominant kernels: the O-passes v = Ohat^T q and u = Ohat v (ozaki_gemm_kernel, digitising
-    # the sample block on the fly, and ozaki_pre_kernel, streaming pre-digitised planes; tcgen05
+    # Dominant kernels: the O-passes v = Ohat^T q and u = Ohat v (ozaki_gemm_kernel /
+    # ozaki_gemm_t_kernel, digitising the sample block on the fly, and ozaki_pre_kernel, streaming
+    # pre-digitised planes; tcgen05
     # kind::i8 exact digit products).  Each pass streams the sample block once: algorithmic bytes
     # per pass = N*P*esize; achieved = those bytes / the CUDA-event average pass
     # duration over the timed region (events on the launching stream around every pass,
@@ -452,8 +453,10 @@ def measure(cfg_name, args, rank, world, local_rank, e2e_numpy=False, cpu=True):
         "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
         "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
         "traffic_source": traffic_src or "no ncu --set full capture committed for this config",
-        "kernel": "O-passes v=Ohat^T q / u=Ohat v: oz::ozaki_gemm_kernel (digits on the fly) + "
-                  "oz::ozaki_pre_kernel (pre-digitised planes), tcgen05.mma kind::i8",
+        "kernel": "O-passes v=Ohat^T q / u=Ohat v: oz::ozaki_pre_kernel on the sample rows whose "
+                  "digit planes fit in HBM + digits on the fly for the rest "
+                  "(oz::ozaki_gemm_t_kernel at 65-128 thin columns, oz::ozaki_gemm_kernel up to "
+                  "64), tcgen05.mma kind::i8",
         "launches": g_n, "avg_launch_ms": g_ms / g_n if g_n else None,
         "bytes_per_launch": g_by / g_n if g_n else None,
         "peak_source": peak_src,
