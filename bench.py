@@ -299,8 +299,9 @@ def run_reference(args, rank):
 def workload_config(cfg, args):
     esize = 4 if cfg["dtype"] == "f32" else 8
     return {
-        "workload": f"{cfg['name']}: BASELINE configs[{cfg['name'][1:]}] N={cfg['N']} samples, "
-                    f"P={cfg['P']} params, k={cfg['k']}, {cfg['dtype']}",
+        "workload": cfg.get("label") or (
+            f"{cfg['name']}: BASELINE configs[{cfg['name'][1:]}] N={cfg['N']} samples, "
+            f"P={cfg['P']} params, k={cfg['k']}, {cfg['dtype']}"),
         "N": cfg["N"], "P": cfg["P"], "k": cfg["k"], "lambda": cfg["lam"],
         "delta": cfg["delta"], "latent_rank": cfg["L"], "alpha": cfg["alpha"],
         "drift": cfg["drift"], "ssi_max_iters": 3, "ssi_residual_tol": 1e-10,

@@ -28,6 +28,12 @@ CONFIGS = {
                T=20, dtype="f32"),
     "c4": dict(N=32768, P=2097152, k=256, L=512, alpha=0.8, delta=0.95, lam=1e-4, drift=5e-4,
                T=10, dtype="f64"),
+    # one 8-way rank's share of c4's sample rows at c4's full width and rank: what a single
+    # B200 can hold of the 550 GB block (bench.py --config c4s; not a BASELINE entry of its own)
+    "c4s": dict(N=4096, P=2097152, k=256, L=512, alpha=0.8, delta=0.95, lam=1e-4, drift=5e-4,
+                T=10, dtype="f64",
+                label="c4s: 4096 of BASELINE configs[4]'s 32768 sample rows (one 8-way rank's "
+                      "share) at its full P=2097152 params, k=256, delta=0.95, f64"),
 }
 
 

@@ -206,3 +206,15 @@ def test_c4_semantics_slice_T10_vs_transliteration(release_memory):
     _need_big_gpu()
     cfg = synthetic.config("c4", P=262144)
     _closed_loop(cfg, cfg["T"], seed=404, tag="c4 slice T=10")
+
+
+def test_c4_full_width_rank_shard_vs_transliteration(release_memory):
+    """BASELINE configs[4] at its full width and rank (P = 2^21 parameters, k = 256, history
+    averaging delta = 0.95) on the sample rows one GPU can hold next to the independent FP64
+    transliteration's own copy: N = 2048 of c4's 32768 walkers (34 GB; an 8-way rank holds
+    4096), three closed-loop steps so the P x 256 history block is live from the second one."""
+    from paper_2512_05749_b200 import synthetic
+
+    _need_big_gpu()
+    cfg = synthetic.config("c4", N=2048)
+    _closed_loop(cfg, 3, seed=405, tag="c4 full width, N=2048")
