@@ -408,6 +408,51 @@ double read_scalar(Context& ctx, const double* dev) {
 }
 
 // ---- k x k Cholesky + inverse ---------------------------------------------------------------
+void launch_chol_packed(Context& ctx, const double* G, int k, double* R, double* Rinv, int* status,
+                        const double* dref, const double* tref, int pivot_base) {
+  static std::atomic<uint64_t> attr{0};
+  WSSR_CUDA(smem_attr_once(attr, chol_inv_packed_kernel, 200 * 1024));
+  launch_pdl(chol_inv_packed_kernel, 1, 256, sizeof(double) * chol_packed_doubles(k), ctx.stream,
+             G, k, R, Rinv, status, kCholPivotRel, ctx.chol_series ? 1 : 0, dref, tref,
+             pivot_base);
+  post_launch(ctx);
+}
+
+// 160 < k <= 256 (BASELINE configs[4], k = 256): two diagonal blocks through the shared-memory
+// kernel instead of one sweep over global scratch (7 ms per call at k = 256).  With
+// G = [[G11, G12], [G12^T, G22]] and R upper: R11 = chol(G11), R12 = R11^-T G12,
+// R22 = chol(G22 - R12^T R12), R^-1 = [[R11^-1, -R11^-1 R12 R22^-1], [0, R22^-1]].  The pivot
+// tests of both blocks refer to the original diagonal and trace of G, as the one-sweep kernel's.
+void chol_inv_blocked2(Context& ctx, const double* G, int k, double* R, double* Rinv,
+                       int* status) {
+  cudaStream_t st = ctx.stream;
+  const int h = (k + 1) / 2, k2 = k - h;
+  Buf dt((size_t)k + 1, st), G11((size_t)h * h, st), R11((size_t)h * h, st),
+      R11i((size_t)h * h, st), R12((size_t)h * k2, st), S((size_t)k2 * k2, st),
+      R22((size_t)k2 * k2, st), R22i((size_t)k2 * k2, st), W((size_t)h * k2, st),
+      T((size_t)h * k2, st);
+  auto sgemm = [&](int m, int n, int kk, const double* A, int64_t a_rs, int64_t a_cs,
+                   const double* B, int64_t b_rs, int64_t b_cs, const double* C0, int64_t c0_ld,
+                   double alpha, double* C, int64_t ldc) {
+    launch_pdl(small_gemm_kernel, dim3((unsigned)((n + 15) / 16), (unsigned)((m + 15) / 16)), 256,
+               0, st, m, n, kk, A, a_rs, a_cs, B, b_rs, b_cs, C0, c0_ld, alpha, C, ldc);
+    post_launch(ctx);
+  };
+  launch_pdl(chol_diag_trace_kernel, 1, 256, 0, st, G, k, dt.p);
+  post_launch(ctx);
+  copy2d(ctx, G, k, h, h, 1.0, G11, h);
+  launch_chol_packed(ctx, G11, h, R11, R11i, status, nullptr, dt + k, 0);
+  sgemm(h, k2, h, R11i, 1, h, G + h, k, 1, nullptr, 0, 1.0, R12, k2);        // R11^-T G12
+  sgemm(k2, k2, h, R12, 1, k2, R12, k2, 1, G + (size_t)h * k + h, k, -1.0, S, k2);
+  launch_chol_packed(ctx, S, k2, R22, R22i, status, dt + h, dt + k, h);
+  sgemm(h, k2, k2, R12, k2, 1, R22i, k2, 1, nullptr, 0, 1.0, W, k2);          // R12 R22^-1
+  sgemm(h, k2, h, R11i, h, 1, W, k2, 1, nullptr, 0, -1.0, T, k2);             // -R11^-1 (...)
+  launch_pdl(chol_assemble2_kernel, blocks_for((int64_t)k * k, 256, 256), 256, 0, st, k, h,
+             (const double*)R11, (const double*)R11i, (const double*)R12, (const double*)T,
+             (const double*)R22, (const double*)R22i, R, Rinv);
+  post_launch(ctx);
+}
+
 void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int* status) {
   const size_t smem = sizeof(double) * chol_scratch_doubles(k);
   if (k <= 64) {
@@ -424,10 +469,11 @@ void chol_inv(Context& ctx, const double* G, int k, double* R, double* Rinv, int
     launch_pdl(chol_inv_smem_kernel, 1, 256, smem, ctx.stream, G, k, R, Rinv, status, kCholPivotRel);
   } else if (sizeof(double) * chol_packed_doubles(k) <= 200 * 1024) {
     // k = 128 (BASELINE configs[2], [3]): L and L^-1 share one shared-memory array
-    static std::atomic<uint64_t> attr{0};
-    WSSR_CUDA(smem_attr_once(attr, chol_inv_packed_kernel, 200 * 1024));
-    launch_pdl(chol_inv_packed_kernel, 1, 256, sizeof(double) * chol_packed_doubles(k), ctx.stream,
-               G, k, R, Rinv, status, kCholPivotRel, ctx.chol_series ? 1 : 0);
+    launch_chol_packed(ctx, G, k, R, Rinv, status, nullptr, nullptr, 0);
+    return;
+  } else if (sizeof(double) * chol_packed_doubles((k + 1) / 2) <= 200 * 1024) {
+    chol_inv_blocked2(ctx, G, k, R, Rinv, status);
+    return;
   } else {
     Buf W(chol_scratch_doubles(k), ctx.stream);
     launch_pdl(chol_inv_gmem_kernel, 1, 256, 0, ctx.stream, G, k, W, R, Rinv, status, kCholPivotRel);

@@ -330,7 +330,9 @@ __global__ void matrix_sumsq_partials_kernel(const double* __restrict__ x, int64
 template <bool PACKED>
 __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, double* X,
                               double* dorig, double* __restrict__ R, double* __restrict__ Rinv,
-                              int* __restrict__ status, double pivot_rel) {
+                              int* __restrict__ status, double pivot_rel,
+                              const double* __restrict__ dref = nullptr,
+                              const double* __restrict__ tref = nullptr, int pivot_base = 0) {
   __shared__ double s_gmax, s_trace;
   __shared__ int s_fail;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -342,7 +344,9 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
       if (!PACKED || c <= r) W[r * ld + c] = G[r * k + c];
       if (!PACKED || c <= r) XA(r, c) = (r == c) ? 1.0 : 0.0;
     }
-  for (int j = tid; j < k; j += nt) dorig[j] = G[j * k + j];
+  // dref / tref (a diagonal block of a larger Gram, see chol_inv_blocked2 in engine.cu): the
+  // pivot tests refer to the ORIGINAL diagonal entries of these rows and to the whole trace
+  for (int j = tid; j < k; j += nt) dorig[j] = dref ? dref[j] : G[j * k + j];
   __syncthreads();
   if (tid == 0) {  // from shared memory: a serial loop over global loads would cost ~k x 600 cycles
     double gm = 0.0, tr = 0.0;
@@ -351,7 +355,7 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
       tr += dorig[j];
     }
     s_gmax = gm;
-    s_trace = tr;
+    s_trace = tref ? *tref : tr;
     s_fail = 0;
   }
   __syncthreads();
@@ -404,7 +408,7 @@ __device__ void chol_inv_body(const double* __restrict__ G, int k, double* W, do
     __syncthreads();
   }
   if (s_fail) {
-    if (tid == 0) atomicCAS(status, 0, s_fail);
+    if (tid == 0) atomicCAS(status, 0, s_fail + pivot_base);
     return;
   }
   for (int r = ty; r < k; r += 16)
@@ -772,7 +776,10 @@ __global__ void __launch_bounds__(256) chol_inv_smem_kernel(const double* G, int
 constexpr double kCholFirstOrderMax = 1e-9;
 __global__ void __launch_bounds__(256) chol_inv_packed_kernel(const double* G, int k, double* R,
                                                               double* Rinv, int* status,
-                                                              double pivot_rel, int use_series) {
+                                                              double pivot_rel, int use_series,
+                                                              const double* dref,
+                                                              const double* tref,
+                                                              int pivot_base) {
   pdl_wait();
   extern __shared__ __align__(16) double smem[];
   double* W = smem;
@@ -794,7 +801,75 @@ __global__ void __launch_bounds__(256) chol_inv_packed_kernel(const double* G, i
       return;
     }
   }
-  chol_inv_body<true>(G, k, W, nullptr, W + (size_t)k * (k + 1), R, Rinv, status, pivot_rel);
+  chol_inv_body<true>(G, k, W, nullptr, W + (size_t)k * (k + 1), R, Rinv, status, pivot_rel, dref,
+                      tref, pivot_base);
+}
+
+// ---- pieces of the two-block Cholesky for 160 < k <= 256 (engine.cu chol_inv_blocked2) ----------
+// diag[j] = G_jj, diag[k] = trace(G)
+__global__ void chol_diag_trace_kernel(const double* __restrict__ G, int k,
+                                       double* __restrict__ diag) {
+  pdl_wait();
+  __shared__ double scratch[32];
+  double t = 0.0;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const double d = G[(size_t)j * k + j];
+    diag[j] = d;
+    t += d;
+  }
+  t = block_sum(t, scratch);
+  if (threadIdx.x == 0) diag[k] = t;
+}
+// C (m x n, ldc) = C0 + alpha A B for small operands given by element strides (a transpose is a
+// stride swap): A(i, q) = A[i a_rs + q a_cs], B(q, j) = B[q b_rs + j b_cs]; C0 may be null.
+// 16 x 16 tiles, fixed summation order.
+__global__ void __launch_bounds__(256)
+    small_gemm_kernel(int m, int n, int kk, const double* __restrict__ A, int64_t a_rs,
+                      int64_t a_cs, const double* __restrict__ B, int64_t b_rs, int64_t b_cs,
+                      const double* __restrict__ C0, int64_t c0_ld, double alpha,
+                      double* __restrict__ C, int64_t ldc) {
+  pdl_wait();
+  __shared__ double sa[16][17], sb[16][17];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i = blockIdx.y * 16 + ty, j = blockIdx.x * 16 + tx;
+  double acc = 0.0;
+  for (int q0 = 0; q0 < kk; q0 += 16) {
+    sa[ty][tx] = (i < m && q0 + tx < kk) ? A[i * a_rs + (q0 + tx) * a_cs] : 0.0;
+    sb[ty][tx] = (q0 + ty < kk && j < n) ? B[(q0 + ty) * b_rs + j * b_cs] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc = fma(sa[ty][q], sb[q][tx], acc);
+    __syncthreads();
+  }
+  if (i < m && j < n) C[i * ldc + j] = (C0 ? C0[i * c0_ld + j] : 0.0) + alpha * acc;
+}
+// R = [[R11, R12], [0, R22]], R^-1 = [[R11i, T], [0, R22i]] (k x k, row-major) from the blocks
+__global__ void chol_assemble2_kernel(int k, int h, const double* __restrict__ R11,
+                                      const double* __restrict__ R11i,
+                                      const double* __restrict__ R12, const double* __restrict__ T,
+                                      const double* __restrict__ R22,
+                                      const double* __restrict__ R22i, double* __restrict__ R,
+                                      double* __restrict__ Rinv) {
+  pdl_wait();
+  const int k2 = k - h;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    const int r = e / k, c = e % k;
+    double a, b;
+    if (r < h && c < h) {
+      a = R11[r * h + c];
+      b = R11i[r * h + c];
+    } else if (r < h) {
+      a = R12[r * k2 + (c - h)];
+      b = T[r * k2 + (c - h)];
+    } else if (c < h) {
+      a = b = 0.0;
+    } else {
+      a = R22[(r - h) * k2 + (c - h)];
+      b = R22i[(r - h) * k2 + (c - h)];
+    }
+    R[e] = a;
+    Rinv[e] = b;
+  }
 }
 __global__ void __launch_bounds__(256) chol_inv_gmem_kernel(const double* G, int k, double* ws,
                                                             double* R, double* Rinv, int* status,

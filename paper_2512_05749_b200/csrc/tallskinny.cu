@@ -560,19 +560,23 @@ cudaError_t ts_gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, in
 }
 
 cudaError_t ts_gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
-                    double* G) {
-  if (rows <= 0) return cudaMemsetAsync(G, 0, sizeof(double) * k * k, ctx.stream);
-  if (k == 128) return ts::gram_launch<128, true>(ctx, rows, A, lda, A, lda, G, k);
-  if (k == 64) return ts::gram_launch<64, true>(ctx, rows, A, lda, A, lda, G, k);
-  return ts::gram_launch<32, true>(ctx, rows, A, lda, A, lda, G, k);
+                    double* G, int64_t ldg) {
+  if (ldg <= 0) ldg = k;
+  if (rows <= 0)
+    return cudaMemset2DAsync(G, sizeof(double) * ldg, 0, sizeof(double) * k, k, ctx.stream);
+  if (k == 128) return ts::gram_launch<128, true>(ctx, rows, A, lda, A, lda, G, ldg);
+  if (k == 64) return ts::gram_launch<64, true>(ctx, rows, A, lda, A, lda, G, ldg);
+  return ts::gram_launch<32, true>(ctx, rows, A, lda, A, lda, G, ldg);
 }
 
 cudaError_t ts_cross(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
-                     const double* B, int64_t ldb, double* C) {
-  if (rows <= 0) return cudaMemsetAsync(C, 0, sizeof(double) * k * k, ctx.stream);
-  if (k == 128) return ts::gram_launch<128, false>(ctx, rows, A, lda, B, ldb, C, k);
-  if (k == 64) return ts::gram_launch<64, false>(ctx, rows, A, lda, B, ldb, C, k);
-  return ts::gram_launch<32, false>(ctx, rows, A, lda, B, ldb, C, k);
+                     const double* B, int64_t ldb, double* C, int64_t ldc) {
+  if (ldc <= 0) ldc = k;
+  if (rows <= 0)
+    return cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * k, k, ctx.stream);
+  if (k == 128) return ts::gram_launch<128, false>(ctx, rows, A, lda, B, ldb, C, ldc);
+  if (k == 64) return ts::gram_launch<64, false>(ctx, rows, A, lda, B, ldb, C, ldc);
+  return ts::gram_launch<32, false>(ctx, rows, A, lda, B, ldb, C, ldc);
 }
 
 bool ts_mul_supported(int64_t k, const double* A, int64_t lda, const double* Y, int64_t ldy) {
@@ -584,10 +588,10 @@ namespace {
 template <int MODE>
 cudaError_t mul_dispatch(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                          const double* M, bool upper, double alpha, const double* Cin,
-                         int64_t ldcin, double* Y, int64_t ldy, double* out) {
+                         int64_t ldcin, double* Y, int64_t ldy, double* out, int64_t ldm = 0) {
   auto go = [&](auto kc, auto tri) {
     return ts::mul_launch<decltype(kc)::value, decltype(tri)::value, MODE>(
-        ctx, rows, A, lda, M, k, alpha, Cin, ldcin, Y, ldy, out);
+        ctx, rows, A, lda, M, ldm > 0 ? ldm : k, alpha, Cin, ldcin, Y, ldy, out);
   };
   using T = std::true_type;
   using F = std::false_type;
@@ -601,18 +605,19 @@ cudaError_t mul_dispatch(Context& ctx, int64_t rows, int64_t k, const double* A,
 }  // namespace
 
 cudaError_t ts_mul(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
-                   const double* M, bool upper, double alpha, double* Y, int64_t ldy) {
+                   const double* M, bool upper, double alpha, double* Y, int64_t ldy,
+                   int64_t ldm) {
   if (rows <= 0) return cudaSuccess;
   return mul_dispatch<ts::kStore>(ctx, rows, k, A, lda, M, upper, alpha, nullptr, 0, Y, ldy,
-                                  nullptr);
+                                  nullptr, ldm);
 }
 
 cudaError_t ts_mul_add(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                        const double* M, double alpha, const double* Cin, int64_t ldcin, double* Y,
-                       int64_t ldy) {
+                       int64_t ldy, int64_t ldm) {
   if (rows <= 0) return cudaSuccess;
   return mul_dispatch<ts::kAddStore>(ctx, rows, k, A, lda, M, false, alpha, Cin, ldcin, Y, ldy,
-                                     nullptr);
+                                     nullptr, ldm);
 }
 
 cudaError_t ts_mul_add_sumsq(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,

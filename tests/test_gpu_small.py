@@ -21,7 +21,7 @@ def _small(op, a):
     return o1.cpu().numpy(), o2.cpu().numpy(), (st[0], st[1])
 
 
-@pytest.mark.parametrize("k", [1, 2, 7, 32, 64, 100, 128, 150, 200])
+@pytest.mark.parametrize("k", [1, 2, 7, 32, 64, 100, 128, 150, 161, 200, 255, 256, 300])
 def test_cholesky_inverse(k):
     rng = np.random.default_rng(k)
     x = rng.standard_normal((3 * k + 5, k)) * np.exp(rng.uniform(-3, 3, k))
@@ -32,6 +32,17 @@ def test_cholesky_inverse(k):
     np.testing.assert_allclose(r, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
     np.testing.assert_allclose(rinv @ r, np.eye(k), atol=1e-10)
     assert np.all(np.tril(rinv, -1) == 0.0) and np.all(np.tril(r, -1) == 0.0)
+
+
+@pytest.mark.parametrize("dup", [(5, 40), (10, 200), (130, 250)])
+def test_cholesky_two_block_flags_deficient_column(dup):
+    """k = 256 runs as two diagonal blocks (engine.cu chol_inv_blocked2): a duplicated column is
+    flagged at its own index whichever block it falls in, against the original diagonal."""
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((800, 256))
+    x[:, dup[1]] = x[:, dup[0]]
+    _, _, st = _small(0, x.T @ x)
+    assert st[0] == dup[1] + 1, st
 
 
 def test_cholesky_flags_deficient_and_zero():
@@ -75,7 +86,7 @@ def test_maxeig_clustered_top():
     assert abs(lam[0, 0] - 1.0) < 1e-13
 
 
-@pytest.mark.parametrize("k", [1, 5, 32, 64, 100, 128, 150])
+@pytest.mark.parametrize("k", [1, 5, 32, 64, 100, 128, 150, 256])
 @pytest.mark.parametrize("eps", [0.0, 1e-15, 1e-12, 1e-10, 3e-6])
 def test_cholesky_near_identity_series(k, eps):
     """Near-identity Grams (the second CholeskyQR2 pass) take the series path: R and R^-1 agree
