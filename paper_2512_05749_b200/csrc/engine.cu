@@ -308,10 +308,28 @@ void gemm_rm_add(Context& ctx, int64_t M, int64_t N, int64_t K, const double* A,
   WSSR_CUDA(gemm(ctx, Layout::RM, a, 1024, ctx.stream));
 }
 
+// k = 256 (BASELINE configs[4]) runs on the k = 128 tall-skinny kernels as 2 x 2 blocks: the two
+// 128-column halves of a rows x 256 block and the four 128 x 128 blocks of a 256 x 256 operand are
+// addressed in place through their leading dimensions.
+constexpr int64_t kTsHalf = 128;
+bool ts_blocked(const Context& ctx, int64_t k) { return ctx.tallskinny && k == 2 * kTsHalf; }
+bool ts_blocked_rows(const double* A, int64_t lda, const double* Y, int64_t ldy) {
+  return ts_mul_supported(kTsHalf, A, lda, Y, ldy) &&
+         ts_mul_supported(kTsHalf, A + kTsHalf, lda, Y + kTsHalf, ldy);
+}
+void transpose(Context& ctx, const double* in, int64_t ldi, int64_t rows, int64_t cols,
+               const double* shift, double scale, double* out, int64_t ldo);
+
 // Gram G (k x k) = A^T A, A rows x k (lda); allreduced over ranks when rows are sharded.
 void gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, double* G,
           bool distributed) {
-  if (ctx.tallskinny && ts_supported(k)) {
+  if (ts_blocked(ctx, k)) {
+    const int64_t h = kTsHalf;
+    WSSR_CUDA(ts_gram(ctx, rows, h, A, lda, G, k));
+    WSSR_CUDA(ts_gram(ctx, rows, h, A + h, lda, G + h * k + h, k));
+    WSSR_CUDA(ts_cross(ctx, rows, h, A, lda, A + h, lda, G + h, k));
+    transpose(ctx, G + h, k, h, h, nullptr, 1.0, G + h * k, k);  // G21 = G12^T
+  } else if (ctx.tallskinny && ts_supported(k)) {
     WSSR_CUDA(ts_gram(ctx, rows, k, A, lda, G));
   } else {
     gemm_cm(ctx, k, k, rows, A, lda, nullptr, A, lda, G, k, 1.0, false);
@@ -322,7 +340,12 @@ void gram(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, d
 // C (k x k) = A^T B for rows x k blocks
 void cross(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda, const double* B,
            int64_t ldb, double* C) {
-  if (ctx.tallskinny && ts_supported(k)) {
+  if (ts_blocked(ctx, k)) {
+    const int64_t h = kTsHalf;
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j)
+        WSSR_CUDA(ts_cross(ctx, rows, h, A + i * h, lda, B + j * h, ldb, C + i * h * k + j * h, k));
+  } else if (ctx.tallskinny && ts_supported(k)) {
     WSSR_CUDA(ts_cross(ctx, rows, k, A, lda, B, ldb, C));
   } else {
     gemm_cm(ctx, k, k, rows, A, lda, nullptr, B, ldb, C, k, 1.0, false);
@@ -342,7 +365,14 @@ void gemv_t(Context& ctx, int64_t rows, int64_t n, const double* A, int64_t lda,
 // Y = A M for a rows x k block A and a k x k M (upper: M upper triangular, e.g. R^-1)
 void mul_small(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                const double* M, bool upper, double* Y, int64_t ldy) {
-  if (ctx.tallskinny && ts_mul_supported(k, A, lda, Y, ldy)) {
+  if (ts_blocked(ctx, k) && ts_blocked_rows(A, lda, Y, ldy) && A != Y) {
+    // [Y1 Y2] = [A1 A2] [[M11, M12], [M21, M22]]  (M21 = 0 when upper)
+    const int64_t h = kTsHalf;
+    WSSR_CUDA(ts_mul(ctx, rows, h, A, lda, M, upper, 1.0, Y, ldy, k));
+    if (!upper) WSSR_CUDA(ts_mul_add(ctx, rows, h, A + h, lda, M + h * k, 1.0, Y, ldy, Y, ldy, k));
+    WSSR_CUDA(ts_mul(ctx, rows, h, A, lda, M + h, false, 1.0, Y + h, ldy, k));
+    WSSR_CUDA(ts_mul_add(ctx, rows, h, A + h, lda, M + h * k + h, 1.0, Y + h, ldy, Y + h, ldy, k));
+  } else if (ctx.tallskinny && ts_mul_supported(k, A, lda, Y, ldy)) {
     WSSR_CUDA(ts_mul(ctx, rows, k, A, lda, M, upper, 1.0, Y, ldy));
   } else {
     gemm_rm(ctx, rows, k, k, A, lda, nullptr, M, k, Y, ldy, 1.0, false);
@@ -352,7 +382,16 @@ void mul_small(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t l
 // Y = Cin - A M
 void sub_mul_small(Context& ctx, int64_t rows, int64_t k, const double* A, int64_t lda,
                    const double* M, const double* Cin, int64_t ldcin, double* Y, int64_t ldy) {
-  if (ctx.tallskinny && ts_mul_supported(k, A, lda, Y, ldy) &&
+  if (ts_blocked(ctx, k) && ts_blocked_rows(A, lda, Y, ldy) && ts_blocked_rows(Cin, ldcin, Y, ldy) &&
+      A != Y) {
+    const int64_t h = kTsHalf;
+    for (int j = 0; j < 2; ++j) {  // Y_j = Cin_j - A1 M_1j - A2 M_2j
+      WSSR_CUDA(ts_mul_add(ctx, rows, h, A, lda, M + j * h, -1.0, Cin + j * h, ldcin, Y + j * h,
+                           ldy, k));
+      WSSR_CUDA(ts_mul_add(ctx, rows, h, A + h, lda, M + h * k + j * h, -1.0, Y + j * h, ldy,
+                           Y + j * h, ldy, k));
+    }
+  } else if (ctx.tallskinny && ts_mul_supported(k, A, lda, Y, ldy) &&
       ts_mul_supported(k, Cin, ldcin, Y, ldy)) {
     WSSR_CUDA(ts_mul_add(ctx, rows, k, A, lda, M, -1.0, Cin, ldcin, Y, ldy));
   } else {
@@ -995,7 +1034,7 @@ SsiResult ssi_core(Context& ctx, const Ohat& o, int64_t k, int64_t max_iters,
         WSSR_CUDA(ts_mul_add_sumsq(ctx, nr, k, qs, k, quot, -1.0, ws, k, scal));
       } else {
         Buf tmp((size_t)nr * k, st);
-        gemm_rm_add(ctx, nr, k, k, qs, k, quot, k, ws, k, tmp, k, -1.0);  // w - q quotient
+        sub_mul_small(ctx, nr, k, qs, k, quot, ws, k, tmp, k);  // w - q quotient
         sumsq_matrix(ctx, tmp, nr, k, k, scal);
       }
       if (sl.on) allreduce(ctx, scal, 1);
@@ -2240,6 +2279,26 @@ int wssr_debug_tallskinny(wssr_ctx* ctx, int op, int64_t rows, int64_t k, const 
                           double* out) {
   return guarded(ctx, [&] {
     Context& c = ctx->c;
+    if (k == 2 * kTsHalf && rows >= 0 && c.tallskinny) {
+      // k = 256: the engine's 2 x 2 block composition of the k = 128 kernels (alpha = 1 for the
+      // products, alpha = -1 for op 4, as the engine uses them)
+      switch (op) {
+        case 0: gram(c, rows, k, a, k, out, false); break;
+        case 1: cross(c, rows, k, a, k, b, k, out); break;
+        case 2:
+        case 3:
+          if (alpha != 1.0) throw Fail{WSSR_ERR_VALUE, "tall-skinny k = 256: alpha must be 1"};
+          mul_small(c, rows, k, a, k, m, op == 2, out, k);
+          break;
+        case 4:
+          if (alpha != -1.0) throw Fail{WSSR_ERR_VALUE, "tall-skinny k = 256: alpha must be -1"};
+          sub_mul_small(c, rows, k, a, k, m, cin, k, out, k);
+          break;
+        default: throw Fail{WSSR_ERR_VALUE, "tall-skinny k = 256: ops 0-4"};
+      }
+      sync(c);
+      return;
+    }
     if (!ts_supported(k) || rows < 0) throw Fail{WSSR_ERR_VALUE, "tall-skinny: k must be 32, 64 or 128"};
     static const int reps = [] {
       const char* e = std::getenv("WSSR_DEBUG_REPS");  // profiling: back-to-back launches

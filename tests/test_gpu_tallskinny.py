@@ -73,6 +73,39 @@ def test_products(k, rows, alpha):
     assert ((g - ref).abs().max() / ref.abs().max()).item() < 1e-13
 
 
+@pytest.mark.parametrize("rows", [1, 17, 1000, 4099, 65536 + 3])
+def test_k256_as_blocks_of_the_k128_kernels(rows):
+    """k = 256 (BASELINE configs[4]): Grams, cross products and the row-block products composed
+    from the k = 128 kernels on the two 128-column halves (engine.cu ts_blocked)."""
+    from paper_2512_05749_b200 import _lib
+
+    ctx = _lib.context()
+    k = 256
+    A, B, M, C = _ops(rows, k, rows * 7 + k)
+    U = torch.triu(M)
+    out = torch.full((k, k), float("nan"), dtype=torch.float64, device="cuda")
+    Y = torch.full((rows, k), float("nan"), dtype=torch.float64, device="cuda")
+
+    def call(op, b=None, m=None, cin=None, alpha=1.0, dst=out):
+        ctx.call("wssr_debug_tallskinny", op, rows, k, _lib.ptr(A),
+                 _lib.ptr(b) if b is not None else None, _lib.ptr(m) if m is not None else None,
+                 _lib.ptr(cin) if cin is not None else None, alpha, _lib.ptr(dst))
+
+    def close(x, ref):
+        return ((x - ref).abs().max() / ref.abs().max()).item() < 1e-14
+
+    call(0)
+    assert torch.equal(out, out.t()) and close(out, A.t() @ A)
+    call(1, b=B)
+    assert close(out, A.t() @ B)
+    call(2, m=U, dst=Y)
+    assert close(Y, A @ U)
+    call(3, m=M, dst=Y)
+    assert close(Y, A @ M)
+    call(4, m=M, cin=C, alpha=-1.0, dst=Y)
+    assert close(Y, C - A @ M)
+
+
 def test_bitwise_repeatable():
     from paper_2512_05749_b200 import _lib
 
