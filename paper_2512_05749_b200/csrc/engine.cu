@@ -810,12 +810,36 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
         rowcnt = nullptr;
       }
     }
+    // On-the-fly passes with more than 128 thin columns (k = 256, BASELINE configs[4]) run per
+    // 128-column group, each on the transposed kernel (one conversion of a sample tile serves
+    // 128 columns; the 64-column kernel would convert it once per 64).  The plane store and the
+    // guard's row counts ride on the first group only.
+    auto ozaki_fly = [&](const GemmArgs& g, int8_t* st_planes, unsigned long long* rc) {
+      constexpr int64_t kGroup = 128;
+      if (g.N <= kGroup)
+        return ozaki_gemm(ctx, layout, g, o.f32, tab, ctx.stream, nullptr, st_planes, rc, nds);
+      for (int64_t c0 = 0; c0 < g.N; c0 += kGroup) {
+        GemmArgs sub = g;
+        sub.N = std::min<int64_t>(kGroup, g.N - c0);
+        sub.B = g.B + c0;
+        sub.C = g.C + c0;
+        const cudaError_t e = ozaki_gemm(ctx, layout, sub, o.f32, tab, ctx.stream, nullptr,
+                                         c0 == 0 ? st_planes : nullptr, c0 == 0 ? rc : nullptr,
+                                         nds);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    };
     if (n_pl == 0 || n_pl >= o.n) {
       // profiling (WSSR_FINE_PHASES): 14 = the step's digitising first pass, 15 = the other
       // row-major (v) passes
       const int fp = (ctx.fine_phases && layout == Layout::RM) ? (store ? 14 : 15) : -1;
       PhaseTimer tm(ctx, fp, 0.0, 0.0);
-      WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowcnt, nds));
+      if (planes) {
+        WSSR_CUDA(ozaki_gemm(ctx, layout, a, o.f32, tab, ctx.stream, planes, store, rowcnt, nds));
+      } else {
+        WSSR_CUDA(ozaki_fly(a, store, rowcnt));
+      }
       if (rowcnt) WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
       return;
     }
@@ -835,9 +859,12 @@ void gemm_samples(Context& ctx, Layout layout, const Ohat& o, int64_t M, int64_t
       a2.B = B + n_pl * ldb;
       a2.accumulate = 1;
     }
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowcnt, nds));
-    WSSR_CUDA(ozaki_gemm(ctx, layout, a2, o.f32, tab, ctx.stream, nullptr, nullptr,
-                         rowcnt ? rowcnt + n_pl : nullptr, nds));
+    if (planes) {
+      WSSR_CUDA(ozaki_gemm(ctx, layout, a1, o.f32, tab, ctx.stream, planes, store, rowcnt, nds));
+    } else {
+      WSSR_CUDA(ozaki_fly(a1, store, rowcnt));
+    }
+    WSSR_CUDA(ozaki_fly(a2, nullptr, rowcnt ? rowcnt + n_pl : nullptr));
     if (rowcnt) WSSR_CUDA(ozaki_row_guard(ctx, rowcnt, o.n, o.status + 2, ctx.stream));
     return;
   }
